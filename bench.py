@@ -1,0 +1,407 @@
+#!/usr/bin/env python
+"""Benchmark: edge-intersections/s of the fused Bloom triangle-count pass.
+
+Workload (BASELINE.json configs[1], the metric's config that fits one GPU):
+R-MAT scale 20, edge factor 16, seed 1 (15.7 M undirected edges), Bloom
+sketches B=1024, b=2, seed DEFAULT_HASH_SEED; one step = one
+``tc_estimate(graph, sketched, "bf_and")`` pass over every edge (the fused
+gather + AND + popcount + histogram kernel) plus, for N>1, the NCCL
+all-reduce of the popcount histogram.  Other configs are parity-test cases.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One JSON line on rank 0.  ``--impl reference`` times the reference's CPU
+algorithm (oracle/ numpy port: the reference's own vectorised strategy and
+16,384-edge thread-pool grid) on the host's cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+WORKLOAD = {
+    "c2": dict(desc="R-MAT s20 ef16 seed1 (a,b,c,d=.57,.19,.19,.05), Bloom B=1024 b=2, "
+                    "tc_estimate bf_and", scale=20, ef=16, seed=1, bits=1024, b=2),
+    "c5": dict(desc="R-MAT s24 ef16 seed4, Bloom B=2048 b=2, tc_estimate bf_and",
+               scale=24, ef=16, seed=4, bits=2048, b=2),
+}
+METRIC = "edge-intersections/s (BF/MinHash TC) at 1/2/4/8 B200; % of HBM roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(WORKLOAD), default="c2")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def make_graph(cfg):
+    from paper_2208_11469_b200.graphs import generate_kronecker
+    return generate_kronecker(cfg["scale"], cfg["ef"], cfg["seed"])
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def load_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def load_traffic(config: str):
+    """dram bytes per launch of the TC kernel from the committed ncu summary."""
+    path = os.path.join(REPO, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as fh:
+            return json.load(fh).get(config, {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+
+def run_ours(args, cfg, rank, world, local):
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_2208_11469_b200 as pg
+    from paper_2208_11469_b200 import _native as N
+    from paper_2208_11469_b200.sharding import allreduce_counts, edge_range
+
+    t0 = time.time()
+    g = make_graph(cfg)
+    gen_s = time.time() - t0
+    bits, b = cfg["bits"], cfg["b"]
+    stream = torch.cuda.current_stream()
+
+    # sketch build on the device (reported separately, not in the timed step)
+    dev = g.device()
+    us, vs = dev.upper_edges()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    build_ms = []
+    for _ in range(3):
+        ev0.record(stream)
+        sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=b, bits_override=bits)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        build_ms.append(ev0.elapsed_time(ev1))
+    provider = pg.make_provider("bf_and", sketched=sk)
+    m = us.numel()
+    e_begin, e_end = edge_range(m, rank, world)
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def l2_flush():
+        N.call("pg_l2_flush", N.ptr(flush), flush.numel(), N.stream_handle())
+
+    def step():
+        counts = provider._tc_counts(us, vs, e_begin, e_end)
+        return allreduce_counts(counts)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    kends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    with ClockSampler(local) as clk:
+        time.sleep(0.2)
+        for i in range(args.steps):
+            l2_flush()  # between timed steps, outside the events
+            starts[i].record(stream)
+            counts = provider._tc_counts(us, vs, e_begin, e_end)
+            kends[i].record(stream)
+            counts = allreduce_counts(counts)
+            ends[i].record(stream)
+        torch.cuda.synchronize()
+        # keep the GPU busy for the clock sampler's benefit, untimed
+        tq = time.time()
+        while time.time() - tq < 0.5:
+            provider._tc_counts(us, vs, e_begin, e_end)
+        torch.cuda.synchronize()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    kern_ms = [s.elapsed_time(e) for s, e in zip(starts, kends)]
+    total_ms = sum(step_ms)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms, sum(kern_ms)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, kern_total = t.tolist()
+    else:
+        kern_total = sum(kern_ms)
+    ms_per_step = total_ms / args.steps
+    kern_ms_avg = kern_total / args.steps
+    value = m / (ms_per_step / 1e3)
+
+    counts = step().cpu().numpy()
+    estimate = provider._tc_combine(counts) / 3.0
+
+    # roofline: algorithmic bytes per launch = edges of this rank x (2 rows + 2 int32)
+    bytes_per_edge = 2 * (bits // 8) + 8
+    launch_bytes = (e_end - e_begin) * bytes_per_edge
+    achieved = launch_bytes / (kern_ms_avg / 1e3) / 1e9
+    peak, peak_src = load_peaks()
+    traffic = load_traffic(args.config) if world == 1 else None
+
+    # e2e through the public API: pinned host graph + host sketches -> device ->
+    # fused pass -> host estimate, every step
+    e2e = None
+    if rank == 0 and world == 1 and args.e2e_steps > 0:
+        e2e = run_e2e(pg, g, sk, args.e2e_steps, bits, b, m)
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(g, cfg, estimate)
+        out = {
+            "metric": METRIC, "value": value, "unit": "edge-intersections/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (seeded R-MAT, reference generator draw order)",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "m": m,
+                       "edges_per_rank": e_end - e_begin,
+                       "sketch_bytes": g.n * bits // 8,
+                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
+                       "parallelism": f"edge-range shards x{world}, replicated sketches, "
+                                      "NCCL all_reduce(int64[B+2])" if world > 1 else "1 GPU"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "bytes_per_edge": bytes_per_edge, "kernel_ms": kern_ms_avg,
+                         "peak_source": peak_src},
+            "clocks": clk.summary(),
+            "gpu_launches": args.steps,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "estimate": estimate,
+            "build": {"bloom_build_ms": min(build_ms), "graph_gen_s": gen_s,
+                      "rows_per_s": g.n / (min(build_ms) / 1e3)},
+        }
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def run_e2e(pg, g, sk, steps, bits, b, m):
+    """Same metric through tc_estimate() with HOST inputs copied every step."""
+    import torch
+    from paper_2208_11469_b200.sketches import SketchedGraph
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    off_h, adj_h = pinned(g.offsets), pinned(g.adjacency)
+    rows_h, ones_h = pinned(sk.bit_matrix), pinned(sk.ones)
+    sizes_h = pinned(sk.sizes)
+    h2d = off_h.nbytes + adj_h.nbytes + rows_h.nbytes + ones_h.nbytes + sizes_h.nbytes
+    times, est = [], None
+    for i in range(steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        graph = pg.CsrGraph(off_h, adj_h)
+        skh = SketchedGraph("bloom", sk.plan, sk.family, "undirected", sizes_h,
+                            bit_matrix=rows_h, ones=ones_h)
+        est = pg.tc_estimate(graph, skh, "bf_and")  # includes the D2H of the histogram
+        torch.cuda.synchronize()
+        if i:  # first call is warm-up
+            times.append(time.perf_counter() - t0)
+    t = statistics.median(times)
+    return {"value": m / t, "unit": "edge-intersections/s", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": 8 * (bits + 2), "ms_per_step": t * 1e3,
+            "path": "tc_estimate(CsrGraph(pinned int64 CSR), SketchedGraph(pinned host "
+                    "bit_matrix)) -> upload, device edge list, fused kernel, histogram D2H",
+            "estimate": est}
+
+
+# ---------------------------------------------------------------------------
+# CPU: the reference's algorithm on the host cores
+
+
+def cpu_baseline(g, cfg, gpu_estimate, budget_s=12.0):
+    from oracle import oracle as O
+    threads = len(os.sched_getaffinity(0))
+    port = O.NumpyPort(threads=threads)
+    bits, b = cfg["bits"], cfg["b"]
+    rows, _ = port.build_bloom(g.offsets, g.adjacency, bits, b)
+    us, vs = O.upper_edges(g.offsets, g.adjacency)
+    sizes = np.diff(g.offsets)
+
+    def chunk(a, c):
+        return O.NumpyPort.bloom_chunk(rows, bits, b, "bf_and", sizes, a, c)
+
+    port.tc_sum(chunk, us[:1 << 18], vs[:1 << 18])  # warm-up
+    passes, edges, t0 = 0, 0, time.perf_counter()
+    full = None
+    while True:
+        full = port.tc_sum(chunk, us, vs) / 3.0
+        passes += 1
+        edges += len(us)
+        if time.perf_counter() - t0 > budget_s or passes >= 3:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": edges / dt, "unit": "edge-intersections/s", "cores": threads,
+            "kind": "port",
+            "sample": f"{passes} full tc_estimate pass(es) over all {len(us)} edges "
+                      "(numpy port of the reference's chunked thread-pool path)",
+            "estimate": full,
+            "parity_rel_err_vs_gpu": abs(full - gpu_estimate) / max(1.0, abs(full))}
+
+
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return None
+    from oracle import oracle as O
+    threads = len(os.sched_getaffinity(0))
+    port = O.NumpyPort(threads=threads)
+    g = make_graph(cfg)
+    bits, b = cfg["bits"], cfg["b"]
+    rows, _ = port.build_bloom(g.offsets, g.adjacency, bits, b)
+    us, vs = O.upper_edges(g.offsets, g.adjacency)
+    sizes = np.diff(g.offsets)
+    sample = min(len(us), 1 << 21)  # each step: a bounded 2 Mi-edge sample
+
+    def chunk(a, c):
+        return O.NumpyPort.bloom_chunk(rows, bits, b, "bf_and", sizes, a, c)
+
+    rng = np.random.default_rng(0)
+    starts = rng.integers(0, max(1, len(us) - sample), size=args.warmup + args.steps)
+    for i in range(args.warmup):
+        s0 = int(starts[i])
+        port.tc_sum(chunk, us[s0:s0 + sample], vs[s0:s0 + sample])
+    times = []
+    for i in range(args.steps):
+        s0 = int(starts[args.warmup + i])
+        t0 = time.perf_counter()
+        port.tc_sum(chunk, us[s0:s0 + sample], vs[s0:s0 + sample])
+        times.append(time.perf_counter() - t0)
+    ms = 1e3 * sum(times) / len(times)
+    value = sample / (ms / 1e3)
+    out = {"metric": METRIC, "value": value, "unit": "edge-intersections/s", "impl": "reference",
+           "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
+           "data": "synthetic (seeded R-MAT)",
+           "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "m": len(us)},
+           "cpu_baseline": {"value": value, "unit": "edge-intersections/s", "cores": threads,
+                            "kind": "port",
+                            "sample": f"per step a contiguous {sample}-edge slice of the "
+                                      "upper edge list (random offset, seed 0)"},
+           "e2e": {"value": value, "unit": "edge-intersections/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return out
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    cfg = WORKLOAD[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg, rank, world)
+        return
+    run_ours(args, cfg, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,189 @@
+/*
+ * probgraph_b200.h -- C ABI of the B200-native per-edge sketch-intersection
+ * engine (ProbGraph, arxiv 2208.11469).
+ *
+ * This is the drop-in boundary that sits under the reference's Python
+ * provider/plugin API (`make_provider`, `IntersectionProvider.pair_many`,
+ * `build_sketched_graph`, `tc_estimate`, `four_clique_count`,
+ * `jarvis_patrick_cluster`).  Every entry point names the reference
+ * interface it replaces (paths relative to /root/reference/pkg/src/probgraph).
+ *
+ * Conventions (all functions):
+ *   - return 0 on success, a negative PG_ERR_* code on failure; the message
+ *     of the last failure on the calling thread is read with pg_last_error;
+ *   - every array argument is a DEVICE pointer owned by the caller (torch
+ *     tensors or cudaMalloc), unless the name ends in `_host`;
+ *   - `stream` is a cudaStream_t passed as void*; NULL means the legacy
+ *     default stream.  Calls are asynchronous and stream-ordered; none of
+ *     them synchronises the host except where stated;
+ *   - vertex IDs are int32 (n < 2^31), CSR offsets are int64;
+ *   - sketch layouts in HBM (row-major, one row per vertex):
+ *       Bloom : uint64 rows[n][bits/64], little-endian bit p of the row is
+ *               word p>>6, bit p&63; ones int32[n]
+ *       k-Hash: int32 entries[n][k], -1 for an empty neighbourhood
+ *       1-Hash: int32 entries[n][k] ascending IDs, -1 pad; lengths int32[n]
+ *       KMV   : double values[n][k] ascending, +inf pad; lengths int32[n]
+ */
+#ifndef PROBGRAPH_B200_H
+#define PROBGRAPH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define PG_API __attribute__((visibility("default")))
+#else
+#define PG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PG_ABI_VERSION 1
+
+#define PG_OK 0
+#define PG_ERR_INVALID (-1)     /* bad argument            -> ValueError     */
+#define PG_ERR_CUDA (-2)        /* CUDA runtime failure    -> RuntimeError   */
+#define PG_ERR_UNSUPPORTED (-3) /* parameter outside the device kernels'
+                                   supported range (e.g. k > 256)            */
+
+/* estimator / op selectors (reference EstimatorKind, estimators.py:54-62) */
+#define PG_BF_AND 0
+#define PG_BF_L 1
+#define PG_BF_OR 2
+#define PG_KHASH 3
+#define PG_ONEHASH 4
+#define PG_KMV 5
+
+/* ---- runtime -------------------------------------------------------- */
+PG_API int pg_abi_version(void);
+/* copies the calling thread's last error message (NUL terminated) */
+PG_API int pg_last_error(char* buf, size_t len);
+/* SM count of the current device */
+PG_API int pg_device_sm_count(int* out_host);
+
+/* ---- a2: hash family  (hashing.py:78-111 HashFamily.__post_init__) --- */
+/* seed_i = mix64(base ^ mix64(i+1)), i < count; host-only, no device use */
+PG_API int pg_family_seeds(uint64_t base, int32_t count, uint64_t* out_host);
+/* a1/a3 words: out[j] = mix64(seed ^ (uint64)keys[j])  (hashing.py:114-118) */
+PG_API int pg_hash_words(const int64_t* keys, int64_t count, uint64_t seed,
+                  uint64_t* out, void* stream);
+
+/* ---- graph preparation (graphs.py:101-105 CsrGraph.edges,
+ *      mining.py:83-85 _directed_edge_arrays) ----------------------------- */
+/* bytes of scratch pg_csr_upper_edges needs for n vertices */
+PG_API int pg_csr_upper_edges_workspace(int64_t n, size_t* out_bytes_host);
+/* Writes every undirected edge once, u < v, in CSR order (== graph.edges()).
+ * us/vs hold `capacity` entries (m = nnz/2 for a symmetric CSR); m_host
+ * receives the count (host sync); a count above capacity is an error. */
+PG_API int pg_csr_upper_edges(const int64_t* offsets, const int32_t* adj, int64_t n,
+                       int32_t* us, int32_t* vs, int64_t capacity, int64_t* m_host,
+                       void* workspace, size_t workspace_bytes, void* stream);
+/* src[j] = row of adjacency entry j (np.repeat(arange(n), degrees)) */
+PG_API int pg_csr_expand_rows(const int64_t* offsets, int64_t n, int64_t nnz,
+                       int32_t* src, void* stream);
+
+/* ---- (1) sketch builders  (sketches.py:314-396 _build_*_matrix,
+ *      :399-451 build_sketched_graph) ------------------------------------ */
+/* seeds_dev: the HashFamily seeds (count = b, k, 1, 1 respectively) */
+PG_API int pg_build_bloom(const int64_t* offsets, const int32_t* adj, int64_t n,
+                   int32_t bits, int32_t b, const uint64_t* seeds_dev,
+                   uint64_t* rows, int32_t* ones, void* stream);
+PG_API int pg_build_khash(const int64_t* offsets, const int32_t* adj, int64_t n,
+                   int32_t k, const uint64_t* seeds_dev, int32_t* entries,
+                   void* stream);
+PG_API int pg_build_onehash(const int64_t* offsets, const int32_t* adj, int64_t n,
+                     int32_t k, const uint64_t* seeds_dev, int32_t* entries,
+                     int32_t* lengths, void* stream);
+PG_API int pg_build_kmv(const int64_t* offsets, const int32_t* adj, int64_t n,
+                 int32_t k, const uint64_t* seeds_dev, double* values,
+                 int32_t* lengths, void* stream);
+
+/* ---- (2) per-edge estimators, parity path
+ *      (providers.py:150-162 BloomProvider.pair_many,
+ *       :205-232 MinHashProvider.pair_many, :266-301 KmvProvider.pair_many) */
+/* op: PG_BF_AND | PG_BF_L | PG_BF_OR.  lut: double[bits+1] =
+ * swamidass_value(bits, b, 0..bits) (estimators.py:65-70).  out_count
+ * (popcount of AND / OR) and out_est are each nullable. */
+PG_API int pg_pairs_bloom(const uint64_t* rows, int32_t bits, int32_t b, int32_t op,
+                   const int32_t* sizes, const double* lut,
+                   const int32_t* us, const int32_t* vs, int64_t count,
+                   int32_t* out_count, double* out_est, void* stream);
+/* onehash != 0 selects 1-Hash semantics; out_count = match count */
+PG_API int pg_pairs_minhash(const int32_t* entries, int32_t k, int32_t onehash,
+                     const int32_t* sizes, const int32_t* us,
+                     const int32_t* vs, int64_t count, int32_t* out_count,
+                     double* out_est, void* stream);
+/* out_common / out_union: common and distinct-union counts; out_kth: the
+ * max(k_eff,1)-th smallest distinct union value (all nullable) */
+PG_API int pg_pairs_kmv(const double* values, const int32_t* lengths, int32_t k,
+                 const int32_t* sizes, const int32_t* us, const int32_t* vs,
+                 int64_t count, int32_t* out_common, int32_t* out_union,
+                 double* out_kth, double* out_est, void* stream);
+
+/* ---- (2)+(3) fused whole-graph passes over edges [e_begin, e_end) -------
+ *      mining.py:105-130 tc_estimate, :63-80 _chunked_sum                */
+/* Bloom TC.  out_hist: int64[bits+1] histogram of per-edge popcounts
+ * (for PG_BF_OR only edges with raw > 0 are counted, and out_sum_pos
+ * receives the int64 sum of (s_u+s_v) over those edges).  Overwrites
+ * the outputs.  Final estimate is formed on the host from the integers. */
+PG_API int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op,
+                const int32_t* sizes, const double* lut, const int32_t* us,
+                const int32_t* vs, int64_t e_begin, int64_t e_end,
+                int64_t* out_hist, int64_t* out_sum_pos, void* stream);
+/* k-/1-Hash TC: out_cnt[m], out_ssum[m] (m = 0..k): number of edges and
+ * int64 sum of (s_u+s_v) of non-verbatim edges with m matches;
+ * out_verbatim[0] = sum of matches over verbatim 1-Hash edges. */
+PG_API int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash,
+                  const int32_t* sizes, const int32_t* us, const int32_t* vs,
+                  int64_t e_begin, int64_t e_end, int64_t* out_cnt,
+                  int64_t* out_ssum, int64_t* out_verbatim, void* stream);
+/* KMV TC: out_sum[0] = sum of per-edge estimates (fixed-order fp64) */
+PG_API int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k,
+              const int32_t* sizes, const int32_t* us, const int32_t* vs,
+              int64_t e_begin, int64_t e_end, double* out_sum, void* stream);
+/* Jaccard clustering count (config 4; estimators.py:123-131 + 148-154 and
+ * mining.py:157-186).  out_counts[0] = #edges with matches >= min_matches
+ * (J-hat = m/k >= tau), out_counts[1] = #edges whose vertex_similarity
+ * JACCARD reading (clamped intersection) is >= tau, out_counts[2..k+2] =
+ * histogram of matches. */
+PG_API int pg_jaccard_count_khash(const int32_t* entries, int32_t k,
+                           const int32_t* degrees, const int32_t* us,
+                           const int32_t* vs, int64_t e_begin, int64_t e_end,
+                           int32_t min_matches, double tau,
+                           int64_t* out_counts, void* stream);
+/* 4-clique, Bloom over N+ (mining.py:133-154 + providers.py:164-175):
+ * for each directed edge j in [e_begin,e_end) with src[j]=u, dir_adj[j]=v:
+ * C3 = N+u & N+v exactly, then for w in C3 histogram
+ * popcount(rows_plus[w] op BF(C3)).  op = PG_BF_AND | PG_BF_L | PG_BF_OR
+ * (OR: out_hist counts positive edges, out_sum_pos gets sum(s_w + |C3|)).
+ * out_triples[0] = number of (u,v,w) triples. */
+PG_API int pg_4clique_bloom(const int64_t* dir_off, const int32_t* dir_adj,
+                     const int32_t* src, int64_t e_begin, int64_t e_end,
+                     const uint64_t* rows_plus, int32_t bits, int32_t b,
+                     const uint64_t* seeds_dev, int32_t op,
+                     const int32_t* sizes, const double* lut,
+                     int64_t* out_hist, int64_t* out_sum_pos,
+                     int64_t* out_triples, void* stream);
+
+/* exact 4-clique count over N+ (mining.py:133-154 with ExactProvider):
+ * out_count[0] = sum over directed edges (u,v) and w in C3 of |N+w & C3| */
+PG_API int pg_4clique_exact(const int64_t* dir_off, const int32_t* dir_adj,
+                     const int32_t* src, int64_t e_begin, int64_t e_end,
+                     int64_t* out_count, void* stream);
+
+/* exact |N(u) & N(v)| per pair over a sorted CSR (providers.py:102-115
+ * ExactProvider.pair_many; setops.py:23-51) */
+PG_API int pg_pairs_exact(const int64_t* offsets, const int32_t* adj,
+                   const int32_t* us, const int32_t* vs, int64_t count,
+                   int64_t* out_count, void* stream);
+
+/* ---- utilities ------------------------------------------------------- */
+/* writes `bytes` bytes to a scratch buffer (L2 flush between timed runs) */
+PG_API int pg_l2_flush(void* buf, size_t bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PROBGRAPH_B200_H */

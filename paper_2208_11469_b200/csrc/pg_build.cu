@@ -1,0 +1,510 @@
+// (1) Per-vertex sketch builders.
+//
+// Reference semantics (paths under /root/reference/pkg/src/probgraph):
+//   Bloom  : sketches.py:314-325 _build_bloom_matrix   (bit word%B of every
+//            (neighbour, hash fn); ones = row popcount)
+//   k-Hash : sketches.py:328-343 _build_khash_matrix   (argmin (h_i(x), x))
+//   1-Hash : sketches.py:346-372 _select_bottom_k + _build_onehash_matrix
+//            (k smallest (h_0(x), x), re-sorted by ID, -1 pad)
+//   KMV    : sketches.py:375-396 _build_kmv_matrix     (k smallest DISTINCT
+//            unit values, +inf pad)
+//
+// Design: one CTA of 8 warps walks chunks of 64 consecutive vertices.  A warp
+// owns one vertex at a time and builds its sketch in shared memory or
+// registers; vertices with more than kHub neighbours are deferred to the end
+// of the chunk and built by the whole CTA, so R-MAT hubs (d up to 4e5) do not
+// serialise on one warp.  The adjacency row is read once, coalesced.
+#include <algorithm>
+
+#include "pg_common.cuh"
+
+namespace pg {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = kWarps * 32;
+constexpr int kChunk = 64;      // vertices per CTA chunk
+constexpr int64_t kHub = 4096;  // degree above which the whole CTA builds
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+__device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
+
+// ============================================================== Bloom ====
+// smem: kWarps rows of bits/32 words (the CTA reuses warp 0's row for hubs),
+// then up to 64 seeds, then the hub list.
+template <bool kPow2>
+__device__ __forceinline__ uint32_t bloom_pos(uint64_t w, uint32_t bits) {
+  if (kPow2) return static_cast<uint32_t>(w & (bits - 1));
+  return static_cast<uint32_t>(w % bits);
+}
+
+template <bool kPow2>
+__global__ void __launch_bounds__(kThreads) build_bloom_kernel(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n,
+    uint32_t bits, int b, const uint64_t* __restrict__ seeds_dev,
+    uint64_t* __restrict__ rows, int32_t* __restrict__ ones) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  const uint32_t words32 = bits >> 5;
+  const uint32_t words64 = bits >> 6;
+  uint32_t* my_row = smem + warp_id() * words32;
+  uint64_t* seeds = reinterpret_cast<uint64_t*>(smem + kWarps * words32);
+  int* hub_list = reinterpret_cast<int*>(seeds + 64);
+  __shared__ int hub_count;
+  __shared__ int red[kWarps];
+
+  for (int i = threadIdx.x; i < b; i += kThreads) seeds[i] = seeds_dev[i];
+  __syncthreads();
+  const int lane = lane_id();
+
+  for (int64_t cb = (int64_t)blockIdx.x * kChunk; cb < n; cb += (int64_t)gridDim.x * kChunk) {
+    if (threadIdx.x == 0) hub_count = 0;
+    __syncthreads();
+    const int64_t ce = min(cb + kChunk, n);
+    for (int64_t v = cb + warp_id(); v < ce; v += kWarps) {
+      const int64_t o = offsets[v];
+      const int64_t d = offsets[v + 1] - o;
+      if (d > kHub) {
+        if (lane == 0) hub_list[atomicAdd(&hub_count, 1)] = (int)(v - cb);
+        continue;
+      }
+      for (uint32_t i = lane; i < words32; i += 32) my_row[i] = 0u;
+      __syncwarp();
+      for (int64_t j = lane; j < d; j += 32) {
+        const int32_t x = adj[o + j];
+        for (int h = 0; h < b; ++h) {
+          const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x), bits);
+          atomicOr(&my_row[p >> 5], 1u << (p & 31));
+        }
+      }
+      __syncwarp();
+      int cnt = 0;
+      const uint64_t* row64 = reinterpret_cast<const uint64_t*>(my_row);
+      for (uint32_t i = lane; i < words64; i += 32) {
+        const uint64_t w = row64[i];
+        cnt += __popcll(w);
+        rows[v * words64 + i] = w;
+      }
+      cnt = __reduce_add_sync(0xffffffffu, cnt);
+      if (lane == 0) ones[v] = cnt;
+      __syncwarp();
+    }
+    __syncthreads();
+    const int nh = hub_count;
+    for (int hi = 0; hi < nh; ++hi) {
+      const int64_t v = cb + hub_list[hi];
+      const int64_t o = offsets[v];
+      const int64_t d = offsets[v + 1] - o;
+      uint32_t* row = smem;  // whole CTA shares warp 0's row
+      for (uint32_t i = threadIdx.x; i < words32; i += kThreads) row[i] = 0u;
+      __syncthreads();
+      for (int64_t j = threadIdx.x; j < d; j += kThreads) {
+        const int32_t x = adj[o + j];
+        for (int h = 0; h < b; ++h) {
+          const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x), bits);
+          atomicOr(&row[p >> 5], 1u << (p & 31));
+        }
+      }
+      __syncthreads();
+      int cnt = 0;
+      const uint64_t* row64 = reinterpret_cast<const uint64_t*>(row);
+      for (uint32_t i = threadIdx.x; i < words64; i += kThreads) {
+        const uint64_t w = row64[i];
+        cnt += __popcll(w);
+        rows[v * words64 + i] = w;
+      }
+      cnt = __reduce_add_sync(0xffffffffu, cnt);
+      if (lane == 0) red[warp_id()] = cnt;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int t = 0;
+        for (int w = 0; w < kWarps; ++w) t += red[w];
+        ones[v] = t;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ============================================================= k-Hash ====
+// Lane = hash function (i = lane + 32*s).  Each lane keeps the running
+// lexicographic minimum of (h_i(x), x) over the neighbour row, which is
+// exactly argmin with the smaller-ID tie-break of the reference.
+template <int S>
+__device__ __forceinline__ void khash_scan(const int32_t* __restrict__ row, int64_t beg, int64_t end,
+                                           int64_t step, const uint64_t (&seed)[S],
+                                           uint64_t (&best_h)[S], int32_t (&best_x)[S]) {
+  const int lane = lane_id();
+  for (int64_t base = beg; base < end; base += step) {
+    const int64_t j = base + lane;
+    const int32_t xl = j < end ? row[j] : 0;
+    const int cnt = (end - base) < 32 ? (int)(end - base) : 32;
+    for (int t = 0; t < cnt; ++t) {
+      const int32_t x = __shfl_sync(0xffffffffu, xl, t);
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const uint64_t h = hash_word(seed[s], x);
+        if (h < best_h[s] || (h == best_h[s] && x < best_x[s])) {
+          best_h[s] = h;
+          best_x[s] = x;
+        }
+      }
+    }
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(kThreads) build_khash_kernel(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n, int k,
+    const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries) {
+  __shared__ uint64_t red_h[kWarps][32 * S];
+  __shared__ int32_t red_x[kWarps][32 * S];
+  __shared__ int hub_list[kChunk];
+  __shared__ int hub_count;
+  const int lane = lane_id();
+  uint64_t seed[S];
+#pragma unroll
+  for (int s = 0; s < S; ++s) {
+    const int i = lane + 32 * s;
+    seed[s] = i < k ? seeds_dev[i] : 0ull;
+  }
+  for (int64_t cb = (int64_t)blockIdx.x * kChunk; cb < n; cb += (int64_t)gridDim.x * kChunk) {
+    if (threadIdx.x == 0) hub_count = 0;
+    __syncthreads();
+    const int64_t ce = min(cb + kChunk, n);
+    for (int64_t v = cb + warp_id(); v < ce; v += kWarps) {
+      const int64_t o = offsets[v];
+      const int64_t d = offsets[v + 1] - o;
+      if (d > kHub) {
+        if (lane == 0) hub_list[atomicAdd(&hub_count, 1)] = (int)(v - cb);
+        continue;
+      }
+      uint64_t bh[S];
+      int32_t bx[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) { bh[s] = ~0ull; bx[s] = 0x7fffffff; }
+      khash_scan<S>(adj + o, 0, d, 32, seed, bh, bx);
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        const int i = lane + 32 * s;
+        if (i < k) entries[v * k + i] = d > 0 ? bx[s] : -1;
+      }
+    }
+    __syncthreads();
+    const int nh = hub_count;
+    for (int hi = 0; hi < nh; ++hi) {
+      const int64_t v = cb + hub_list[hi];
+      const int64_t o = offsets[v];
+      const int64_t d = offsets[v + 1] - o;
+      uint64_t bh[S];
+      int32_t bx[S];
+#pragma unroll
+      for (int s = 0; s < S; ++s) { bh[s] = ~0ull; bx[s] = 0x7fffffff; }
+      khash_scan<S>(adj + o, 32 * warp_id(), d, kThreads, seed, bh, bx);
+#pragma unroll
+      for (int s = 0; s < S; ++s) {
+        red_h[warp_id()][lane + 32 * s] = bh[s];
+        red_x[warp_id()][lane + 32 * s] = bx[s];
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < k; i += kThreads) {
+        uint64_t h = red_h[0][i];
+        int32_t x = red_x[0][i];
+        for (int w = 1; w < kWarps; ++w) {
+          const uint64_t h2 = red_h[w][i];
+          const int32_t x2 = red_x[w][i];
+          if (h2 < h || (h2 == h && x2 < x)) { h = h2; x = x2; }
+        }
+        entries[v * k + i] = x;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ===================================================== bottom-k (1-Hash, KMV)
+// A warp-wide sorted list of up to 32*P 64-bit keys held in registers; lane
+// L owns slots L, L+32, ...  `cnt` (warp-uniform) slots are valid.  Keys are
+// unique (1-Hash: mix64 is a bijection, so distinct IDs hash apart; KMV:
+// duplicates are rejected on insertion, which is the reference's dedup).
+template <int P, bool kDedup>
+struct WarpBottomK {
+  uint64_t key[P];
+  int cnt;
+  int k;
+
+  __device__ __forceinline__ void init(int k_) {
+    k = k_;
+    cnt = 0;
+#pragma unroll
+    for (int s = 0; s < P; ++s) key[s] = ~0ull;
+  }
+  __device__ __forceinline__ bool full() const { return cnt >= k; }
+  __device__ __forceinline__ uint64_t at(int idx) const {
+    uint64_t r = 0;
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const uint64_t t = shfl64(key[s], idx & 31);
+      if ((idx >> 5) == s) r = t;
+    }
+    return r;
+  }
+  __device__ __forceinline__ uint64_t threshold() const { return at(k - 1); }
+
+  __device__ __forceinline__ void insert(uint64_t c) {
+    const int lane = lane_id();
+    int pos = 0;
+    bool dup = false;
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const bool valid = lane + 32 * s < cnt;
+      pos += __popc(__ballot_sync(0xffffffffu, valid && key[s] < c));
+      if (kDedup) dup |= valid && key[s] == c;
+    }
+    if (kDedup && __any_sync(0xffffffffu, dup)) return;
+    if (pos >= k) return;
+    uint64_t prev[P];
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const uint64_t up = shfl_up64(key[s], 1);
+      const uint64_t wrap = s > 0 ? shfl64(key[s > 0 ? s - 1 : 0], 31) : 0ull;
+      prev[s] = lane == 0 ? wrap : up;
+    }
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const int idx = lane + 32 * s;
+      if (idx == pos) key[s] = c;
+      else if (idx > pos) key[s] = prev[s];
+    }
+    cnt = min(cnt + 1, k);
+  }
+
+  // offer one candidate per lane (valid lanes only)
+  __device__ __forceinline__ void offer(uint64_t c, bool valid) {
+    uint64_t thr = full() ? threshold() : ~0ull;
+    bool pass_all = !full();
+    unsigned mask = __ballot_sync(0xffffffffu, valid && (pass_all || c < thr));
+    while (mask) {
+      const int t = __ffs(mask) - 1;
+      mask &= mask - 1;
+      const uint64_t ct = shfl64(c, t);
+      insert(ct);
+      if (full()) {
+        thr = threshold();
+        mask &= __ballot_sync(0xffffffffu, c < thr);
+      }
+    }
+  }
+};
+
+template <bool kKmv>
+__device__ __forceinline__ uint64_t bottomk_key(uint64_t seed0, int32_t x) {
+  const uint64_t w = hash_word(seed0, x);
+  return kKmv ? dbits(unit_value(w)) : w;
+}
+
+template <int P, bool kKmv>
+__device__ __forceinline__ void bottomk_scan(WarpBottomK<P, kKmv>& L, const int32_t* __restrict__ row,
+                                             int64_t beg, int64_t end, int64_t step, uint64_t seed0) {
+  const int lane = lane_id();
+  for (int64_t base = beg; base < end; base += step) {
+    const int64_t j = base + lane;
+    const bool valid = j < end;
+    const uint64_t c = valid ? bottomk_key<kKmv>(seed0, row[j]) : ~0ull;
+    L.offer(c, valid);
+  }
+}
+
+// write the final list of vertex v.  1-Hash: IDs ascending (rank sort in
+// the warp's smem scratch), -1 pad; KMV: values ascending, +inf pad.
+template <int P, bool kKmv>
+__device__ __forceinline__ void bottomk_emit(const WarpBottomK<P, kKmv>& L, int64_t v, int k,
+                                             uint64_t seed0, int32_t* scratch,
+                                             int32_t* __restrict__ entries, double* __restrict__ values,
+                                             int32_t* __restrict__ lengths) {
+  const int lane = lane_id();
+  const int cnt = L.cnt;
+  if (kKmv) {
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const int idx = lane + 32 * s;
+      if (idx < k) values[v * k + idx] = idx < cnt ? bitsd(L.key[s]) : bitsd(kInfBits);
+    }
+  } else {
+    int32_t id[P];
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const int idx = lane + 32 * s;
+      id[s] = (int32_t)(unmix64(L.key[s]) ^ seed0);
+      if (idx < cnt) scratch[idx] = id[s];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const int idx = lane + 32 * s;
+      if (idx < cnt) {
+        int rank = 0;
+        for (int j = 0; j < cnt; ++j) rank += scratch[j] < id[s];
+        entries[v * k + rank] = id[s];
+      } else if (idx < k) {
+        entries[v * k + idx] = -1;
+      }
+    }
+    __syncwarp();
+  }
+  if (lane == 0) lengths[v] = cnt;
+}
+
+template <int P, bool kKmv>
+__global__ void __launch_bounds__(kThreads) build_bottomk_kernel(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n, int k,
+    const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries,
+    double* __restrict__ values, int32_t* __restrict__ lengths) {
+  __shared__ int32_t scratch[kWarps][32 * P];
+  __shared__ uint64_t merge_keys[kWarps][32 * P];
+  __shared__ int merge_cnt[kWarps];
+  __shared__ int hub_list[kChunk];
+  __shared__ int hub_count;
+  const int lane = lane_id();
+  const uint64_t seed0 = seeds_dev[0];
+
+  for (int64_t cb = (int64_t)blockIdx.x * kChunk; cb < n; cb += (int64_t)gridDim.x * kChunk) {
+    if (threadIdx.x == 0) hub_count = 0;
+    __syncthreads();
+    const int64_t ce = min(cb + kChunk, n);
+    for (int64_t v = cb + warp_id(); v < ce; v += kWarps) {
+      const int64_t o = offsets[v];
+      const int64_t d = offsets[v + 1] - o;
+      if (d > kHub) {
+        if (lane == 0) hub_list[atomicAdd(&hub_count, 1)] = (int)(v - cb);
+        continue;
+      }
+      if (!kKmv && d <= k) {
+        // every neighbour is kept and the CSR row is already ID-sorted
+        for (int j = lane; j < k; j += 32) entries[v * k + j] = j < d ? adj[o + j] : -1;
+        if (lane == 0) lengths[v] = (int32_t)d;
+        continue;
+      }
+      WarpBottomK<P, kKmv> L;
+      L.init(k);
+      bottomk_scan<P, kKmv>(L, adj + o, 0, d, 32, seed0);
+      bottomk_emit<P, kKmv>(L, v, k, seed0, scratch[warp_id()], entries, values, lengths);
+    }
+    __syncthreads();
+    const int nh = hub_count;
+    for (int hi = 0; hi < nh; ++hi) {
+      const int64_t v = cb + hub_list[hi];
+      const int64_t o = offsets[v];
+      const int64_t d = offsets[v + 1] - o;
+      WarpBottomK<P, kKmv> L;
+      L.init(k);
+      bottomk_scan<P, kKmv>(L, adj + o, 32 * warp_id(), d, kThreads, seed0);
+#pragma unroll
+      for (int s = 0; s < P; ++s) merge_keys[warp_id()][lane + 32 * s] = L.key[s];
+      if (lane == 0) merge_cnt[warp_id()] = L.cnt;
+      __syncthreads();
+      if (warp_id() == 0) {
+        WarpBottomK<P, kKmv> M;
+        M.init(k);
+        for (int w = 0; w < kWarps; ++w) {
+          const int cw = merge_cnt[w];
+          for (int base = 0; base < cw; base += 32) {
+            const int idx = base + lane;
+            const bool valid = idx < cw;
+            M.offer(valid ? merge_keys[w][idx] : ~0ull, valid);
+          }
+        }
+        bottomk_emit<P, kKmv>(M, v, k, seed0, scratch[0], entries, values, lengths);
+      }
+      __syncthreads();
+    }
+  }
+}
+
+static int grid_for(int64_t n) {
+  const int64_t chunks = (n + kChunk - 1) / kChunk;
+  const int64_t cap = (int64_t)sm_count() * 8;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(chunks, cap));
+}
+
+template <bool kKmv>
+int launch_bottomk(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t k,
+                          const uint64_t* seeds_dev, int32_t* entries, double* values,
+                          int32_t* lengths, void* stream) {
+  const int grid = grid_for(n);
+  cudaStream_t s = as_stream(stream);
+  if (k <= 32)
+    build_bottomk_kernel<1, kKmv><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, lengths);
+  else if (k <= 64)
+    build_bottomk_kernel<2, kKmv><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, lengths);
+  else if (k <= 128)
+    build_bottomk_kernel<4, kKmv><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, lengths);
+  else
+    build_bottomk_kernel<8, kKmv><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, lengths);
+  return check_launch(kKmv ? "build_kmv" : "build_onehash");
+}
+
+}  // namespace pg
+
+using namespace pg;
+
+extern "C" {
+
+int pg_build_bloom(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t bits, int32_t b,
+                   const uint64_t* seeds_dev, uint64_t* rows, int32_t* ones, void* stream) {
+  PG_REQUIRE(n >= 0, "n must be >= 0");
+  PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
+  if (bits > kMaxBloomBits)
+    return fail(PG_ERR_UNSUPPORTED, "Bloom width %d exceeds the device limit %d", bits, kMaxBloomBits);
+  PG_REQUIRE(b >= 1 && b <= 64, "Bloom hash count must be in [1, 64]");
+  PG_REQUIRE(offsets && seeds_dev && rows && ones, "null pointer");
+  if (n == 0) return PG_OK;
+  const size_t smem = (size_t)kWarps * (bits / 8) + 64 * sizeof(uint64_t) + kChunk * sizeof(int);
+  const bool pow2 = (bits & (bits - 1)) == 0;
+  const int grid = grid_for(n);
+  cudaStream_t s = as_stream(stream);
+  if (pow2) {
+    cudaFuncSetAttribute(build_bloom_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    build_bloom_kernel<true><<<grid, kThreads, smem, s>>>(offsets, adj, n, bits, b, seeds_dev, rows, ones);
+  } else {
+    cudaFuncSetAttribute(build_bloom_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    build_bloom_kernel<false><<<grid, kThreads, smem, s>>>(offsets, adj, n, bits, b, seeds_dev, rows, ones);
+  }
+  return check_launch("build_bloom");
+}
+
+int pg_build_khash(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t k,
+                   const uint64_t* seeds_dev, int32_t* entries, void* stream) {
+  PG_REQUIRE(n >= 0, "n must be >= 0");
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(offsets && seeds_dev && entries, "null pointer");
+  if (n == 0) return PG_OK;
+  const int grid = grid_for(n);
+  cudaStream_t s = as_stream(stream);
+  if (k <= 32) build_khash_kernel<1><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries);
+  else if (k <= 64) build_khash_kernel<2><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries);
+  else if (k <= 128) build_khash_kernel<4><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries);
+  else build_khash_kernel<8><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries);
+  return check_launch("build_khash");
+}
+
+int pg_build_onehash(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t k,
+                     const uint64_t* seeds_dev, int32_t* entries, int32_t* lengths, void* stream) {
+  PG_REQUIRE(n >= 0, "n must be >= 0");
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(offsets && seeds_dev && entries && lengths, "null pointer");
+  if (n == 0) return PG_OK;
+  return launch_bottomk<false>(offsets, adj, n, k, seeds_dev, entries, nullptr, lengths, stream);
+}
+
+int pg_build_kmv(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t k,
+                 const uint64_t* seeds_dev, double* values, int32_t* lengths, void* stream) {
+  PG_REQUIRE(n >= 0, "n must be >= 0");
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(offsets && seeds_dev && values && lengths, "null pointer");
+  if (n == 0) return PG_OK;
+  return launch_bottomk<true>(offsets, adj, n, k, seeds_dev, nullptr, values, lengths, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,1011 @@
+// (2)+(3) Per-edge estimator kernels and their fused whole-graph reductions.
+//
+// Reference semantics (paths under /root/reference/pkg/src/probgraph):
+//   Bloom   providers.py:137-162 (pair_many, _estimate_ones), estimators.py:65-70
+//   k-Hash  providers.py:197-198,205-232   1-Hash providers.py:200-203,205-232
+//   KMV     providers.py:266-301
+//   TC      mining.py:105-130 (tc_estimate) over _chunked_sum (:63-80)
+//   Jaccard estimators.py:123-131,148-168; mining.py:157-186 (vertex_similarity)
+//
+// Fixed-width row kernels (Bloom, k-Hash) use a "group" of G lanes per edge,
+// each lane issuing V 128-bit loads per row.  A warp walks a contiguous edge
+// range 32 edges at a time: lane i loads edge e0+i (coalesced), the group of
+// lane i streams the rows of its G edges and a G-lane transpose-reduction
+// leaves the count of edge e0+i back in lane i, which runs the epilogue.  The
+// u row of consecutive edges is the same CSR row, so it is loaded through L1
+// (ld.global.nc) while v rows bypass L1 (L1::no_allocate).
+//
+// Variable-length sorted rows (1-Hash IDs, KMV values) use one warp per edge,
+// rows staged in shared memory and binary searched.
+//
+// Reductions are exact integers (histograms / per-match sums) wherever the
+// reference's per-edge value is a function of an integer count, so sharded
+// runs reproduce the single-GPU result bit for bit; only KMV sums doubles.
+#include <algorithm>
+
+#include "pg_common.cuh"
+
+namespace pg {
+
+constexpr int kBlock = 256;
+
+// ------------------------------------------------------------ row ops ----
+struct OpAnd {
+  __device__ __forceinline__ static int apply(uint4 a, uint4 b) {
+    return __popc(a.x & b.x) + __popc(a.y & b.y) + __popc(a.z & b.z) + __popc(a.w & b.w);
+  }
+};
+struct OpOr {
+  __device__ __forceinline__ static int apply(uint4 a, uint4 b) {
+    return __popc(a.x | b.x) + __popc(a.y | b.y) + __popc(a.z | b.z) + __popc(a.w | b.w);
+  }
+};
+// k-Hash positional matches: (eu == ev) & (eu >= 0)   (providers.py:197-198)
+struct OpEqPos {
+  __device__ __forceinline__ static int apply(uint4 a, uint4 b) {
+    return (a.x == b.x && (int)a.x >= 0) + (a.y == b.y && (int)a.y >= 0) +
+           (a.z == b.z && (int)a.z >= 0) + (a.w == b.w && (int)a.w >= 0);
+  }
+};
+
+// G-lane transpose-reduction: on entry c[j] is this lane's partial count of
+// edge j of its group; on exit the lane with group index gl holds the full
+// count of edge gl in c[0].
+template <int G>
+__device__ __forceinline__ int group_transpose_reduce(int (&c)[G], int gl) {
+#pragma unroll
+  for (int w = G / 2; w >= 1; w >>= 1) {
+    const bool upper = (gl & w) != 0;
+#pragma unroll
+    for (int j = 0; j < w; ++j) {
+      const int send = upper ? c[j] : c[j + w];
+      const int keep = upper ? c[j + w] : c[j];
+      c[j] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+    }
+  }
+  return c[0];
+}
+
+// contiguous per-warp slice of [e_begin, e_end), rounded to 32 edges
+__device__ __forceinline__ void warp_slice(int64_t e_begin, int64_t e_end, int64_t& wb, int64_t& we) {
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t gw = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t total = e_end - e_begin;
+  int64_t per = (total + nwarps - 1) / nwarps;
+  per = (per + 31) & ~int64_t(31);
+  wb = e_begin + gw * per;
+  we = min(wb + per, e_end);
+  if (wb > e_end) wb = e_end;
+}
+
+// Group engine: calls epi.edge(e, u, v, count) once per edge of the warp's
+// slice, from the lane that loaded the edge.
+template <int V, int G, class Op, class Epi>
+__device__ __forceinline__ void group_edge_loop(const uint4* __restrict__ rows, const int32_t* __restrict__ us,
+                                                const int32_t* __restrict__ vs, int64_t e_begin,
+                                                int64_t e_end, Epi& epi) {
+  constexpr int W4 = V * G;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int gbase = lane & ~(G - 1);
+  int64_t wb, we;
+  warp_slice(e_begin, e_end, wb, we);
+  for (int64_t e0 = wb; e0 < we; e0 += 32) {
+    const int64_t e = e0 + lane;
+    const bool valid = e < we;
+    const int32_t ul = valid ? us[e] : 0;
+    const int32_t vl = valid ? vs[e] : 0;
+    int c[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int32_t uj = __shfl_sync(0xffffffffu, ul, gbase + j);
+      const int32_t vj = __shfl_sync(0xffffffffu, vl, gbase + j);
+      const uint4* ru = rows + (int64_t)uj * W4 + gl;
+      const uint4* rv = rows + (int64_t)vj * W4 + gl;
+      int acc = 0;
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc += Op::apply(ldg_keep(ru + i * G), ldg_stream(rv + i * G));
+      c[j] = acc;
+    }
+    const int cnt = group_transpose_reduce<G>(c, gl);
+    if (valid) epi.edge(e, ul, vl, cnt);
+  }
+}
+
+// Generic fallback: one lane per edge, 64-bit words (any multiple of 64 bits,
+// or any k for k-Hash).
+template <class Epi>
+__device__ void scalar_edge_loop_bloom(const uint64_t* __restrict__ rows, int words, int op,
+                                       const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
+                                       int64_t e_begin, int64_t e_end, Epi& epi) {
+  for (int64_t e = e_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e_end;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = us[e], v = vs[e];
+    const uint64_t* ru = rows + (int64_t)u * words;
+    const uint64_t* rv = rows + (int64_t)v * words;
+    int c = 0;
+    if (op == PG_BF_OR)
+      for (int i = 0; i < words; ++i) c += __popcll(ru[i] | rv[i]);
+    else
+      for (int i = 0; i < words; ++i) c += __popcll(ru[i] & rv[i]);
+    epi.edge(e, u, v, c);
+  }
+}
+template <class Epi>
+__device__ void scalar_edge_loop_khash(const int32_t* __restrict__ ent, int k, const int32_t* __restrict__ us,
+                                       const int32_t* __restrict__ vs, int64_t e_begin, int64_t e_end,
+                                       Epi& epi) {
+  for (int64_t e = e_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e_end;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = us[e], v = vs[e];
+    const int32_t* a = ent + (int64_t)u * k;
+    const int32_t* b = ent + (int64_t)v * k;
+    int c = 0;
+    for (int i = 0; i < k; ++i) c += (a[i] == b[i] && a[i] >= 0);
+    epi.edge(e, u, v, c);
+  }
+}
+
+// ------------------------------------------------------ estimate math ----
+// All double arithmetic below uses explicit _rn intrinsics so that no FMA
+// contraction can change a per-edge value relative to numpy.
+__device__ __forceinline__ double bloom_estimate(int op, int c, int b, int32_t su, int32_t sv,
+                                                 const double* __restrict__ lut) {
+  if (op == PG_BF_AND) return lut[c];
+  if (op == PG_BF_L) return __ddiv_rn((double)c, (double)b);
+  const double raw = __dsub_rn((double)((int64_t)su + sv), lut[c]);
+  return raw > 0.0 ? raw : 0.0;  // np.maximum(raw, 0.0)
+}
+// (j/(1+j)) * (s_u+s_v), j = m/k   (providers.py:223-227)
+__device__ __forceinline__ double minhash_estimate(int m, int k, int32_t su, int32_t sv) {
+  const double j = __ddiv_rn((double)m, (double)k);
+  return __dmul_rn(__ddiv_rn(j, __dadd_rn(1.0, j)), (double)((int64_t)su + sv));
+}
+
+// ---------------------------------------------------------- epilogues ----
+struct EpiBloomPairs {
+  int op, b;
+  const int32_t* sizes;
+  const double* lut;
+  int32_t* out_count;
+  double* out_est;
+  __device__ __forceinline__ void edge(int64_t e, int32_t u, int32_t v, int c) {
+    if (out_count) out_count[e] = c;
+    if (out_est) out_est[e] = bloom_estimate(op, c, b, op == PG_BF_OR ? sizes[u] : 0, op == PG_BF_OR ? sizes[v] : 0, lut);
+  }
+};
+
+struct EpiBloomHist {
+  int op;
+  const int32_t* sizes;
+  const double* lut;
+  int* hist_s;
+  long long sum_pos;
+  __device__ __forceinline__ void edge(int64_t, int32_t u, int32_t v, int c) {
+    if (op == PG_BF_OR) {
+      const int64_t S = (int64_t)sizes[u] + sizes[v];
+      if (__dsub_rn((double)S, lut[c]) > 0.0) {
+        atomicAdd(hist_s + c, 1);
+        sum_pos += S;
+      }
+    } else {
+      atomicAdd(hist_s + c, 1);
+    }
+  }
+};
+
+struct EpiMinhashPairs {
+  int k;
+  const int32_t* sizes;
+  int32_t* out_count;
+  double* out_est;
+  __device__ __forceinline__ void edge(int64_t e, int32_t u, int32_t v, int m) {
+    if (out_count) out_count[e] = m;
+    if (out_est) out_est[e] = minhash_estimate(m, k, sizes[u], sizes[v]);
+  }
+};
+
+// per match count m: number of edges and sum of (s_u+s_v)
+struct EpiMinhashHist {
+  const int32_t* sizes;
+  int* cnt_s;
+  unsigned long long* ssum_s;
+  __device__ __forceinline__ void edge(int64_t, int32_t u, int32_t v, int m) {
+    atomicAdd(cnt_s + m, 1);
+    atomicAdd(ssum_s + m, (unsigned long long)((int64_t)sizes[u] + sizes[v]));
+  }
+};
+
+// Jaccard clustering counts (config 4)
+struct EpiJaccard {
+  int k, min_matches;
+  double tau;
+  const int32_t* deg;
+  int* hist_s;
+  long long n_hat, n_sim;
+  __device__ __forceinline__ void edge(int64_t, int32_t u, int32_t v, int m) {
+    atomicAdd(hist_s + m, 1);
+    n_hat += (m >= min_matches);
+    // vertex_similarity(JACCARD) over the k-Hash intersection estimate
+    const int32_t du = deg[u], dv = deg[v];
+    const double est = minhash_estimate(m, k, du, dv);
+    const double lo = (double)min(du, dv);
+    const double c = fmin(fmax(est, 0.0), lo);  // _feasible_count
+    const double denom = __dsub_rn((double)((int64_t)du + dv), c);
+    const double J = denom > 0.0 ? __ddiv_rn(c, denom) : 0.0;
+    n_sim += (J >= tau);
+  }
+};
+
+// ------------------------------------------------ fixed-row kernels ----
+template <int V, int G, class Op>
+__global__ void __launch_bounds__(kBlock) pairs_rows_kernel_bloom(const uint4* rows, const int32_t* us,
+                                                                 const int32_t* vs, int64_t count,
+                                                                 EpiBloomPairs epi) {
+  group_edge_loop<V, G, Op>(rows, us, vs, 0, count, epi);
+}
+__global__ void __launch_bounds__(kBlock) pairs_scalar_kernel_bloom(const uint64_t* rows, int words,
+                                                                   const int32_t* us, const int32_t* vs,
+                                                                   int64_t count, EpiBloomPairs epi) {
+  scalar_edge_loop_bloom(rows, words, epi.op, us, vs, 0, count, epi);
+}
+
+template <int V, int G, class Op, bool kScalar>
+__global__ void __launch_bounds__(kBlock) tc_bloom_kernel(const uint4* rows, int bits, const int32_t* us,
+                                                         const int32_t* vs, int64_t e_begin,
+                                                         int64_t e_end, EpiBloomHist epi,
+                                                         int64_t* out_hist, int64_t* out_sum_pos) {
+  extern __shared__ int hist_s[];
+  for (int i = threadIdx.x; i <= bits; i += blockDim.x) hist_s[i] = 0;
+  __syncthreads();
+  epi.hist_s = hist_s;
+  epi.sum_pos = 0;
+  if (kScalar)
+    scalar_edge_loop_bloom(reinterpret_cast<const uint64_t*>(rows), bits / 64, epi.op, us, vs, e_begin,
+                           e_end, epi);
+  else
+    group_edge_loop<V, G, Op>(rows, us, vs, e_begin, e_end, epi);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= bits; i += blockDim.x)
+    if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_hist + i), (unsigned long long)hist_s[i]);
+  if (epi.op == PG_BF_OR) {
+    long long s = epi.sum_pos;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if ((threadIdx.x & 31) == 0 && s) atomicAdd(reinterpret_cast<unsigned long long*>(out_sum_pos), (unsigned long long)s);
+  }
+}
+
+template <int V, int G, bool kScalar>
+__global__ void __launch_bounds__(kBlock) pairs_khash_kernel(const uint4* ent, int k, const int32_t* us,
+                                                            const int32_t* vs, int64_t count,
+                                                            EpiMinhashPairs epi) {
+  if (kScalar) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, 0, count, epi);
+  else group_edge_loop<V, G, OpEqPos>(ent, us, vs, 0, count, epi);
+}
+
+template <int V, int G, bool kScalar>
+__global__ void __launch_bounds__(kBlock) tc_khash_kernel(const uint4* ent, int k, const int32_t* sizes,
+                                                         const int32_t* us, const int32_t* vs,
+                                                         int64_t e_begin, int64_t e_end, int64_t* out_cnt,
+                                                         int64_t* out_ssum) {
+  __shared__ int cnt_s[kMaxSketchK + 1];
+  __shared__ unsigned long long ssum_s[kMaxSketchK + 1];
+  for (int i = threadIdx.x; i <= k; i += blockDim.x) { cnt_s[i] = 0; ssum_s[i] = 0; }
+  __syncthreads();
+  EpiMinhashHist epi{sizes, cnt_s, ssum_s};
+  if (kScalar) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
+  else group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+    if (cnt_s[i]) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(out_cnt + i), (unsigned long long)cnt_s[i]);
+      atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i), ssum_s[i]);
+    }
+  }
+}
+
+template <int V, int G, bool kScalar>
+__global__ void __launch_bounds__(kBlock) jaccard_khash_kernel(const uint4* ent, int k, const int32_t* deg,
+                                                              const int32_t* us, const int32_t* vs,
+                                                              int64_t e_begin, int64_t e_end,
+                                                              int min_matches, double tau,
+                                                              int64_t* out_counts) {
+  __shared__ int hist_s[kMaxSketchK + 1];
+  for (int i = threadIdx.x; i <= k; i += blockDim.x) hist_s[i] = 0;
+  __syncthreads();
+  EpiJaccard epi{k, min_matches, tau, deg, hist_s, 0, 0};
+  if (kScalar) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
+  else group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= k; i += blockDim.x)
+    if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_counts + 2 + i), (unsigned long long)hist_s[i]);
+  long long a = epi.n_hat, b = epi.n_sim;
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (a) atomicAdd(reinterpret_cast<unsigned long long*>(out_counts + 0), (unsigned long long)a);
+    if (b) atomicAdd(reinterpret_cast<unsigned long long*>(out_counts + 1), (unsigned long long)b);
+  }
+}
+
+// ------------------------------------------------------------ 1-Hash ----
+// lower_bound over a shared array of `len` ascending elements
+template <class T>
+__device__ __forceinline__ int smem_lower_bound(const T* a, int len, T x) {
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo;
+}
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// warp-per-edge match count of two ascending ID lists (-1 padded); returns
+// m and the two list lengths (warp-uniform)
+template <int P>
+__device__ __forceinline__ int onehash_matches(const int32_t* __restrict__ ent, int k, int32_t u, int32_t v,
+                                               int32_t* vbuf, int& lu, int& lv) {
+  const int lane = threadIdx.x & 31;
+  int32_t a[P], b[P];
+  lu = 0;
+  lv = 0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int idx = lane + 32 * s;
+    a[s] = idx < k ? ent[(int64_t)u * k + idx] : -1;
+    b[s] = idx < k ? ent[(int64_t)v * k + idx] : -1;
+    lu += __popc(__ballot_sync(0xffffffffu, a[s] >= 0));
+    lv += __popc(__ballot_sync(0xffffffffu, b[s] >= 0));
+  }
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int idx = lane + 32 * s;
+    if (idx < lv) vbuf[idx] = b[s];
+  }
+  __syncwarp();
+  int m = 0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int idx = lane + 32 * s;
+    bool hit = false;
+    if (idx < lu) {
+      const int p = smem_lower_bound(vbuf, lv, a[s]);
+      hit = p < lv && vbuf[p] == a[s];
+    }
+    m += __popc(__ballot_sync(0xffffffffu, hit));
+  }
+  __syncwarp();
+  return m;
+}
+
+template <int P, bool kFused>
+__global__ void __launch_bounds__(kBlock) onehash_kernel(const int32_t* ent, int k, const int32_t* sizes,
+                                                        const int32_t* us, const int32_t* vs,
+                                                        int64_t e_begin, int64_t e_end,
+                                                        int32_t* out_count, double* out_est,
+                                                        int64_t* out_cnt, int64_t* out_ssum,
+                                                        int64_t* out_verbatim) {
+  __shared__ int32_t vbuf[kBlock / 32][32 * P];
+  __shared__ int cnt_s[kMaxSketchK + 1];
+  __shared__ unsigned long long ssum_s[kMaxSketchK + 1];
+  if (kFused) {
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) { cnt_s[i] = 0; ssum_s[i] = 0; }
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  long long verb = 0;
+  int64_t wb, we;
+  warp_slice(e_begin, e_end, wb, we);
+  for (int64_t e = wb; e < we; ++e) {
+    const int32_t u = us[e], v = vs[e];
+    int lu, lv;
+    const int m = onehash_matches<P>(ent, k, u, v, vbuf[threadIdx.x >> 5], lu, lv);
+    if (lane == 0) {
+      const int32_t su = sizes[u], sv = sizes[v];
+      const bool verbatim = su <= k && sv <= k;
+      if (kFused) {
+        if (verbatim) verb += m;
+        else {
+          atomicAdd(cnt_s + m, 1);
+          atomicAdd(ssum_s + m, (unsigned long long)((int64_t)su + sv));
+        }
+      } else {
+        if (out_count) out_count[e] = m;
+        if (out_est) out_est[e] = verbatim ? (double)m : minhash_estimate(m, k, su, sv);
+      }
+    }
+  }
+  if (kFused) {
+    __syncthreads();
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+      if (cnt_s[i]) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_cnt + i), (unsigned long long)cnt_s[i]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i), ssum_s[i]);
+      }
+    }
+    if (lane == 0 && verb) atomicAdd(reinterpret_cast<unsigned long long*>(out_verbatim), (unsigned long long)verb);
+  }
+}
+
+// --------------------------------------------------------------- KMV ----
+// Warp-per-edge restatement of the merged-row logic of providers.py:266-301:
+// common = |U & V|, union = |U| + |V| - common, k_eff = min(|U|,|V|), kth =
+// the max(k_eff,1)-th smallest distinct value of U | V (or merged[0] when
+// the union is smaller).  Ranks of union elements are computed from
+// lower_bound positions in the other row and prefix counts of common
+// elements, so no merge buffer is needed.
+struct KmvEdge {
+  int common, uni, k_eff;
+  double kth;
+};
+
+template <int P>
+__device__ __forceinline__ KmvEdge kmv_edge(const uint64_t* __restrict__ vals, int k, int32_t u, int32_t v,
+                                            uint64_t* ubuf, uint64_t* vbuf) {
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = lanemask_lt();
+  uint64_t a[P], b[P];
+  int lu = 0, lv = 0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int idx = lane + 32 * s;
+    a[s] = idx < k ? vals[(int64_t)u * k + idx] : kInfBits;
+    b[s] = idx < k ? vals[(int64_t)v * k + idx] : kInfBits;
+    lu += __popc(__ballot_sync(0xffffffffu, a[s] < kInfBits));
+    lv += __popc(__ballot_sync(0xffffffffu, b[s] < kInfBits));
+    if (idx < k) { ubuf[idx] = a[s]; vbuf[idx] = b[s]; }
+  }
+  __syncwarp();
+  int ltv[P], ltu[P];
+  bool inv[P], inu[P];
+  int common = 0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int idx = lane + 32 * s;
+    inv[s] = false;
+    inu[s] = false;
+    ltv[s] = 0;
+    ltu[s] = 0;
+    if (idx < lu) {
+      ltv[s] = smem_lower_bound(vbuf, lv, a[s]);
+      inv[s] = ltv[s] < lv && vbuf[ltv[s]] == a[s];
+    }
+    if (idx < lv) {
+      ltu[s] = smem_lower_bound(ubuf, lu, b[s]);
+      inu[s] = ltu[s] < lu && ubuf[ltu[s]] == b[s];
+    }
+    common += __popc(__ballot_sync(0xffffffffu, inv[s]));
+  }
+  KmvEdge r;
+  r.common = common;
+  r.uni = lu + lv - common;
+  r.k_eff = min(lu, lv);
+  const int T = max(r.k_eff, 1);
+  // rank (1-based) of each distinct union element; find rank T
+  int before_u = 0, before_v = 0;
+  uint64_t found = 0;
+  bool have = false;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int idx = lane + 32 * s;
+    const unsigned bu = __ballot_sync(0xffffffffu, inv[s]);
+    const unsigned bv = __ballot_sync(0xffffffffu, inu[s]);
+    const int cbu = before_u + __popc(bu & lt);
+    const int cbv = before_v + __popc(bv & lt);
+    if (idx < lu && idx + 1 + ltv[s] - cbu == T) { found = a[s]; have = true; }
+    if (idx < lv && !inu[s] && idx + 1 + ltu[s] - cbv == T) { found = b[s]; have = true; }
+    before_u += __popc(bu);
+    before_v += __popc(bv);
+  }
+  const unsigned hm = __ballot_sync(0xffffffffu, have);
+  uint64_t kth_bits;
+  if (hm) kth_bits = shfl64(found, __ffs(hm) - 1);
+  else kth_bits = min(shfl64(a[0], 0), shfl64(b[0], 0));  // argmax of all-False -> merged[0]
+  r.kth = bitsd(kth_bits);
+  __syncwarp();
+  return r;
+}
+
+__device__ __forceinline__ double kmv_estimate(const KmvEdge& r, int k, int32_t isu, int32_t isv) {
+  const double su = (double)isu, sv = (double)isv;
+  const double ssum = __dadd_rn(su, sv);
+  double raw;
+  if (isu <= k && isv <= k) raw = __dsub_rn(ssum, (double)r.uni);
+  else if (r.k_eff < 2) raw = (double)r.common;
+  else raw = __dsub_rn(ssum, __ddiv_rn((double)(r.k_eff - 1), r.kth));
+  return fmin(fmax(raw, 0.0), fmin(su, sv));  // np.clip(raw, 0, min(su, sv))
+}
+
+template <int P, bool kFused>
+__global__ void __launch_bounds__(kBlock) kmv_kernel(const uint64_t* vals, int k, const int32_t* sizes,
+                                                    const int32_t* us, const int32_t* vs, int64_t e_begin,
+                                                    int64_t e_end, int32_t* out_common, int32_t* out_union,
+                                                    double* out_kth, double* out_est, double* out_sum) {
+  __shared__ uint64_t ubuf[kBlock / 32][32 * P];
+  __shared__ uint64_t vbuf[kBlock / 32][32 * P];
+  __shared__ double red[kBlock / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double acc = 0.0;
+  int64_t wb, we;
+  warp_slice(e_begin, e_end, wb, we);
+  for (int64_t e = wb; e < we; ++e) {
+    const int32_t u = us[e], v = vs[e];
+    const KmvEdge r = kmv_edge<P>(vals, k, u, v, ubuf[w], vbuf[w]);
+    if (lane == 0) {
+      const double est = kmv_estimate(r, k, sizes[u], sizes[v]);
+      if (kFused) acc = __dadd_rn(acc, est);
+      else {
+        if (out_common) out_common[e] = r.common;
+        if (out_union) out_union[e] = r.uni;
+        if (out_kth) out_kth[e] = r.kth;
+        if (out_est) out_est[e] = est;
+      }
+    }
+  }
+  if (kFused) {
+    if (lane == 0) red[w] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int i = 0; i < kBlock / 32; ++i) t = __dadd_rn(t, red[i]);
+      if (t != 0.0) atomicAdd(out_sum, t);
+    }
+  }
+}
+
+// ---------------------------------------------------------- 4-clique ----
+// Warp per directed edge (u,v): C3 = N+u & N+v by binary search of the
+// shorter row in the longer (pass 1 builds BF(C3) in shared memory with the
+// reference's per-set builder semantics, sketches.py:187-198), pass 2
+// re-derives the members and ANDs BF+(w) with BF(C3) for every w in C3
+// (providers.py:164-175).  Histogram of popcounts per block.
+__device__ __forceinline__ bool gmem_contains(const int32_t* __restrict__ a, int64_t len, int32_t x) {
+  int64_t lo = 0, hi = len;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo < len && a[lo] == x;
+}
+
+__global__ void __launch_bounds__(kBlock) clique4_bloom_kernel(
+    const int64_t* __restrict__ off, const int32_t* __restrict__ adjp, const int32_t* __restrict__ src,
+    int64_t e_begin, int64_t e_end, const uint64_t* __restrict__ rows, int bits, int b,
+    const uint64_t* __restrict__ seeds_dev, int op, const int32_t* __restrict__ sizes,
+    const double* __restrict__ lut, int64_t* out_hist, int64_t* out_sum_pos, int64_t* out_triples) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int words32 = bits >> 5, words64 = bits >> 6;
+  int* hist_s = reinterpret_cast<int*>(smem_raw);                                   // bits+1
+  uint64_t* seeds = reinterpret_cast<uint64_t*>(smem_raw + ((bits + 1) * 4 + 15) / 16 * 16);  // 64
+  uint32_t* bf_all = reinterpret_cast<uint32_t*>(seeds + 64);                       // warps * words32
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  uint32_t* bf = bf_all + w * words32;
+  const uint64_t* bf64 = reinterpret_cast<const uint64_t*>(bf);
+  for (int i = threadIdx.x; i <= bits; i += blockDim.x) hist_s[i] = 0;
+  for (int i = threadIdx.x; i < b; i += blockDim.x) seeds[i] = seeds_dev[i];
+  __syncthreads();
+  const bool pow2 = (bits & (bits - 1)) == 0;
+  long long triples = 0, sum_pos = 0;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = e_begin + (int64_t)blockIdx.x * (blockDim.x >> 5) + w; j < e_end; j += nwarps) {
+    const int32_t u = src[j], v = adjp[j];
+    const int32_t* A = adjp + off[u];
+    int64_t la = off[u + 1] - off[u];
+    const int32_t* Bv = adjp + off[v];
+    int64_t lb = off[v + 1] - off[v];
+    if (la > lb) {
+      const int32_t* t = A; A = Bv; Bv = t;
+      const int64_t tl = la; la = lb; lb = tl;
+    }
+    for (int i = lane; i < words32; i += 32) bf[i] = 0u;
+    __syncwarp();
+    int c3 = 0;
+    for (int64_t base = 0; base < la; base += 32) {  // pass 1: BF(C3)
+      const int64_t idx = base + lane;
+      const int32_t x = idx < la ? A[idx] : -1;
+      const bool hit = idx < la && gmem_contains(Bv, lb, x);
+      if (hit) {
+        for (int h = 0; h < b; ++h) {
+          const uint64_t hw = hash_word(seeds[h], x);
+          const uint32_t p = pow2 ? (uint32_t)(hw & (uint64_t)(bits - 1)) : (uint32_t)(hw % (uint64_t)bits);
+          atomicOr(&bf[p >> 5], 1u << (p & 31));
+        }
+      }
+      c3 += __popc(__ballot_sync(0xffffffffu, hit));
+    }
+    __syncwarp();
+    if (c3 == 0) continue;
+    triples += c3;
+    for (int64_t base = 0; base < la; base += 32) {  // pass 2: w in C3
+      const int64_t idx = base + lane;
+      const int32_t x = idx < la ? A[idx] : -1;
+      const bool hit = idx < la && gmem_contains(Bv, lb, x);
+      unsigned mask = __ballot_sync(0xffffffffu, hit);
+      while (mask) {
+        const int t = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int32_t wv = __shfl_sync(0xffffffffu, x, t);
+        const uint64_t* rw = rows + (int64_t)wv * words64;
+        int cnt = 0;
+        for (int i = lane; i < words64; i += 32) {
+          const uint64_t r = rw[i];
+          cnt += __popcll(op == PG_BF_OR ? (r | bf64[i]) : (r & bf64[i]));
+        }
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0) {
+          if (op == PG_BF_OR) {
+            const int64_t S = (int64_t)sizes[wv] + c3;
+            if (__dsub_rn((double)S, lut[cnt]) > 0.0) {
+              atomicAdd(hist_s + cnt, 1);
+              sum_pos += S;
+            }
+          } else {
+            atomicAdd(hist_s + cnt, 1);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= bits; i += blockDim.x)
+    if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_hist + i), (unsigned long long)hist_s[i]);
+  if (lane == 0) {
+    if (triples) atomicAdd(reinterpret_cast<unsigned long long*>(out_triples), (unsigned long long)triples);
+    if (sum_pos) atomicAdd(reinterpret_cast<unsigned long long*>(out_sum_pos), (unsigned long long)sum_pos);
+  }
+}
+
+// Exact 4-clique: for w in C3, count x in N+w with x in N+u and x in N+v
+// (two binary searches; C3 never materialised).
+__global__ void __launch_bounds__(kBlock) clique4_exact_kernel(
+    const int64_t* __restrict__ off, const int32_t* __restrict__ adjp, const int32_t* __restrict__ src,
+    int64_t e_begin, int64_t e_end, int64_t* out_count) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  long long total = 0;
+  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t j = e_begin + (int64_t)blockIdx.x * (blockDim.x >> 5) + w; j < e_end; j += nwarps) {
+    const int32_t u = src[j], v = adjp[j];
+    const int32_t* A = adjp + off[u];
+    int64_t la = off[u + 1] - off[u];
+    const int32_t* Bv = adjp + off[v];
+    int64_t lb = off[v + 1] - off[v];
+    if (la > lb) {
+      const int32_t* t = A; A = Bv; Bv = t;
+      const int64_t tl = la; la = lb; lb = tl;
+    }
+    for (int64_t base = 0; base < la; base += 32) {
+      const int64_t idx = base + lane;
+      const int32_t x = idx < la ? A[idx] : -1;
+      const bool hit = idx < la && gmem_contains(Bv, lb, x);
+      unsigned mask = __ballot_sync(0xffffffffu, hit);
+      while (mask) {
+        const int t = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const int32_t wv = __shfl_sync(0xffffffffu, x, t);
+        const int32_t* Wr = adjp + off[wv];
+        const int64_t lw = off[wv + 1] - off[wv];
+        for (int64_t q = lane; q < lw; q += 32) {
+          const int32_t y = Wr[q];
+          total += gmem_contains(A, la, y) && gmem_contains(Bv, lb, y);
+        }
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(0xffffffffu, total, o);
+  if (lane == 0 && total) atomicAdd(reinterpret_cast<unsigned long long*>(out_count), (unsigned long long)total);
+}
+
+// ---------------------------------------------------------- launching ----
+template <class K>
+static int grid_for_kernel(K kernel, size_t smem) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, smem) != cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  return sm_count() * per_sm;
+}
+
+static int grid_cap(int grid, int64_t items, int per_block) {
+  const int64_t need = (items + per_block - 1) / per_block;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(grid, need));
+}
+
+}  // namespace pg
+
+using namespace pg;
+
+// dispatch helpers: (W4 = row bytes / 16) -> (V, G)
+#define PG_ROW_DISPATCH(W4, MACRO) \
+  switch (W4) {                    \
+    case 1: MACRO(1, 1); break;    \
+    case 2: MACRO(1, 2); break;    \
+    case 4: MACRO(1, 4); break;    \
+    case 8: MACRO(1, 8); break;    \
+    case 16: MACRO(2, 8); break;   \
+    case 32: MACRO(4, 8); break;   \
+    default: MACRO(1, 1); break;   \
+  }
+
+static bool fast_w4(int w4) { return w4 == 1 || w4 == 2 || w4 == 4 || w4 == 8 || w4 == 16 || w4 == 32; }
+
+extern "C" {
+
+int pg_pairs_bloom(const uint64_t* rows, int32_t bits, int32_t b, int32_t op, const int32_t* sizes,
+                   const double* lut, const int32_t* us, const int32_t* vs, int64_t count,
+                   int32_t* out_count, double* out_est, void* stream) {
+  PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
+  PG_REQUIRE(b >= 1, "need at least one hash function");
+  PG_REQUIRE(op == PG_BF_AND || op == PG_BF_L || op == PG_BF_OR, "op is not a Bloom estimator");
+  PG_REQUIRE(count >= 0, "count must be >= 0");
+  if (count == 0) return PG_OK;
+  PG_REQUIRE(rows && us && vs, "null pointer");
+  PG_REQUIRE(!out_est || op == PG_BF_L || lut, "estimate needs the Swamidass table");
+  PG_REQUIRE(!(out_est && op == PG_BF_OR) || sizes, "BF_OR needs sizes");
+  EpiBloomPairs epi{op, b, sizes, lut, out_count, out_est};
+  cudaStream_t s = as_stream(stream);
+  const int w4 = bits % 128 == 0 ? bits / 128 : 0;
+  const int grid = grid_cap(sm_count() * 8, count, kBlock);
+  if (!fast_w4(w4)) {
+    pairs_scalar_kernel_bloom<<<grid, kBlock, 0, s>>>(rows, bits / 64, us, vs, count, epi);
+  } else {
+    const uint4* r4 = reinterpret_cast<const uint4*>(rows);
+#define PG_L(V, G)                                                                         \
+  if (op == PG_BF_OR) pairs_rows_kernel_bloom<V, G, OpOr><<<grid, kBlock, 0, s>>>(r4, us, vs, count, epi); \
+  else pairs_rows_kernel_bloom<V, G, OpAnd><<<grid, kBlock, 0, s>>>(r4, us, vs, count, epi);
+    PG_ROW_DISPATCH(w4, PG_L)
+#undef PG_L
+  }
+  return check_launch("pairs_bloom");
+}
+
+int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* sizes, const double* lut,
+                const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end, int64_t* out_hist,
+                int64_t* out_sum_pos, void* stream) {
+  PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
+  PG_REQUIRE(op == PG_BF_AND || op == PG_BF_L || op == PG_BF_OR, "op is not a Bloom estimator");
+  PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
+  PG_REQUIRE(out_hist, "null histogram");
+  PG_REQUIRE(op != PG_BF_OR || (sizes && lut && out_sum_pos), "BF_OR needs sizes, table and sum output");
+  cudaStream_t s = as_stream(stream);
+  cudaError_t ce = cudaMemsetAsync(out_hist, 0, sizeof(int64_t) * (bits + 1), s);
+  if (ce == cudaSuccess && out_sum_pos) ce = cudaMemsetAsync(out_sum_pos, 0, sizeof(int64_t), s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  if (e_end == e_begin) return PG_OK;
+  PG_REQUIRE(rows && us && vs, "null pointer");
+  EpiBloomHist epi{op, sizes, lut, nullptr, 0};
+  const size_t smem = sizeof(int) * (bits + 1);
+  const int w4 = bits % 128 == 0 ? bits / 128 : 0;
+  const uint4* r4 = reinterpret_cast<const uint4*>(rows);
+  if (!fast_w4(w4)) {
+    auto k = tc_bloom_kernel<1, 1, OpAnd, true>;
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const int grid = grid_cap(grid_for_kernel(k, smem), e_end - e_begin, kBlock);
+    k<<<grid, kBlock, smem, s>>>(r4, bits, us, vs, e_begin, e_end, epi, out_hist, out_sum_pos);
+  } else {
+#define PG_L(V, G)                                                                                   \
+  {                                                                                                  \
+    auto k = op == PG_BF_OR ? tc_bloom_kernel<V, G, OpOr, false> : tc_bloom_kernel<V, G, OpAnd, false>; \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                 \
+    const int grid = grid_cap(grid_for_kernel(k, smem), e_end - e_begin, kBlock);                    \
+    k<<<grid, kBlock, smem, s>>>(r4, bits, us, vs, e_begin, e_end, epi, out_hist, out_sum_pos);      \
+  }
+    PG_ROW_DISPATCH(w4, PG_L)
+#undef PG_L
+  }
+  return check_launch("tc_bloom");
+}
+
+int pg_pairs_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int32_t* sizes,
+                     const int32_t* us, const int32_t* vs, int64_t count, int32_t* out_count,
+                     double* out_est, void* stream) {
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(count >= 0, "count must be >= 0");
+  if (count == 0) return PG_OK;
+  PG_REQUIRE(entries && us && vs, "null pointer");
+  PG_REQUIRE(!out_est || sizes, "estimate needs sizes");
+  cudaStream_t s = as_stream(stream);
+  if (onehash) {
+    PG_REQUIRE(sizes, "1-Hash needs sizes");
+    const int grid = grid_cap(sm_count() * 8, count, kBlock / 32);
+#define PG_OH(P) onehash_kernel<P, false><<<grid, kBlock, 0, s>>>(entries, k, sizes, us, vs, 0, count, out_count, out_est, nullptr, nullptr, nullptr)
+    if (k <= 32) PG_OH(1);
+    else if (k <= 64) PG_OH(2);
+    else if (k <= 128) PG_OH(4);
+    else PG_OH(8);
+#undef PG_OH
+    return check_launch("pairs_onehash");
+  }
+  EpiMinhashPairs epi{k, sizes, out_count, out_est};
+  const int grid = grid_cap(sm_count() * 8, count, kBlock);
+  const int w4 = k % 4 == 0 ? k / 4 : 0;
+  const uint4* e4 = reinterpret_cast<const uint4*>(entries);
+  if (!fast_w4(w4)) {
+    pairs_khash_kernel<1, 1, true><<<grid, kBlock, 0, s>>>(e4, k, us, vs, count, epi);
+  } else {
+#define PG_L(V, G) pairs_khash_kernel<V, G, false><<<grid, kBlock, 0, s>>>(e4, k, us, vs, count, epi);
+    PG_ROW_DISPATCH(w4, PG_L)
+#undef PG_L
+  }
+  return check_launch("pairs_khash");
+}
+
+int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int32_t* sizes,
+                  const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end, int64_t* out_cnt,
+                  int64_t* out_ssum, int64_t* out_verbatim, void* stream) {
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
+  PG_REQUIRE(out_cnt && out_ssum && out_verbatim && sizes, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  cudaError_t ce = cudaMemsetAsync(out_cnt, 0, sizeof(int64_t) * (k + 1), s);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(out_ssum, 0, sizeof(int64_t) * (k + 1), s);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(out_verbatim, 0, sizeof(int64_t), s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  if (e_end == e_begin) return PG_OK;
+  PG_REQUIRE(entries && us && vs, "null pointer");
+  if (onehash) {
+#define PG_OH(P)                                                                                  \
+  {                                                                                               \
+    auto kern = onehash_kernel<P, true>;                                                          \
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock / 32);            \
+    kern<<<grid, kBlock, 0, s>>>(entries, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, out_cnt, out_ssum, out_verbatim); \
+  }
+    if (k <= 32) PG_OH(1)
+    else if (k <= 64) PG_OH(2)
+    else if (k <= 128) PG_OH(4)
+    else PG_OH(8)
+#undef PG_OH
+    return check_launch("tc_onehash");
+  }
+  const int w4 = k % 4 == 0 ? k / 4 : 0;
+  const uint4* e4 = reinterpret_cast<const uint4*>(entries);
+  if (!fast_w4(w4)) {
+    auto kern = tc_khash_kernel<1, 1, true>;
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);
+    kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum);
+  } else {
+#define PG_L(V, G)                                                                       \
+  {                                                                                      \
+    auto kern = tc_khash_kernel<V, G, false>;                                            \
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);        \
+    kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum); \
+  }
+    PG_ROW_DISPATCH(w4, PG_L)
+#undef PG_L
+  }
+  return check_launch("tc_khash");
+}
+
+int pg_jaccard_count_khash(const int32_t* entries, int32_t k, const int32_t* degrees, const int32_t* us,
+                           const int32_t* vs, int64_t e_begin, int64_t e_end, int32_t min_matches,
+                           double tau, int64_t* out_counts, void* stream) {
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
+  PG_REQUIRE(out_counts && degrees, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  cudaError_t ce = cudaMemsetAsync(out_counts, 0, sizeof(int64_t) * (k + 3), s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  if (e_end == e_begin) return PG_OK;
+  PG_REQUIRE(entries && us && vs, "null pointer");
+  const int w4 = k % 4 == 0 ? k / 4 : 0;
+  const uint4* e4 = reinterpret_cast<const uint4*>(entries);
+  if (!fast_w4(w4)) {
+    auto kern = jaccard_khash_kernel<1, 1, true>;
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);
+    kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts);
+  } else {
+#define PG_L(V, G)                                                                                         \
+  {                                                                                                        \
+    auto kern = jaccard_khash_kernel<V, G, false>;                                                         \
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);                          \
+    kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts);    \
+  }
+    PG_ROW_DISPATCH(w4, PG_L)
+#undef PG_L
+  }
+  return check_launch("jaccard_khash");
+}
+
+int pg_pairs_kmv(const double* values, const int32_t* lengths, int32_t k, const int32_t* sizes,
+                 const int32_t* us, const int32_t* vs, int64_t count, int32_t* out_common,
+                 int32_t* out_union, double* out_kth, double* out_est, void* stream) {
+  (void)lengths;  // lengths are implied by the +inf pads of each row
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(count >= 0, "count must be >= 0");
+  if (count == 0) return PG_OK;
+  PG_REQUIRE(values && sizes && us && vs, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  const uint64_t* vb = reinterpret_cast<const uint64_t*>(values);
+  const int grid = grid_cap(sm_count() * 8, count, kBlock / 32);
+#define PG_KM(P) kmv_kernel<P, false><<<grid, kBlock, 0, s>>>(vb, k, sizes, us, vs, 0, count, out_common, out_union, out_kth, out_est, nullptr)
+  if (k <= 32) PG_KM(1);
+  else if (k <= 64) PG_KM(2);
+  else if (k <= 128) PG_KM(4);
+  else PG_KM(8);
+#undef PG_KM
+  return check_launch("pairs_kmv");
+}
+
+int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k, const int32_t* sizes,
+              const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end, double* out_sum,
+              void* stream) {
+  (void)lengths;
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
+  PG_REQUIRE(out_sum && sizes, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  cudaError_t ce = cudaMemsetAsync(out_sum, 0, sizeof(double), s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  if (e_end == e_begin) return PG_OK;
+  PG_REQUIRE(values && us && vs, "null pointer");
+  const uint64_t* vb = reinterpret_cast<const uint64_t*>(values);
+#define PG_KM(P)                                                                                    \
+  {                                                                                                 \
+    auto kern = kmv_kernel<P, true>;                                                                \
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock / 32);              \
+    kern<<<grid, kBlock, 0, s>>>(vb, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, nullptr, nullptr, out_sum); \
+  }
+  if (k <= 32) PG_KM(1)
+  else if (k <= 64) PG_KM(2)
+  else if (k <= 128) PG_KM(4)
+  else PG_KM(8)
+#undef PG_KM
+  return check_launch("tc_kmv");
+}
+
+int pg_4clique_bloom(const int64_t* dir_off, const int32_t* dir_adj, const int32_t* src, int64_t e_begin,
+                     int64_t e_end, const uint64_t* rows_plus, int32_t bits, int32_t b,
+                     const uint64_t* seeds_dev, int32_t op, const int32_t* sizes, const double* lut,
+                     int64_t* out_hist, int64_t* out_sum_pos, int64_t* out_triples, void* stream) {
+  PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
+  if (bits > 16384) return fail(PG_ERR_UNSUPPORTED, "4-clique kernel supports Bloom widths up to 16384");
+  PG_REQUIRE(b >= 1 && b <= 64, "Bloom hash count must be in [1, 64]");
+  PG_REQUIRE(op == PG_BF_AND || op == PG_BF_L || op == PG_BF_OR, "op is not a Bloom estimator");
+  PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
+  PG_REQUIRE(out_hist && out_triples, "null output");
+  PG_REQUIRE(op != PG_BF_OR || (sizes && lut && out_sum_pos), "BF_OR needs sizes, table and sum output");
+  cudaStream_t s = as_stream(stream);
+  cudaError_t ce = cudaMemsetAsync(out_hist, 0, sizeof(int64_t) * (bits + 1), s);
+  if (ce == cudaSuccess) ce = cudaMemsetAsync(out_triples, 0, sizeof(int64_t), s);
+  if (ce == cudaSuccess && out_sum_pos) ce = cudaMemsetAsync(out_sum_pos, 0, sizeof(int64_t), s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  if (e_end == e_begin) return PG_OK;
+  PG_REQUIRE(dir_off && dir_adj && src && rows_plus && seeds_dev, "null pointer");
+  const size_t smem = ((size_t)(bits + 1) * 4 + 15) / 16 * 16 + 64 * 8 + (size_t)(kBlock / 32) * (bits / 8);
+  cudaFuncSetAttribute(clique4_bloom_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int grid = grid_cap(grid_for_kernel(clique4_bloom_kernel, smem), e_end - e_begin, kBlock / 32);
+  clique4_bloom_kernel<<<grid, kBlock, smem, s>>>(dir_off, dir_adj, src, e_begin, e_end, rows_plus, bits, b,
+                                                  seeds_dev, op, sizes, lut, out_hist, out_sum_pos,
+                                                  out_triples);
+  return check_launch("4clique_bloom");
+}
+
+int pg_4clique_exact(const int64_t* dir_off, const int32_t* dir_adj, const int32_t* src, int64_t e_begin,
+                     int64_t e_end, int64_t* out_count, void* stream) {
+  PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
+  PG_REQUIRE(out_count, "null output");
+  cudaStream_t s = as_stream(stream);
+  cudaError_t ce = cudaMemsetAsync(out_count, 0, sizeof(int64_t), s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  if (e_end == e_begin) return PG_OK;
+  PG_REQUIRE(dir_off && dir_adj && src, "null pointer");
+  const int grid = grid_cap(grid_for_kernel(clique4_exact_kernel, 0), e_end - e_begin, kBlock / 32);
+  clique4_exact_kernel<<<grid, kBlock, 0, s>>>(dir_off, dir_adj, src, e_begin, e_end, out_count);
+  return check_launch("4clique_exact");
+}
+
+}  // extern "C"

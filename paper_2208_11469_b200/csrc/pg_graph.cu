@@ -1,0 +1,182 @@
+// Graph preparation on the device: upper-triangular edge list (the
+// reference's CsrGraph.edges(), graphs.py:101-105), CSR row expansion
+// (mining.py:83-85 _directed_edge_arrays), exact pair intersection counts
+// (providers.py:102-115, setops.py:23-51) and raw hash words
+// (hashing.py:114-118).
+#include <cub/device/device_scan.cuh>
+
+#include "pg_common.cuh"
+
+namespace pg {
+
+// first index of row u holding a neighbour > u, and the row's upper count
+__global__ void upper_count_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj,
+                                   int64_t n, int64_t* __restrict__ first, int64_t* __restrict__ cnt) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = offsets[u], hi = offsets[u + 1];
+    const int64_t end = hi;
+    while (lo < hi) {  // lower_bound of u+1
+      const int64_t mid = (lo + hi) >> 1;
+      if (adj[mid] <= u) lo = mid + 1;
+      else hi = mid;
+    }
+    first[u] = lo;
+    cnt[u] = end - lo;
+  }
+}
+
+__global__ void upper_fill_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj,
+                                  int64_t n, const int64_t* __restrict__ first,
+                                  const int64_t* __restrict__ start, int32_t* __restrict__ us,
+                                  int32_t* __restrict__ vs, int64_t cap) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
+    const int64_t f = first[u], e = offsets[u + 1], s = start[u];
+    for (int64_t j = f + lane; j < e; j += 32) {
+      const int64_t o = s + (j - f);
+      if (o < cap) {
+        us[o] = (int32_t)u;
+        vs[o] = adj[j];
+      }
+    }
+  }
+}
+
+__global__ void expand_rows_kernel(const int64_t* __restrict__ offsets, int64_t n,
+                                   int32_t* __restrict__ src) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
+    const int64_t b = offsets[u], e = offsets[u + 1];
+    for (int64_t j = b + lane; j < e; j += 32) src[j] = (int32_t)u;
+  }
+}
+
+__global__ void hash_words_kernel(const int64_t* __restrict__ keys, int64_t count, uint64_t seed,
+                                  uint64_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = mix64(seed ^ static_cast<uint64_t>(keys[i]));
+}
+
+// warp per pair: every element of the shorter row is binary-searched in the
+// longer row (both sorted, duplicate free)
+__global__ void pairs_exact_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj,
+                                   const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
+                                   int64_t count, int64_t* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t e = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; e < count; e += warps) {
+    const int32_t u = us[e], v = vs[e];
+    int64_t ab = offsets[u], ae = offsets[u + 1], bb = offsets[v], be = offsets[v + 1];
+    if (ae - ab > be - bb) {
+      int64_t t = ab; ab = bb; bb = t;
+      t = ae; ae = be; be = t;
+    }
+    int64_t hits = 0;
+    for (int64_t j = ab + lane; j < ae; j += 32) {
+      const int32_t x = adj[j];
+      int64_t lo = bb, hi = be;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (adj[mid] < x) lo = mid + 1;
+        else hi = mid;
+      }
+      hits += (lo < be && adj[lo] == x);
+    }
+    for (int o = 16; o > 0; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
+    if (lane == 0) out[e] = hits;
+  }
+}
+
+static size_t scan_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int64_t*)nullptr, (int64_t*)nullptr, n);
+  return bytes;
+}
+
+static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+}  // namespace pg
+
+using namespace pg;
+
+extern "C" {
+
+int pg_csr_upper_edges_workspace(int64_t n, size_t* out_bytes_host) {
+  PG_REQUIRE(n >= 0 && out_bytes_host, "bad arguments");
+  const size_t arr = align256(sizeof(int64_t) * (size_t)(n + 1));
+  *out_bytes_host = 3 * arr + align256(scan_temp_bytes(n > 0 ? n : 1));
+  return PG_OK;
+}
+
+int pg_csr_upper_edges(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t* us, int32_t* vs,
+                       int64_t capacity, int64_t* m_host, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  PG_REQUIRE(n >= 0, "n must be >= 0");
+  PG_REQUIRE(offsets && workspace, "null pointer");
+  size_t need = 0;
+  pg_csr_upper_edges_workspace(n, &need);
+  PG_REQUIRE(workspace_bytes >= need, "workspace too small (%zu < %zu)", workspace_bytes, need);
+  cudaStream_t s = as_stream(stream);
+  if (n == 0) {
+    if (m_host) *m_host = 0;
+    return PG_OK;
+  }
+  const size_t arr = align256(sizeof(int64_t) * (size_t)(n + 1));
+  char* ws = static_cast<char*>(workspace);
+  int64_t* first = reinterpret_cast<int64_t*>(ws);
+  int64_t* cnt = reinterpret_cast<int64_t*>(ws + arr);
+  int64_t* start = reinterpret_cast<int64_t*>(ws + 2 * arr);
+  void* temp = ws + 3 * arr;
+  size_t temp_bytes = workspace_bytes - 3 * arr;
+  const int grid = sm_count() * 8;
+  upper_count_kernel<<<grid, 256, 0, s>>>(offsets, adj, n, first, cnt);
+  if (int rc = check_launch("upper_count")) return rc;
+  cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, cnt, start, n, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "scan: %s", cudaGetErrorString(e));
+  upper_fill_kernel<<<grid, 256, 0, s>>>(offsets, adj, n, first, start, us, vs, capacity);
+  if (int rc = check_launch("upper_fill")) return rc;
+  if (m_host) {
+    int64_t last_start = 0, last_cnt = 0;
+    e = cudaMemcpyAsync(&last_start, start + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(&last_cnt, cnt + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(PG_ERR_CUDA, "upper edge count: %s", cudaGetErrorString(e));
+    *m_host = last_start + last_cnt;
+    if (*m_host > capacity)
+      return fail(PG_ERR_INVALID, "adjacency is not symmetric: %lld upper edges > capacity %lld",
+                  (long long)*m_host, (long long)capacity);
+  }
+  return PG_OK;
+}
+
+int pg_csr_expand_rows(const int64_t* offsets, int64_t n, int64_t nnz, int32_t* src, void* stream) {
+  PG_REQUIRE(n >= 0 && nnz >= 0, "bad sizes");
+  if (n == 0 || nnz == 0) return PG_OK;
+  PG_REQUIRE(offsets && src, "null pointer");
+  expand_rows_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(offsets, n, src);
+  return check_launch("expand_rows");
+}
+
+int pg_hash_words(const int64_t* keys, int64_t count, uint64_t seed, uint64_t* out, void* stream) {
+  PG_REQUIRE(count >= 0, "count must be >= 0");
+  if (count == 0) return PG_OK;
+  PG_REQUIRE(keys && out, "null pointer");
+  hash_words_kernel<<<sm_count() * 4, 256, 0, as_stream(stream)>>>(keys, count, seed, out);
+  return check_launch("hash_words");
+}
+
+int pg_pairs_exact(const int64_t* offsets, const int32_t* adj, const int32_t* us, const int32_t* vs,
+                   int64_t count, int64_t* out_count, void* stream) {
+  PG_REQUIRE(count >= 0, "count must be >= 0");
+  if (count == 0) return PG_OK;
+  PG_REQUIRE(offsets && us && vs && out_count, "null pointer");
+  pairs_exact_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(offsets, adj, us, vs, count, out_count);
+  return check_launch("pairs_exact");
+}
+
+}  // extern "C"

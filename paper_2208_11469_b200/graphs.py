@@ -1,0 +1,323 @@
+"""CSR graphs: the input contract of the engine, plus seeded generators.
+
+Host arrays follow the reference contract exactly (reference graphs.py:32-166:
+int64 ``offsets``/``adjacency``, sorted symmetric loop-free rows, ``edges()``
+yielding u < v in CSR order, ``degree_order`` ranking by (degree, id)).  The
+device mirror (:class:`DeviceCsr`) narrows the adjacency to int32 and keeps
+int64 offsets; it is built once per graph and cached.
+
+Generators (input preparation, outside every timed region):
+  * ``generate_kronecker`` -- R-MAT with the reference's initiator and draw
+    order (reference graphs.py:251-276), so a given seed yields the same graph;
+  * ``generate_erdos_renyi_gnm`` -- config 1's G(n, m), defined here;
+  * ``generate_chung_lu`` -- config 4's power-law graph, defined here.
+The last two are absent from the reference; their exact
+definitions are documented in DESIGN.md.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+__all__ = ["CsrGraph", "DirectedView", "DeviceCsr", "degree_order",
+           "generate_kronecker", "generate_erdos_renyi_gnm",
+           "generate_chung_lu", "degree_stats", "DegreeStats"]
+
+
+# ---------------------------------------------------------------------------
+# device mirror
+
+
+def _to_device(a, dtype):
+    """Upload a host array (pinned memory is copied asynchronously) and cast
+    on the device."""
+    import torch
+    t = torch.from_numpy(np.ascontiguousarray(a))
+    return t.to("cuda", non_blocking=t.is_pinned()).to(dtype)
+
+
+class DeviceCsr:
+    """Device copy of a CSR (graph or directed view) and derived edge lists."""
+
+    def __init__(self, offsets: np.ndarray, adjacency: np.ndarray):
+        import torch
+        if len(offsets) - 1 >= 2 ** 31:
+            raise ValueError("vertex IDs must fit in int32 on the device")
+        self.n = len(offsets) - 1
+        self.nnz = len(adjacency)
+        # host arrays go up as they are (int64 in the reference contract) and
+        # are narrowed on the device: no host-side conversion pass
+        self.offsets = _to_device(offsets, torch.int64)
+        self.adj = _to_device(adjacency, torch.int32)
+        self.degrees = (self.offsets[1:] - self.offsets[:-1]).to(torch.int32)
+        self._upper = None
+        self._src = None
+
+    def upper_edges(self):
+        """(us, vs) int32 device arrays: every undirected edge once, u < v."""
+        if self._upper is None:
+            import torch
+            from . import _native as N
+            m_alloc = max(1, self.nnz // 2)
+            us = torch.empty(m_alloc, dtype=torch.int32, device="cuda")
+            vs = torch.empty(m_alloc, dtype=torch.int32, device="cuda")
+            import ctypes
+            ws_bytes = ctypes.c_size_t()
+            N.call("pg_csr_upper_edges_workspace", self.n, ctypes.byref(ws_bytes))
+            ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8,
+                             device="cuda")
+            m = ctypes.c_int64()
+            N.call("pg_csr_upper_edges", N.ptr(self.offsets), N.ptr(self.adj),
+                   self.n, N.ptr(us), N.ptr(vs), m_alloc, ctypes.byref(m),
+                   N.ptr(ws), ws_bytes.value, N.stream_handle())
+            self._upper = (us[:m.value], vs[:m.value])
+        return self._upper
+
+    def row_sources(self):
+        """int32 device array src[j] = row of adjacency entry j."""
+        if self._src is None:
+            import torch
+            from . import _native as N
+            src = torch.empty(max(1, self.nnz), dtype=torch.int32, device="cuda")
+            N.call("pg_csr_expand_rows", N.ptr(self.offsets), self.n, self.nnz,
+                   N.ptr(src), N.stream_handle())
+            self._src = src[:self.nnz]
+        return self._src
+
+
+# ---------------------------------------------------------------------------
+# host CSR
+
+
+class CsrGraph:
+    """Undirected simple graph in CSR form (reference graphs.py:32-129)."""
+
+    __slots__ = ("n", "m", "offsets", "adjacency", "original_ids",
+                 "self_loops_dropped", "duplicates_dropped", "_dev")
+
+    def __init__(self, offsets, adjacency, original_ids=None):
+        self.offsets = np.asarray(offsets, dtype=np.int64)
+        self.adjacency = np.asarray(adjacency, dtype=np.int64)
+        self.n = len(self.offsets) - 1
+        self.m = len(self.adjacency) // 2
+        self.original_ids = original_ids
+        self.self_loops_dropped = 0
+        self.duplicates_dropped = 0
+        self._dev = None
+
+    @classmethod
+    def from_edges(cls, edges, n: int | None = None) -> "CsrGraph":
+        """Symmetrise, deduplicate and drop self loops."""
+        e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+        lo = np.minimum(e[:, 0], e[:, 1])
+        hi = np.maximum(e[:, 0], e[:, 1])
+        proper = lo != hi
+        loops = int(len(e) - np.count_nonzero(proper))
+        lo, hi = lo[proper], hi[proper]
+        if n is None:
+            n = int(hi.max()) + 1 if len(hi) else 0
+        if len(hi) and int(hi.max()) >= n:
+            raise ValueError("edge endpoint exceeds vertex count")
+        # canonical pair key; n < 2**31 keeps n*n inside int64
+        key = np.unique(lo * n + hi)
+        dups = len(lo) - len(key)
+        g = cls._from_canonical_keys(key, n)
+        g.self_loops_dropped = loops
+        g.duplicates_dropped = int(dups)
+        return g
+
+    @classmethod
+    def _from_canonical_keys(cls, key: np.ndarray, n: int) -> "CsrGraph":
+        """CSR from sorted unique keys lo*n+hi (lo < hi)."""
+        if n == 0:
+            return cls(np.zeros(1, dtype=np.int64), np.empty(0, dtype=np.int64))
+        lo, hi = np.divmod(key, n)
+        both = np.concatenate([lo * n + hi, hi * n + lo])
+        del lo, hi
+        both.sort(kind="stable")
+        src, dst = np.divmod(both, n)
+        del both
+        counts = np.bincount(src, minlength=n)
+        offsets = np.zeros(n + 1, dtype=np.int64)
+        np.cumsum(counts, out=offsets[1:])
+        return cls(offsets, dst)
+
+    def neighbors(self, v: int) -> np.ndarray:
+        return self.adjacency[self.offsets[v]:self.offsets[v + 1]]
+
+    def degree(self, v: int) -> int:
+        return int(self.offsets[v + 1] - self.offsets[v])
+
+    def degrees(self) -> np.ndarray:
+        return np.diff(self.offsets)
+
+    def edges(self) -> np.ndarray:
+        """(m, 2) int64: each undirected edge once, u < v, CSR order."""
+        src = np.repeat(np.arange(self.n, dtype=np.int64), self.degrees())
+        upper = src < self.adjacency
+        return np.stack([src[upper], self.adjacency[upper]], axis=1)
+
+    def validate(self) -> None:
+        if len(self.offsets) != self.n + 1 or (self.n >= 0 and self.offsets[0] != 0):
+            raise ValueError("bad offsets")
+        if np.any(np.diff(self.offsets) < 0):
+            raise ValueError("offsets not non-decreasing")
+        if self.offsets[-1] != len(self.adjacency) or len(self.adjacency) % 2:
+            raise ValueError("offsets[n] != 2m")
+        src = np.repeat(np.arange(self.n, dtype=np.int64), self.degrees())
+        key = src * max(self.n, 1) + self.adjacency
+        if len(key) and np.any(np.diff(key) <= 0):
+            raise ValueError("neighbourhoods not sorted/unique")
+        if np.any(src == self.adjacency):
+            raise ValueError("self loop")
+        rev = np.sort(self.adjacency * max(self.n, 1) + src)
+        if not np.array_equal(rev, key):
+            raise ValueError("adjacency not symmetric")
+
+    def device(self) -> DeviceCsr:
+        """Device mirror (built on first use, then cached)."""
+        if self._dev is None:
+            self._dev = DeviceCsr(self.offsets, self.adjacency)
+        return self._dev
+
+
+@dataclass(frozen=True)
+class DirectedView:
+    """Degree-ordered orientation (reference graphs.py:132-166)."""
+
+    n: int
+    m: int
+    rank: np.ndarray
+    offsets: np.ndarray
+    adjacency: np.ndarray
+    _dev: list = field(default_factory=list, repr=False, compare=False)
+
+    def out_neighbors(self, v: int) -> np.ndarray:
+        return self.adjacency[self.offsets[v]:self.offsets[v + 1]]
+
+    def out_degrees(self) -> np.ndarray:
+        return np.diff(self.offsets)
+
+    def device(self) -> DeviceCsr:
+        if not self._dev:
+            self._dev.append(DeviceCsr(self.offsets, self.adjacency))
+        return self._dev[0]
+
+
+def degree_order(graph: CsrGraph) -> DirectedView:
+    """Keep u in N+(v) iff (deg v, v) < (deg u, u)."""
+    deg = graph.degrees()
+    order = np.argsort(deg, kind="stable")  # ties -> ascending ID
+    rank = np.empty(graph.n, dtype=np.int64)
+    rank[order] = np.arange(graph.n, dtype=np.int64)
+    src = np.repeat(np.arange(graph.n, dtype=np.int64), deg)
+    keep = rank[src] < rank[graph.adjacency]
+    out_src = src[keep]
+    counts = np.bincount(out_src, minlength=graph.n)
+    offsets = np.zeros(graph.n + 1, dtype=np.int64)
+    np.cumsum(counts, out=offsets[1:])
+    return DirectedView(graph.n, graph.m, rank, offsets, graph.adjacency[keep])
+
+
+# ---------------------------------------------------------------------------
+# generators
+
+
+def generate_kronecker(scale: int, edge_factor: int, seed: int) -> CsrGraph:
+    """R-MAT, initiator (a, b, c, d) = (0.57, 0.19, 0.19, 0.05).
+
+    Per level l (LSB first) each sample draws ``rng.random(count)`` for the
+    source bit, then ``rng.random(count)`` for the destination bit whose
+    threshold depends on the source bit -- the reference's draw order, so
+    graphs are identical for a given seed.
+    """
+    if scale < 1:
+        raise ValueError("scale must be >= 1")
+    n = 1 << scale
+    count = edge_factor * n
+    rng = np.random.default_rng(seed)
+    p_ab = 0.57 + 0.19
+    thr_given_src0 = 0.57 / p_ab            # P(dst bit 0 | src bit 0)
+    thr_given_src1 = 0.19 / (1.0 - p_ab)    # P(dst bit 0 | src bit 1)
+    src = np.zeros(count, dtype=np.int64)
+    dst = np.zeros(count, dtype=np.int64)
+    thr = np.empty(count, dtype=np.float64)
+    for level in range(scale):
+        sbit = rng.random(count) > p_ab
+        np.copyto(thr, thr_given_src0)
+        thr[sbit] = thr_given_src1
+        dbit = rng.random(count) > thr
+        src |= sbit.astype(np.int64) << level
+        dst |= dbit.astype(np.int64) << level
+    del thr
+    return CsrGraph.from_edges(np.stack([src, dst], axis=1), n=n)
+
+
+def generate_erdos_renyi_gnm(n: int, m: int, seed: int) -> CsrGraph:
+    """Uniform simple graph with exactly m edges (config 1).
+
+    Draws batches of endpoint pairs ``rng.integers(0, n, size=(B, 2))``,
+    drops self loops, and keeps each unordered pair at its first occurrence
+    in draw order until m distinct pairs are collected.
+    """
+    if m > n * (n - 1) // 2:
+        raise ValueError("too many edges for a simple graph")
+    rng = np.random.default_rng(seed)
+    chosen = np.empty(0, dtype=np.int64)
+    while len(chosen) < m:
+        batch = int((m - len(chosen)) * 1.25) + 1024
+        pairs = rng.integers(0, n, size=(batch, 2), dtype=np.int64)
+        lo = np.minimum(pairs[:, 0], pairs[:, 1])
+        hi = np.maximum(pairs[:, 0], pairs[:, 1])
+        key = (lo * n + hi)[lo != hi]
+        uniq, first = np.unique(key, return_index=True)
+        fresh = ~np.isin(uniq, chosen)
+        new_keys = key[np.sort(first[fresh])]
+        chosen = np.concatenate([chosen, new_keys[:m - len(chosen)]])
+    return CsrGraph._from_canonical_keys(np.sort(chosen), n)
+
+
+def generate_chung_lu(n: int, avg_degree: float, gamma: float, seed: int,
+                      weight_cap: float | None = None) -> CsrGraph:
+    """Chung-Lu power-law graph (config 4).
+
+    Weights w_i = (i+1)^(-1/(gamma-1)) scaled to mean ``avg_degree`` and capped
+    at ``weight_cap`` (default sqrt(n * avg_degree), the structural cutoff),
+    then M = round(n * avg_degree / 2) edge samples draw both endpoints
+    independently with probability proportional to w (inverse-CDF on
+    ``rng.random(M)`` for u, then for v); the result is symmetrised,
+    deduplicated and loop-free.  Vertex 0 carries the largest weight.
+    """
+    if gamma <= 2.0:
+        raise ValueError("gamma must exceed 2")
+    rng = np.random.default_rng(seed)
+    w = np.arange(1, n + 1, dtype=np.float64) ** (-1.0 / (gamma - 1.0))
+    w *= avg_degree * n / w.sum()
+    cap = float(np.sqrt(n * avg_degree)) if weight_cap is None else weight_cap
+    np.minimum(w, cap, out=w)
+    cdf = np.cumsum(w)
+    cdf /= cdf[-1]
+    samples = int(round(n * avg_degree / 2.0))
+    u = np.searchsorted(cdf, rng.random(samples), side="right")
+    v = np.searchsorted(cdf, rng.random(samples), side="right")
+    np.minimum(u, n - 1, out=u)
+    np.minimum(v, n - 1, out=v)
+    return CsrGraph.from_edges(np.stack([u, v], axis=1), n=n)
+
+
+@dataclass(frozen=True)
+class DegreeStats:
+    max_degree: int
+    mean_degree: float
+    sum_d2: int
+    sum_d3: int
+
+
+def degree_stats(graph: CsrGraph) -> DegreeStats:
+    d = graph.degrees().astype(np.int64)
+    if graph.n == 0:
+        return DegreeStats(0, 0.0, 0, 0)
+    return DegreeStats(int(d.max(initial=0)), float(d.mean()),
+                       int((d * d).sum()), int((d * d * d).sum()))

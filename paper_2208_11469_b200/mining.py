@@ -1,0 +1,246 @@
+"""Mining entry points on the device (the callers of the per-edge path).
+
+Same names and signatures as reference ``mining.py``: ``triangle_count``
+(:88-102), ``tc_estimate`` (:105-130), ``four_clique_count`` (:133-154),
+``vertex_similarity`` (:162-203), ``jarvis_patrick_cluster`` (:213-245).
+``threads`` is accepted for compatibility; the device does the fan-out.
+
+Where the reference sums per-edge floats over a fixed 16,384-edge chunk grid
+(:63-80), the device kernels reduce exact integer statistics (popcount
+histograms, per-match-count sums) that the host turns into the estimate with
+``math.fsum``; the result agrees with the reference to ~1e-15 relative and is
+independent of the grid, the shard count and the thread count.
+
+``jaccard_cluster_count`` is the config-4 entry point (k-Hash Jaccard >= tau,
+count surviving edges); the reference has no batch form of it.
+"""
+
+from __future__ import annotations
+
+import enum
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as N
+from .estimators import EstimatorKind, swamidass_table
+from .graphs import CsrGraph, DirectedView
+from .providers import (BloomProvider, ExactProvider, IntersectionProvider,
+                        UnsupportedCombinationError, make_provider)
+from .sketches import SketchedGraph, SketchKind
+
+__all__ = ["SimilarityMeasure", "ClusterResult", "JaccardCount",
+           "triangle_count", "tc_estimate", "tc_counts", "four_clique_count",
+           "vertex_similarity", "jarvis_patrick_cluster",
+           "jaccard_cluster_count", "jaccard_min_matches"]
+
+
+class SimilarityMeasure(str, enum.Enum):
+    JACCARD = "jaccard"
+    OVERLAP = "overlap"
+    COMMON_NEIGHBORS = "common_neighbors"
+    TOTAL_NEIGHBORS = "total_neighbors"
+    ADAMIC_ADAR = "adamic_adar"
+    RESOURCE_ALLOCATION = "resource_allocation"
+
+
+_COUNTING = (SimilarityMeasure.JACCARD, SimilarityMeasure.OVERLAP,
+             SimilarityMeasure.COMMON_NEIGHBORS, SimilarityMeasure.TOTAL_NEIGHBORS)
+
+
+def _is_exact(kind: EstimatorKind) -> bool:
+    return kind in (EstimatorKind.EXACT_MERGE, EstimatorKind.EXACT_GALLOP)
+
+
+def triangle_count(view: DirectedView, provider: IntersectionProvider,
+                   threads: int = 1):
+    """Sum of |N+v & N+u| over directed edges (exact int for exact providers)."""
+    dev = view.device()
+    part = provider._pairs_device(dev.row_sources(), dev.adj)
+    if provider.is_exact:
+        return int(part.sum().item()) if part.numel() else 0
+    return float(part.sum().item()) if part.numel() else 0.0
+
+
+def _tc_provider(graph: CsrGraph, sketched, kind):
+    kind = EstimatorKind(kind)
+    if _is_exact(kind):
+        return make_provider(kind, graph=graph)
+    if sketched is None:
+        raise ValueError("sketch-based estimate needs a SketchedGraph")
+    if sketched.source != "undirected":
+        raise ValueError("triangle-count estimation needs sketches of the "
+                         "undirected neighborhoods")
+    return make_provider(kind, sketched=sketched)
+
+
+def tc_counts(provider, us, vs, e_begin: int, e_end: int):
+    """Device integer (or fp64 for KMV) partials of edges [e_begin, e_end)."""
+    import torch
+    if provider.is_exact:
+        part = provider._pairs_device(us[e_begin:e_end], vs[e_begin:e_end])
+        return part.sum().reshape(1) if part.numel() else torch.zeros(
+            1, dtype=torch.int64, device="cuda")
+    return provider._tc_counts(us, vs, e_begin, e_end)
+
+
+def tc_combine(provider, counts: np.ndarray) -> float:
+    """Sum over edges of the per-edge estimates, from tc_counts outputs."""
+    if provider.is_exact:
+        return float(int(counts[0]))
+    return provider._tc_combine(counts)
+
+
+def tc_estimate(graph: CsrGraph, sketched: SketchedGraph | None = None,
+                kind=EstimatorKind.BF_AND, threads: int = 1) -> float:
+    """(1/3) * sum over undirected edges of the intersection estimate."""
+    provider = _tc_provider(graph, sketched, kind)
+    us, vs = graph.device().upper_edges()
+    counts = tc_counts(provider, us, vs, 0, us.numel()).cpu().numpy()
+    return tc_combine(provider, counts) / 3.0
+
+
+def four_clique_count(view: DirectedView, provider: IntersectionProvider,
+                      threads: int = 1):
+    """sum over directed (u,v), w in C3 = N+u & N+v of |N+w & C3|.
+
+    Exact providers give the exact integer count; Bloom providers estimate
+    |N+w & C3| from BF+(w) and BF(C3), fused in one kernel.
+    """
+    import torch
+    dev = view.device()
+    src, nnz = dev.row_sources(), dev.nnz
+    if isinstance(provider, ExactProvider):
+        out = torch.empty(1, dtype=torch.int64, device="cuda")
+        N.call("pg_4clique_exact", N.ptr(dev.offsets), N.ptr(dev.adj), N.ptr(src),
+               0, nnz, N.ptr(out), N.stream_handle())
+        return int(out.item())
+    if not isinstance(provider, BloomProvider):
+        raise UnsupportedCombinationError(
+            f"four_clique_count on the device supports exact and Bloom "
+            f"providers, not {provider.kind.value}")
+    counts = four_clique_counts(view, provider, 0, nnz).cpu().numpy()
+    return four_clique_combine(provider, counts)
+
+
+def four_clique_counts(view: DirectedView, provider: BloomProvider,
+                       e_begin: int, e_end: int):
+    """Device int64 [hist(B+1), sum_pos, triples] for directed edges range."""
+    import torch
+    dev = view.device()
+    sg = provider.sketched
+    d = sg.device_tensors()
+    bits = sg.bit_length
+    hist = torch.empty(bits + 1, dtype=torch.int64, device="cuda")
+    spos = torch.empty(1, dtype=torch.int64, device="cuda")
+    trip = torch.empty(1, dtype=torch.int64, device="cuda")
+    N.call("pg_4clique_bloom", N.ptr(dev.offsets), N.ptr(dev.adj),
+           N.ptr(dev.row_sources()), e_begin, e_end, N.ptr(d["rows"]), bits,
+           sg.hash_count, N.ptr(d["seeds"]), provider.op, N.ptr(d["sizes"]),
+           N.ptr(provider.lut_device()), N.ptr(hist), N.ptr(spos), N.ptr(trip),
+           N.stream_handle())
+    return torch.cat([hist, spos, trip])
+
+
+def four_clique_combine(provider: BloomProvider, counts: np.ndarray) -> float:
+    return provider._tc_combine(counts[:-1])
+
+
+def _feasible(c: float, du: int, dv: int) -> float:
+    return min(max(c, 0.0), float(min(du, dv)))
+
+
+def vertex_similarity(u: int, v: int, measure, provider: IntersectionProvider,
+                      graph: CsrGraph) -> float:
+    if u == v:
+        raise ValueError("vertex similarity needs two distinct vertices")
+    measure = SimilarityMeasure(measure)
+    du, dv = graph.degree(u), graph.degree(v)
+    if measure in _COUNTING:
+        c = float(provider.pair(u, v))
+        if measure is SimilarityMeasure.COMMON_NEIGHBORS:
+            return c
+        c = _feasible(c, du, dv)
+        if measure is SimilarityMeasure.JACCARD:
+            denom = du + dv - c
+            return c / denom if denom > 0 else 0.0
+        if measure is SimilarityMeasure.OVERLAP:
+            lo = min(du, dv)
+            return c / lo if lo > 0 else 0.0
+        return du + dv - c
+    members = provider.common_members(u, v)
+    degs = graph.degrees()[members] if len(members) else np.empty(0)
+    if measure is SimilarityMeasure.ADAMIC_ADAR:
+        return math.fsum(1.0 / math.log(d) for d in degs.tolist() if d > 1)
+    return math.fsum(1.0 / d for d in degs.tolist() if d > 0)
+
+
+@dataclass
+class ClusterResult:
+    kept_edges: np.ndarray
+    cluster_count: int
+    singleton_count: int
+
+
+def jarvis_patrick_cluster(graph: CsrGraph, provider: IntersectionProvider,
+                           tau: float, threads: int = 1) -> ClusterResult:
+    """Keep edges whose score strictly exceeds tau; count components."""
+    us, vs = graph.device().upper_edges()
+    scores = provider._pairs_device(us, vs)
+    keep = scores > tau
+    ku = us[keep].cpu().numpy().astype(np.int64)
+    kv = vs[keep].cpu().numpy().astype(np.int64)
+    kept = np.stack([ku, kv], axis=1) if len(ku) else np.empty((0, 2), np.int64)
+    touched = np.unique(kept.reshape(-1))
+    if len(kept):
+        from scipy.sparse import coo_matrix
+        from scipy.sparse.csgraph import connected_components
+        a = coo_matrix((np.ones(len(ku)), (ku, kv)), shape=(graph.n, graph.n))
+        _, labels = connected_components(a, directed=False)
+        clusters = len(np.unique(labels[touched]))
+    else:
+        clusters = 0
+    return ClusterResult(kept, clusters, graph.n - len(touched))
+
+
+@dataclass
+class JaccardCount:
+    kept_hat: int          # edges with J-hat = m/k >= tau  (est_jaccard_minhash)
+    kept_similarity: int   # edges with vertex_similarity(JACCARD) >= tau
+    match_hist: np.ndarray  # int64[k+1] edges per positional-match count
+    min_matches: int
+
+
+def jaccard_min_matches(k: int, tau: float) -> int:
+    """Smallest m with float32(m)/float32(k) >= float32(tau) (fp32 J-hat)."""
+    kf, tf = np.float32(k), np.float32(tau)
+    for m in range(k + 1):
+        if np.float32(m) / kf >= tf:
+            return m
+    return k + 1
+
+
+def jaccard_counts(graph: CsrGraph, sketched: SketchedGraph, tau: float,
+                   e_begin: int, e_end: int):
+    import torch
+    if sketched.kind is not SketchKind.KHASH:
+        raise ValueError("Jaccard clustering needs k-Hash sketches")
+    k = sketched.capacity
+    d = sketched.device_tensors()
+    dev = graph.device()
+    us, vs = dev.upper_edges()
+    out = torch.empty(k + 3, dtype=torch.int64, device="cuda")
+    N.call("pg_jaccard_count_khash", N.ptr(d["entries"]), k, N.ptr(dev.degrees),
+           N.ptr(us), N.ptr(vs), e_begin, e_end, jaccard_min_matches(k, tau),
+           float(tau), N.ptr(out), N.stream_handle())
+    return out
+
+
+def jaccard_cluster_count(graph: CsrGraph, sketched: SketchedGraph,
+                          tau: float = 0.1) -> JaccardCount:
+    """Config 4: per-edge k-Hash Jaccard, kept if >= tau, surviving count."""
+    us, _ = graph.device().upper_edges()
+    c = jaccard_counts(graph, sketched, tau, 0, us.numel()).cpu().numpy()
+    return JaccardCount(int(c[0]), int(c[1]), c[2:].copy(),
+                        jaccard_min_matches(sketched.capacity, tau))

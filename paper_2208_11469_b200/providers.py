@@ -1,0 +1,384 @@
+"""Intersection providers: the plugin surface the mining drivers call.
+
+Same names, signatures and errors as reference ``providers.py``
+(``IntersectionProvider`` :44-64, ``ExactProvider`` :67-121,
+``BloomProvider`` :124-175, ``MinHashProvider`` :178-250, ``KmvProvider``
+:253-307, ``make_provider`` :310-338).  Every batch call runs the sm_100a
+kernels of the C ABI:
+
+  * ``pair_many(us, vs)`` accepts host numpy arrays (returns numpy, like the
+    reference) or int CUDA tensors (returns a float64 CUDA tensor, no host
+    round trip);
+  * ``_tc_counts(e_begin, e_end)`` is the fused whole-graph pass used by
+    ``tc_estimate`` (integer outputs, combined on the host by
+    ``_tc_combine``), also per edge shard for the multi-GPU driver.
+
+Providers are read-only after construction; concurrent ``pair_many`` calls
+from several threads each allocate their own buffers and enqueue on the
+current stream, which is safe.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from . import _native as N
+from .estimators import (EstimatorKind, est_intersection_kmv,
+                         est_intersection_minhash, swamidass_table,
+                         swamidass_value)
+from .graphs import CsrGraph, DeviceCsr, DirectedView
+from .sketches import (SketchKind, SketchedGraph, build_bloom, build_khash,
+                       build_kmv, build_onehash)
+
+__all__ = ["UnsupportedCombinationError", "IntersectionProvider",
+           "ExactProvider", "BloomProvider", "MinHashProvider", "KmvProvider",
+           "make_provider"]
+
+
+class UnsupportedCombinationError(ValueError):
+    """Asked a provider for something its sketch kind cannot deliver."""
+
+
+def _as_device_ids(a):
+    import torch
+    if isinstance(a, torch.Tensor):
+        return a.to(device="cuda", dtype=torch.int32).contiguous(), True
+    arr = np.asarray(a, dtype=np.int64).reshape(-1)
+    return torch.from_numpy(arr.astype(np.int32)).cuda(), False
+
+
+class IntersectionProvider:
+    kind: EstimatorKind
+    is_exact = False
+
+    def pair(self, u: int, v: int) -> float:
+        return float(self.pair_many(np.asarray([u]), np.asarray([v]))[0])
+
+    def pair_many(self, us, vs):
+        import torch
+        du, on_dev = _as_device_ids(us)
+        dv, _ = _as_device_ids(vs)
+        if du.shape != dv.shape:
+            raise ValueError("us and vs must have the same length")
+        out = self._pairs_device(du, dv)
+        return out if on_dev else out.cpu().numpy()
+
+    def _pairs_device(self, us, vs):
+        raise NotImplementedError
+
+    def with_set(self, w: int, members) -> float:
+        raise NotImplementedError
+
+    def common_members(self, u: int, v: int) -> np.ndarray:
+        raise UnsupportedCombinationError(
+            f"{self.kind.value} cannot enumerate intersection members")
+
+
+class ExactProvider(IntersectionProvider):
+    """Exact |N(u) & N(v)| from sorted CSR rows, on the device."""
+
+    is_exact = True
+
+    def __init__(self, offsets, adjacency, strategy: str = "merge"):
+        if strategy not in ("merge", "gallop", "auto"):
+            raise ValueError("strategy must be merge, gallop, or auto")
+        self.offsets = np.asarray(offsets, dtype=np.int64)
+        self.adjacency = np.asarray(adjacency, dtype=np.int64)
+        self.strategy = strategy
+        self.sizes = np.diff(self.offsets)
+        self.kind = (EstimatorKind.EXACT_GALLOP if strategy == "gallop"
+                     else EstimatorKind.EXACT_MERGE)
+        self._dev = None
+
+    @classmethod
+    def for_graph(cls, graph: CsrGraph, strategy: str = "merge"):
+        p = cls(graph.offsets, graph.adjacency, strategy)
+        p._dev = graph.device()
+        return p
+
+    @classmethod
+    def for_view(cls, view: DirectedView, strategy: str = "merge"):
+        p = cls(view.offsets, view.adjacency, strategy)
+        p._dev = view.device()
+        return p
+
+    def device(self) -> DeviceCsr:
+        if self._dev is None:
+            self._dev = DeviceCsr(self.offsets, self.adjacency)
+        return self._dev
+
+    def pair(self, u: int, v: int) -> int:
+        return int(self.pair_many(np.asarray([u]), np.asarray([v]))[0])
+
+    def _pairs_device(self, us, vs):
+        import torch
+        d = self.device()
+        out = torch.empty(max(1, us.numel()), dtype=torch.int64, device="cuda")
+        N.call("pg_pairs_exact", N.ptr(d.offsets), N.ptr(d.adj), N.ptr(us),
+               N.ptr(vs), us.numel(), N.ptr(out), N.stream_handle())
+        return out[:us.numel()]
+
+    def with_set(self, w: int, members) -> int:
+        m = np.unique(np.asarray(members, dtype=np.int64))
+        return int(np.count_nonzero(np.isin(
+            self.adjacency[self.offsets[w]:self.offsets[w + 1]], m,
+            assume_unique=True)))
+
+    def common_members(self, u: int, v: int) -> np.ndarray:
+        a = self.adjacency[self.offsets[u]:self.offsets[u + 1]]
+        b = self.adjacency[self.offsets[v]:self.offsets[v + 1]]
+        return np.intersect1d(a, b, assume_unique=True)
+
+
+class _SketchProvider(IntersectionProvider):
+    def __init__(self, sketched: SketchedGraph):
+        self.sketched = sketched
+        self.sizes = sketched.sizes
+
+    def _dev(self) -> dict:
+        return self.sketched.device_tensors()
+
+
+class BloomProvider(_SketchProvider):
+    """Bloom estimates; ``kind`` picks the AND, limit or OR form."""
+
+    def __init__(self, sketched: SketchedGraph, kind: EstimatorKind):
+        if sketched.kind is not SketchKind.BLOOM:
+            raise ValueError("BloomProvider needs Bloom sketches")
+        kind = EstimatorKind(kind)
+        if kind not in (EstimatorKind.BF_AND, EstimatorKind.BF_L,
+                        EstimatorKind.BF_OR):
+            raise ValueError(f"{kind} is not a Bloom estimator")
+        super().__init__(sketched)
+        self.kind = kind
+        self._lut = None
+
+    @property
+    def op(self) -> int:
+        return {EstimatorKind.BF_AND: N.PG_BF_AND, EstimatorKind.BF_L: N.PG_BF_L,
+                EstimatorKind.BF_OR: N.PG_BF_OR}[self.kind]
+
+    def lut_device(self):
+        if self._lut is None:
+            import torch
+            sg = self.sketched
+            self._lut = torch.from_numpy(
+                swamidass_table(sg.bit_length, sg.hash_count).copy()).cuda()
+        return self._lut
+
+    def _pairs_device(self, us, vs):
+        import torch
+        d, sg = self._dev(), self.sketched
+        out = torch.empty(max(1, us.numel()), dtype=torch.float64, device="cuda")
+        N.call("pg_pairs_bloom", N.ptr(d["rows"]), sg.bit_length,
+               sg.hash_count, self.op, N.ptr(d["sizes"]),
+               N.ptr(self.lut_device()), N.ptr(us), N.ptr(vs), us.numel(), None,
+               N.ptr(out), N.stream_handle())
+        return out[:us.numel()]
+
+    def pair_counts(self, us, vs):
+        """Per-edge popcounts of AND (OR for BF_OR) -- the integer core."""
+        import torch
+        du, on_dev = _as_device_ids(us)
+        dv, _ = _as_device_ids(vs)
+        d, sg = self._dev(), self.sketched
+        out = torch.empty(max(1, du.numel()), dtype=torch.int32, device="cuda")
+        N.call("pg_pairs_bloom", N.ptr(d["rows"]), sg.bit_length,
+               sg.hash_count, self.op, None, None, N.ptr(du), N.ptr(dv),
+               du.numel(), N.ptr(out), None, N.stream_handle())
+        out = out[:du.numel()]
+        return out if on_dev else out.cpu().numpy().astype(np.int64)
+
+    def _tc_counts(self, us, vs, e_begin: int, e_end: int):
+        import torch
+        d, sg = self._dev(), self.sketched
+        hist = torch.empty(sg.bit_length + 1, dtype=torch.int64, device="cuda")
+        spos = torch.empty(1, dtype=torch.int64, device="cuda")
+        N.call("pg_tc_bloom", N.ptr(d["rows"]), sg.bit_length, self.op,
+               N.ptr(d["sizes"]), N.ptr(self.lut_device()), N.ptr(us),
+               N.ptr(vs), e_begin, e_end, N.ptr(hist), N.ptr(spos),
+               N.stream_handle())
+        return torch.cat([hist, spos])
+
+    def _tc_combine(self, counts: np.ndarray) -> float:
+        """Sum of per-edge estimates from the exact integer outputs."""
+        sg = self.sketched
+        hist, spos = counts[:-1], int(counts[-1])
+        if self.kind is EstimatorKind.BF_L:
+            return float(int(np.dot(hist, np.arange(len(hist), dtype=np.int64)))
+                         / sg.hash_count)
+        lut = swamidass_table(sg.bit_length, sg.hash_count)
+        nz = np.nonzero(hist)[0]
+        weighted = math.fsum(float(hist[o]) * float(lut[o]) for o in nz)
+        if self.kind is EstimatorKind.BF_AND:
+            return weighted
+        return float(spos) - weighted
+
+    def with_set(self, w: int, members) -> float:
+        sg = self.sketched
+        members = np.asarray(members, dtype=np.int64)
+        mem = build_bloom(members, sg.plan, sg.family)
+        from .estimators import _bloom_count
+        from .sketches import BloomSketch
+        row = sg.sketch(w)
+        ones = _bloom_count(row, BloomSketch(mem.words, sg.bit_length,
+                                             sg.hash_count, mem.ones, sg.seed),
+                            self.kind is EstimatorKind.BF_OR)
+        if self.kind is EstimatorKind.BF_OR:
+            raw = (int(self.sizes[w]) + len(members)
+                   - swamidass_value(sg.bit_length, sg.hash_count, ones))
+            return max(0.0, float(raw))
+        if self.kind is EstimatorKind.BF_L:
+            return ones / sg.hash_count
+        return float(swamidass_value(sg.bit_length, sg.hash_count, ones))
+
+
+class MinHashProvider(_SketchProvider):
+    """k-Hash or 1-Hash estimates from entry matrices."""
+
+    def __init__(self, sketched: SketchedGraph):
+        if sketched.kind is SketchKind.KHASH:
+            self.kind = EstimatorKind.KHASH
+        elif sketched.kind is SketchKind.ONEHASH:
+            self.kind = EstimatorKind.ONEHASH
+        else:
+            raise ValueError("MinHashProvider needs MinHash sketches")
+        super().__init__(sketched)
+
+    @property
+    def onehash(self) -> bool:
+        return self.kind is EstimatorKind.ONEHASH
+
+    def _pairs_device(self, us, vs):
+        import torch
+        d, sg = self._dev(), self.sketched
+        out = torch.empty(max(1, us.numel()), dtype=torch.float64, device="cuda")
+        N.call("pg_pairs_minhash", N.ptr(d["entries"]), sg.capacity,
+               int(self.onehash), N.ptr(d["sizes"]), N.ptr(us), N.ptr(vs),
+               us.numel(), None, N.ptr(out), N.stream_handle())
+        return out[:us.numel()]
+
+    def pair_counts(self, us, vs):
+        """Per-edge match counts (positional for k-Hash, set for 1-Hash)."""
+        import torch
+        du, on_dev = _as_device_ids(us)
+        dv, _ = _as_device_ids(vs)
+        d, sg = self._dev(), self.sketched
+        out = torch.empty(max(1, du.numel()), dtype=torch.int32, device="cuda")
+        N.call("pg_pairs_minhash", N.ptr(d["entries"]), sg.capacity,
+               int(self.onehash), N.ptr(d["sizes"]), N.ptr(du), N.ptr(dv),
+               du.numel(), N.ptr(out), None, N.stream_handle())
+        out = out[:du.numel()]
+        return out if on_dev else out.cpu().numpy().astype(np.int64)
+
+    def _tc_counts(self, us, vs, e_begin: int, e_end: int):
+        import torch
+        d, sg = self._dev(), self.sketched
+        k = sg.capacity
+        cnt = torch.empty(k + 1, dtype=torch.int64, device="cuda")
+        ssum = torch.empty(k + 1, dtype=torch.int64, device="cuda")
+        verb = torch.empty(1, dtype=torch.int64, device="cuda")
+        N.call("pg_tc_minhash", N.ptr(d["entries"]), k, int(self.onehash),
+               N.ptr(d["sizes"]), N.ptr(us), N.ptr(vs), e_begin, e_end,
+               N.ptr(cnt), N.ptr(ssum), N.ptr(verb), N.stream_handle())
+        return torch.cat([cnt, ssum, verb])
+
+    def _tc_combine(self, counts: np.ndarray) -> float:
+        k = self.sketched.capacity
+        ssum, verb = counts[k + 1:2 * k + 2], int(counts[-1])
+        terms = []
+        for m in np.nonzero(ssum)[0]:
+            j = float(m) / k
+            terms.append((j / (1.0 + j)) * float(ssum[m]))
+        return math.fsum(terms) + float(verb)
+
+    def with_set(self, w: int, members) -> float:
+        sg = self.sketched
+        members = np.asarray(members, dtype=np.int64)
+        if sg.kind is SketchKind.KHASH:
+            mem = build_khash(members, sg.capacity, sg.family)
+        else:
+            mem = build_onehash(members, sg.capacity, sg.family)
+        return est_intersection_minhash(sg.sketch(w), mem, int(self.sizes[w]),
+                                        len(members))
+
+    def common_members(self, u: int, v: int) -> np.ndarray:
+        a, b = self.sketched.sketch(u).entries, self.sketched.sketch(v).entries
+        return np.intersect1d(np.unique(a), np.unique(b))
+
+
+class KmvProvider(_SketchProvider):
+    def __init__(self, sketched: SketchedGraph):
+        if sketched.kind is not SketchKind.KMV:
+            raise ValueError("KmvProvider needs KMV sketches")
+        super().__init__(sketched)
+        self.kind = EstimatorKind.KMV
+
+    def _pairs_device(self, us, vs):
+        import torch
+        d, sg = self._dev(), self.sketched
+        out = torch.empty(max(1, us.numel()), dtype=torch.float64, device="cuda")
+        N.call("pg_pairs_kmv", N.ptr(d["values"]), N.ptr(d["lengths"]),
+               sg.capacity, N.ptr(d["sizes"]), N.ptr(us), N.ptr(vs), us.numel(),
+               None, None, None, N.ptr(out), N.stream_handle())
+        return out[:us.numel()]
+
+    def pair_stats(self, us, vs):
+        """Per-edge (common, union) counts of the stored values."""
+        import torch
+        du, _ = _as_device_ids(us)
+        dv, _ = _as_device_ids(vs)
+        d, sg = self._dev(), self.sketched
+        n = max(1, du.numel())
+        com = torch.empty(n, dtype=torch.int32, device="cuda")
+        uni = torch.empty(n, dtype=torch.int32, device="cuda")
+        N.call("pg_pairs_kmv", N.ptr(d["values"]), N.ptr(d["lengths"]),
+               sg.capacity, N.ptr(d["sizes"]), N.ptr(du), N.ptr(dv), du.numel(),
+               N.ptr(com), N.ptr(uni), None, None, N.stream_handle())
+        return (com[:du.numel()].cpu().numpy().astype(np.int64),
+                uni[:du.numel()].cpu().numpy().astype(np.int64))
+
+    def _tc_counts(self, us, vs, e_begin: int, e_end: int):
+        import torch
+        d, sg = self._dev(), self.sketched
+        out = torch.empty(1, dtype=torch.float64, device="cuda")
+        N.call("pg_tc_kmv", N.ptr(d["values"]), N.ptr(d["lengths"]),
+               sg.capacity, N.ptr(d["sizes"]), N.ptr(us), N.ptr(vs), e_begin,
+               e_end, N.ptr(out), N.stream_handle())
+        return out
+
+    def _tc_combine(self, counts: np.ndarray) -> float:
+        return float(counts[0])
+
+    def with_set(self, w: int, members) -> float:
+        sg = self.sketched
+        members = np.asarray(members, dtype=np.int64)
+        mem = build_kmv(members, sg.capacity, sg.family)
+        return est_intersection_kmv(sg.sketch(w), mem, int(self.sizes[w]),
+                                    len(members))
+
+
+def make_provider(kind, *, graph: CsrGraph | None = None,
+                  view: DirectedView | None = None,
+                  sketched: SketchedGraph | None = None) -> IntersectionProvider:
+    kind = EstimatorKind(kind)
+    if kind in (EstimatorKind.EXACT_MERGE, EstimatorKind.EXACT_GALLOP):
+        strategy = "gallop" if kind is EstimatorKind.EXACT_GALLOP else "merge"
+        if view is not None:
+            return ExactProvider.for_view(view, strategy)
+        if graph is not None:
+            return ExactProvider.for_graph(graph, strategy)
+        raise ValueError("exact provider needs a graph or a directed view")
+    if sketched is None:
+        raise ValueError(f"{kind.value} provider needs sketches")
+    if kind in (EstimatorKind.BF_AND, EstimatorKind.BF_L, EstimatorKind.BF_OR):
+        return BloomProvider(sketched, kind)
+    if kind in (EstimatorKind.KHASH, EstimatorKind.ONEHASH):
+        provider = MinHashProvider(sketched)
+        if provider.kind is not kind:
+            raise ValueError(f"sketches are {sketched.kind.value}, "
+                             f"estimator wants {kind.value}")
+        return provider
+    return KmvProvider(sketched)
