@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--config", choices=sorted(WORKLOAD), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-busy", action="store_true",
+                    help="skip the untimed clock-sampling tail (for ncu runs)")
     return ap.parse_args()
 
 
@@ -212,7 +214,7 @@ def run_ours(args, cfg, rank, world, local):
         torch.cuda.synchronize()
         # keep the GPU busy for the clock sampler's benefit, untimed
         tq = time.time()
-        while time.time() - tq < 0.5:
+        while not args.no_busy and time.time() - tq < 0.5:
             provider._tc_counts(us, vs, e_begin, e_end)
         torch.cuda.synchronize()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]

@@ -22,6 +22,7 @@
 // reference's per-edge value is a function of an integer count, so sharded
 // runs reproduce the single-GPU result bit for bit; only KMV sums doubles.
 #include <algorithm>
+#include <cstdlib>
 
 #include "pg_common.cuh"
 
@@ -34,10 +35,22 @@ struct OpAnd {
   __device__ __forceinline__ static int apply(uint4 a, uint4 b) {
     return __popc(a.x & b.x) + __popc(a.y & b.y) + __popc(a.z & b.z) + __popc(a.w & b.w);
   }
+  __device__ __forceinline__ static int apply8(const uint32_t (&a)[8], const uint32_t (&b)[8]) {
+    int c = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) c += __popc(a[w] & b[w]);
+    return c;
+  }
 };
 struct OpOr {
   __device__ __forceinline__ static int apply(uint4 a, uint4 b) {
     return __popc(a.x | b.x) + __popc(a.y | b.y) + __popc(a.z | b.z) + __popc(a.w | b.w);
+  }
+  __device__ __forceinline__ static int apply8(const uint32_t (&a)[8], const uint32_t (&b)[8]) {
+    int c = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) c += __popc(a[w] | b[w]);
+    return c;
   }
 };
 // k-Hash positional matches: (eu == ev) & (eu >= 0)   (providers.py:197-198)
@@ -45,6 +58,12 @@ struct OpEqPos {
   __device__ __forceinline__ static int apply(uint4 a, uint4 b) {
     return (a.x == b.x && (int)a.x >= 0) + (a.y == b.y && (int)a.y >= 0) +
            (a.z == b.z && (int)a.z >= 0) + (a.w == b.w && (int)a.w >= 0);
+  }
+  __device__ __forceinline__ static int apply8(const uint32_t (&a)[8], const uint32_t (&b)[8]) {
+    int c = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) c += (a[w] == b[w] && (int)a[w] >= 0);
+    return c;
   }
 };
 
@@ -80,7 +99,14 @@ __device__ __forceinline__ void warp_slice(int64_t e_begin, int64_t e_end, int64
 
 // Group engine: calls epi.edge(e, u, v, count) once per edge of the warp's
 // slice, from the lane that loaded the edge.
-template <int V, int G, class Op, class Epi>
+//
+// Latency structure (the kernel is load-latency bound): the edge indices of
+// iteration i+1 are loaded while the rows of iteration i are in flight, all
+// G*V v-row loads of an iteration are issued before any is consumed, and the
+// u row is cached in registers across consecutive edges (edges are in CSR
+// order, so u changes on average once per ~40 edges at R-MAT scale 20) and
+// only reloaded when it changes.
+template <int V, int G, class Op, class Epi, bool kVCache = false>
 __device__ __forceinline__ void group_edge_loop(const uint4* __restrict__ rows, const int32_t* __restrict__ us,
                                                 const int32_t* __restrict__ vs, int64_t e_begin,
                                                 int64_t e_end, Epi& epi) {
@@ -90,25 +116,137 @@ __device__ __forceinline__ void group_edge_loop(const uint4* __restrict__ rows, 
   const int gbase = lane & ~(G - 1);
   int64_t wb, we;
   warp_slice(e_begin, e_end, wb, we);
+  if (wb >= we) return;
+  int32_t ul = 0, vl = 0;
+  if (wb + lane < we) {
+    ul = us[wb + lane];
+    vl = vs[wb + lane];
+  }
+  int32_t ucur = -1;
+  uint4 ur[V];
+#pragma unroll
+  for (int i = 0; i < V; ++i) ur[i] = make_uint4(0, 0, 0, 0);
+#pragma unroll 1
   for (int64_t e0 = wb; e0 < we; e0 += 32) {
     const int64_t e = e0 + lane;
     const bool valid = e < we;
-    const int32_t ul = valid ? us[e] : 0;
-    const int32_t vl = valid ? vs[e] : 0;
+    // prefetch the next iteration's edge indices
+    int32_t un = 0, vn = 0;
+    if (e + 32 < we) {
+      un = us[e + 32];
+      vn = vs[e + 32];
+    }
+    uint4 vr[G][V];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int32_t vj = __shfl_sync(0xffffffffu, vl, gbase + j);
+      const uint4* rv = rows + (int64_t)vj * W4 + gl;
+#pragma unroll
+      for (int i = 0; i < V; ++i) vr[j][i] = kVCache ? ldg_keep(rv + i * G) : ldg_stream(rv + i * G);
+    }
     int c[G];
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       const int32_t uj = __shfl_sync(0xffffffffu, ul, gbase + j);
-      const int32_t vj = __shfl_sync(0xffffffffu, vl, gbase + j);
-      const uint4* ru = rows + (int64_t)uj * W4 + gl;
-      const uint4* rv = rows + (int64_t)vj * W4 + gl;
+      if (uj != ucur) {  // group-uniform; rare
+        ucur = uj;
+        const uint4* ru = rows + (int64_t)uj * W4 + gl;
+#pragma unroll
+        for (int i = 0; i < V; ++i) ur[i] = ldg_keep(ru + i * G);
+      }
       int acc = 0;
 #pragma unroll
-      for (int i = 0; i < V; ++i) acc += Op::apply(ldg_keep(ru + i * G), ldg_stream(rv + i * G));
+      for (int i = 0; i < V; ++i) acc += Op::apply(ur[i], vr[j][i]);
       c[j] = acc;
     }
     const int cnt = group_transpose_reduce<G>(c, gl);
     if (valid) epi.edge(e, ul, vl, cnt);
+    ul = un;
+    vl = vn;
+  }
+}
+
+// ------------------------------------------------- wide (256-bit) engine
+// sm_100 has 256-bit global loads (LDG.E.ENL2.256): a lane moves 32 bytes per
+// instruction, so a 128-byte Bloom row is 4 lanes and a 256-byte row 8 lanes.
+// Same warp/group/transpose structure as group_edge_loop with half the load
+// instructions and twice the bytes in flight per register.
+__device__ __forceinline__ void ldg256(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.nc.L1::no_allocate.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "l"(p));
+}
+__device__ __forceinline__ void ldg256_keep(const void* p, uint32_t (&r)[8]) {
+  asm volatile("ld.global.nc.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                 "=r"(r[7])
+               : "l"(p));
+}
+
+template <int W8, class Op, class Epi, bool kVCache = false>
+__device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__ rows,
+                                               const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
+                                               int64_t e_begin, int64_t e_end, Epi& epi) {
+  constexpr int G = W8 < 8 ? W8 : 8;  // lanes per edge
+  constexpr int V = W8 / G;           // 32-byte chunks per lane per row
+  constexpr int64_t kRowBytes = W8 * 32;
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int gbase = lane & ~(G - 1);
+  int64_t wb, we;
+  warp_slice(e_begin, e_end, wb, we);
+  if (wb >= we) return;
+  int32_t ul = 0, vl = 0;
+  if (wb + lane < we) {
+    ul = us[wb + lane];
+    vl = vs[wb + lane];
+  }
+  int32_t ucur = -1;
+  uint32_t ur[V][8];
+#pragma unroll
+  for (int i = 0; i < V; ++i)
+#pragma unroll
+    for (int w = 0; w < 8; ++w) ur[i][w] = 0;
+#pragma unroll 1
+  for (int64_t e0 = wb; e0 < we; e0 += 32) {
+    const int64_t e = e0 + lane;
+    const bool valid = e < we;
+    int32_t un = 0, vn = 0;
+    if (e + 32 < we) {
+      un = us[e + 32];
+      vn = vs[e + 32];
+    }
+    uint32_t vr[G][V][8];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int32_t vj = __shfl_sync(0xffffffffu, vl, gbase + j);
+      const unsigned char* rv = rows + (int64_t)vj * kRowBytes + gl * 32;
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        if (kVCache) ldg256_keep(rv + i * G * 32, vr[j][i]);
+        else ldg256(rv + i * G * 32, vr[j][i]);
+      }
+    }
+    int c[G];
+#pragma unroll
+    for (int j = 0; j < G; ++j) {
+      const int32_t uj = __shfl_sync(0xffffffffu, ul, gbase + j);
+      if (uj != ucur) {  // group-uniform; rare
+        ucur = uj;
+        const unsigned char* ru = rows + (int64_t)uj * kRowBytes + gl * 32;
+#pragma unroll
+        for (int i = 0; i < V; ++i) ldg256_keep(ru + i * G * 32, ur[i]);
+      }
+      int acc = 0;
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc += Op::apply8(ur[i], vr[j][i]);
+      c[j] = acc;
+    }
+    const int cnt = group_transpose_reduce<G>(c, gl);
+    if (valid) epi.edge(e, ul, vl, cnt);
+    ul = un;
+    vl = vn;
   }
 }
 
@@ -250,8 +388,8 @@ __global__ void __launch_bounds__(kBlock) pairs_scalar_kernel_bloom(const uint64
   scalar_edge_loop_bloom(rows, words, epi.op, us, vs, 0, count, epi);
 }
 
-template <int V, int G, class Op, bool kScalar>
-__global__ void __launch_bounds__(kBlock) tc_bloom_kernel(const uint4* rows, int bits, const int32_t* us,
+template <int V, int G, class Op, bool kScalar, int MINB = 1, bool kVCache = false>
+__global__ void __launch_bounds__(kBlock, MINB) tc_bloom_kernel(const uint4* rows, int bits, const int32_t* us,
                                                          const int32_t* vs, int64_t e_begin,
                                                          int64_t e_end, EpiBloomHist epi,
                                                          int64_t* out_hist, int64_t* out_sum_pos) {
@@ -264,7 +402,7 @@ __global__ void __launch_bounds__(kBlock) tc_bloom_kernel(const uint4* rows, int
     scalar_edge_loop_bloom(reinterpret_cast<const uint64_t*>(rows), bits / 64, epi.op, us, vs, e_begin,
                            e_end, epi);
   else
-    group_edge_loop<V, G, Op>(rows, us, vs, e_begin, e_end, epi);
+    group_edge_loop<V, G, Op, EpiBloomHist, kVCache>(rows, us, vs, e_begin, e_end, epi);
   __syncthreads();
   for (int i = threadIdx.x; i <= bits; i += blockDim.x)
     if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_hist + i), (unsigned long long)hist_s[i]);
@@ -272,6 +410,28 @@ __global__ void __launch_bounds__(kBlock) tc_bloom_kernel(const uint4* rows, int
     long long s = epi.sum_pos;
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if ((threadIdx.x & 31) == 0 && s) atomicAdd(reinterpret_cast<unsigned long long*>(out_sum_pos), (unsigned long long)s);
+  }
+}
+
+template <int W8, class Op, int MINB, bool kVCache>
+__global__ void __launch_bounds__(kBlock, MINB) tc_bloom_wide_kernel(const unsigned char* rows, int bits,
+                                                                    const int32_t* us, const int32_t* vs,
+                                                                    int64_t e_begin, int64_t e_end,
+                                                                    EpiBloomHist epi, int64_t* out_hist,
+                                                                    int64_t* out_sum_pos) {
+  extern __shared__ int hist_s[];
+  for (int i = threadIdx.x; i <= bits; i += blockDim.x) hist_s[i] = 0;
+  __syncthreads();
+  epi.hist_s = hist_s;
+  epi.sum_pos = 0;
+  wide_edge_loop<W8, Op, EpiBloomHist, kVCache>(rows, us, vs, e_begin, e_end, epi);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= bits; i += blockDim.x)
+    if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_hist + i), (unsigned long long)hist_s[i]);
+  if (epi.op == PG_BF_OR) {
+    long long sp = epi.sum_pos;
+    for (int o = 16; o > 0; o >>= 1) sp += __shfl_xor_sync(0xffffffffu, sp, o);
+    if ((threadIdx.x & 31) == 0 && sp) atomicAdd(reinterpret_cast<unsigned long long*>(out_sum_pos), (unsigned long long)sp);
   }
 }
 
@@ -707,6 +867,31 @@ __global__ void __launch_bounds__(kBlock) clique4_exact_kernel(
 }
 
 // ---------------------------------------------------------- launching ----
+// Occupancy hint of the Bloom TC kernel (blocks of 256 per SM the register
+// allocation must allow); PG_TC_MINB overrides it for tuning sweeps.
+static int tc_minb(int w4) {
+  static int env = [] {
+    const char* e = getenv("PG_TC_MINB");
+    return e ? atoi(e) : 0;
+  }();
+  if (env >= 1 && env <= 4) return env;
+  (void)w4;
+  return 2;  // measured best for B = 512..2048 (higher hints spill)
+}
+
+template <int V, int G>
+static auto pick_tc_bloom(int op, int minb) {
+  const bool o = op == PG_BF_OR;
+  static const bool vcache = getenv("PG_TC_VCACHE") != nullptr;
+  if (vcache) return o ? tc_bloom_kernel<V, G, OpOr, false, 2, true> : tc_bloom_kernel<V, G, OpAnd, false, 2, true>;
+  switch (minb) {
+    case 2: return o ? tc_bloom_kernel<V, G, OpOr, false, 2> : tc_bloom_kernel<V, G, OpAnd, false, 2>;
+    case 3: return o ? tc_bloom_kernel<V, G, OpOr, false, 3> : tc_bloom_kernel<V, G, OpAnd, false, 3>;
+    case 4: return o ? tc_bloom_kernel<V, G, OpOr, false, 4> : tc_bloom_kernel<V, G, OpAnd, false, 4>;
+    default: return o ? tc_bloom_kernel<V, G, OpOr, false, 1> : tc_bloom_kernel<V, G, OpAnd, false, 1>;
+  }
+}
+
 template <class K>
 static int grid_for_kernel(K kernel, size_t smem) {
   int per_sm = 0;
@@ -786,6 +971,39 @@ int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* s
   const size_t smem = sizeof(int) * (bits + 1);
   const int w4 = bits % 128 == 0 ? bits / 128 : 0;
   const uint4* r4 = reinterpret_cast<const uint4*>(rows);
+  static const int engine = [] {
+    const char* e = getenv("PG_TC_ENGINE");
+    if (e && e[0] == 'r') return 0;  // 128-bit loads (group_edge_loop)
+    return 2;                        // 256-bit loads (wide_edge_loop, default)
+  }();
+  if (engine == 2 && (w4 == 4 || w4 == 8 || w4 == 16)) {
+    static const bool vcache = getenv("PG_TC_VCACHE") != nullptr;
+    const int minb = tc_minb(w4);
+    const unsigned char* rb = reinterpret_cast<const unsigned char*>(rows);
+    cudaError_t le = cudaSuccess;
+#define PG_W(W8, MB, VC)                                                                              \
+  {                                                                                                  \
+    auto k = op == PG_BF_OR ? tc_bloom_wide_kernel<W8, OpOr, MB, VC> : tc_bloom_wide_kernel<W8, OpAnd, MB, VC>; \
+    le = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+    if (le != cudaSuccess) return fail(PG_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(le));  \
+    const int grid = grid_cap(grid_for_kernel(k, smem), e_end - e_begin, kBlock);                    \
+    k<<<grid, kBlock, smem, s>>>(rb, bits, us, vs, e_begin, e_end, epi, out_hist, out_sum_pos);      \
+  }
+#define PG_WM(W8)                                                     \
+  if (vcache) {                                                      \
+    if (minb >= 3) PG_W(W8, 3, true) else PG_W(W8, 2, true)          \
+  } else {                                                           \
+    if (minb >= 4) PG_W(W8, 4, false)                                \
+    else if (minb == 3) PG_W(W8, 3, false)                           \
+    else PG_W(W8, 2, false)                                          \
+  }
+    if (w4 == 4) PG_WM(2)
+    else if (w4 == 8) PG_WM(4)
+    else PG_WM(8)
+#undef PG_WM
+#undef PG_W
+    return check_launch("tc_bloom_wide");
+  }
   if (!fast_w4(w4)) {
     auto k = tc_bloom_kernel<1, 1, OpAnd, true>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -794,7 +1012,7 @@ int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* s
   } else {
 #define PG_L(V, G)                                                                                   \
   {                                                                                                  \
-    auto k = op == PG_BF_OR ? tc_bloom_kernel<V, G, OpOr, false> : tc_bloom_kernel<V, G, OpAnd, false>; \
+    auto k = pick_tc_bloom<V, G>(op, tc_minb(w4));                                                   \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                 \
     const int grid = grid_cap(grid_for_kernel(k, smem), e_end - e_begin, kBlock);                    \
     k<<<grid, kBlock, smem, s>>>(r4, bits, us, vs, e_begin, e_end, epi, out_hist, out_sum_pos);      \
