@@ -181,7 +181,10 @@ def run_ours(args, cfg, rank, world, local):
         build_ms.append(ev0.elapsed_time(ev1))
     provider = pg.make_provider("bf_and", sketched=sk)
     m = us.numel()
-    e_begin, e_end = edge_range(m, rank, world)
+    # the fused kernel's edge-slot layout (rows padded to its lane-group size)
+    lus, lvs, slots, padded = provider._tc_layout(dev)
+    e_begin, e_end = edge_range(slots, rank, world, align=32 if padded else 1)
+    rank_edges = int(((lvs[e_begin:e_end] >= 0).sum()).item())
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -189,7 +192,7 @@ def run_ours(args, cfg, rank, world, local):
         N.call("pg_l2_flush", N.ptr(flush), flush.numel(), N.stream_handle())
 
     def step():
-        counts = provider._tc_counts(us, vs, e_begin, e_end)
+        counts = provider._tc_counts(lus, lvs, e_begin, e_end, padded)
         return allreduce_counts(counts)
 
     for _ in range(args.warmup):
@@ -207,7 +210,7 @@ def run_ours(args, cfg, rank, world, local):
         for i in range(args.steps):
             l2_flush()  # between timed steps, outside the events
             starts[i].record(stream)
-            counts = provider._tc_counts(us, vs, e_begin, e_end)
+            counts = provider._tc_counts(lus, lvs, e_begin, e_end, padded)
             kends[i].record(stream)
             counts = allreduce_counts(counts)
             ends[i].record(stream)
@@ -215,7 +218,7 @@ def run_ours(args, cfg, rank, world, local):
         # keep the GPU busy for the clock sampler's benefit, untimed
         tq = time.time()
         while not args.no_busy and time.time() - tq < 0.5:
-            provider._tc_counts(us, vs, e_begin, e_end)
+            provider._tc_counts(lus, lvs, e_begin, e_end, padded)
         torch.cuda.synchronize()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     kern_ms = [s.elapsed_time(e) for s, e in zip(starts, kends)]
@@ -236,7 +239,7 @@ def run_ours(args, cfg, rank, world, local):
 
     # roofline: algorithmic bytes per launch = edges of this rank x (2 rows + 2 int32)
     bytes_per_edge = 2 * (bits // 8) + 8
-    launch_bytes = (e_end - e_begin) * bytes_per_edge
+    launch_bytes = rank_edges * bytes_per_edge
     achieved = launch_bytes / (kern_ms_avg / 1e3) / 1e9
     peak, peak_src = load_peaks()
     traffic = load_traffic(args.config) if world == 1 else None
@@ -259,7 +262,8 @@ def run_ours(args, cfg, rank, world, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded R-MAT, reference generator draw order)",
             "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "m": m,
-                       "edges_per_rank": e_end - e_begin,
+                       "edges_per_rank": rank_edges,
+                       "edge_slots": slots, "row_padded_layout": padded,
                        "sketch_bytes": g.n * bits // 8,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": f"edge-range shards x{world}, replicated sketches, "

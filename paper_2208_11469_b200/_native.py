@@ -39,6 +39,10 @@ SIGNATURES = {
     "pg_csr_upper_edges_workspace": [c_i64, ctypes.POINTER(c_size)],
     "pg_csr_upper_edges": [c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i64,
                            ctypes.POINTER(c_i64), c_ptr, c_size, c_ptr],
+    "pg_csr_upper_edges_padded": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr,
+                                  c_i64, ctypes.POINTER(c_i64), c_ptr, c_size,
+                                  c_ptr],
+    "pg_tc_bloom_pad": [c_i32, ctypes.POINTER(c_i32)],
     "pg_csr_expand_rows": [c_ptr, c_i64, c_i64, c_ptr, c_ptr],
     "pg_build_bloom": [c_ptr, c_ptr, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr,
                        c_ptr],
@@ -54,6 +58,8 @@ SIGNATURES = {
                      c_ptr, c_ptr, c_ptr, c_ptr],
     "pg_tc_bloom": [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_i64,
                     c_i64, c_ptr, c_ptr, c_ptr],
+    "pg_tc_bloom_padded": [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr,
+                           c_i64, c_i64, c_ptr, c_ptr, c_ptr],
     "pg_tc_minhash": [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_i64, c_i64,
                       c_ptr, c_ptr, c_ptr, c_ptr],
     "pg_tc_kmv": [c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64, c_i64,

@@ -184,7 +184,7 @@ __device__ __forceinline__ void ldg256_keep(const void* p, uint32_t (&r)[8]) {
                : "l"(p));
 }
 
-template <int W8, class Op, class Epi, bool kVCache = false>
+template <int W8, class Op, class Epi, bool kVCache = false, bool kPadded = false>
 __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__ rows,
                                                const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
                                                int64_t e_begin, int64_t e_end, Epi& epi) {
@@ -211,7 +211,7 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
 #pragma unroll 1
   for (int64_t e0 = wb; e0 < we; e0 += 32) {
     const int64_t e = e0 + lane;
-    const bool valid = e < we;
+    const bool valid = e < we && vl >= 0;  // v < 0: padding slot
     int32_t un = 0, vn = 0;
     if (e + 32 < we) {
       un = us[e + 32];
@@ -221,27 +221,52 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       const int32_t vj = __shfl_sync(0xffffffffu, vl, gbase + j);
-      const unsigned char* rv = rows + (int64_t)vj * kRowBytes + gl * 32;
+      const unsigned char* rv = rows + (int64_t)(vj < 0 ? 0 : vj) * kRowBytes + gl * 32;
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         if (kVCache) ldg256_keep(rv + i * G * 32, vr[j][i]);
         else ldg256(rv + i * G * 32, vr[j][i]);
       }
     }
-    int c[G];
+    // u rows: with the row-padded edge layout (pg_csr_upper_edges_padded)
+    // all G edges of a group share one u, cached across iterations; for any
+    // other input the per-edge rows are loaded speculatively in parallel.
+    const int32_t u0 = __shfl_sync(0xffffffffu, ul, gbase);
+    bool uniform = true;
+    if (!kPadded) {
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
-      const int32_t uj = __shfl_sync(0xffffffffu, ul, gbase + j);
-      if (uj != ucur) {  // group-uniform; rare
-        ucur = uj;
-        const unsigned char* ru = rows + (int64_t)uj * kRowBytes + gl * 32;
+      for (int j = 1; j < G; ++j) uniform &= __shfl_sync(0xffffffffu, ul, gbase + j) == u0;
+    }
+    int c[G];
+    if (kPadded || __all_sync(0xffffffffu, uniform)) {
+      if (u0 != ucur) {
+        ucur = u0;
+        const unsigned char* ru = rows + (int64_t)u0 * kRowBytes + gl * 32;
 #pragma unroll
         for (int i = 0; i < V; ++i) ldg256_keep(ru + i * G * 32, ur[i]);
       }
-      int acc = 0;
 #pragma unroll
-      for (int i = 0; i < V; ++i) acc += Op::apply8(ur[i], vr[j][i]);
-      c[j] = acc;
+      for (int j = 0; j < G; ++j) {
+        int acc = 0;
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc += Op::apply8(ur[i], vr[j][i]);
+        c[j] = acc;
+      }
+    } else if (!kPadded) {
+#pragma unroll
+      for (int j = 0; j < G; ++j) {
+        const int32_t uj = __shfl_sync(0xffffffffu, ul, gbase + j);
+        if (uj != ucur) {
+          ucur = uj;
+          const unsigned char* ru = rows + (int64_t)uj * kRowBytes + gl * 32;
+#pragma unroll
+          for (int i = 0; i < V; ++i) ldg256_keep(ru + i * G * 32, ur[i]);
+        }
+        int acc = 0;
+#pragma unroll
+        for (int i = 0; i < V; ++i) acc += Op::apply8(ur[i], vr[j][i]);
+        c[j] = acc;
+      }
     }
     const int cnt = group_transpose_reduce<G>(c, gl);
     if (valid) epi.edge(e, ul, vl, cnt);
@@ -413,7 +438,7 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_bloom_kernel(const uint4* row
   }
 }
 
-template <int W8, class Op, int MINB, bool kVCache>
+template <int W8, class Op, int MINB, bool kVCache, bool kPadded>
 __global__ void __launch_bounds__(kBlock, MINB) tc_bloom_wide_kernel(const unsigned char* rows, int bits,
                                                                     const int32_t* us, const int32_t* vs,
                                                                     int64_t e_begin, int64_t e_end,
@@ -424,7 +449,7 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_bloom_wide_kernel(const unsig
   __syncthreads();
   epi.hist_s = hist_s;
   epi.sum_pos = 0;
-  wide_edge_loop<W8, Op, EpiBloomHist, kVCache>(rows, us, vs, e_begin, e_end, epi);
+  wide_edge_loop<W8, Op, EpiBloomHist, kVCache, kPadded>(rows, us, vs, e_begin, e_end, epi);
   __syncthreads();
   for (int i = threadIdx.x; i <= bits; i += blockDim.x)
     if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_hist + i), (unsigned long long)hist_s[i]);
@@ -869,14 +894,14 @@ __global__ void __launch_bounds__(kBlock) clique4_exact_kernel(
 // ---------------------------------------------------------- launching ----
 // Occupancy hint of the Bloom TC kernel (blocks of 256 per SM the register
 // allocation must allow); PG_TC_MINB overrides it for tuning sweeps.
-static int tc_minb(int w4) {
+static int tc_minb(int w4, bool padded) {
   static int env = [] {
     const char* e = getenv("PG_TC_MINB");
     return e ? atoi(e) : 0;
   }();
   if (env >= 1 && env <= 4) return env;
-  (void)w4;
-  return 2;  // measured best for B = 512..2048 (higher hints spill)
+  if (!padded) return 2;  // general layout: speculative u loads need ~110 regs
+  return 3;
 }
 
 template <int V, int G>
@@ -921,6 +946,8 @@ using namespace pg;
     default: MACRO(1, 1); break;   \
   }
 
+extern "C" int pg_tc_bloom_pad(int32_t bits, int32_t* pad_host);
+
 static bool fast_w4(int w4) { return w4 == 1 || w4 == 2 || w4 == 4 || w4 == 8 || w4 == 16 || w4 == 32; }
 
 extern "C" {
@@ -953,9 +980,9 @@ int pg_pairs_bloom(const uint64_t* rows, int32_t bits, int32_t b, int32_t op, co
   return check_launch("pairs_bloom");
 }
 
-int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* sizes, const double* lut,
-                const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end, int64_t* out_hist,
-                int64_t* out_sum_pos, void* stream) {
+static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* sizes,
+                         const double* lut, const int32_t* us, const int32_t* vs, int64_t e_begin,
+                         int64_t e_end, int64_t* out_hist, int64_t* out_sum_pos, void* stream, bool padded) {
   PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
   PG_REQUIRE(op == PG_BF_AND || op == PG_BF_L || op == PG_BF_OR, "op is not a Bloom estimator");
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
@@ -977,25 +1004,31 @@ int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* s
     return 2;                        // 256-bit loads (wide_edge_loop, default)
   }();
   if (engine == 2 && (w4 == 4 || w4 == 8 || w4 == 16)) {
-    static const bool vcache = getenv("PG_TC_VCACHE") != nullptr;
-    const int minb = tc_minb(w4);
+    // measured on B200 (scripts/sweep_tc.py, R-MAT s20/s22): B=1024 best with
+    // 3 blocks/SM and streaming v rows; B=2048 best with L1-allocated v rows
+    // (hub rows reused within an SM)
+    static const char* vc_env = getenv("PG_TC_VCACHE");
+    const bool vcache = vc_env ? vc_env[0] != '0' : (padded && w4 == 16);
+    const int minb = tc_minb(w4, padded);
     const unsigned char* rb = reinterpret_cast<const unsigned char*>(rows);
     cudaError_t le = cudaSuccess;
-#define PG_W(W8, MB, VC)                                                                              \
+#define PG_W(W8, MB, VC, PD)                                                                          \
   {                                                                                                  \
-    auto k = op == PG_BF_OR ? tc_bloom_wide_kernel<W8, OpOr, MB, VC> : tc_bloom_wide_kernel<W8, OpAnd, MB, VC>; \
+    auto k = op == PG_BF_OR ? tc_bloom_wide_kernel<W8, OpOr, MB, VC, PD>                             \
+                            : tc_bloom_wide_kernel<W8, OpAnd, MB, VC, PD>;                           \
     le = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
     if (le != cudaSuccess) return fail(PG_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(le));  \
     const int grid = grid_cap(grid_for_kernel(k, smem), e_end - e_begin, kBlock);                    \
     k<<<grid, kBlock, smem, s>>>(rb, bits, us, vs, e_begin, e_end, epi, out_hist, out_sum_pos);      \
   }
-#define PG_WM(W8)                                                     \
-  if (vcache) {                                                      \
-    if (minb >= 3) PG_W(W8, 3, true) else PG_W(W8, 2, true)          \
-  } else {                                                           \
-    if (minb >= 4) PG_W(W8, 4, false)                                \
-    else if (minb == 3) PG_W(W8, 3, false)                           \
-    else PG_W(W8, 2, false)                                          \
+#define PG_WM(W8)                                                                  \
+  if (padded) {                                                                  \
+    if (vcache) PG_W(W8, 3, true, true)                                          \
+    else if (minb >= 4) PG_W(W8, 4, false, true)                                 \
+    else if (minb == 3) PG_W(W8, 3, false, true)                                 \
+    else PG_W(W8, 2, false, true)                                                \
+  } else {                                                                       \
+    PG_W(W8, 2, false, false)                                                    \
   }
     if (w4 == 4) PG_WM(2)
     else if (w4 == 8) PG_WM(4)
@@ -1012,7 +1045,7 @@ int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* s
   } else {
 #define PG_L(V, G)                                                                                   \
   {                                                                                                  \
-    auto k = pick_tc_bloom<V, G>(op, tc_minb(w4));                                                   \
+    auto k = pick_tc_bloom<V, G>(op, tc_minb(w4, false));                                                   \
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                 \
     const int grid = grid_cap(grid_for_kernel(k, smem), e_end - e_begin, kBlock);                    \
     k<<<grid, kBlock, smem, s>>>(r4, bits, us, vs, e_begin, e_end, epi, out_hist, out_sum_pos);      \
@@ -1021,6 +1054,23 @@ int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* s
 #undef PG_L
   }
   return check_launch("tc_bloom");
+}
+
+int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* sizes, const double* lut,
+                const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end, int64_t* out_hist,
+                int64_t* out_sum_pos, void* stream) {
+  return tc_bloom_impl(rows, bits, op, sizes, lut, us, vs, e_begin, e_end, out_hist, out_sum_pos, stream,
+                       false);
+}
+
+int pg_tc_bloom_padded(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* sizes,
+                       const double* lut, const int32_t* us, const int32_t* vs, int64_t e_begin,
+                       int64_t e_end, int64_t* out_hist, int64_t* out_sum_pos, void* stream) {
+  int32_t pad = 1;
+  pg_tc_bloom_pad(bits, &pad);
+  PG_REQUIRE(e_begin % pad == 0, "e_begin must be a multiple of the layout pad %d", pad);
+  return tc_bloom_impl(rows, bits, op, sizes, lut, us, vs, e_begin, e_end, out_hist, out_sum_pos, stream,
+                       pad > 1);
 }
 
 int pg_pairs_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int32_t* sizes,
@@ -1227,3 +1277,11 @@ int pg_4clique_exact(const int64_t* dir_off, const int32_t* dir_adj, const int32
 }
 
 }  // extern "C"
+
+extern "C" int pg_tc_bloom_pad(int32_t bits, int32_t* pad_host) {
+  PG_REQUIRE(pad_host, "null output");
+  PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
+  const int w8 = bits % 256 == 0 ? bits / 256 : 0;
+  *pad_host = (w8 == 2 || w8 == 4) ? w8 : (w8 == 8 ? 8 : 1);
+  return PG_OK;
+}

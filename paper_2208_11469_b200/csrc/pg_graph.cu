@@ -11,7 +11,8 @@ namespace pg {
 
 // first index of row u holding a neighbour > u, and the row's upper count
 __global__ void upper_count_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj,
-                                   int64_t n, int64_t* __restrict__ first, int64_t* __restrict__ cnt) {
+                                   int64_t n, int64_t* __restrict__ first, int64_t* __restrict__ cnt,
+                                   int64_t pad) {
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
        u += (int64_t)gridDim.x * blockDim.x) {
     int64_t lo = offsets[u], hi = offsets[u + 1];
@@ -22,23 +23,24 @@ __global__ void upper_count_kernel(const int64_t* __restrict__ offsets, const in
       else hi = mid;
     }
     first[u] = lo;
-    cnt[u] = end - lo;
+    cnt[u] = (end - lo + pad - 1) / pad * pad;  // slots of row u (rounded up to pad)
   }
 }
 
 __global__ void upper_fill_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj,
                                   int64_t n, const int64_t* __restrict__ first,
                                   const int64_t* __restrict__ start, int32_t* __restrict__ us,
-                                  int32_t* __restrict__ vs, int64_t cap) {
+                                  int32_t* __restrict__ vs, int64_t cap, int64_t pad) {
   const int lane = threadIdx.x & 31;
   const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
     const int64_t f = first[u], e = offsets[u + 1], s = start[u];
-    for (int64_t j = f + lane; j < e; j += 32) {
-      const int64_t o = s + (j - f);
+    const int64_t slots = (e - f + pad - 1) / pad * pad;
+    for (int64_t j = lane; j < slots; j += 32) {
+      const int64_t o = s + j;
       if (o < cap) {
         us[o] = (int32_t)u;
-        vs[o] = adj[j];
+        vs[o] = f + j < e ? adj[f + j] : -1;  // -1: padding slot
       }
     }
   }
@@ -112,9 +114,9 @@ int pg_csr_upper_edges_workspace(int64_t n, size_t* out_bytes_host) {
   return PG_OK;
 }
 
-int pg_csr_upper_edges(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t* us, int32_t* vs,
-                       int64_t capacity, int64_t* m_host, void* workspace, size_t workspace_bytes,
-                       void* stream) {
+static int upper_edges_impl(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t* us, int32_t* vs,
+                            int64_t capacity, int64_t* m_host, void* workspace, size_t workspace_bytes,
+                            void* stream, int64_t pad) {
   PG_REQUIRE(n >= 0, "n must be >= 0");
   PG_REQUIRE(offsets && workspace, "null pointer");
   size_t need = 0;
@@ -133,11 +135,11 @@ int pg_csr_upper_edges(const int64_t* offsets, const int32_t* adj, int64_t n, in
   void* temp = ws + 3 * arr;
   size_t temp_bytes = workspace_bytes - 3 * arr;
   const int grid = sm_count() * 8;
-  upper_count_kernel<<<grid, 256, 0, s>>>(offsets, adj, n, first, cnt);
+  upper_count_kernel<<<grid, 256, 0, s>>>(offsets, adj, n, first, cnt, pad);
   if (int rc = check_launch("upper_count")) return rc;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, cnt, start, n, s);
   if (e != cudaSuccess) return fail(PG_ERR_CUDA, "scan: %s", cudaGetErrorString(e));
-  upper_fill_kernel<<<grid, 256, 0, s>>>(offsets, adj, n, first, start, us, vs, capacity);
+  upper_fill_kernel<<<grid, 256, 0, s>>>(offsets, adj, n, first, start, us, vs, capacity, pad);
   if (int rc = check_launch("upper_fill")) return rc;
   if (m_host) {
     int64_t last_start = 0, last_cnt = 0;
@@ -148,10 +150,24 @@ int pg_csr_upper_edges(const int64_t* offsets, const int32_t* adj, int64_t n, in
     if (e != cudaSuccess) return fail(PG_ERR_CUDA, "upper edge count: %s", cudaGetErrorString(e));
     *m_host = last_start + last_cnt;
     if (*m_host > capacity)
-      return fail(PG_ERR_INVALID, "adjacency is not symmetric: %lld upper edges > capacity %lld",
+      return fail(PG_ERR_INVALID, "%lld upper edge slots exceed capacity %lld (asymmetric adjacency?)",
                   (long long)*m_host, (long long)capacity);
   }
   return PG_OK;
+}
+
+int pg_csr_upper_edges(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t* us, int32_t* vs,
+                       int64_t capacity, int64_t* m_host, void* workspace, size_t workspace_bytes,
+                       void* stream) {
+  return upper_edges_impl(offsets, adj, n, us, vs, capacity, m_host, workspace, workspace_bytes, stream, 1);
+}
+
+int pg_csr_upper_edges_padded(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t pad,
+                              int32_t* us, int32_t* vs, int64_t capacity, int64_t* slots_host,
+                              void* workspace, size_t workspace_bytes, void* stream) {
+  PG_REQUIRE(pad >= 1 && pad <= 32 && (pad & (pad - 1)) == 0, "pad must be a power of two <= 32");
+  return upper_edges_impl(offsets, adj, n, us, vs, capacity, slots_host, workspace, workspace_bytes, stream,
+                          pad);
 }
 
 int pg_csr_expand_rows(const int64_t* offsets, int64_t n, int64_t nnz, int32_t* src, void* stream) {

@@ -54,6 +54,7 @@ class DeviceCsr:
         self.degrees = (self.offsets[1:] - self.offsets[:-1]).to(torch.int32)
         self._upper = None
         self._src = None
+        self._layouts = {}
 
     def upper_edges(self):
         """(us, vs) int32 device arrays: every undirected edge once, u < v."""
@@ -74,6 +75,33 @@ class DeviceCsr:
                    N.ptr(ws), ws_bytes.value, N.stream_handle())
             self._upper = (us[:m.value], vs[:m.value])
         return self._upper
+
+    def upper_edges_padded(self, pad: int):
+        """Row-padded upper edge slots (pad >= 2): (us, vs, slots), vs = -1 on
+        padding slots; every aligned group of `pad` slots shares one u."""
+        if pad <= 1:
+            us, vs = self.upper_edges()
+            return us, vs, us.numel()
+        key = ("padded", pad)
+        if key not in self._layouts:
+            import ctypes
+            import torch
+            from . import _native as N
+            # upper bound on slots: m + (pad-1) per non-empty row
+            cap = self.nnz // 2 + (pad - 1) * self.n + 1
+            us = torch.empty(cap, dtype=torch.int32, device="cuda")
+            vs = torch.empty(cap, dtype=torch.int32, device="cuda")
+            ws_bytes = ctypes.c_size_t()
+            N.call("pg_csr_upper_edges_workspace", self.n, ctypes.byref(ws_bytes))
+            ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device="cuda")
+            slots = ctypes.c_int64()
+            N.call("pg_csr_upper_edges_padded", N.ptr(self.offsets), N.ptr(self.adj),
+                   self.n, pad, N.ptr(us), N.ptr(vs), cap, ctypes.byref(slots),
+                   N.ptr(ws), ws_bytes.value, N.stream_handle())
+            k = slots.value
+            self._layouts[key] = (us[:k].clone(), vs[:k].clone(), k)
+            del us, vs
+        return self._layouts[key]
 
     def row_sources(self):
         """int32 device array src[j] = row of adjacency entry j."""

@@ -75,14 +75,20 @@ def _tc_provider(graph: CsrGraph, sketched, kind):
     return make_provider(kind, sketched=sketched)
 
 
-def tc_counts(provider, us, vs, e_begin: int, e_end: int):
-    """Device integer (or fp64 for KMV) partials of edges [e_begin, e_end)."""
+def tc_counts(provider, dev, rank: int = 0, world: int = 1):
+    """Device partial statistics of this rank's share of the edge slots:
+    int64 histograms / per-match sums (fp64 sum for KMV), see _tc_combine."""
     import torch
+    from .sharding import edge_range
     if provider.is_exact:
-        part = provider._pairs_device(us[e_begin:e_end], vs[e_begin:e_end])
+        us, vs = dev.upper_edges()
+        b, e = edge_range(us.numel(), rank, world)
+        part = provider._pairs_device(us[b:e], vs[b:e])
         return part.sum().reshape(1) if part.numel() else torch.zeros(
             1, dtype=torch.int64, device="cuda")
-    return provider._tc_counts(us, vs, e_begin, e_end)
+    us, vs, slots, padded = provider._tc_layout(dev)
+    b, e = edge_range(slots, rank, world, align=32 if padded else 1)
+    return provider._tc_counts(us, vs, b, e, padded)
 
 
 def tc_combine(provider, counts: np.ndarray) -> float:
@@ -96,8 +102,7 @@ def tc_estimate(graph: CsrGraph, sketched: SketchedGraph | None = None,
                 kind=EstimatorKind.BF_AND, threads: int = 1) -> float:
     """(1/3) * sum over undirected edges of the intersection estimate."""
     provider = _tc_provider(graph, sketched, kind)
-    us, vs = graph.device().upper_edges()
-    counts = tc_counts(provider, us, vs, 0, us.numel()).cpu().numpy()
+    counts = tc_counts(provider, graph.device()).cpu().numpy()
     return tc_combine(provider, counts) / 3.0
 
 

@@ -137,6 +137,10 @@ class _SketchProvider(IntersectionProvider):
         self.sketched = sketched
         self.sizes = sketched.sizes
 
+    def _tc_layout(self, dev):
+        us, vs = dev.upper_edges()
+        return us, vs, us.numel(), False
+
     def _dev(self) -> dict:
         return self.sketched.device_tensors()
 
@@ -191,14 +195,31 @@ class BloomProvider(_SketchProvider):
         out = out[:du.numel()]
         return out if on_dev else out.cpu().numpy().astype(np.int64)
 
-    def _tc_counts(self, us, vs, e_begin: int, e_end: int):
+    def tc_pad(self) -> int:
+        """Group size of the fused kernel = pad of its edge-slot layout."""
+        import ctypes
+        pad = ctypes.c_int32()
+        N.check(N.load_library().pg_tc_bloom_pad(self.sketched.bit_length,
+                                                 ctypes.byref(pad)), "pg_tc_bloom_pad")
+        return pad.value
+
+    def _tc_layout(self, dev):
+        """(us, vs, slots, padded) edge-slot arrays the fused kernel consumes."""
+        pad = self.tc_pad()
+        if pad > 1:
+            us, vs, slots = dev.upper_edges_padded(pad)
+            return us, vs, slots, True
+        us, vs = dev.upper_edges()
+        return us, vs, us.numel(), False
+
+    def _tc_counts(self, us, vs, e_begin: int, e_end: int, padded: bool = False):
         import torch
         d, sg = self._dev(), self.sketched
         hist = torch.empty(sg.bit_length + 1, dtype=torch.int64, device="cuda")
         spos = torch.empty(1, dtype=torch.int64, device="cuda")
-        N.call("pg_tc_bloom", N.ptr(d["rows"]), sg.bit_length, self.op,
-               N.ptr(d["sizes"]), N.ptr(self.lut_device()), N.ptr(us),
-               N.ptr(vs), e_begin, e_end, N.ptr(hist), N.ptr(spos),
+        N.call("pg_tc_bloom_padded" if padded else "pg_tc_bloom", N.ptr(d["rows"]),
+               sg.bit_length, self.op, N.ptr(d["sizes"]), N.ptr(self.lut_device()),
+               N.ptr(us), N.ptr(vs), e_begin, e_end, N.ptr(hist), N.ptr(spos),
                N.stream_handle())
         return torch.cat([hist, spos])
 
@@ -273,7 +294,7 @@ class MinHashProvider(_SketchProvider):
         out = out[:du.numel()]
         return out if on_dev else out.cpu().numpy().astype(np.int64)
 
-    def _tc_counts(self, us, vs, e_begin: int, e_end: int):
+    def _tc_counts(self, us, vs, e_begin: int, e_end: int, padded: bool = False):
         import torch
         d, sg = self._dev(), self.sketched
         k = sg.capacity
@@ -340,7 +361,7 @@ class KmvProvider(_SketchProvider):
         return (com[:du.numel()].cpu().numpy().astype(np.int64),
                 uni[:du.numel()].cpu().numpy().astype(np.int64))
 
-    def _tc_counts(self, us, vs, e_begin: int, e_end: int):
+    def _tc_counts(self, us, vs, e_begin: int, e_end: int, padded: bool = False):
         import torch
         d, sg = self._dev(), self.sketched
         out = torch.empty(1, dtype=torch.float64, device="cuda")

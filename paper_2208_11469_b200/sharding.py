@@ -19,10 +19,15 @@ __all__ = ["edge_range", "weighted_edge_range", "allreduce_counts",
            "tc_estimate_sharded", "four_clique_count_sharded"]
 
 
-def edge_range(m: int, rank: int, world: int) -> tuple[int, int]:
-    """Contiguous, balanced [begin, end) share of m edges for ``rank``."""
+def edge_range(m: int, rank: int, world: int, align: int = 1) -> tuple[int, int]:
+    """Contiguous, balanced [begin, end) share of m edge slots for ``rank``;
+    interior boundaries are multiples of ``align`` (padded layouts)."""
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad rank/world")
+    if align > 1:
+        units = (m + align - 1) // align
+        b, e = edge_range(units, rank, world)
+        return min(b * align, m), min(e * align, m)
     base, extra = divmod(m, world)
     begin = rank * base + min(rank, extra)
     return begin, begin + base + (1 if rank < extra else 0)
@@ -54,9 +59,7 @@ def tc_estimate_sharded(graph, sketched=None, kind="bf_and", group=None):
     rank = dist.get_rank(group) if dist.is_initialized() else 0
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     provider = _tc_provider(graph, sketched, kind)
-    us, vs = graph.device().upper_edges()
-    b, e = edge_range(us.numel(), rank, world)
-    counts = allreduce_counts(tc_counts(provider, us, vs, b, e), group)
+    counts = allreduce_counts(tc_counts(provider, graph.device(), rank, world), group)
     return tc_combine(provider, counts.cpu().numpy()) / 3.0
 
 

@@ -20,7 +20,8 @@ else:
 sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=2, bits_override=bits)
 p = pg.make_provider("bf_and", sketched=sk)
 us, vs = g.device().upper_edges()
+lus, lvs, slots, padded = p._tc_layout(g.device())
 for _ in range(4):
-    out = p._tc_counts(us, vs, 0, us.numel())
+    out = p._tc_counts(lus, lvs, 0, slots, padded)
 torch.cuda.synchronize()
 print("tc", p._tc_combine(out.cpu().numpy()) / 3.0)

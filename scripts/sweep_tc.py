@@ -37,16 +37,17 @@ else:
 sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=args.b, bits_override=args.bits)
 p = pg.make_provider(args.kind, sketched=sk)
 us, vs = g.device().upper_edges()
+lus, lvs, slots, padded = p._tc_layout(g.device())
 m = us.numel()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-ref = p._tc_counts(us, vs, 0, m).cpu().numpy()
+ref = p._tc_counts(lus, lvs, 0, slots, padded).cpu().numpy()
 times = []
 st = torch.cuda.current_stream()
 for i in range(args.reps + 3):
     N.call("pg_l2_flush", N.ptr(flush), flush.numel(), N.stream_handle())
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(st)
-    out = p._tc_counts(us, vs, 0, m)
+    out = p._tc_counts(lus, lvs, 0, slots, padded)
     b.record(st)
     torch.cuda.synchronize()
     if i >= 3:

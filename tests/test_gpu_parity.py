@@ -162,9 +162,14 @@ def test_config2_full_parity(pg):
     sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=2, bits_override=1024)
     assert sha(sk.bit_matrix.astype("<u8")) == rec["bit_matrix"]
     assert sha(sk.ones.astype("<i8")) == rec["ones"]
-    us, vs = g.device().upper_edges()
     p = pg.make_provider("bf_and", sketched=sk)
-    counts = p._tc_counts(us, vs, 0, us.numel()).cpu().numpy()
+    from paper_2208_11469_b200.mining import tc_counts
+    counts = tc_counts(p, g.device()).cpu().numpy()
     assert counts[:-1].tolist() == rec["and_popcount_hist"]
+    # the general (unpadded) layout and any shard split give the same integers
+    us, vs = g.device().upper_edges()
+    assert p._tc_counts(us, vs, 0, us.numel()).cpu().numpy().tolist() == counts.tolist()
+    parts = sum(tc_counts(p, g.device(), r, 3).cpu().numpy() for r in range(3))
+    assert parts.tolist() == counts.tolist()
     for kind, want in rec["tc"].items():
         assert pg.tc_estimate(g, sk, kind) == pytest.approx(want, rel=RTOL_SUM)
