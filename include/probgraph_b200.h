@@ -83,14 +83,15 @@ PG_API int pg_csr_upper_edges(const int64_t* offsets, const int32_t* adj, int64_
 /* Same edge list with every CSR row's run of upper edges padded to a
  * multiple of `pad` (power of two <= 32) with (u, -1) slots, so groups of
  * `pad` consecutive slots never straddle two u rows -- the layout the fused
- * Bloom TC kernel consumes (pad = its lanes-per-edge group size, see
- * pg_tc_bloom_pad).  slots_host receives the slot count (host sync). */
+ * row kernels consume (pad = their lanes-per-edge group size, see
+ * pg_group_pad).  slots_host receives the slot count (host sync). */
 PG_API int pg_csr_upper_edges_padded(const int64_t* offsets, const int32_t* adj, int64_t n,
                               int32_t pad, int32_t* us, int32_t* vs, int64_t capacity,
                               int64_t* slots_host, void* workspace, size_t workspace_bytes,
                               void* stream);
-/* group size the fused Bloom TC kernel uses for `bits` (pad for the above) */
-PG_API int pg_tc_bloom_pad(int32_t bits, int32_t* pad_host);
+/* lanes-per-edge group size of the fused kernels for rows of `row_bytes`
+ * (Bloom: bits/8, k-Hash: 4k) = the pad of the layout above (1: no pad) */
+PG_API int pg_group_pad(int32_t row_bytes, int32_t* pad_host);
 /* src[j] = row of adjacency entry j (np.repeat(arange(n), degrees)) */
 PG_API int pg_csr_expand_rows(const int64_t* offsets, int64_t n, int64_t nnz,
                        int32_t* src, void* stream);
@@ -135,29 +136,26 @@ PG_API int pg_pairs_kmv(const double* values, const int32_t* lengths, int32_t k,
 
 /* ---- (2)+(3) fused whole-graph passes over edges [e_begin, e_end) -------
  *      mining.py:105-130 tc_estimate, :63-80 _chunked_sum                */
-/* Bloom TC.  Edge slots with vs[j] < 0 are padding and skipped.
+/* Fused passes take `padded`: 0 = any (us, vs) edge list, 1 = the
+ * row-padded layout of pg_csr_upper_edges_padded with pad =
+ * pg_group_pad(row bytes) and e_begin a multiple of pad (precondition, not
+ * checked: every aligned group of pad slots holds one u).  Slots with
+ * vs[j] < 0 are padding and skipped.
+ * Bloom TC.
  * out_hist: int64[bits+1] histogram of per-edge popcounts
  * (for PG_BF_OR only edges with raw > 0 are counted, and out_sum_pos
  * receives the int64 sum of (s_u+s_v) over those edges).  Overwrites
  * the outputs.  Final estimate is formed on the host from the integers. */
 PG_API int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op,
                 const int32_t* sizes, const double* lut, const int32_t* us,
-                const int32_t* vs, int64_t e_begin, int64_t e_end,
-                int64_t* out_hist, int64_t* out_sum_pos, void* stream);
-/* Same as pg_tc_bloom over the row-padded layout of
- * pg_csr_upper_edges_padded(pad = pg_tc_bloom_pad(bits)); e_begin must be a
- * multiple of pad.  Precondition (not checked): every aligned group of pad
- * slots holds one u.  Lets the kernel keep one u row per lane group. */
-PG_API int pg_tc_bloom_padded(const uint64_t* rows, int32_t bits, int32_t op,
-                const int32_t* sizes, const double* lut, const int32_t* us,
-                const int32_t* vs, int64_t e_begin, int64_t e_end,
+                const int32_t* vs, int64_t e_begin, int64_t e_end, int32_t padded,
                 int64_t* out_hist, int64_t* out_sum_pos, void* stream);
 /* k-/1-Hash TC: out_cnt[m], out_ssum[m] (m = 0..k): number of edges and
  * int64 sum of (s_u+s_v) of non-verbatim edges with m matches;
  * out_verbatim[0] = sum of matches over verbatim 1-Hash edges. */
 PG_API int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash,
                   const int32_t* sizes, const int32_t* us, const int32_t* vs,
-                  int64_t e_begin, int64_t e_end, int64_t* out_cnt,
+                  int64_t e_begin, int64_t e_end, int32_t padded, int64_t* out_cnt,
                   int64_t* out_ssum, int64_t* out_verbatim, void* stream);
 /* KMV TC: out_sum[0] = sum of per-edge estimates (fixed-order fp64) */
 PG_API int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k,
@@ -171,7 +169,7 @@ PG_API int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k,
 PG_API int pg_jaccard_count_khash(const int32_t* entries, int32_t k,
                            const int32_t* degrees, const int32_t* us,
                            const int32_t* vs, int64_t e_begin, int64_t e_end,
-                           int32_t min_matches, double tau,
+                           int32_t padded, int32_t min_matches, double tau,
                            int64_t* out_counts, void* stream);
 /* 4-clique, Bloom over N+ (mining.py:133-154 + providers.py:164-175):
  * for each directed edge j in [e_begin,e_end) with src[j]=u, dir_adj[j]=v:

@@ -42,7 +42,7 @@ SIGNATURES = {
     "pg_csr_upper_edges_padded": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr,
                                   c_i64, ctypes.POINTER(c_i64), c_ptr, c_size,
                                   c_ptr],
-    "pg_tc_bloom_pad": [c_i32, ctypes.POINTER(c_i32)],
+    "pg_group_pad": [c_i32, ctypes.POINTER(c_i32)],
     "pg_csr_expand_rows": [c_ptr, c_i64, c_i64, c_ptr, c_ptr],
     "pg_build_bloom": [c_ptr, c_ptr, c_i64, c_i32, c_i32, c_ptr, c_ptr, c_ptr,
                        c_ptr],
@@ -57,15 +57,13 @@ SIGNATURES = {
     "pg_pairs_kmv": [c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64, c_ptr,
                      c_ptr, c_ptr, c_ptr, c_ptr],
     "pg_tc_bloom": [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_i64,
-                    c_i64, c_ptr, c_ptr, c_ptr],
-    "pg_tc_bloom_padded": [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr,
-                           c_i64, c_i64, c_ptr, c_ptr, c_ptr],
+                    c_i64, c_i32, c_ptr, c_ptr, c_ptr],
     "pg_tc_minhash": [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_i64, c_i64,
-                      c_ptr, c_ptr, c_ptr, c_ptr],
+                      c_i32, c_ptr, c_ptr, c_ptr, c_ptr],
     "pg_tc_kmv": [c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64, c_i64,
                   c_ptr, c_ptr],
     "pg_jaccard_count_khash": [c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
-                               c_i64, c_i32, c_dbl, c_ptr, c_ptr],
+                               c_i64, c_i32, c_i32, c_dbl, c_ptr, c_ptr],
     "pg_4clique_bloom": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i32,
                          c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr,
                          c_ptr, c_ptr],
@@ -143,6 +141,13 @@ def ptr(t) -> int | None:
     if t is None:
         return None
     return t.data_ptr()
+
+
+def group_pad(row_bytes: int) -> int:
+    """Lane-group size of the fused row kernels = pad of their slot layout."""
+    pad = ctypes.c_int32()
+    check(load_library().pg_group_pad(int(row_bytes), ctypes.byref(pad)), "pg_group_pad")
+    return pad.value
 
 
 def stream_handle(stream=None) -> int:

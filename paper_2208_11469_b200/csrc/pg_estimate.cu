@@ -23,6 +23,7 @@
 // runs reproduce the single-GPU result bit for bit; only KMV sums doubles.
 #include <algorithm>
 #include <cstdlib>
+#include <type_traits>
 
 #include "pg_common.cuh"
 
@@ -129,7 +130,7 @@ __device__ __forceinline__ void group_edge_loop(const uint4* __restrict__ rows, 
 #pragma unroll 1
   for (int64_t e0 = wb; e0 < we; e0 += 32) {
     const int64_t e = e0 + lane;
-    const bool valid = e < we;
+    const bool valid = e < we && vl >= 0;  // v < 0: padding slot
     // prefetch the next iteration's edge indices
     int32_t un = 0, vn = 0;
     if (e + 32 < we) {
@@ -140,7 +141,7 @@ __device__ __forceinline__ void group_edge_loop(const uint4* __restrict__ rows, 
 #pragma unroll
     for (int j = 0; j < G; ++j) {
       const int32_t vj = __shfl_sync(0xffffffffu, vl, gbase + j);
-      const uint4* rv = rows + (int64_t)vj * W4 + gl;
+      const uint4* rv = rows + (int64_t)(vj < 0 ? 0 : vj) * W4 + gl;
 #pragma unroll
       for (int i = 0; i < V; ++i) vr[j][i] = kVCache ? ldg_keep(rv + i * G) : ldg_stream(rv + i * G);
     }
@@ -275,6 +276,244 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
   }
 }
 
+// ------------------------------------------------ sorted-row group engine
+// 1-Hash (ascending int32 IDs, -1 pad) and KMV (ascending doubles as uint64
+// bits, +inf pad) rows of k = 8*G*CH elements.  G lanes per edge (32/G edges
+// per warp iteration); lane gl holds the CH chunks c = s*G + gl of 8
+// consecutive elements, loaded with 256-bit loads.  A membership / rank
+// query for x against a row uses (1) the broadcast heads of all k/8 chunks
+// held in registers to pick the chunk, then (2) a 4-probe lower_bound inside
+// that 8-element chunk, read from the row's shared-memory copy.
+template <class T>
+struct SortedTraits;
+template <>
+struct SortedTraits<int32_t> {
+  static constexpr int kLoads = 1;  // 256-bit loads per 8-element chunk
+  __device__ static int32_t pad() { return 0x7fffffff; }
+  __device__ static int32_t fix(int32_t x) { return x < 0 ? 0x7fffffff : x; }  // -1 pad sorts last
+  __device__ static bool valid(int32_t x) { return x != 0x7fffffff; }
+};
+template <>
+struct SortedTraits<uint64_t> {
+  static constexpr int kLoads = 2;
+  __device__ static uint64_t pad() { return kInfBits; }
+  __device__ static uint64_t fix(uint64_t x) { return x; }
+  __device__ static bool valid(uint64_t x) { return x < kInfBits; }
+};
+
+template <class T, int CH, bool kKeep>
+__device__ __forceinline__ void load_sorted_chunks(const T* row, int G, int gl, T (&c)[CH][8]) {
+#pragma unroll
+  for (int s = 0; s < CH; ++s) {
+    const T* p = row + (s * G + gl) * 8;
+    uint32_t r[8];
+#pragma unroll
+    for (int h = 0; h < SortedTraits<T>::kLoads; ++h) {
+      if (kKeep) ldg256_keep(reinterpret_cast<const unsigned char*>(p) + 32 * h, r);
+      else ldg256(reinterpret_cast<const unsigned char*>(p) + 32 * h, r);
+      if (sizeof(T) == 4) {
+#pragma unroll
+        for (int w = 0; w < 8; ++w) c[s][w] = SortedTraits<T>::fix((T)r[w]);
+      } else {
+#pragma unroll
+        for (int w = 0; w < 4; ++w)
+          c[s][4 * h + w] = (T)(((uint64_t)r[2 * w + 1] << 32) | r[2 * w]);
+      }
+    }
+  }
+}
+
+// lower_bound of x in a row: heads[i] = first element of chunk i (NC chunks),
+// srow = the row in element order (shared memory).  lt = #elements < x.
+template <class T, int NC>
+__device__ __forceinline__ int sorted_lower_bound(T x, const T (&heads)[NC], const T* srow, bool& found) {
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < NC; ++i) c += heads[i] <= x;
+  if (c == 0) {
+    found = false;
+    return 0;
+  }
+  const T* ch = srow + (c - 1) * 8;
+  int p = 0;
+  if (ch[3] < x) p = 4;
+  if (ch[p + 1] < x) p += 2;
+  if (ch[p] < x) p += 1;
+  if (p < 8 && ch[p] < x) p += 1;
+  found = p < 8 && ch[p] == x;
+  return (c - 1) * 8 + p;
+}
+
+struct SortedStats {
+  int common, lu, lv;
+  double kth;
+};
+
+// G-lane group sums / exclusive scans (groups are aligned lane ranges)
+template <int G>
+__device__ __forceinline__ int group_sum(int x) {
+#pragma unroll
+  for (int o = G / 2; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+template <int G>
+__device__ __forceinline__ int group_excl_scan(int x, int gl) {
+  int inc = x;
+#pragma unroll
+  for (int o = 1; o < G; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, inc, o);
+    if (gl >= o) inc += y;
+  }
+  return inc - x;
+}
+
+template <int G, int CH, bool kKmv, class Epi>
+__device__ __forceinline__ void sorted_edge_loop(const void* __restrict__ rows, int k,
+                                                 const int32_t* __restrict__ us,
+                                                 const int32_t* __restrict__ vs, int64_t e_begin,
+                                                 int64_t e_end, unsigned char* warp_smem, Epi& epi) {
+  using T = typename std::conditional<kKmv, uint64_t, int32_t>::type;
+  using TR = SortedTraits<T>;
+  constexpr int NC = G * CH;  // chunks per row (k / 8)
+  constexpr int E = 32 / G;   // edges per warp iteration
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int gbase = lane & ~(G - 1);
+  const int grp = lane / G;
+  const T* R = reinterpret_cast<const T*>(rows);
+  T* sv = reinterpret_cast<T*>(warp_smem) + grp * (kKmv ? 2 : 1) * NC * 8;
+  T* su = sv + NC * 8;  // KMV only
+  int64_t wb, we;
+  warp_slice(e_begin, e_end, wb, we);
+  if (wb >= we) return;
+  int32_t ul = 0, vl = 0;
+  if (wb + grp < we) {
+    ul = us[wb + grp];
+    vl = vs[wb + grp];
+  }
+#pragma unroll 1
+  for (int64_t e0 = wb; e0 < we; e0 += E) {
+    const int64_t e = e0 + grp;
+    const bool valid = e < we;
+    int32_t un = 0, vn = 0;
+    if (e + E < we) {
+      un = us[e + E];
+      vn = vs[e + E];
+    }
+    T a[CH][8], b[CH][8];
+    load_sorted_chunks<T, CH, true>(R + (int64_t)ul * k, G, gl, a);
+    load_sorted_chunks<T, CH, false>(R + (int64_t)vl * k, G, gl, b);
+    int la = 0, lb = 0;
+#pragma unroll
+    for (int s = 0; s < CH; ++s) {
+      const int c = s * G + gl;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        sv[c * 8 + w] = b[s][w];
+        if constexpr (kKmv) su[c * 8 + w] = a[s][w];
+        la += TR::valid(a[s][w]);
+        lb += TR::valid(b[s][w]);
+      }
+    }
+    la = group_sum<G>(la);
+    lb = group_sum<G>(lb);
+    T hb[NC], ha[NC];
+#pragma unroll
+    for (int i = 0; i < NC; ++i) {
+      hb[i] = __shfl_sync(0xffffffffu, b[i / G][0], gbase + i % G);
+      if constexpr (kKmv) ha[i] = __shfl_sync(0xffffffffu, a[i / G][0], gbase + i % G);
+    }
+    __syncwarp();
+    // U elements against V: membership (and lower_bound for KMV ranks)
+    int ltb[CH][8];
+    bool inb[CH][8];
+    int found = 0;
+#pragma unroll
+    for (int s = 0; s < CH; ++s)
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        bool f = false;
+        int lt = 0;
+        if (TR::valid(a[s][w])) lt = sorted_lower_bound<T, NC>(a[s][w], hb, sv, f);
+        ltb[s][w] = lt;
+        inb[s][w] = f;
+        found += f;
+      }
+    SortedStats st;
+    st.common = group_sum<G>(found);
+    st.lu = la;
+    st.lv = lb;
+    st.kth = 0.0;
+    if constexpr (kKmv) {
+      const int T_ = max(min(la, lb), 1);
+      T cand = TR::pad();
+      bool have = false;
+      // ranks of U elements: idx + 1 + lt_V - (#common among U[0..idx-1])
+      int carry = 0;
+#pragma unroll
+      for (int s = 0; s < CH; ++s) {
+        int cnt = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) cnt += inb[s][w];
+        const int before = carry + group_excl_scan<G>(cnt, gl);
+        carry += group_sum<G>(cnt);
+        int run = 0;
+        const int c = s * G + gl;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const int idx = c * 8 + w;
+          if (TR::valid(a[s][w]) && idx + 1 + ltb[s][w] - (before + run) == T_) {
+            cand = a[s][w];
+            have = true;
+          }
+          run += inb[s][w];
+        }
+      }
+      // V elements not in U: idx + 1 + lt_U - (#common among V[0..idx-1])
+      carry = 0;
+#pragma unroll
+      for (int s = 0; s < CH; ++s) {
+        int ltu[8];
+        bool inu[8];
+        int cnt = 0;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          bool f = false;
+          int lt = 0;
+          if (TR::valid(b[s][w])) lt = sorted_lower_bound<T, NC>(b[s][w], ha, su, f);
+          ltu[w] = lt;
+          inu[w] = f;
+          cnt += f;
+        }
+        const int before = carry + group_excl_scan<G>(cnt, gl);
+        carry += group_sum<G>(cnt);
+        int run = 0;
+        const int c = s * G + gl;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const int idx = c * 8 + w;
+          if (TR::valid(b[s][w]) && !inu[w] && idx + 1 + ltu[w] - (before + run) == T_) {
+            cand = b[s][w];
+            have = true;
+          }
+          run += inu[w];
+        }
+      }
+      // the unique rank-T element, else merged[0] (reference argmax of all-False)
+      const unsigned gmask = ((G == 32) ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
+      const unsigned hm = __ballot_sync(0xffffffffu, have) & gmask;
+      // shuffles are executed by every lane (hm differs between groups)
+      const uint64_t c1 = shfl64((uint64_t)cand, hm ? __ffs(hm) - 1 : gbase);
+      const uint64_t a0 = shfl64((uint64_t)a[0][0], gbase), b0 = shfl64((uint64_t)b[0][0], gbase);
+      st.kth = bitsd(hm ? c1 : (a0 < b0 ? a0 : b0));
+    }
+    if (valid && gl == 0) epi.edge(e, ul, vl, st);
+    __syncwarp();
+    ul = un;
+    vl = vn;
+  }
+}
+
 // Generic fallback: one lane per edge, 64-bit words (any multiple of 64 bits,
 // or any k for k-Hash).
 template <class Epi>
@@ -284,6 +523,7 @@ __device__ void scalar_edge_loop_bloom(const uint64_t* __restrict__ rows, int wo
   for (int64_t e = e_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e_end;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t u = us[e], v = vs[e];
+    if (v < 0) continue;  // padding slot
     const uint64_t* ru = rows + (int64_t)u * words;
     const uint64_t* rv = rows + (int64_t)v * words;
     int c = 0;
@@ -301,6 +541,7 @@ __device__ void scalar_edge_loop_khash(const int32_t* __restrict__ ent, int k, c
   for (int64_t e = e_begin + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < e_end;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int32_t u = us[e], v = vs[e];
+    if (v < 0) continue;  // padding slot
     const int32_t* a = ent + (int64_t)u * k;
     const int32_t* b = ent + (int64_t)v * k;
     int c = 0;
@@ -368,14 +609,25 @@ struct EpiMinhashPairs {
   }
 };
 
+// exact 64-bit per-bin sums in shared memory from native 32-bit atomics:
+// lo accumulates mod 2^32, hi counts the wrap-arounds (a CAS-free
+// replacement for 64-bit shared atomics, which compile to a spin loop)
+__device__ __forceinline__ void smem_add64(unsigned* lo, unsigned* hi, uint64_t x) {
+  const unsigned xl = (unsigned)x;
+  const unsigned old = atomicAdd(lo, xl);
+  unsigned carry = (unsigned)(x >> 32) + (old > 0xFFFFFFFFu - xl ? 1u : 0u);
+  if (carry) atomicAdd(hi, carry);
+}
+
 // per match count m: number of edges and sum of (s_u+s_v)
 struct EpiMinhashHist {
   const int32_t* sizes;
   int* cnt_s;
-  unsigned long long* ssum_s;
+  unsigned* slo_s;
+  unsigned* shi_s;
   __device__ __forceinline__ void edge(int64_t, int32_t u, int32_t v, int m) {
     atomicAdd(cnt_s + m, 1);
-    atomicAdd(ssum_s + m, (unsigned long long)((int64_t)sizes[u] + sizes[v]));
+    smem_add64(slo_s + m, shi_s + m, (uint64_t)((int64_t)sizes[u] + sizes[v]));
   }
 };
 
@@ -468,39 +720,45 @@ __global__ void __launch_bounds__(kBlock) pairs_khash_kernel(const uint4* ent, i
   else group_edge_loop<V, G, OpEqPos>(ent, us, vs, 0, count, epi);
 }
 
-template <int V, int G, bool kScalar>
-__global__ void __launch_bounds__(kBlock) tc_khash_kernel(const uint4* ent, int k, const int32_t* sizes,
-                                                         const int32_t* us, const int32_t* vs,
-                                                         int64_t e_begin, int64_t e_end, int64_t* out_cnt,
-                                                         int64_t* out_ssum) {
+// kEngine: 0 scalar fallback, 1 group (128-bit) engine, 2 wide padded engine
+template <int V, int G, int kEngine, int MINB = 1>
+__global__ void __launch_bounds__(kBlock, MINB) tc_khash_kernel(const uint4* ent, int k, const int32_t* sizes,
+                                                               const int32_t* us, const int32_t* vs,
+                                                               int64_t e_begin, int64_t e_end,
+                                                               int64_t* out_cnt, int64_t* out_ssum) {
   __shared__ int cnt_s[kMaxSketchK + 1];
-  __shared__ unsigned long long ssum_s[kMaxSketchK + 1];
-  for (int i = threadIdx.x; i <= k; i += blockDim.x) { cnt_s[i] = 0; ssum_s[i] = 0; }
+  __shared__ unsigned slo_s[kMaxSketchK + 1], shi_s[kMaxSketchK + 1];
+  for (int i = threadIdx.x; i <= k; i += blockDim.x) { cnt_s[i] = 0; slo_s[i] = 0; shi_s[i] = 0; }
   __syncthreads();
-  EpiMinhashHist epi{sizes, cnt_s, ssum_s};
-  if (kScalar) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
-  else group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
+  EpiMinhashHist epi{sizes, cnt_s, slo_s, shi_s};
+  if (kEngine == 0) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
+  else if (kEngine == 1) group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
+  else wide_edge_loop<V, OpEqPos, EpiMinhashHist, false, true>(reinterpret_cast<const unsigned char*>(ent), us,
+                                                                vs, e_begin, e_end, epi);
   __syncthreads();
   for (int i = threadIdx.x; i <= k; i += blockDim.x) {
     if (cnt_s[i]) {
       atomicAdd(reinterpret_cast<unsigned long long*>(out_cnt + i), (unsigned long long)cnt_s[i]);
-      atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i), ssum_s[i]);
+      atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i),
+                ((unsigned long long)shi_s[i] << 32) + slo_s[i]);
     }
   }
 }
 
-template <int V, int G, bool kScalar>
-__global__ void __launch_bounds__(kBlock) jaccard_khash_kernel(const uint4* ent, int k, const int32_t* deg,
-                                                              const int32_t* us, const int32_t* vs,
-                                                              int64_t e_begin, int64_t e_end,
-                                                              int min_matches, double tau,
-                                                              int64_t* out_counts) {
+template <int V, int G, int kEngine, int MINB = 1>
+__global__ void __launch_bounds__(kBlock, MINB) jaccard_khash_kernel(const uint4* ent, int k, const int32_t* deg,
+                                                                    const int32_t* us, const int32_t* vs,
+                                                                    int64_t e_begin, int64_t e_end,
+                                                                    int min_matches, double tau,
+                                                                    int64_t* out_counts) {
   __shared__ int hist_s[kMaxSketchK + 1];
   for (int i = threadIdx.x; i <= k; i += blockDim.x) hist_s[i] = 0;
   __syncthreads();
   EpiJaccard epi{k, min_matches, tau, deg, hist_s, 0, 0};
-  if (kScalar) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
-  else group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
+  if (kEngine == 0) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
+  else if (kEngine == 1) group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
+  else wide_edge_loop<V, OpEqPos, EpiJaccard, false, true>(reinterpret_cast<const unsigned char*>(ent), us, vs,
+                                                            e_begin, e_end, epi);
   __syncthreads();
   for (int i = threadIdx.x; i <= k; i += blockDim.x)
     if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_counts + 2 + i), (unsigned long long)hist_s[i]);
@@ -581,9 +839,9 @@ __global__ void __launch_bounds__(kBlock) onehash_kernel(const int32_t* ent, int
                                                         int64_t* out_verbatim) {
   __shared__ int32_t vbuf[kBlock / 32][32 * P];
   __shared__ int cnt_s[kMaxSketchK + 1];
-  __shared__ unsigned long long ssum_s[kMaxSketchK + 1];
+  __shared__ unsigned slo_s[kMaxSketchK + 1], shi_s[kMaxSketchK + 1];
   if (kFused) {
-    for (int i = threadIdx.x; i <= k; i += blockDim.x) { cnt_s[i] = 0; ssum_s[i] = 0; }
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) { cnt_s[i] = 0; slo_s[i] = 0; shi_s[i] = 0; }
     __syncthreads();
   }
   const int lane = threadIdx.x & 31;
@@ -601,7 +859,7 @@ __global__ void __launch_bounds__(kBlock) onehash_kernel(const int32_t* ent, int
         if (verbatim) verb += m;
         else {
           atomicAdd(cnt_s + m, 1);
-          atomicAdd(ssum_s + m, (unsigned long long)((int64_t)su + sv));
+          smem_add64(slo_s + m, shi_s + m, (uint64_t)((int64_t)su + sv));
         }
       } else {
         if (out_count) out_count[e] = m;
@@ -614,7 +872,8 @@ __global__ void __launch_bounds__(kBlock) onehash_kernel(const int32_t* ent, int
     for (int i = threadIdx.x; i <= k; i += blockDim.x) {
       if (cnt_s[i]) {
         atomicAdd(reinterpret_cast<unsigned long long*>(out_cnt + i), (unsigned long long)cnt_s[i]);
-        atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i), ssum_s[i]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i),
+                  ((unsigned long long)shi_s[i] << 32) + slo_s[i]);
       }
     }
     if (lane == 0 && verb) atomicAdd(reinterpret_cast<unsigned long long*>(out_verbatim), (unsigned long long)verb);
@@ -692,10 +951,9 @@ __device__ __forceinline__ KmvEdge kmv_edge(const uint64_t* __restrict__ vals, i
     before_v += __popc(bv);
   }
   const unsigned hm = __ballot_sync(0xffffffffu, have);
-  uint64_t kth_bits;
-  if (hm) kth_bits = shfl64(found, __ffs(hm) - 1);
-  else kth_bits = min(shfl64(a[0], 0), shfl64(b[0], 0));  // argmax of all-False -> merged[0]
-  r.kth = bitsd(kth_bits);
+  const uint64_t c1 = shfl64(found, hm ? __ffs(hm) - 1 : 0);
+  const uint64_t a0 = shfl64(a[0], 0), b0 = shfl64(b[0], 0);
+  r.kth = bitsd(hm ? c1 : min(a0, b0));  // no rank-T element: argmax of all-False -> merged[0]
   __syncwarp();
   return r;
 }
@@ -738,6 +996,122 @@ __global__ void __launch_bounds__(kBlock) kmv_kernel(const uint64_t* vals, int k
   }
   if (kFused) {
     if (lane == 0) red[w] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int i = 0; i < kBlock / 32; ++i) t = __dadd_rn(t, red[i]);
+      if (t != 0.0) atomicAdd(out_sum, t);
+    }
+  }
+}
+
+// ----------------------------------------- sorted-engine epilogues/kernels
+struct EpiOnehash {
+  int k;
+  const int32_t* sizes;
+  int32_t* out_count;  // pairs mode
+  double* out_est;
+  int* cnt_s;          // fused mode
+  unsigned* slo_s;
+  unsigned* shi_s;
+  long long verb;
+  __device__ __forceinline__ void edge(int64_t e, int32_t u, int32_t v, const SortedStats& st) {
+    const int m = st.common;
+    const int32_t su = sizes[u], sv = sizes[v];
+    const bool verbatim = su <= k && sv <= k;
+    if (cnt_s) {
+      if (verbatim) verb += m;
+      else {
+        atomicAdd(cnt_s + m, 1);
+        smem_add64(slo_s + m, shi_s + m, (uint64_t)((int64_t)su + sv));
+      }
+    } else {
+      if (out_count) out_count[e] = m;
+      if (out_est) out_est[e] = verbatim ? (double)m : minhash_estimate(m, k, su, sv);
+    }
+  }
+};
+
+struct EpiKmv {
+  int k;
+  const int32_t* sizes;
+  int32_t* out_common;
+  int32_t* out_union;
+  double* out_kth;
+  double* out_est;
+  bool fused;
+  double acc;
+  __device__ __forceinline__ void edge(int64_t e, int32_t u, int32_t v, const SortedStats& st) {
+    KmvEdge r;
+    r.common = st.common;
+    r.uni = st.lu + st.lv - st.common;
+    r.k_eff = min(st.lu, st.lv);
+    r.kth = st.kth;
+    const double est = kmv_estimate(r, k, sizes[u], sizes[v]);
+    if (fused) {
+      acc = __dadd_rn(acc, est);
+    } else {
+      if (out_common) out_common[e] = r.common;
+      if (out_union) out_union[e] = r.uni;
+      if (out_kth) out_kth[e] = r.kth;
+      if (out_est) out_est[e] = est;
+    }
+  }
+};
+
+template <int G, int CH, bool kKmv>
+__host__ __device__ constexpr int sorted_warp_smem() {
+  return (32 / G) * (kKmv ? 2 : 1) * G * CH * 8 * (kKmv ? 8 : 4);
+}
+
+template <int G, int CH, bool kFused>
+__global__ void __launch_bounds__(kBlock) onehash_sorted_kernel(const int32_t* ent, int k, const int32_t* sizes,
+                                                               const int32_t* us, const int32_t* vs,
+                                                               int64_t e_begin, int64_t e_end,
+                                                               int32_t* out_count, double* out_est,
+                                                               int64_t* out_cnt, int64_t* out_ssum,
+                                                               int64_t* out_verbatim) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int cnt_s[kMaxSketchK + 1];
+  __shared__ unsigned slo_s[kMaxSketchK + 1], shi_s[kMaxSketchK + 1];
+  if (kFused) {
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) { cnt_s[i] = 0; slo_s[i] = 0; shi_s[i] = 0; }
+    __syncthreads();
+  }
+  EpiOnehash epi{k, sizes, out_count, out_est, kFused ? cnt_s : nullptr, slo_s, shi_s, 0};
+  sorted_edge_loop<G, CH, false>(ent, k, us, vs, e_begin, e_end,
+                                 smem_raw + (threadIdx.x >> 5) * sorted_warp_smem<G, CH, false>(), epi);
+  if (kFused) {
+    __syncthreads();
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+      if (cnt_s[i]) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_cnt + i), (unsigned long long)cnt_s[i]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i),
+                  ((unsigned long long)shi_s[i] << 32) + slo_s[i]);
+      }
+    }
+    long long vb = epi.verb;
+    for (int o = 16; o > 0; o >>= 1) vb += __shfl_xor_sync(0xffffffffu, vb, o);
+    if ((threadIdx.x & 31) == 0 && vb)
+      atomicAdd(reinterpret_cast<unsigned long long*>(out_verbatim), (unsigned long long)vb);
+  }
+}
+
+template <int G, bool kFused>
+__global__ void __launch_bounds__(kBlock) kmv_sorted_kernel(const uint64_t* vals, int k, const int32_t* sizes,
+                                                           const int32_t* us, const int32_t* vs,
+                                                           int64_t e_begin, int64_t e_end, int32_t* out_common,
+                                                           int32_t* out_union, double* out_kth,
+                                                           double* out_est, double* out_sum) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[kBlock / 32];
+  EpiKmv epi{k, sizes, out_common, out_union, out_kth, out_est, kFused, 0.0};
+  sorted_edge_loop<G, 1, true>(vals, k, us, vs, e_begin, e_end,
+                               smem_raw + (threadIdx.x >> 5) * sorted_warp_smem<G, 1, true>(), epi);
+  if (kFused) {
+    double a = epi.acc;
+    for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0.0;
@@ -930,6 +1304,66 @@ static int grid_cap(int grid, int64_t items, int per_block) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(grid, need));
 }
 
+// sorted-engine launchers; return false when k has no specialisation
+template <int G, int CH, bool kFused>
+static void launch_onehash_sorted(cudaStream_t s, const int32_t* ent, int k, const int32_t* sizes,
+                                  const int32_t* us, const int32_t* vs, int64_t b, int64_t e,
+                                  int32_t* out_count, double* out_est, int64_t* out_cnt,
+                                  int64_t* out_ssum, int64_t* out_verbatim) {
+  auto kern = onehash_sorted_kernel<G, CH, kFused>;
+  const size_t sm = (size_t)(kBlock / 32) * sorted_warp_smem<G, CH, false>();
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / G);
+  kern<<<grid, kBlock, sm, s>>>(ent, k, sizes, us, vs, b, e, out_count, out_est, out_cnt, out_ssum,
+                                out_verbatim);
+}
+
+static bool onehash_sorted(cudaStream_t s, bool fused, const int32_t* ent, int k, const int32_t* sizes,
+                           const int32_t* us, const int32_t* vs, int64_t b, int64_t e, int32_t* out_count,
+                           double* out_est, int64_t* out_cnt, int64_t* out_ssum, int64_t* out_verbatim) {
+#define PG_OS(G, CH)                                                                                     \
+  {                                                                                                      \
+    if (fused) launch_onehash_sorted<G, CH, true>(s, ent, k, sizes, us, vs, b, e, out_count, out_est,    \
+                                                  out_cnt, out_ssum, out_verbatim);                      \
+    else launch_onehash_sorted<G, CH, false>(s, ent, k, sizes, us, vs, b, e, out_count, out_est,        \
+                                             out_cnt, out_ssum, out_verbatim);                           \
+    return true;                                                                                         \
+  }
+  if (k == 32) PG_OS(4, 1)
+  if (k == 64) PG_OS(8, 1)
+  if (k == 128) PG_OS(8, 2)
+#undef PG_OS
+  return false;
+}
+
+template <int G, bool kFused>
+static void launch_kmv_sorted(cudaStream_t s, const uint64_t* vals, int k, const int32_t* sizes,
+                              const int32_t* us, const int32_t* vs, int64_t b, int64_t e, int32_t* out_common,
+                              int32_t* out_union, double* out_kth, double* out_est, double* out_sum) {
+  auto kern = kmv_sorted_kernel<G, kFused>;
+  const size_t sm = (size_t)(kBlock / 32) * sorted_warp_smem<G, 1, true>();
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / G);
+  kern<<<grid, kBlock, sm, s>>>(vals, k, sizes, us, vs, b, e, out_common, out_union, out_kth, out_est, out_sum);
+}
+
+static bool kmv_sorted(cudaStream_t s, bool fused, const uint64_t* vals, int k, const int32_t* sizes,
+                       const int32_t* us, const int32_t* vs, int64_t b, int64_t e, int32_t* out_common,
+                       int32_t* out_union, double* out_kth, double* out_est, double* out_sum) {
+#define PG_KS(G)                                                                                        \
+  {                                                                                                     \
+    if (fused) launch_kmv_sorted<G, true>(s, vals, k, sizes, us, vs, b, e, out_common, out_union,      \
+                                          out_kth, out_est, out_sum);                                   \
+    else launch_kmv_sorted<G, false>(s, vals, k, sizes, us, vs, b, e, out_common, out_union, out_kth, \
+                                     out_est, out_sum);                                                 \
+    return true;                                                                                        \
+  }
+  if (k == 32) PG_KS(4)
+  if (k == 64) PG_KS(8)
+#undef PG_KS
+  return false;
+}
+
 }  // namespace pg
 
 using namespace pg;
@@ -946,7 +1380,7 @@ using namespace pg;
     default: MACRO(1, 1); break;   \
   }
 
-extern "C" int pg_tc_bloom_pad(int32_t bits, int32_t* pad_host);
+extern "C" int pg_group_pad(int32_t row_bytes, int32_t* pad_host);
 
 static bool fast_w4(int w4) { return w4 == 1 || w4 == 2 || w4 == 4 || w4 == 8 || w4 == 16 || w4 == 32; }
 
@@ -1057,20 +1491,15 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
 }
 
 int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* sizes, const double* lut,
-                const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end, int64_t* out_hist,
-                int64_t* out_sum_pos, void* stream) {
-  return tc_bloom_impl(rows, bits, op, sizes, lut, us, vs, e_begin, e_end, out_hist, out_sum_pos, stream,
-                       false);
-}
-
-int pg_tc_bloom_padded(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* sizes,
-                       const double* lut, const int32_t* us, const int32_t* vs, int64_t e_begin,
-                       int64_t e_end, int64_t* out_hist, int64_t* out_sum_pos, void* stream) {
+                const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end, int32_t padded,
+                int64_t* out_hist, int64_t* out_sum_pos, void* stream) {
   int32_t pad = 1;
-  pg_tc_bloom_pad(bits, &pad);
-  PG_REQUIRE(e_begin % pad == 0, "e_begin must be a multiple of the layout pad %d", pad);
+  if (padded) {
+    pg_group_pad(bits / 8, &pad);
+    PG_REQUIRE(e_begin % pad == 0, "e_begin must be a multiple of the layout pad %d", pad);
+  }
   return tc_bloom_impl(rows, bits, op, sizes, lut, us, vs, e_begin, e_end, out_hist, out_sum_pos, stream,
-                       pad > 1);
+                       padded && pad > 1);
 }
 
 int pg_pairs_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int32_t* sizes,
@@ -1085,6 +1514,9 @@ int pg_pairs_minhash(const int32_t* entries, int32_t k, int32_t onehash, const i
   cudaStream_t s = as_stream(stream);
   if (onehash) {
     PG_REQUIRE(sizes, "1-Hash needs sizes");
+    if (onehash_sorted(s, false, entries, k, sizes, us, vs, 0, count, out_count, out_est, nullptr, nullptr,
+                       nullptr))
+      return check_launch("pairs_onehash_sorted");
     const int grid = grid_cap(sm_count() * 8, count, kBlock / 32);
 #define PG_OH(P) onehash_kernel<P, false><<<grid, kBlock, 0, s>>>(entries, k, sizes, us, vs, 0, count, out_count, out_est, nullptr, nullptr, nullptr)
     if (k <= 32) PG_OH(1);
@@ -1109,8 +1541,8 @@ int pg_pairs_minhash(const int32_t* entries, int32_t k, int32_t onehash, const i
 }
 
 int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int32_t* sizes,
-                  const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end, int64_t* out_cnt,
-                  int64_t* out_ssum, int64_t* out_verbatim, void* stream) {
+                  const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end, int32_t padded,
+                  int64_t* out_cnt, int64_t* out_ssum, int64_t* out_verbatim, void* stream) {
   PG_REQUIRE(k >= 1, "k must be >= 1");
   if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
@@ -1122,6 +1554,9 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
   if (e_end == e_begin) return PG_OK;
   PG_REQUIRE(entries && us && vs, "null pointer");
+  if (onehash && onehash_sorted(s, true, entries, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, out_cnt,
+                                out_ssum, out_verbatim))
+    return check_launch("tc_onehash_sorted");
   if (onehash) {
 #define PG_OH(P)                                                                                  \
   {                                                                                               \
@@ -1138,14 +1573,24 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
   }
   const int w4 = k % 4 == 0 ? k / 4 : 0;
   const uint4* e4 = reinterpret_cast<const uint4*>(entries);
-  if (!fast_w4(w4)) {
-    auto kern = tc_khash_kernel<1, 1, true>;
+  const int w8 = k % 8 == 0 ? k / 8 : 0;  // 32-byte chunks per row
+  if (padded && (w8 == 2 || w8 == 4 || w8 == 8)) {
+#define PG_KW(W8)                                                                        \
+  {                                                                                      \
+    auto kern = tc_khash_kernel<W8, 1, 2, 3>;                                            \
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);        \
+    kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum); \
+  }
+    if (w8 == 2) PG_KW(2) else if (w8 == 4) PG_KW(4) else PG_KW(8)
+#undef PG_KW
+  } else if (!fast_w4(w4)) {
+    auto kern = tc_khash_kernel<1, 1, 0>;
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);
     kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum);
   } else {
 #define PG_L(V, G)                                                                       \
   {                                                                                      \
-    auto kern = tc_khash_kernel<V, G, false>;                                            \
+    auto kern = tc_khash_kernel<V, G, 1>;                                                \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);        \
     kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum); \
   }
@@ -1156,8 +1601,8 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
 }
 
 int pg_jaccard_count_khash(const int32_t* entries, int32_t k, const int32_t* degrees, const int32_t* us,
-                           const int32_t* vs, int64_t e_begin, int64_t e_end, int32_t min_matches,
-                           double tau, int64_t* out_counts, void* stream) {
+                           const int32_t* vs, int64_t e_begin, int64_t e_end, int32_t padded,
+                           int32_t min_matches, double tau, int64_t* out_counts, void* stream) {
   PG_REQUIRE(k >= 1, "k must be >= 1");
   if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
@@ -1169,14 +1614,24 @@ int pg_jaccard_count_khash(const int32_t* entries, int32_t k, const int32_t* deg
   PG_REQUIRE(entries && us && vs, "null pointer");
   const int w4 = k % 4 == 0 ? k / 4 : 0;
   const uint4* e4 = reinterpret_cast<const uint4*>(entries);
-  if (!fast_w4(w4)) {
-    auto kern = jaccard_khash_kernel<1, 1, true>;
+  const int w8 = k % 8 == 0 ? k / 8 : 0;  // 32-byte chunks per row
+  if (padded && (w8 == 2 || w8 == 4 || w8 == 8)) {
+#define PG_JW(W8)                                                                                      \
+  {                                                                                                    \
+    auto kern = jaccard_khash_kernel<W8, 1, 2, 3>;                                                     \
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);                      \
+    kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts); \
+  }
+    if (w8 == 2) PG_JW(2) else if (w8 == 4) PG_JW(4) else PG_JW(8)
+#undef PG_JW
+  } else if (!fast_w4(w4)) {
+    auto kern = jaccard_khash_kernel<1, 1, 0>;
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);
     kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts);
   } else {
 #define PG_L(V, G)                                                                                         \
   {                                                                                                        \
-    auto kern = jaccard_khash_kernel<V, G, false>;                                                         \
+    auto kern = jaccard_khash_kernel<V, G, 1>;                                                             \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);                          \
     kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts);    \
   }
@@ -1197,6 +1652,8 @@ int pg_pairs_kmv(const double* values, const int32_t* lengths, int32_t k, const 
   PG_REQUIRE(values && sizes && us && vs, "null pointer");
   cudaStream_t s = as_stream(stream);
   const uint64_t* vb = reinterpret_cast<const uint64_t*>(values);
+  if (kmv_sorted(s, false, vb, k, sizes, us, vs, 0, count, out_common, out_union, out_kth, out_est, nullptr))
+    return check_launch("pairs_kmv_sorted");
   const int grid = grid_cap(sm_count() * 8, count, kBlock / 32);
 #define PG_KM(P) kmv_kernel<P, false><<<grid, kBlock, 0, s>>>(vb, k, sizes, us, vs, 0, count, out_common, out_union, out_kth, out_est, nullptr)
   if (k <= 32) PG_KM(1);
@@ -1221,6 +1678,8 @@ int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k, const int
   if (e_end == e_begin) return PG_OK;
   PG_REQUIRE(values && us && vs, "null pointer");
   const uint64_t* vb = reinterpret_cast<const uint64_t*>(values);
+  if (kmv_sorted(s, true, vb, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, nullptr, nullptr, out_sum))
+    return check_launch("tc_kmv_sorted");
 #define PG_KM(P)                                                                                    \
   {                                                                                                 \
     auto kern = kmv_kernel<P, true>;                                                                \
@@ -1278,10 +1737,10 @@ int pg_4clique_exact(const int64_t* dir_off, const int32_t* dir_adj, const int32
 
 }  // extern "C"
 
-extern "C" int pg_tc_bloom_pad(int32_t bits, int32_t* pad_host) {
+extern "C" int pg_group_pad(int32_t row_bytes, int32_t* pad_host) {
   PG_REQUIRE(pad_host, "null output");
-  PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
-  const int w8 = bits % 256 == 0 ? bits / 256 : 0;
-  *pad_host = (w8 == 2 || w8 == 4) ? w8 : (w8 == 8 ? 8 : 1);
+  PG_REQUIRE(row_bytes > 0, "row_bytes must be positive");
+  const int w8 = row_bytes % 32 == 0 ? row_bytes / 32 : 0;
+  *pad_host = (w8 == 2 || w8 == 4 || w8 == 8) ? w8 : 1;
   return PG_OK;
 }

@@ -227,17 +227,22 @@ def jaccard_min_matches(k: int, tau: float) -> int:
 
 
 def jaccard_counts(graph: CsrGraph, sketched: SketchedGraph, tau: float,
-                   e_begin: int, e_end: int):
+                   rank: int = 0, world: int = 1):
+    """Device int64 [kept_hat, kept_similarity, match_hist(k+1)] of this
+    rank's share of the edge slots."""
     import torch
+    from .providers import MinHashProvider
+    from .sharding import edge_range
     if sketched.kind is not SketchKind.KHASH:
         raise ValueError("Jaccard clustering needs k-Hash sketches")
     k = sketched.capacity
     d = sketched.device_tensors()
     dev = graph.device()
-    us, vs = dev.upper_edges()
+    us, vs, slots, padded = MinHashProvider(sketched)._tc_layout(dev)
+    b, e = edge_range(slots, rank, world, align=32 if padded else 1)
     out = torch.empty(k + 3, dtype=torch.int64, device="cuda")
     N.call("pg_jaccard_count_khash", N.ptr(d["entries"]), k, N.ptr(dev.degrees),
-           N.ptr(us), N.ptr(vs), e_begin, e_end, jaccard_min_matches(k, tau),
+           N.ptr(us), N.ptr(vs), b, e, int(padded), jaccard_min_matches(k, tau),
            float(tau), N.ptr(out), N.stream_handle())
     return out
 
@@ -245,7 +250,6 @@ def jaccard_counts(graph: CsrGraph, sketched: SketchedGraph, tau: float,
 def jaccard_cluster_count(graph: CsrGraph, sketched: SketchedGraph,
                           tau: float = 0.1) -> JaccardCount:
     """Config 4: per-edge k-Hash Jaccard, kept if >= tau, surviving count."""
-    us, _ = graph.device().upper_edges()
-    c = jaccard_counts(graph, sketched, tau, 0, us.numel()).cpu().numpy()
+    c = jaccard_counts(graph, sketched, tau).cpu().numpy()
     return JaccardCount(int(c[0]), int(c[1]), c[2:].copy(),
                         jaccard_min_matches(sketched.capacity, tau))

@@ -137,7 +137,16 @@ class _SketchProvider(IntersectionProvider):
         self.sketched = sketched
         self.sizes = sketched.sizes
 
+    def tc_pad(self) -> int:
+        """Lane-group size of the fused kernel = pad of its edge-slot layout."""
+        return 1
+
     def _tc_layout(self, dev):
+        """(us, vs, slots, padded) edge-slot arrays the fused kernel consumes."""
+        pad = self.tc_pad()
+        if pad > 1:
+            us, vs, slots = dev.upper_edges_padded(pad)
+            return us, vs, slots, True
         us, vs = dev.upper_edges()
         return us, vs, us.numel(), False
 
@@ -196,30 +205,16 @@ class BloomProvider(_SketchProvider):
         return out if on_dev else out.cpu().numpy().astype(np.int64)
 
     def tc_pad(self) -> int:
-        """Group size of the fused kernel = pad of its edge-slot layout."""
-        import ctypes
-        pad = ctypes.c_int32()
-        N.check(N.load_library().pg_tc_bloom_pad(self.sketched.bit_length,
-                                                 ctypes.byref(pad)), "pg_tc_bloom_pad")
-        return pad.value
-
-    def _tc_layout(self, dev):
-        """(us, vs, slots, padded) edge-slot arrays the fused kernel consumes."""
-        pad = self.tc_pad()
-        if pad > 1:
-            us, vs, slots = dev.upper_edges_padded(pad)
-            return us, vs, slots, True
-        us, vs = dev.upper_edges()
-        return us, vs, us.numel(), False
+        return N.group_pad(self.sketched.bit_length // 8)
 
     def _tc_counts(self, us, vs, e_begin: int, e_end: int, padded: bool = False):
         import torch
         d, sg = self._dev(), self.sketched
         hist = torch.empty(sg.bit_length + 1, dtype=torch.int64, device="cuda")
         spos = torch.empty(1, dtype=torch.int64, device="cuda")
-        N.call("pg_tc_bloom_padded" if padded else "pg_tc_bloom", N.ptr(d["rows"]),
-               sg.bit_length, self.op, N.ptr(d["sizes"]), N.ptr(self.lut_device()),
-               N.ptr(us), N.ptr(vs), e_begin, e_end, N.ptr(hist), N.ptr(spos),
+        N.call("pg_tc_bloom", N.ptr(d["rows"]), sg.bit_length, self.op,
+               N.ptr(d["sizes"]), N.ptr(self.lut_device()), N.ptr(us), N.ptr(vs),
+               e_begin, e_end, int(padded), N.ptr(hist), N.ptr(spos),
                N.stream_handle())
         return torch.cat([hist, spos])
 
@@ -272,6 +267,9 @@ class MinHashProvider(_SketchProvider):
     def onehash(self) -> bool:
         return self.kind is EstimatorKind.ONEHASH
 
+    def tc_pad(self) -> int:
+        return 1 if self.onehash else N.group_pad(4 * self.sketched.capacity)
+
     def _pairs_device(self, us, vs):
         import torch
         d, sg = self._dev(), self.sketched
@@ -303,7 +301,7 @@ class MinHashProvider(_SketchProvider):
         verb = torch.empty(1, dtype=torch.int64, device="cuda")
         N.call("pg_tc_minhash", N.ptr(d["entries"]), k, int(self.onehash),
                N.ptr(d["sizes"]), N.ptr(us), N.ptr(vs), e_begin, e_end,
-               N.ptr(cnt), N.ptr(ssum), N.ptr(verb), N.stream_handle())
+               int(padded), N.ptr(cnt), N.ptr(ssum), N.ptr(verb), N.stream_handle())
         return torch.cat([cnt, ssum, verb])
 
     def _tc_combine(self, counts: np.ndarray) -> float:
