@@ -344,6 +344,33 @@ __device__ __forceinline__ int sorted_lower_bound(T x, const T (&heads)[NC], con
   return (c - 1) * 8 + p;
 }
 
+// lower_bound of x in a row held in registers across the group: chunk c
+// (8 sorted values) lives in lane gbase + c % G (slot c / G, CH == 1 here),
+// heads[] are the broadcast chunk heads.  The chunk is fetched with 8
+// register shuffles -- no shared memory, so no bank conflicts.  Every lane
+// must call this (shuffles); `active` masks the result.
+template <class T, int NC>
+__device__ __forceinline__ int shfl_lower_bound(T x, bool active, const T (&heads)[NC], const T (&mine)[8],
+                                                int gbase, bool& found) {
+  int c = 0;
+#pragma unroll
+  for (int i = 0; i < NC; ++i) c += heads[i] <= x;
+  const int chunk = c > 0 ? c - 1 : 0;
+  const int src = gbase + chunk;  // CH == 1: chunk i is lane i of the group
+  int lt = 0;
+  bool eq = false;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    T y;
+    if constexpr (sizeof(T) == 8) y = (T)shfl64((uint64_t)mine[w], src);
+    else y = __shfl_sync(0xffffffffu, mine[w], src);
+    lt += y < x;
+    eq |= y == x;
+  }
+  found = active && c > 0 && eq;
+  return (active && c > 0) ? chunk * 8 + lt : 0;
+}
+
 struct SortedStats {
   int common, lu, lv;
   double kth;
@@ -406,17 +433,25 @@ __device__ __forceinline__ void sorted_edge_loop(const void* __restrict__ rows, 
     int la = 0, lb = 0;
 #pragma unroll
     for (int s = 0; s < CH; ++s) {
-      const int c = s * G + gl;
 #pragma unroll
       for (int w = 0; w < 8; ++w) {
-        sv[c * 8 + w] = b[s][w];
-        if constexpr (kKmv) su[c * 8 + w] = a[s][w];
         la += TR::valid(a[s][w]);
         lb += TR::valid(b[s][w]);
       }
     }
     la = group_sum<G>(la);
     lb = group_sum<G>(lb);
+    if constexpr (CH > 1) {  // shared-memory copies for the chunk searches
+#pragma unroll
+      for (int s = 0; s < CH; ++s) {
+        const int c = s * G + gl;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          sv[c * 8 + w] = b[s][w];
+          if constexpr (kKmv) su[c * 8 + w] = a[s][w];
+        }
+      }
+    }
     T hb[NC], ha[NC];
 #pragma unroll
     for (int i = 0; i < NC; ++i) {
@@ -434,7 +469,11 @@ __device__ __forceinline__ void sorted_edge_loop(const void* __restrict__ rows, 
       for (int w = 0; w < 8; ++w) {
         bool f = false;
         int lt = 0;
-        if (TR::valid(a[s][w])) lt = sorted_lower_bound<T, NC>(a[s][w], hb, sv, f);
+        if constexpr (CH == 1) {
+          lt = shfl_lower_bound<T, NC>(a[s][w], TR::valid(a[s][w]), hb, b[0], gbase, f);
+        } else {
+          if (TR::valid(a[s][w])) lt = sorted_lower_bound<T, NC>(a[s][w], hb, sv, f);
+        }
         ltb[s][w] = lt;
         inb[s][w] = f;
         found += f;
@@ -480,7 +519,11 @@ __device__ __forceinline__ void sorted_edge_loop(const void* __restrict__ rows, 
         for (int w = 0; w < 8; ++w) {
           bool f = false;
           int lt = 0;
-          if (TR::valid(b[s][w])) lt = sorted_lower_bound<T, NC>(b[s][w], ha, su, f);
+          if constexpr (CH == 1) {
+            lt = shfl_lower_bound<T, NC>(b[s][w], TR::valid(b[s][w]), ha, a[0], gbase, f);
+          } else {
+            if (TR::valid(b[s][w])) lt = sorted_lower_bound<T, NC>(b[s][w], ha, su, f);
+          }
           ltu[w] = lt;
           inu[w] = f;
           cnt += f;
@@ -1061,7 +1104,8 @@ struct EpiKmv {
 
 template <int G, int CH, bool kKmv>
 __host__ __device__ constexpr int sorted_warp_smem() {
-  return (32 / G) * (kKmv ? 2 : 1) * G * CH * 8 * (kKmv ? 8 : 4);
+  // row copies for the shared-memory chunk search (CH > 1 only)
+  return CH == 1 ? 16 : (32 / G) * (kKmv ? 2 : 1) * G * CH * 8 * (kKmv ? 8 : 4);
 }
 
 template <int G, int CH, bool kFused>
