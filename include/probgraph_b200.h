@@ -72,8 +72,10 @@ PG_API int pg_hash_words(const int64_t* keys, int64_t count, uint64_t seed,
 
 /* ---- graph preparation (graphs.py:101-105 CsrGraph.edges,
  *      mining.py:83-85 _directed_edge_arrays) ----------------------------- */
-/* bytes of scratch pg_csr_upper_edges needs for n vertices */
-PG_API int pg_csr_upper_edges_workspace(int64_t n, size_t* out_bytes_host);
+/* bytes of scratch pg_csr_upper_edges(_padded) needs for n vertices and
+ * `capacity` output slots */
+PG_API int pg_csr_upper_edges_workspace(int64_t n, int64_t capacity,
+                                        size_t* out_bytes_host);
 /* Writes every undirected edge once, u < v, in CSR order (== graph.edges()).
  * us/vs hold `capacity` entries (m = nnz/2 for a symmetric CSR); m_host
  * receives the count (host sync); a count above capacity is an error. */

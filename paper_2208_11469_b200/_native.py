@@ -36,7 +36,7 @@ SIGNATURES = {
     "pg_device_sm_count": [ctypes.POINTER(ctypes.c_int)],
     "pg_family_seeds": [c_u64, c_i32, ctypes.POINTER(c_u64)],
     "pg_hash_words": [c_ptr, c_i64, c_u64, c_ptr, c_ptr],
-    "pg_csr_upper_edges_workspace": [c_i64, ctypes.POINTER(c_size)],
+    "pg_csr_upper_edges_workspace": [c_i64, c_i64, ctypes.POINTER(c_size)],
     "pg_csr_upper_edges": [c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i64,
                            ctypes.POINTER(c_i64), c_ptr, c_size, c_ptr],
     "pg_csr_upper_edges_padded": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr,

@@ -37,33 +37,36 @@ __device__ __forceinline__ uint32_t bloom_pos(uint64_t w, uint32_t bits) {
   return static_cast<uint32_t>(w % bits);
 }
 
+// pass 1: one warp per vertex with d <= kHub; hubs are appended to a device
+// list (processed by pass 2, spread over the whole grid)
 template <bool kPow2>
 __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n,
     uint32_t bits, int b, const uint64_t* __restrict__ seeds_dev,
-    uint64_t* __restrict__ rows, int32_t* __restrict__ ones) {
+    uint64_t* __restrict__ rows, int32_t* __restrict__ ones, int32_t* __restrict__ hubs,
+    int32_t* __restrict__ hub_count) {
   extern __shared__ __align__(16) uint32_t smem[];
   const uint32_t words32 = bits >> 5;
   const uint32_t words64 = bits >> 6;
   uint32_t* my_row = smem + warp_id() * words32;
   uint64_t* seeds = reinterpret_cast<uint64_t*>(smem + kWarps * words32);
-  int* hub_list = reinterpret_cast<int*>(seeds + 64);
-  __shared__ int hub_count;
-  __shared__ int red[kWarps];
-
   for (int i = threadIdx.x; i < b; i += kThreads) seeds[i] = seeds_dev[i];
   __syncthreads();
   const int lane = lane_id();
-
-  for (int64_t cb = (int64_t)blockIdx.x * kChunk; cb < n; cb += (int64_t)gridDim.x * kChunk) {
-    if (threadIdx.x == 0) hub_count = 0;
-    __syncthreads();
-    const int64_t ce = min(cb + kChunk, n);
-    for (int64_t v = cb + warp_id(); v < ce; v += kWarps) {
-      const int64_t o = offsets[v];
-      const int64_t d = offsets[v + 1] - o;
+  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+  // each warp takes batches of 32 consecutive vertices; their offsets come in
+  // with one coalesced load and are broadcast by shuffles
+  for (int64_t vb = ((int64_t)blockIdx.x * kWarps + warp_id()) * 32; vb < n; vb += nwarps * 32) {
+    const int64_t vl = vb + lane_id();
+    const int64_t ol = vl < n ? offsets[vl] : 0;
+    const int64_t el = vl < n ? offsets[vl + 1] : 0;
+    const int nb = (int)((n - vb) < 32 ? (n - vb) : 32);
+    for (int t = 0; t < nb; ++t) {
+      const int64_t v = vb + t;
+      const int64_t o = __shfl_sync(0xffffffffu, ol, t);
+      const int64_t d = __shfl_sync(0xffffffffu, el, t) - o;
       if (d > kHub) {
-        if (lane == 0) hub_list[atomicAdd(&hub_count, 1)] = (int)(v - cb);
+        if (lane == 0) hubs[atomicAdd(hub_count, 1)] = (int32_t)v;
         continue;
       }
       for (uint32_t i = lane; i < words32; i += 32) my_row[i] = 0u;
@@ -87,40 +90,54 @@ __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
       if (lane == 0) ones[v] = cnt;
       __syncwarp();
     }
+  }
+}
+
+// pass 2: one CTA per hub (grid-stride over the hub list)
+template <bool kPow2>
+__global__ void __launch_bounds__(kThreads) build_bloom_hubs_kernel(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, uint32_t bits, int b,
+    const uint64_t* __restrict__ seeds_dev, uint64_t* __restrict__ rows, int32_t* __restrict__ ones,
+    const int32_t* __restrict__ hubs, const int32_t* __restrict__ hub_count) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  __shared__ int red[kWarps];
+  const uint32_t words32 = bits >> 5;
+  const uint32_t words64 = bits >> 6;
+  uint32_t* row = smem;
+  uint64_t* seeds = reinterpret_cast<uint64_t*>(smem + words32 + (words32 & 1));
+  for (int i = threadIdx.x; i < b; i += kThreads) seeds[i] = seeds_dev[i];
+  const int nh = *hub_count;
+  const int lane = lane_id();
+  for (int hi = blockIdx.x; hi < nh; hi += gridDim.x) {
+    const int64_t v = hubs[hi];
+    const int64_t o = offsets[v];
+    const int64_t d = offsets[v + 1] - o;
+    for (uint32_t i = threadIdx.x; i < words32; i += kThreads) row[i] = 0u;
     __syncthreads();
-    const int nh = hub_count;
-    for (int hi = 0; hi < nh; ++hi) {
-      const int64_t v = cb + hub_list[hi];
-      const int64_t o = offsets[v];
-      const int64_t d = offsets[v + 1] - o;
-      uint32_t* row = smem;  // whole CTA shares warp 0's row
-      for (uint32_t i = threadIdx.x; i < words32; i += kThreads) row[i] = 0u;
-      __syncthreads();
-      for (int64_t j = threadIdx.x; j < d; j += kThreads) {
-        const int32_t x = adj[o + j];
-        for (int h = 0; h < b; ++h) {
-          const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x), bits);
-          atomicOr(&row[p >> 5], 1u << (p & 31));
-        }
+    for (int64_t j = threadIdx.x; j < d; j += kThreads) {
+      const int32_t x = adj[o + j];
+      for (int h = 0; h < b; ++h) {
+        const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x), bits);
+        atomicOr(&row[p >> 5], 1u << (p & 31));
       }
-      __syncthreads();
-      int cnt = 0;
-      const uint64_t* row64 = reinterpret_cast<const uint64_t*>(row);
-      for (uint32_t i = threadIdx.x; i < words64; i += kThreads) {
-        const uint64_t w = row64[i];
-        cnt += __popcll(w);
-        rows[v * words64 + i] = w;
-      }
-      cnt = __reduce_add_sync(0xffffffffu, cnt);
-      if (lane == 0) red[warp_id()] = cnt;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        int t = 0;
-        for (int w = 0; w < kWarps; ++w) t += red[w];
-        ones[v] = t;
-      }
-      __syncthreads();
     }
+    __syncthreads();
+    int cnt = 0;
+    const uint64_t* row64 = reinterpret_cast<const uint64_t*>(row);
+    for (uint32_t i = threadIdx.x; i < words64; i += kThreads) {
+      const uint64_t w = row64[i];
+      cnt += __popcll(w);
+      rows[v * words64 + i] = w;
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) red[warp_id()] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int w = 0; w < kWarps; ++w) t += red[w];
+      ones[v] = t;
+    }
+    __syncthreads();
   }
 }
 
@@ -154,11 +171,8 @@ __device__ __forceinline__ void khash_scan(const int32_t* __restrict__ row, int6
 template <int S>
 __global__ void __launch_bounds__(kThreads) build_khash_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n, int k,
-    const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries) {
-  __shared__ uint64_t red_h[kWarps][32 * S];
-  __shared__ int32_t red_x[kWarps][32 * S];
-  __shared__ int hub_list[kChunk];
-  __shared__ int hub_count;
+    const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries, int32_t* __restrict__ hubs,
+    int32_t* __restrict__ hub_count) {
   const int lane = lane_id();
   uint64_t seed[S];
 #pragma unroll
@@ -166,15 +180,20 @@ __global__ void __launch_bounds__(kThreads) build_khash_kernel(
     const int i = lane + 32 * s;
     seed[s] = i < k ? seeds_dev[i] : 0ull;
   }
-  for (int64_t cb = (int64_t)blockIdx.x * kChunk; cb < n; cb += (int64_t)gridDim.x * kChunk) {
-    if (threadIdx.x == 0) hub_count = 0;
-    __syncthreads();
-    const int64_t ce = min(cb + kChunk, n);
-    for (int64_t v = cb + warp_id(); v < ce; v += kWarps) {
-      const int64_t o = offsets[v];
-      const int64_t d = offsets[v + 1] - o;
+  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+  // each warp takes batches of 32 consecutive vertices; their offsets come in
+  // with one coalesced load and are broadcast by shuffles
+  for (int64_t vb = ((int64_t)blockIdx.x * kWarps + warp_id()) * 32; vb < n; vb += nwarps * 32) {
+    const int64_t vl = vb + lane_id();
+    const int64_t ol = vl < n ? offsets[vl] : 0;
+    const int64_t el = vl < n ? offsets[vl + 1] : 0;
+    const int nb = (int)((n - vb) < 32 ? (n - vb) : 32);
+    for (int t = 0; t < nb; ++t) {
+      const int64_t v = vb + t;
+      const int64_t o = __shfl_sync(0xffffffffu, ol, t);
+      const int64_t d = __shfl_sync(0xffffffffu, el, t) - o;
       if (d > kHub) {
-        if (lane == 0) hub_list[atomicAdd(&hub_count, 1)] = (int)(v - cb);
+        if (lane == 0) hubs[atomicAdd(hub_count, 1)] = (int32_t)v;
         continue;
       }
       uint64_t bh[S];
@@ -188,35 +207,50 @@ __global__ void __launch_bounds__(kThreads) build_khash_kernel(
         if (i < k) entries[v * k + i] = d > 0 ? bx[s] : -1;
       }
     }
-    __syncthreads();
-    const int nh = hub_count;
-    for (int hi = 0; hi < nh; ++hi) {
-      const int64_t v = cb + hub_list[hi];
-      const int64_t o = offsets[v];
-      const int64_t d = offsets[v + 1] - o;
-      uint64_t bh[S];
-      int32_t bx[S];
+  }
+}
+
+template <int S>
+__global__ void __launch_bounds__(kThreads) build_khash_hubs_kernel(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int k,
+    const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries, const int32_t* __restrict__ hubs,
+    const int32_t* __restrict__ hub_count) {
+  __shared__ uint64_t red_h[kWarps][32 * S];
+  __shared__ int32_t red_x[kWarps][32 * S];
+  const int lane = lane_id();
+  uint64_t seed[S];
 #pragma unroll
-      for (int s = 0; s < S; ++s) { bh[s] = ~0ull; bx[s] = 0x7fffffff; }
-      khash_scan<S>(adj + o, 32 * warp_id(), d, kThreads, seed, bh, bx);
+  for (int s = 0; s < S; ++s) {
+    const int i = lane + 32 * s;
+    seed[s] = i < k ? seeds_dev[i] : 0ull;
+  }
+  const int nh = *hub_count;
+  for (int hi = blockIdx.x; hi < nh; hi += gridDim.x) {
+    const int64_t v = hubs[hi];
+    const int64_t o = offsets[v];
+    const int64_t d = offsets[v + 1] - o;
+    uint64_t bh[S];
+    int32_t bx[S];
 #pragma unroll
-      for (int s = 0; s < S; ++s) {
-        red_h[warp_id()][lane + 32 * s] = bh[s];
-        red_x[warp_id()][lane + 32 * s] = bx[s];
-      }
-      __syncthreads();
-      for (int i = threadIdx.x; i < k; i += kThreads) {
-        uint64_t h = red_h[0][i];
-        int32_t x = red_x[0][i];
-        for (int w = 1; w < kWarps; ++w) {
-          const uint64_t h2 = red_h[w][i];
-          const int32_t x2 = red_x[w][i];
-          if (h2 < h || (h2 == h && x2 < x)) { h = h2; x = x2; }
-        }
-        entries[v * k + i] = x;
-      }
-      __syncthreads();
+    for (int s = 0; s < S; ++s) { bh[s] = ~0ull; bx[s] = 0x7fffffff; }
+    khash_scan<S>(adj + o, 32 * warp_id(), d, kThreads, seed, bh, bx);
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      red_h[warp_id()][lane + 32 * s] = bh[s];
+      red_x[warp_id()][lane + 32 * s] = bx[s];
     }
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += kThreads) {
+      uint64_t h = red_h[0][i];
+      int32_t x = red_x[0][i];
+      for (int w = 1; w < kWarps; ++w) {
+        const uint64_t h2 = red_h[w][i];
+        const int32_t x2 = red_x[w][i];
+        if (h2 < h || (h2 == h && x2 < x)) { h = h2; x = x2; }
+      }
+      entries[v * k + i] = x;
+    }
+    __syncthreads();
   }
 }
 
@@ -357,24 +391,25 @@ template <int P, bool kKmv>
 __global__ void __launch_bounds__(kThreads) build_bottomk_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n, int k,
     const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries,
-    double* __restrict__ values, int32_t* __restrict__ lengths) {
+    double* __restrict__ values, int32_t* __restrict__ lengths, int32_t* __restrict__ hubs,
+    int32_t* __restrict__ hub_count) {
   __shared__ int32_t scratch[kWarps][32 * P];
-  __shared__ uint64_t merge_keys[kWarps][32 * P];
-  __shared__ int merge_cnt[kWarps];
-  __shared__ int hub_list[kChunk];
-  __shared__ int hub_count;
   const int lane = lane_id();
   const uint64_t seed0 = seeds_dev[0];
-
-  for (int64_t cb = (int64_t)blockIdx.x * kChunk; cb < n; cb += (int64_t)gridDim.x * kChunk) {
-    if (threadIdx.x == 0) hub_count = 0;
-    __syncthreads();
-    const int64_t ce = min(cb + kChunk, n);
-    for (int64_t v = cb + warp_id(); v < ce; v += kWarps) {
-      const int64_t o = offsets[v];
-      const int64_t d = offsets[v + 1] - o;
+  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
+  // each warp takes batches of 32 consecutive vertices; their offsets come in
+  // with one coalesced load and are broadcast by shuffles
+  for (int64_t vb = ((int64_t)blockIdx.x * kWarps + warp_id()) * 32; vb < n; vb += nwarps * 32) {
+    const int64_t vl = vb + lane_id();
+    const int64_t ol = vl < n ? offsets[vl] : 0;
+    const int64_t el = vl < n ? offsets[vl + 1] : 0;
+    const int nb = (int)((n - vb) < 32 ? (n - vb) : 32);
+    for (int t = 0; t < nb; ++t) {
+      const int64_t v = vb + t;
+      const int64_t o = __shfl_sync(0xffffffffu, ol, t);
+      const int64_t d = __shfl_sync(0xffffffffu, el, t) - o;
       if (d > kHub) {
-        if (lane == 0) hub_list[atomicAdd(&hub_count, 1)] = (int)(v - cb);
+        if (lane == 0) hubs[atomicAdd(hub_count, 1)] = (int32_t)v;
         continue;
       }
       if (!kKmv && d <= k) {
@@ -388,63 +423,114 @@ __global__ void __launch_bounds__(kThreads) build_bottomk_kernel(
       bottomk_scan<P, kKmv>(L, adj + o, 0, d, 32, seed0);
       bottomk_emit<P, kKmv>(L, v, k, seed0, scratch[warp_id()], entries, values, lengths);
     }
-    __syncthreads();
-    const int nh = hub_count;
-    for (int hi = 0; hi < nh; ++hi) {
-      const int64_t v = cb + hub_list[hi];
-      const int64_t o = offsets[v];
-      const int64_t d = offsets[v + 1] - o;
-      WarpBottomK<P, kKmv> L;
-      L.init(k);
-      bottomk_scan<P, kKmv>(L, adj + o, 32 * warp_id(), d, kThreads, seed0);
-#pragma unroll
-      for (int s = 0; s < P; ++s) merge_keys[warp_id()][lane + 32 * s] = L.key[s];
-      if (lane == 0) merge_cnt[warp_id()] = L.cnt;
-      __syncthreads();
-      if (warp_id() == 0) {
-        WarpBottomK<P, kKmv> M;
-        M.init(k);
-        for (int w = 0; w < kWarps; ++w) {
-          const int cw = merge_cnt[w];
-          for (int base = 0; base < cw; base += 32) {
-            const int idx = base + lane;
-            const bool valid = idx < cw;
-            M.offer(valid ? merge_keys[w][idx] : ~0ull, valid);
-          }
-        }
-        bottomk_emit<P, kKmv>(M, v, k, seed0, scratch[0], entries, values, lengths);
-      }
-      __syncthreads();
-    }
   }
 }
 
-static int grid_for(int64_t n) {
-  const int64_t chunks = (n + kChunk - 1) / kChunk;
-  const int64_t cap = (int64_t)sm_count() * 8;
-  return (int)std::max<int64_t>(1, std::min<int64_t>(chunks, cap));
+template <int P, bool kKmv>
+__global__ void __launch_bounds__(kThreads) build_bottomk_hubs_kernel(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int k,
+    const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries, double* __restrict__ values,
+    int32_t* __restrict__ lengths, const int32_t* __restrict__ hubs, const int32_t* __restrict__ hub_count) {
+  __shared__ int32_t scratch[32 * P];
+  __shared__ uint64_t merge_keys[kWarps][32 * P];
+  __shared__ int merge_cnt[kWarps];
+  const int lane = lane_id();
+  const uint64_t seed0 = seeds_dev[0];
+  const int nh = *hub_count;
+  for (int hi = blockIdx.x; hi < nh; hi += gridDim.x) {
+    const int64_t v = hubs[hi];
+    const int64_t o = offsets[v];
+    const int64_t d = offsets[v + 1] - o;
+    WarpBottomK<P, kKmv> L;
+    L.init(k);
+    bottomk_scan<P, kKmv>(L, adj + o, 32 * warp_id(), d, kThreads, seed0);
+#pragma unroll
+    for (int s = 0; s < P; ++s) merge_keys[warp_id()][lane + 32 * s] = L.key[s];
+    if (lane == 0) merge_cnt[warp_id()] = L.cnt;
+    __syncthreads();
+    if (warp_id() == 0) {
+      WarpBottomK<P, kKmv> M;
+      M.init(k);
+      for (int w = 0; w < kWarps; ++w) {
+        const int cw = merge_cnt[w];
+        for (int base = 0; base < cw; base += 32) {
+          const int idx = base + lane;
+          const bool valid = idx < cw;
+          M.offer(valid ? merge_keys[w][idx] : ~0ull, valid);
+        }
+      }
+      bottomk_emit<P, kKmv>(M, v, k, seed0, scratch, entries, values, lengths);
+    }
+    __syncthreads();
+  }
 }
 
-template <bool kKmv>
-int launch_bottomk(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t k,
-                          const uint64_t* seeds_dev, int32_t* entries, double* values,
-                          int32_t* lengths, void* stream) {
-  const int grid = grid_for(n);
-  cudaStream_t s = as_stream(stream);
-  if (k <= 32)
-    build_bottomk_kernel<1, kKmv><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, lengths);
-  else if (k <= 64)
-    build_bottomk_kernel<2, kKmv><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, lengths);
-  else if (k <= 128)
-    build_bottomk_kernel<4, kKmv><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, lengths);
-  else
-    build_bottomk_kernel<8, kKmv><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, lengths);
-  return check_launch(kKmv ? "build_kmv" : "build_onehash");
+// one resident wave of CTAs (each warp loops over 32-vertex batches)
+template <class K>
+static int grid_for(K kernel, size_t smem, int64_t n) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  const int64_t batches = (n + 31) / 32;
+  const int64_t need = (batches + kWarps - 1) / kWarps;
+  return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sm_count() * per_sm));
 }
+
+// transient device hub list: int32 count + up to nnz / kHub vertex IDs
+struct HubList {
+  int32_t* count = nullptr;
+  int32_t* ids = nullptr;
+  void* buf = nullptr;
+  cudaStream_t s = nullptr;
+  int init(const int64_t* offsets, int64_t n, cudaStream_t st) {
+    s = st;
+    int64_t nnz = 0;
+    cudaError_t e = cudaMemcpyAsync(&nnz, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return fail(PG_ERR_CUDA, "hub list: %s", cudaGetErrorString(e));
+    const int64_t cap = nnz / kHub + 1;
+    e = cudaMallocAsync(&buf, sizeof(int32_t) * (size_t)(cap + 1), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, sizeof(int32_t), s);
+    if (e != cudaSuccess) return fail(PG_ERR_CUDA, "hub list: %s", cudaGetErrorString(e));
+    count = static_cast<int32_t*>(buf);
+    ids = count + 1;
+    return PG_OK;
+  }
+  ~HubList() {
+    if (buf) cudaFreeAsync(buf, s);
+  }
+};
+
+int hub_grid() { return sm_count() * 4; }
 
 }  // namespace pg
 
 using namespace pg;
+
+template <bool kKmv>
+static int launch_bottomk(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t k,
+                          const uint64_t* seeds_dev, int32_t* entries, double* values, int32_t* lengths,
+                          void* stream) {
+  cudaStream_t s = as_stream(stream);
+  HubList hubs;
+  if (int rc = hubs.init(offsets, n, s)) return rc;
+#define PG_BK(P)                                                                                         \
+  {                                                                                                      \
+    const int grid = grid_for(build_bottomk_kernel<P, kKmv>, 0, n);                                     \
+    build_bottomk_kernel<P, kKmv><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, \
+                                                            lengths, hubs.ids, hubs.count);              \
+    build_bottomk_hubs_kernel<P, kKmv><<<hub_grid(), kThreads, 0, s>>>(offsets, adj, k, seeds_dev, entries, \
+                                                                        values, lengths, hubs.ids,        \
+                                                                        hubs.count);                     \
+  }
+  if (k <= 32) PG_BK(1)
+  else if (k <= 64) PG_BK(2)
+  else if (k <= 128) PG_BK(4)
+  else PG_BK(8)
+#undef PG_BK
+  return check_launch(kKmv ? "build_kmv" : "build_onehash");
+}
 
 extern "C" {
 
@@ -457,17 +543,26 @@ int pg_build_bloom(const int64_t* offsets, const int32_t* adj, int64_t n, int32_
   PG_REQUIRE(b >= 1 && b <= 64, "Bloom hash count must be in [1, 64]");
   PG_REQUIRE(offsets && seeds_dev && rows && ones, "null pointer");
   if (n == 0) return PG_OK;
-  const size_t smem = (size_t)kWarps * (bits / 8) + 64 * sizeof(uint64_t) + kChunk * sizeof(int);
-  const bool pow2 = (bits & (bits - 1)) == 0;
-  const int grid = grid_for(n);
   cudaStream_t s = as_stream(stream);
-  if (pow2) {
-    cudaFuncSetAttribute(build_bloom_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    build_bloom_kernel<true><<<grid, kThreads, smem, s>>>(offsets, adj, n, bits, b, seeds_dev, rows, ones);
-  } else {
-    cudaFuncSetAttribute(build_bloom_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    build_bloom_kernel<false><<<grid, kThreads, smem, s>>>(offsets, adj, n, bits, b, seeds_dev, rows, ones);
+  HubList hubs;
+  if (int rc = hubs.init(offsets, n, s)) return rc;
+  const size_t smem = (size_t)kWarps * (bits / 8) + 64 * sizeof(uint64_t);
+  const size_t smem_hub = (size_t)(bits / 8) + 8 + 64 * sizeof(uint64_t);
+  const bool pow2 = (bits & (bits - 1)) == 0;
+#define PG_BB(P2)                                                                                       \
+  {                                                                                                     \
+    const int grid = grid_for(build_bloom_kernel<P2>, smem, n);                                         \
+    cudaFuncSetAttribute(build_bloom_kernel<P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+    cudaFuncSetAttribute(build_bloom_hubs_kernel<P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
+                         (int)smem_hub);                                                                \
+    build_bloom_kernel<P2><<<grid, kThreads, smem, s>>>(offsets, adj, n, bits, b, seeds_dev, rows, ones,   \
+                                                        hubs.ids, hubs.count);                          \
+    build_bloom_hubs_kernel<P2><<<hub_grid(), kThreads, smem_hub, s>>>(offsets, adj, bits, b, seeds_dev,  \
+                                                                       rows, ones, hubs.ids, hubs.count); \
   }
+  if (pow2) PG_BB(true)
+  else PG_BB(false)
+#undef PG_BB
   return check_launch("build_bloom");
 }
 
@@ -478,12 +573,22 @@ int pg_build_khash(const int64_t* offsets, const int32_t* adj, int64_t n, int32_
   if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(offsets && seeds_dev && entries, "null pointer");
   if (n == 0) return PG_OK;
-  const int grid = grid_for(n);
   cudaStream_t s = as_stream(stream);
-  if (k <= 32) build_khash_kernel<1><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries);
-  else if (k <= 64) build_khash_kernel<2><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries);
-  else if (k <= 128) build_khash_kernel<4><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries);
-  else build_khash_kernel<8><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries);
+  HubList hubs;
+  if (int rc = hubs.init(offsets, n, s)) return rc;
+#define PG_KB(S)                                                                                         \
+  {                                                                                                      \
+    const int grid = grid_for(build_khash_kernel<S>, 0, n);                                              \
+    build_khash_kernel<S><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, hubs.ids,     \
+                                                    hubs.count);                                         \
+    build_khash_hubs_kernel<S><<<hub_grid(), kThreads, 0, s>>>(offsets, adj, k, seeds_dev, entries,       \
+                                                               hubs.ids, hubs.count);                    \
+  }
+  if (k <= 32) PG_KB(1)
+  else if (k <= 64) PG_KB(2)
+  else if (k <= 128) PG_KB(4)
+  else PG_KB(8)
+#undef PG_KB
   return check_launch("build_khash");
 }
 

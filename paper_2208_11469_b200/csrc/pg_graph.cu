@@ -4,6 +4,7 @@
 // (providers.py:102-115, setops.py:23-51) and raw hash words
 // (hashing.py:114-118).
 #include <cub/device/device_scan.cuh>
+#include <cuda/functional>
 
 #include "pg_common.cuh"
 
@@ -27,33 +28,32 @@ __global__ void upper_count_kernel(const int64_t* __restrict__ offsets, const in
   }
 }
 
-__global__ void upper_fill_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj,
-                                  int64_t n, const int64_t* __restrict__ first,
-                                  const int64_t* __restrict__ start, int32_t* __restrict__ us,
-                                  int32_t* __restrict__ vs, int64_t cap, int64_t pad) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
-    const int64_t f = first[u], e = offsets[u + 1], s = start[u];
-    const int64_t slots = (e - f + pad - 1) / pad * pad;
-    for (int64_t j = lane; j < slots; j += 32) {
-      const int64_t o = s + j;
-      if (o < cap) {
-        us[o] = (int32_t)u;
-        vs[o] = f + j < e ? adj[f + j] : -1;  // -1: padding slot
-      }
-    }
+// marks[start[u]] = u for every row with slots; an inclusive max-scan of the
+// marks then yields the row of every output slot (load-balanced, coalesced)
+__global__ void mark_rows_kernel(const int64_t* __restrict__ start, const int64_t* __restrict__ cnt, int64_t n,
+                                 int32_t* __restrict__ marks) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x)
+    if (cnt[u] > 0) marks[start[u]] = (int32_t)u;
+}
+
+// slot o of row u: the (o - start[u])-th upper neighbour, or -1 (padding)
+__global__ void upper_gather_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj,
+                                    const int64_t* __restrict__ first, const int64_t* __restrict__ start,
+                                    const int32_t* __restrict__ us, int64_t total, int32_t* __restrict__ vs) {
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < total;
+       o += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t u = us[o];
+    const int64_t f = first[u];
+    const int64_t off = o - start[u];
+    vs[o] = off < offsets[u + 1] - f ? adj[f + off] : -1;
   }
 }
 
-__global__ void expand_rows_kernel(const int64_t* __restrict__ offsets, int64_t n,
-                                   int32_t* __restrict__ src) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t u = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; u < n; u += warps) {
-    const int64_t b = offsets[u], e = offsets[u + 1];
-    for (int64_t j = b + lane; j < e; j += 32) src[j] = (int32_t)u;
-  }
+__global__ void mark_csr_rows_kernel(const int64_t* __restrict__ offsets, int64_t n, int32_t* __restrict__ marks) {
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x)
+    if (offsets[u + 1] > offsets[u]) marks[offsets[u]] = (int32_t)u;
 }
 
 __global__ void hash_words_kernel(const int64_t* __restrict__ keys, int64_t count, uint64_t seed,
@@ -98,6 +98,12 @@ static size_t scan_temp_bytes(int64_t n) {
   cub::DeviceScan::ExclusiveSum(nullptr, bytes, (const int64_t*)nullptr, (int64_t*)nullptr, n);
   return bytes;
 }
+static size_t maxscan_temp_bytes(int64_t n) {
+  size_t bytes = 0;
+  cub::DeviceScan::InclusiveScan(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                 ::cuda::maximum<>{}, n);
+  return bytes;
+}
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
@@ -107,26 +113,25 @@ using namespace pg;
 
 extern "C" {
 
-int pg_csr_upper_edges_workspace(int64_t n, size_t* out_bytes_host) {
-  PG_REQUIRE(n >= 0 && out_bytes_host, "bad arguments");
+int pg_csr_upper_edges_workspace(int64_t n, int64_t capacity, size_t* out_bytes_host) {
+  PG_REQUIRE(n >= 0 && capacity >= 0 && out_bytes_host, "bad arguments");
   const size_t arr = align256(sizeof(int64_t) * (size_t)(n + 1));
-  *out_bytes_host = 3 * arr + align256(scan_temp_bytes(n > 0 ? n : 1));
+  const size_t t1 = scan_temp_bytes(n > 0 ? n : 1), t2 = maxscan_temp_bytes(capacity > 0 ? capacity : 1);
+  *out_bytes_host = 3 * arr + align256(t1 > t2 ? t1 : t2);
   return PG_OK;
 }
 
 static int upper_edges_impl(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t* us, int32_t* vs,
                             int64_t capacity, int64_t* m_host, void* workspace, size_t workspace_bytes,
                             void* stream, int64_t pad) {
-  PG_REQUIRE(n >= 0, "n must be >= 0");
-  PG_REQUIRE(offsets && workspace, "null pointer");
+  PG_REQUIRE(n >= 0 && capacity >= 0, "bad sizes");
+  PG_REQUIRE(offsets && workspace && m_host, "null pointer");
   size_t need = 0;
-  pg_csr_upper_edges_workspace(n, &need);
+  pg_csr_upper_edges_workspace(n, capacity, &need);
   PG_REQUIRE(workspace_bytes >= need, "workspace too small (%zu < %zu)", workspace_bytes, need);
   cudaStream_t s = as_stream(stream);
-  if (n == 0) {
-    if (m_host) *m_host = 0;
-    return PG_OK;
-  }
+  *m_host = 0;
+  if (n == 0) return PG_OK;
   const size_t arr = align256(sizeof(int64_t) * (size_t)(n + 1));
   char* ws = static_cast<char*>(workspace);
   int64_t* first = reinterpret_cast<int64_t*>(ws);
@@ -139,21 +144,27 @@ static int upper_edges_impl(const int64_t* offsets, const int32_t* adj, int64_t 
   if (int rc = check_launch("upper_count")) return rc;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, cnt, start, n, s);
   if (e != cudaSuccess) return fail(PG_ERR_CUDA, "scan: %s", cudaGetErrorString(e));
-  upper_fill_kernel<<<grid, 256, 0, s>>>(offsets, adj, n, first, start, us, vs, capacity, pad);
-  if (int rc = check_launch("upper_fill")) return rc;
-  if (m_host) {
-    int64_t last_start = 0, last_cnt = 0;
-    e = cudaMemcpyAsync(&last_start, start + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(&last_cnt, cnt + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return fail(PG_ERR_CUDA, "upper edge count: %s", cudaGetErrorString(e));
-    *m_host = last_start + last_cnt;
-    if (*m_host > capacity)
-      return fail(PG_ERR_INVALID, "%lld upper edge slots exceed capacity %lld (asymmetric adjacency?)",
-                  (long long)*m_host, (long long)capacity);
-  }
-  return PG_OK;
+  int64_t last_start = 0, last_cnt = 0;
+  e = cudaMemcpyAsync(&last_start, start + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(&last_cnt, cnt + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "upper edge count: %s", cudaGetErrorString(e));
+  const int64_t total = last_start + last_cnt;
+  *m_host = total;
+  if (total > capacity)
+    return fail(PG_ERR_INVALID, "%lld upper edge slots exceed capacity %lld (asymmetric adjacency?)",
+                (long long)total, (long long)capacity);
+  if (total == 0) return PG_OK;
+  PG_REQUIRE(us && vs, "null output");
+  // vs serves as the mark buffer; its max-scan is the row of each slot
+  e = cudaMemsetAsync(vs, 0, sizeof(int32_t) * total, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
+  mark_rows_kernel<<<grid, 256, 0, s>>>(start, cnt, n, vs);
+  if (int rc = check_launch("mark_rows")) return rc;
+  e = cub::DeviceScan::InclusiveScan(temp, temp_bytes, vs, us, ::cuda::maximum<>{}, total, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "max-scan: %s", cudaGetErrorString(e));
+  upper_gather_kernel<<<grid, 256, 0, s>>>(offsets, adj, first, start, us, total, vs);
+  return check_launch("upper_gather");
 }
 
 int pg_csr_upper_edges(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t* us, int32_t* vs,
@@ -174,8 +185,26 @@ int pg_csr_expand_rows(const int64_t* offsets, int64_t n, int64_t nnz, int32_t* 
   PG_REQUIRE(n >= 0 && nnz >= 0, "bad sizes");
   if (n == 0 || nnz == 0) return PG_OK;
   PG_REQUIRE(offsets && src, "null pointer");
-  expand_rows_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(offsets, n, src);
-  return check_launch("expand_rows");
+  cudaStream_t s = as_stream(stream);
+  // row marks in a transient stream-ordered buffer, max-scanned into src
+  const size_t tb = maxscan_temp_bytes(nnz);
+  void* buf = nullptr;
+  cudaError_t e = cudaMallocAsync(&buf, align256(sizeof(int32_t) * nnz) + tb, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "cudaMallocAsync: %s", cudaGetErrorString(e));
+  int32_t* marks = static_cast<int32_t*>(buf);
+  void* temp = static_cast<char*>(buf) + align256(sizeof(int32_t) * nnz);
+  size_t temp_bytes = tb;
+  e = cudaMemsetAsync(marks, 0, sizeof(int32_t) * nnz, s);
+  if (e == cudaSuccess) {
+    mark_csr_rows_kernel<<<sm_count() * 8, 256, 0, s>>>(offsets, n, marks);
+    e = cudaGetLastError();
+  }
+  if (e == cudaSuccess)
+    e = cub::DeviceScan::InclusiveScan(temp, temp_bytes, marks, src, ::cuda::maximum<>{}, nnz, s);
+  const cudaError_t e2 = cudaFreeAsync(buf, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "expand_rows: %s", cudaGetErrorString(e));
+  if (e2 != cudaSuccess) return fail(PG_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(e2));
+  return PG_OK;
 }
 
 int pg_hash_words(const int64_t* keys, int64_t count, uint64_t seed, uint64_t* out, void* stream) {

@@ -66,7 +66,7 @@ class DeviceCsr:
             vs = torch.empty(m_alloc, dtype=torch.int32, device="cuda")
             import ctypes
             ws_bytes = ctypes.c_size_t()
-            N.call("pg_csr_upper_edges_workspace", self.n, ctypes.byref(ws_bytes))
+            N.call("pg_csr_upper_edges_workspace", self.n, m_alloc, ctypes.byref(ws_bytes))
             ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8,
                              device="cuda")
             m = ctypes.c_int64()
@@ -92,7 +92,7 @@ class DeviceCsr:
             us = torch.empty(cap, dtype=torch.int32, device="cuda")
             vs = torch.empty(cap, dtype=torch.int32, device="cuda")
             ws_bytes = ctypes.c_size_t()
-            N.call("pg_csr_upper_edges_workspace", self.n, ctypes.byref(ws_bytes))
+            N.call("pg_csr_upper_edges_workspace", self.n, cap, ctypes.byref(ws_bytes))
             ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device="cuda")
             slots = ctypes.c_int64()
             N.call("pg_csr_upper_edges_padded", N.ptr(self.offsets), N.ptr(self.adj),
