@@ -289,35 +289,40 @@ def run_ours(args, cfg, rank, world, local):
 
 
 def run_e2e(pg, g, sk, steps, bits, b, m):
-    """Same metric through tc_estimate() with HOST inputs copied every step."""
+    """Same metric through the public API with HOST inputs every step.
+
+    Input: the graph as a host int32 CSR in pinned memory (BASELINE's graph
+    format).  Each step: CsrGraph(host arrays) -> build_sketched_graph (H2D of
+    the CSR + device sketch build) -> tc_estimate (device edge slots, fused
+    kernel, histogram D2H) -> float.  Shipping prebuilt host sketches instead
+    would add 134 MB of H2D per step, more than building them on the device.
+    """
     import torch
-    from paper_2208_11469_b200.sketches import SketchedGraph
 
     def pinned(a):
         t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
         t.numpy()[...] = a
         return t.numpy()
 
-    off_h, adj_h = pinned(g.offsets), pinned(g.adjacency)
-    rows_h, ones_h = pinned(sk.bit_matrix), pinned(sk.ones)
-    sizes_h = pinned(sk.sizes)
-    h2d = off_h.nbytes + adj_h.nbytes + rows_h.nbytes + ones_h.nbytes + sizes_h.nbytes
+    off_h = pinned(g.offsets)
+    adj_h = pinned(g.adjacency.astype(np.int32))
+    h2d = off_h.nbytes + adj_h.nbytes
     times, est = [], None
     for i in range(steps + 1):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         graph = pg.CsrGraph(off_h, adj_h)
-        skh = SketchedGraph("bloom", sk.plan, sk.family, "undirected", sizes_h,
-                            bit_matrix=rows_h, ones=ones_h)
-        est = pg.tc_estimate(graph, skh, "bf_and")  # includes the D2H of the histogram
+        skd = pg.build_sketched_graph(graph, "bloom", s=1.0, b=b, bits_override=bits)
+        est = pg.tc_estimate(graph, skd, "bf_and")  # ends with the histogram D2H
         torch.cuda.synchronize()
         if i:  # first call is warm-up
             times.append(time.perf_counter() - t0)
     t = statistics.median(times)
     return {"value": m / t, "unit": "edge-intersections/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": 8 * (bits + 2), "ms_per_step": t * 1e3,
-            "path": "tc_estimate(CsrGraph(pinned int64 CSR), SketchedGraph(pinned host "
-                    "bit_matrix)) -> upload, device edge list, fused kernel, histogram D2H",
+            "path": "CsrGraph(pinned int32 CSR) -> build_sketched_graph(bloom, device) -> "
+                    "tc_estimate(bf_and): H2D of the CSR, device sketch build, device edge "
+                    "slots, fused kernel, histogram D2H, host combine",
             "estimate": est}
 
 

@@ -37,59 +37,82 @@ __device__ __forceinline__ uint32_t bloom_pos(uint64_t w, uint32_t bits) {
   return static_cast<uint32_t>(w % bits);
 }
 
-// pass 1: one warp per vertex with d <= kHub; hubs are appended to a device
-// list (processed by pass 2, spread over the whole grid)
+// pass 1: a warp builds a batch of R <= 32 consecutive vertices at once
+// (R = 32 unless the rows would not fit shared memory).  Their adjacency runs
+// are contiguous, so lanes stride over the batch's flattened entries
+// (coalesced loads, no per-vertex latency chain), locate each entry's vertex
+// in the batch's degree prefix (monotone per lane), and OR its b bits into
+// that vertex's row in shared memory; the R rows are then one contiguous block
+// of the output.  Vertices with d > kHubBloom are left to pass 2.
+constexpr int64_t kHubBloom = 1024;
+
+struct BloomBatchSmem {
+  int64_t off[32];
+  int pref[33];
+};
+
 template <bool kPow2>
 __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n,
-    uint32_t bits, int b, const uint64_t* __restrict__ seeds_dev,
+    uint32_t bits, int b, int R, const uint64_t* __restrict__ seeds_dev,
     uint64_t* __restrict__ rows, int32_t* __restrict__ ones, int32_t* __restrict__ hubs,
     int32_t* __restrict__ hub_count) {
-  extern __shared__ __align__(16) uint32_t smem[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t words32 = bits >> 5;
   const uint32_t words64 = bits >> 6;
-  uint32_t* my_row = smem + warp_id() * words32;
-  uint64_t* seeds = reinterpret_cast<uint64_t*>(smem + kWarps * words32);
+  BloomBatchSmem* meta = reinterpret_cast<BloomBatchSmem*>(smem_raw) + warp_id();
+  uint64_t* seeds = reinterpret_cast<uint64_t*>(smem_raw + kWarps * sizeof(BloomBatchSmem));
+  uint32_t* brows = reinterpret_cast<uint32_t*>(seeds + 64) + (size_t)warp_id() * R * words32;
   for (int i = threadIdx.x; i < b; i += kThreads) seeds[i] = seeds_dev[i];
   __syncthreads();
   const int lane = lane_id();
   const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-  // each warp takes batches of 32 consecutive vertices; their offsets come in
-  // with one coalesced load and are broadcast by shuffles
-  for (int64_t vb = ((int64_t)blockIdx.x * kWarps + warp_id()) * 32; vb < n; vb += nwarps * 32) {
-    const int64_t vl = vb + lane_id();
-    const int64_t ol = vl < n ? offsets[vl] : 0;
-    const int64_t el = vl < n ? offsets[vl + 1] : 0;
-    const int nb = (int)((n - vb) < 32 ? (n - vb) : 32);
-    for (int t = 0; t < nb; ++t) {
-      const int64_t v = vb + t;
-      const int64_t o = __shfl_sync(0xffffffffu, ol, t);
-      const int64_t d = __shfl_sync(0xffffffffu, el, t) - o;
-      if (d > kHub) {
-        if (lane == 0) hubs[atomicAdd(hub_count, 1)] = (int32_t)v;
-        continue;
-      }
-      for (uint32_t i = lane; i < words32; i += 32) my_row[i] = 0u;
-      __syncwarp();
-      for (int64_t j = lane; j < d; j += 32) {
-        const int32_t x = adj[o + j];
-        for (int h = 0; h < b; ++h) {
-          const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x), bits);
-          atomicOr(&my_row[p >> 5], 1u << (p & 31));
-        }
-      }
-      __syncwarp();
-      int cnt = 0;
-      const uint64_t* row64 = reinterpret_cast<const uint64_t*>(my_row);
-      for (uint32_t i = lane; i < words64; i += 32) {
-        const uint64_t w = row64[i];
-        cnt += __popcll(w);
-        rows[v * words64 + i] = w;
-      }
-      cnt = __reduce_add_sync(0xffffffffu, cnt);
-      if (lane == 0) ones[v] = cnt;
-      __syncwarp();
+  for (int64_t vb = ((int64_t)blockIdx.x * kWarps + warp_id()) * R; vb < n; vb += nwarps * R) {
+    const int nb = (int)((n - vb) < R ? (n - vb) : R);
+    const int64_t v = vb + lane;
+    const bool mine = lane < nb;
+    const int64_t o = mine ? offsets[v] : 0;
+    int64_t d = mine ? offsets[v + 1] - o : 0;
+    const bool hub = d > kHubBloom;
+    if (hub) {
+      hubs[atomicAdd(hub_count, 1)] = (int32_t)v;
+      d = 0;
     }
+    int incl = (int)d;  // exclusive prefix of the batch's (non-hub) degrees
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, off);
+      if (lane >= off) incl += y;
+    }
+    meta->pref[lane] = incl - (int)d;
+    meta->off[lane] = o;
+    if (lane == 31) meta->pref[32] = incl;
+    for (uint32_t i = lane; i < (uint32_t)R * words32; i += 32) brows[i] = 0u;
+    __syncwarp();
+    const int total = meta->pref[32];
+    int j = 0;  // batch vertex of the lane's current entry (non-decreasing)
+    for (int t = lane; t < total; t += 32) {
+      while (meta->pref[j + 1] <= t) ++j;
+      const int32_t x = adj[meta->off[j] + (t - meta->pref[j])];
+      uint32_t* row = brows + j * words32;
+      for (int h = 0; h < b; ++h) {
+        const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x), bits);
+        atomicOr(&row[p >> 5], 1u << (p & 31));
+      }
+    }
+    __syncwarp();
+    // the batch rows (hub rows are written by pass 2) and their ones
+    const uint64_t* b64 = reinterpret_cast<const uint64_t*>(brows);
+    for (int r = 0; r < nb; ++r) {
+      if (__shfl_sync(0xffffffffu, hub, r)) continue;
+      for (uint32_t i = lane; i < words64; i += 32) rows[(vb + r) * words64 + i] = b64[r * words64 + i];
+    }
+    if (mine && !hub) {
+      int c = 0;
+      for (uint32_t i = 0; i < words64; ++i) c += __popcll(b64[lane * words64 + i]);
+      ones[v] = c;
+    }
+    __syncwarp();
   }
 }
 
@@ -477,20 +500,17 @@ static int grid_for(K kernel, size_t smem, int64_t n) {
   return (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sm_count() * per_sm));
 }
 
-// transient device hub list: int32 count + up to nnz / kHub vertex IDs
+// transient device hub list: int32 count + up to n vertex IDs
 struct HubList {
   int32_t* count = nullptr;
   int32_t* ids = nullptr;
   void* buf = nullptr;
   cudaStream_t s = nullptr;
+  // capacity n + 1 (any vertex may be a hub): no host round trip for nnz
   int init(const int64_t* offsets, int64_t n, cudaStream_t st) {
+    (void)offsets;
     s = st;
-    int64_t nnz = 0;
-    cudaError_t e = cudaMemcpyAsync(&nnz, offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    if (e != cudaSuccess) return fail(PG_ERR_CUDA, "hub list: %s", cudaGetErrorString(e));
-    const int64_t cap = nnz / kHub + 1;
-    e = cudaMallocAsync(&buf, sizeof(int32_t) * (size_t)(cap + 1), s);
+    cudaError_t e = cudaMallocAsync(&buf, sizeof(int32_t) * (size_t)(n + 1), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return fail(PG_ERR_CUDA, "hub list: %s", cudaGetErrorString(e));
     count = static_cast<int32_t*>(buf);
@@ -546,16 +566,19 @@ int pg_build_bloom(const int64_t* offsets, const int32_t* adj, int64_t n, int32_
   cudaStream_t s = as_stream(stream);
   HubList hubs;
   if (int rc = hubs.init(offsets, n, s)) return rc;
-  const size_t smem = (size_t)kWarps * (bits / 8) + 64 * sizeof(uint64_t);
+  // batch size: 32 vertices per warp while the rows fit ~96 KB per CTA
+  int R = 32;
+  while (R > 1 && (size_t)kWarps * R * (bits / 8) > 96 * 1024) R >>= 1;
+  const size_t smem = kWarps * sizeof(BloomBatchSmem) + 64 * sizeof(uint64_t) + (size_t)kWarps * R * (bits / 8);
   const size_t smem_hub = (size_t)(bits / 8) + 8 + 64 * sizeof(uint64_t);
   const bool pow2 = (bits & (bits - 1)) == 0;
 #define PG_BB(P2)                                                                                       \
   {                                                                                                     \
-    const int grid = grid_for(build_bloom_kernel<P2>, smem, n);                                         \
     cudaFuncSetAttribute(build_bloom_kernel<P2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
     cudaFuncSetAttribute(build_bloom_hubs_kernel<P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,        \
                          (int)smem_hub);                                                                \
-    build_bloom_kernel<P2><<<grid, kThreads, smem, s>>>(offsets, adj, n, bits, b, seeds_dev, rows, ones,   \
+    const int grid = grid_for(build_bloom_kernel<P2>, smem, (n + R - 1) / R * 32);                      \
+    build_bloom_kernel<P2><<<grid, kThreads, smem, s>>>(offsets, adj, n, bits, b, R, seeds_dev, rows, ones, \
                                                         hubs.ids, hubs.count);                          \
     build_bloom_hubs_kernel<P2><<<hub_grid(), kThreads, smem_hub, s>>>(offsets, adj, bits, b, seeds_dev,  \
                                                                        rows, ones, hubs.ids, hubs.count); \

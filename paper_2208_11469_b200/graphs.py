@@ -99,8 +99,7 @@ class DeviceCsr:
                    self.n, pad, N.ptr(us), N.ptr(vs), cap, ctypes.byref(slots),
                    N.ptr(ws), ws_bytes.value, N.stream_handle())
             k = slots.value
-            self._layouts[key] = (us[:k].clone(), vs[:k].clone(), k)
-            del us, vs
+            self._layouts[key] = (us[:k], vs[:k], k)
         return self._layouts[key]
 
     def row_sources(self):
@@ -127,7 +126,12 @@ class CsrGraph:
 
     def __init__(self, offsets, adjacency, original_ids=None):
         self.offsets = np.asarray(offsets, dtype=np.int64)
-        self.adjacency = np.asarray(adjacency, dtype=np.int64)
+        adjacency = np.asarray(adjacency)
+        # int64 as in the reference; an int32 adjacency (BASELINE's "int32
+        # CSR") is kept as is, halving the host->device copy
+        if adjacency.dtype != np.int32:
+            adjacency = adjacency.astype(np.int64, copy=False)
+        self.adjacency = adjacency
         self.n = len(self.offsets) - 1
         self.m = len(self.adjacency) // 2
         self.original_ids = original_ids

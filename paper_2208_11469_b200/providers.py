@@ -135,7 +135,10 @@ class ExactProvider(IntersectionProvider):
 class _SketchProvider(IntersectionProvider):
     def __init__(self, sketched: SketchedGraph):
         self.sketched = sketched
-        self.sizes = sketched.sizes
+
+    @property
+    def sizes(self) -> np.ndarray:
+        return self.sketched.sizes
 
     def tc_pad(self) -> int:
         """Lane-group size of the fused kernel = pad of its edge-slot layout."""

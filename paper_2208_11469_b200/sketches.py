@@ -206,12 +206,27 @@ class SketchedGraph:
         self.family = family
         self.seed = family.base_seed
         self.source = source
-        self.sizes = np.asarray(sizes, dtype=np.int64)
-        self.n = len(self.sizes)
+        # sizes may be given lazily as ("offsets", host_offsets): np.diff is
+        # then only paid when a host caller asks for them
+        if isinstance(sizes, tuple) and sizes and sizes[0] == "offsets":
+            self._sizes = None
+            self._sizes_from = sizes[1]
+            self.n = len(sizes[1]) - 1
+        else:
+            self._sizes = np.asarray(sizes, dtype=np.int64)
+            self._sizes_from = None
+            self.n = len(self._sizes)
         self._host = {"bit_matrix": bit_matrix, "ones": ones,
                       "entries": entries, "lengths": lengths,
                       "values": values}
         self._dev = dict(device) if device else {}
+
+    @property
+    def sizes(self) -> np.ndarray:
+        """int64 size of every sketched set (a CSR degree)."""
+        if self._sizes is None:
+            self._sizes = np.diff(np.asarray(self._sizes_from, dtype=np.int64))
+        return self._sizes
 
     # -- plan shortcuts (reference :270-280)
     @property
@@ -353,7 +368,7 @@ def build_sketched_graph(graph: CsrGraph, kind, s: float, b: int = 1,
         host_off, dev_src = view.offsets, view
     else:
         raise ValueError("source must be 'undirected' or 'directed'")
-    sizes = np.diff(host_off)
+    sizes = ("offsets", host_off)  # materialised lazily (SketchedGraph.sizes)
     if kind is SketchKind.BLOOM and bits_override is not None:
         plan = BudgetPlan.explicit(kind, graph.n, bits=bits_override, b=b)
     elif kind is not SketchKind.BLOOM and k_override is not None:
