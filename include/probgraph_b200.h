@@ -199,6 +199,28 @@ PG_API int pg_pairs_exact(const int64_t* offsets, const int32_t* adj,
                    const int32_t* us, const int32_t* vs, int64_t count,
                    int64_t* out_count, void* stream);
 
+/* ---- graph generation (SURVEY 8(f) "next"; graphs.py:251-276) -------
+ * numpy default_rng(seed) == PCG64; (state, inc) are the 128-bit values of
+ * rng.bit_generator.state captured before the first draw. */
+/* R-MAT pairs, bit-identical to generate_kronecker's two rng.random(count)
+ * draws per level (a, b, c = initiator probabilities) */
+PG_API int pg_rmat_pairs(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                  uint64_t inc_lo, int32_t scale, int64_t count, double a,
+                  double b, double c, int64_t* src, int64_t* dst, void* stream);
+/* draws [offset, offset+count) of rng.random() */
+PG_API int pg_pcg64_uniform(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi,
+                     uint64_t inc_lo, int64_t offset, int64_t count,
+                     double* out, void* stream);
+/* np.searchsorted(cdf, u, "right") clipped to n-1 */
+PG_API int pg_searchsorted_right(const double* cdf, int64_t n, const double* u,
+                          int64_t count, int64_t* out, void* stream);
+/* CsrGraph.from_edges on the device (graphs.py:57-89): drop loops,
+ * deduplicate, symmetrise; offsets int64[n+1], adj int32[capacity];
+ * nnz_host receives 2m (host sync) */
+PG_API int pg_csr_from_pairs(const int64_t* a, const int64_t* b, int64_t count,
+                      int64_t n, int64_t* offsets, int32_t* adj,
+                      int64_t capacity, int64_t* nnz_host, void* stream);
+
 /* ---- utilities ------------------------------------------------------- */
 /* writes `bytes` bytes to a scratch buffer (L2 flush between timed runs) */
 PG_API int pg_l2_flush(void* buf, size_t bytes, void* stream);

@@ -70,6 +70,13 @@ SIGNATURES = {
     "pg_4clique_exact": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr],
     "pg_pairs_exact": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
     "pg_l2_flush": [c_ptr, c_size, c_ptr],
+    "pg_rmat_pairs": [c_u64, c_u64, c_u64, c_u64, c_i32, c_i64, c_dbl, c_dbl,
+                      c_dbl, c_ptr, c_ptr, c_ptr],
+    "pg_pcg64_uniform": [c_u64, c_u64, c_u64, c_u64, c_i64, c_i64, c_ptr,
+                         c_ptr],
+    "pg_searchsorted_right": [c_ptr, c_i64, c_ptr, c_i64, c_ptr, c_ptr],
+    "pg_csr_from_pairs": [c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_i64,
+                          ctypes.POINTER(c_i64), c_ptr],
 }
 
 

@@ -56,6 +56,21 @@ class DeviceCsr:
         self._src = None
         self._layouts = {}
 
+    @classmethod
+    def from_tensors(cls, offsets, adj) -> "DeviceCsr":
+        """Wrap device tensors (int64 offsets, int32 adjacency) already in HBM."""
+        import torch
+        self = cls.__new__(cls)
+        self.n = offsets.numel() - 1
+        self.nnz = adj.numel()
+        self.offsets = offsets
+        self.adj = adj
+        self.degrees = (offsets[1:] - offsets[:-1]).to(torch.int32)
+        self._upper = None
+        self._src = None
+        self._layouts = {}
+        return self
+
     def upper_edges(self):
         """(us, vs) int32 device arrays: every undirected edge once, u < v."""
         if self._upper is None:
@@ -257,19 +272,64 @@ def degree_order(graph: CsrGraph) -> DirectedView:
 # generators
 
 
-def generate_kronecker(scale: int, edge_factor: int, seed: int) -> CsrGraph:
+def _cuda_available() -> bool:
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:  # pragma: no cover
+        return False
+
+
+def _pcg64_state(rng) -> tuple[int, int, int, int]:
+    """(state_hi, state_lo, inc_hi, inc_lo) of numpy's PCG64 bit generator."""
+    st = rng.bit_generator.state["state"]
+    m64 = (1 << 64) - 1
+    return (st["state"] >> 64, st["state"] & m64, st["inc"] >> 64, st["inc"] & m64)
+
+
+def _graph_from_device_pairs(a, b, n: int) -> CsrGraph:
+    """CsrGraph.from_edges on the device (pg_csr_from_pairs); the returned
+    graph carries its device mirror, host arrays are copied back once."""
+    import ctypes
+    import torch
+    from . import _native as N
+    off = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    adj = torch.empty(max(1, 2 * a.numel()), dtype=torch.int32, device="cuda")
+    nnz = ctypes.c_int64()
+    N.call("pg_csr_from_pairs", N.ptr(a), N.ptr(b), a.numel(), n, N.ptr(off),
+           N.ptr(adj), adj.numel(), ctypes.byref(nnz), N.stream_handle())
+    adj = adj[:nnz.value].clone()
+    g = CsrGraph(off.cpu().numpy(), adj.cpu().numpy())
+    g._dev = DeviceCsr.from_tensors(off, adj)
+    return g
+
+
+def generate_kronecker(scale: int, edge_factor: int, seed: int,
+                       device: bool | None = None) -> CsrGraph:
     """R-MAT, initiator (a, b, c, d) = (0.57, 0.19, 0.19, 0.05).
 
     Per level l (LSB first) each sample draws ``rng.random(count)`` for the
     source bit, then ``rng.random(count)`` for the destination bit whose
     threshold depends on the source bit -- the reference's draw order, so
-    graphs are identical for a given seed.
+    graphs are identical for a given seed.  With a CUDA device (default when
+    one is present) the same PCG64 stream is generated on the device
+    (pg_rmat_pairs) and deduplicated there (pg_csr_from_pairs).
     """
     if scale < 1:
         raise ValueError("scale must be >= 1")
     n = 1 << scale
     count = edge_factor * n
     rng = np.random.default_rng(seed)
+    if device is None:
+        device = _cuda_available()
+    if device:
+        import torch
+        from . import _native as N
+        src = torch.empty(max(1, count), dtype=torch.int64, device="cuda")
+        dst = torch.empty(max(1, count), dtype=torch.int64, device="cuda")
+        N.call("pg_rmat_pairs", *_pcg64_state(rng), scale, count, 0.57, 0.19,
+               0.19, N.ptr(src), N.ptr(dst), N.stream_handle())
+        return _graph_from_device_pairs(src[:count], dst[:count], n)
     p_ab = 0.57 + 0.19
     thr_given_src0 = 0.57 / p_ab            # P(dst bit 0 | src bit 0)
     thr_given_src1 = 0.19 / (1.0 - p_ab)    # P(dst bit 0 | src bit 1)
@@ -312,7 +372,8 @@ def generate_erdos_renyi_gnm(n: int, m: int, seed: int) -> CsrGraph:
 
 
 def generate_chung_lu(n: int, avg_degree: float, gamma: float, seed: int,
-                      weight_cap: float | None = None) -> CsrGraph:
+                      weight_cap: float | None = None,
+                      device: bool | None = None) -> CsrGraph:
     """Chung-Lu power-law graph (config 4).
 
     Weights w_i = (i+1)^(-1/(gamma-1)) scaled to mean ``avg_degree`` and capped
@@ -332,6 +393,23 @@ def generate_chung_lu(n: int, avg_degree: float, gamma: float, seed: int,
     cdf = np.cumsum(w)
     cdf /= cdf[-1]
     samples = int(round(n * avg_degree / 2.0))
+    if device is None:
+        device = _cuda_available()
+    if device:
+        import torch
+        from . import _native as N
+        st = _pcg64_state(rng)
+        cdf_d = torch.from_numpy(cdf).cuda()
+        draws = torch.empty(max(1, samples), dtype=torch.float64, device="cuda")
+        ends = []
+        for offset in (0, samples):  # u from the first rng.random, v the second
+            N.call("pg_pcg64_uniform", *st, offset, samples, N.ptr(draws),
+                   N.stream_handle())
+            out = torch.empty(max(1, samples), dtype=torch.int64, device="cuda")
+            N.call("pg_searchsorted_right", N.ptr(cdf_d), n, N.ptr(draws), samples,
+                   N.ptr(out), N.stream_handle())
+            ends.append(out[:samples])
+        return _graph_from_device_pairs(ends[0], ends[1], n)
     u = np.searchsorted(cdf, rng.random(samples), side="right")
     v = np.searchsorted(cdf, rng.random(samples), side="right")
     np.minimum(u, n - 1, out=u)
