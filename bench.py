@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-busy", action="store_true",
                     help="skip the untimed clock-sampling tail (for ncu runs)")
+    ap.add_argument("--no-secondary", action="store_true",
+                    help="skip the per-config measurements of configs 1, 3, 4, 5")
     return ap.parse_args()
 
 
@@ -250,6 +252,11 @@ def run_ours(args, cfg, rank, world, local):
     if rank == 0 and world == 1 and args.e2e_steps > 0:
         e2e = run_e2e(pg, g, sk, args.e2e_steps, bits, b, m)
 
+    secondary = None
+    if rank == 0 and world == 1 and not args.no_secondary:
+        del sk, provider
+        secondary = run_secondary()
+
     out = None
     if rank == 0:
         cpu = None
@@ -276,6 +283,7 @@ def run_ours(args, cfg, rank, world, local):
             "gpu_launches": args.steps,
             "e2e": e2e,
             "cpu_baseline": cpu,
+            "secondary": secondary,
             "estimate": estimate,
             "build": {"bloom_build_ms": min(build_ms), "graph_gen_s": gen_s,
                       "rows_per_s": g.n / (min(build_ms) / 1e3)},
@@ -285,6 +293,109 @@ def run_ours(args, cfg, rank, world, local):
         import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
+    return out
+
+
+def _time_device(fn, reps=5, warm=2, flush=None):
+    """Median CUDA-event time (ms) of fn() with an optional L2 flush before
+    each timed call (outside the events)."""
+    import torch
+    st = torch.cuda.current_stream()
+    out = None
+    for _ in range(warm):
+        out = fn()
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            flush()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        out = fn()
+        b.record(st)
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return statistics.median(ts), out
+
+
+def run_secondary():
+    """The other BASELINE configs, one GPU: per-edge estimator throughput
+    (device-resident inputs, L2 flushed before every timed call)."""
+    import gc
+    import torch
+    import paper_2208_11469_b200 as pg
+    from paper_2208_11469_b200 import _native as N
+    from paper_2208_11469_b200.mining import (four_clique_counts, jaccard_counts,
+                                              tc_counts)
+    peak, _ = load_peaks()
+    flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    def flush():
+        N.call("pg_l2_flush", N.ptr(flush_buf), flush_buf.numel(), N.stream_handle())
+
+    def rec(name, g, ms, bytes_per_edge, extra):
+        r = {"graph": name, "n": g.n, "m": g.m, "ms": ms,
+             "edge_intersections_per_s": g.m / (ms / 1e3),
+             "algorithmic_gbs": g.m * bytes_per_edge / (ms / 1e3) / 1e9,
+             "frac_of_hbm_peak": g.m * bytes_per_edge / (ms / 1e3) / 1e9 / peak}
+        r.update(extra)
+        return r
+
+    out = {}
+    try:
+        # config 1: ER G(16384, 262144), Bloom 512/1
+        g = pg.generate_erdos_renyi_gnm(16384, 262144, 0)
+        sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=1, bits_override=512)
+        p = pg.make_provider("bf_and", sketched=sk)
+        ms, c = _time_device(lambda: tc_counts(p, g.device()), flush=flush)
+        out["c1_bloom512_tc"] = rec("ER n=16384 m=262144 seed 0", g, ms, 2 * 64 + 8,
+                                    {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0})
+        # config 3: R-MAT s22 seed 2, 1-Hash k=64 and KMV k=64
+        g = pg.generate_kronecker(22, 16, 2)
+        for kind, bpe in (("onehash", 2 * 4 * 64 + 16), ("kmv", 2 * 8 * 64 + 24)):
+            t0 = time.perf_counter()
+            sk = pg.build_sketched_graph(g, kind, s=1.0, k_override=64)
+            torch.cuda.synchronize()
+            bms = (time.perf_counter() - t0) * 1e3
+            p = pg.make_provider(kind, sketched=sk)
+            ms, c = _time_device(lambda: tc_counts(p, g.device()), reps=3, flush=flush)
+            out[f"c3_{kind}64_tc"] = rec("R-MAT s22 ef16 seed 2", g, ms, bpe,
+                                         {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0,
+                                          "build_ms_wall": bms})
+            del sk, p
+        # config 4: Chung-Lu 2^23, k-Hash k=32 Jaccard >= 0.1
+        g = pg.generate_chung_lu(1 << 23, 32, 2.1, 3)
+        sk = pg.build_sketched_graph(g, "khash", s=1.0, k_override=32)
+        ms, c = _time_device(lambda: jaccard_counts(g, sk, 0.1), flush=flush)
+        c = c.cpu().numpy()
+        out["c4_khash32_jaccard"] = rec("Chung-Lu n=2^23 avg 32 gamma 2.1 seed 3", g, ms, 2 * 4 * 32 + 8,
+                                        {"kept_jhat_ge_0.1": int(c[0]),
+                                         "kept_vertex_similarity_ge_0.1": int(c[1])})
+        del sk
+        # config 5: R-MAT s24 seed 4, Bloom 2048/2
+        g = pg.generate_kronecker(24, 16, 4)
+        sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=2, bits_override=2048)
+        p = pg.make_provider("bf_and", sketched=sk)
+        ms, c = _time_device(lambda: tc_counts(p, g.device()), flush=flush)
+        out["c5_bloom2048_tc"] = rec("R-MAT s24 ef16 seed 4", g, ms, 2 * 256 + 8,
+                                     {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0})
+        del sk, p, g
+        gc.collect()
+        torch.cuda.empty_cache()
+        # config 5b: 4-clique, R-MAT s18 seed 4, Bloom 2048/2 over N+
+        g = pg.generate_kronecker(18, 16, 4)
+        view = pg.degree_order(g)
+        dsk = pg.build_sketched_graph(g, "bloom", s=1.0, b=2, bits_override=2048,
+                                      source="directed", view=view)
+        p = pg.make_provider("bf_and", sketched=dsk)
+        nnz = view.device().nnz
+        ms, c = _time_device(lambda: four_clique_counts(view, p, 0, nnz), reps=3)
+        c = c.cpu().numpy()
+        out["c5b_4clique_bloom2048"] = {"graph": "R-MAT s18 ef16 seed 4", "ms": ms,
+                                        "triples": int(c[-1]),
+                                        "triples_per_s": int(c[-1]) / (ms / 1e3),
+                                        "estimate": p._tc_combine(c[:-1])}
+    except Exception as exc:  # report, keep the headline line valid
+        out["error"] = f"{type(exc).__name__}: {exc}"
     return out
 
 
