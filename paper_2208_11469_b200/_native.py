@@ -13,7 +13,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libprobgraph_b200.so")
+LIB_PATH = os.environ.get("PG_LIB_PATH") or os.path.join(_HERE, "_lib", "libprobgraph_b200.so")
 
 PG_OK = 0
 PG_ERR_INVALID = -1
