@@ -394,12 +394,15 @@ __device__ __forceinline__ int group_excl_scan(int x, int gl) {
   return inc - x;
 }
 
-template <int G, int CH, bool kKmv, class Epi>
-__device__ __forceinline__ void sorted_edge_loop(const void* __restrict__ rows, int k,
+// 1-Hash lookup engine: every U element is looked up in V (chunk heads
+// broadcast, the chunk itself by register shuffles for CH == 1 or from a
+// shared-memory copy for CH > 1); common = number of hits.
+template <int G, int CH, class Epi>
+__device__ __forceinline__ void sorted_edge_loop(const int32_t* __restrict__ R, int k,
                                                  const int32_t* __restrict__ us,
                                                  const int32_t* __restrict__ vs, int64_t e_begin,
                                                  int64_t e_end, unsigned char* warp_smem, Epi& epi) {
-  using T = typename std::conditional<kKmv, uint64_t, int32_t>::type;
+  using T = int32_t;
   using TR = SortedTraits<T>;
   constexpr int NC = G * CH;  // chunks per row (k / 8)
   constexpr int E = 32 / G;   // edges per warp iteration
@@ -407,9 +410,7 @@ __device__ __forceinline__ void sorted_edge_loop(const void* __restrict__ rows, 
   const int gl = lane & (G - 1);
   const int gbase = lane & ~(G - 1);
   const int grp = lane / G;
-  const T* R = reinterpret_cast<const T*>(rows);
-  T* sv = reinterpret_cast<T*>(warp_smem) + grp * (kKmv ? 2 : 1) * NC * 8;
-  T* su = sv + NC * 8;  // KMV only
+  T* sv = reinterpret_cast<T*>(warp_smem) + grp * NC * 8;
   int64_t wb, we;
   warp_slice(e_begin, e_end, wb, we);
   if (wb >= we) return;
@@ -421,7 +422,7 @@ __device__ __forceinline__ void sorted_edge_loop(const void* __restrict__ rows, 
 #pragma unroll 1
   for (int64_t e0 = wb; e0 < we; e0 += E) {
     const int64_t e = e0 + grp;
-    const bool valid = e < we;
+    const bool valid = e < we;  // 1-Hash uses the unpadded edge layout
     int32_t un = 0, vn = 0;
     if (e + E < we) {
       un = us[e + E];
@@ -441,41 +442,29 @@ __device__ __forceinline__ void sorted_edge_loop(const void* __restrict__ rows, 
     }
     la = group_sum<G>(la);
     lb = group_sum<G>(lb);
-    if constexpr (CH > 1) {  // shared-memory copies for the chunk searches
+    if constexpr (CH > 1) {  // shared-memory copy of V for the chunk searches
 #pragma unroll
       for (int s = 0; s < CH; ++s) {
         const int c = s * G + gl;
 #pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          sv[c * 8 + w] = b[s][w];
-          if constexpr (kKmv) su[c * 8 + w] = a[s][w];
-        }
+        for (int w = 0; w < 8; ++w) sv[c * 8 + w] = b[s][w];
       }
     }
-    T hb[NC], ha[NC];
+    T hb[NC];
 #pragma unroll
-    for (int i = 0; i < NC; ++i) {
-      hb[i] = __shfl_sync(0xffffffffu, b[i / G][0], gbase + i % G);
-      if constexpr (kKmv) ha[i] = __shfl_sync(0xffffffffu, a[i / G][0], gbase + i % G);
-    }
+    for (int i = 0; i < NC; ++i) hb[i] = __shfl_sync(0xffffffffu, b[i / G][0], gbase + i % G);
     __syncwarp();
-    // U elements against V: membership (and lower_bound for KMV ranks)
-    int ltb[CH][8];
-    bool inb[CH][8];
     int found = 0;
 #pragma unroll
     for (int s = 0; s < CH; ++s)
 #pragma unroll
       for (int w = 0; w < 8; ++w) {
         bool f = false;
-        int lt = 0;
         if constexpr (CH == 1) {
-          lt = shfl_lower_bound<T, NC>(a[s][w], TR::valid(a[s][w]), hb, b[0], gbase, f);
+          shfl_lower_bound<T, NC>(a[s][w], TR::valid(a[s][w]), hb, b[0], gbase, f);
         } else {
-          if (TR::valid(a[s][w])) lt = sorted_lower_bound<T, NC>(a[s][w], hb, sv, f);
+          if (TR::valid(a[s][w])) sorted_lower_bound<T, NC>(a[s][w], hb, sv, f);
         }
-        ltb[s][w] = lt;
-        inb[s][w] = f;
         found += f;
       }
     SortedStats st;
@@ -483,72 +472,176 @@ __device__ __forceinline__ void sorted_edge_loop(const void* __restrict__ rows, 
     st.lu = la;
     st.lv = lb;
     st.kth = 0.0;
+    if (valid && gl == 0) epi.edge(e, ul, vl, st);
+    __syncwarp();
+    ul = un;
+    vl = vn;
+  }
+}
+
+// ------------------------------------------------ merge-path group engine
+// KMV rows (k = 8*G*CH sorted elements, pads sort last).  G lanes
+// per edge; the 2k-element merge of the two rows is split into G equal
+// diagonals.  Each lane finds its diagonal's split point with a binary
+// search over the rows' shared-memory copies (merge path) and merges its
+// Q = 2k/G outputs sequentially: a value stored in both rows shows up as
+// two adjacent outputs (U's copy first), which counts the common elements;
+// first copies of finite values are the distinct union elements, whose group
+// prefix sum locates KMV's T-th distinct value (providers.py:266-301).
+// One branchless merge step: emit min(ca, cb), advance that row (index
+// clamped to the sentinel pad slot at K).
+template <class T, int K, class SK>
+__device__ __forceinline__ T merge_step(const T* su, const T* sv, int& i, int& j, T& ca, T& cb, SK sk) {
+  const bool ta = ca <= cb;
+  const T x = ta ? ca : cb;
+  const int nxt = min((ta ? i : j) + 1, K);
+  const T y = (ta ? su : sv)[sk(nxt)];
+  i = ta ? nxt : i;
+  j = ta ? j : nxt;
+  ca = ta ? y : ca;
+  cb = ta ? cb : y;
+  return x;
+}
+
+template <int G, int CH, bool kKmv, class Epi>
+__device__ __forceinline__ void merge_edge_loop(const void* __restrict__ rows, int k,
+                                                const int32_t* __restrict__ us,
+                                                const int32_t* __restrict__ vs, int64_t e_begin,
+                                                int64_t e_end, unsigned char* warp_smem, Epi& epi) {
+  using T = typename std::conditional<kKmv, uint64_t, int32_t>::type;
+  using TR = SortedTraits<T>;
+  constexpr int K = 8 * G * CH;  // row length
+  constexpr int Q = 2 * K / G;   // merged outputs per lane
+  constexpr int E = 32 / G;      // edges per warp iteration
+  constexpr int LOG = 32 - __builtin_clz(K);  // bisection steps over [0, K]
+  const int lane = threadIdx.x & 31;
+  const int gl = lane & (G - 1);
+  const int gbase = lane & ~(G - 1);
+  const int grp = lane / G;
+  const T* R = reinterpret_cast<const T*>(rows);
+  // bank-skewed copies: element x at x + x/8 (lane diagonals start ~8 apart
+  // in each row), a sentinel pad at K, groups offset by an odd element count
+  constexpr int KP = K + K / 8 + 1;
+  auto sk = [](int x) { return x + (x >> 3); };
+  T* su = reinterpret_cast<T*>(warp_smem) + grp * (2 * KP + 1);
+  T* sv = su + KP;
+  if (gl == 0) {
+    su[sk(K)] = TR::pad();
+    sv[sk(K)] = TR::pad();
+  }
+  const unsigned gmask = ((G == 32) ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
+  int64_t wb, we;
+  warp_slice(e_begin, e_end, wb, we);
+  if (wb >= we) return;
+  int32_t ul = 0, vl = 0;
+  if (wb + grp < we) {
+    ul = us[wb + grp];
+    vl = vs[wb + grp];
+  }
+#pragma unroll 1
+  for (int64_t e0 = wb; e0 < we; e0 += E) {
+    const int64_t e = e0 + grp;
+    const bool valid = e < we && vl >= 0;
+    int32_t un = 0, vn = 0;
+    if (e + E < we) {
+      un = us[e + E];
+      vn = vs[e + E];
+    }
+    T a[CH][8], b[CH][8];
+    load_sorted_chunks<T, CH, true>(R + (int64_t)ul * k, G, gl, a);
+    load_sorted_chunks<T, CH, false>(R + (int64_t)(vl < 0 ? 0 : vl) * k, G, gl, b);
+    int la = 0, lb = 0;
+#pragma unroll
+    for (int s = 0; s < CH; ++s) {
+      const int c = s * G + gl;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        su[c * 9 + w] = a[s][w];
+        sv[c * 9 + w] = b[s][w];
+        la += TR::valid(a[s][w]);
+        lb += TR::valid(b[s][w]);
+      }
+    }
+    la = group_sum<G>(la);
+    lb = group_sum<G>(lb);
+    __syncwarp();
+    // merge-path split of diagonal d0 (U-first on ties), fixed-trip bisection
+    const int d0 = gl * Q;
+    int lo = d0 > K ? d0 - K : 0, hi = d0 < K ? d0 : K;
+#pragma unroll
+    for (int it = 0; it < LOG; ++it) {
+      const int mid = (lo + hi) >> 1;
+      const bool go = lo < hi;
+      const T x = su[sk(min(mid, K))];
+      const T y = sv[sk(max(d0 - 1 - mid, 0))];
+      const bool right = x <= y;
+      lo = (go && right) ? mid + 1 : lo;
+      hi = (go && !right) ? mid : hi;
+    }
+    const int i0 = lo, j0 = d0 - lo;
+    T prev0 = TR::pad();
+    if (d0 > 0) {
+      const T pu = su[sk(max(i0 - 1, 0))], pv = sv[sk(max(j0 - 1, 0))];
+      prev0 = i0 == 0 ? pv : (j0 == 0 ? pu : (pu > pv ? pu : pv));
+    }
+    int i = i0, j = j0;
+    T ca = su[sk(i)], cb = sv[sk(j)];
+    T prev = prev0;
+    bool has_prev = d0 > 0;
+    int dups = 0, dist = 0;
+    uint32_t dmask = 0;  // bit q: output q is a distinct (first-copy) union value
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+      const T x = merge_step<T, K>(su, sv, i, j, ca, cb, sk);
+      const bool fin = TR::valid(x);
+      const bool dup = fin && has_prev && x == prev;
+      dups += dup;
+      if constexpr (kKmv) dmask |= (uint32_t)(fin && !dup) << q;
+      else dist += fin && !dup;
+      prev = x;
+      has_prev = true;
+    }
+    SortedStats st;
+    st.common = group_sum<G>(dups);
+    st.lu = la;
+    st.lv = lb;
+    st.kth = 0.0;
     if constexpr (kKmv) {
+      // T-th distinct union value: the owning lane selects the t-th set bit
+      // of its mask and re-splits the merge at that position (merge path)
+      dist = __popc(dmask);
       const int T_ = max(min(la, lb), 1);
-      T cand = TR::pad();
-      bool have = false;
-      // ranks of U elements: idx + 1 + lt_V - (#common among U[0..idx-1])
-      int carry = 0;
+      const int before = group_excl_scan<G>(dist, gl);
+      const int t = T_ - before;
+      const bool mine = t >= 1 && t <= dist;
+      int need = mine ? t : 1, pos = 0;
+      uint32_t m = dmask;
 #pragma unroll
-      for (int s = 0; s < CH; ++s) {
-        int cnt = 0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) cnt += inb[s][w];
-        const int before = carry + group_excl_scan<G>(cnt, gl);
-        carry += group_sum<G>(cnt);
-        int run = 0;
-        const int c = s * G + gl;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          const int idx = c * 8 + w;
-          if (TR::valid(a[s][w]) && idx + 1 + ltb[s][w] - (before + run) == T_) {
-            cand = a[s][w];
-            have = true;
-          }
-          run += inb[s][w];
-        }
+      for (int w = Q / 2; w >= 1; w >>= 1) {
+        const int c = __popc(m & ((1u << w) - 1u));
+        const bool up = need > c;
+        need = up ? need - c : need;
+        pos = up ? pos + w : pos;
+        m = up ? m >> w : m;
       }
-      // V elements not in U: idx + 1 + lt_U - (#common among V[0..idx-1])
-      carry = 0;
+      const int d = d0 + pos;
+      int lo2 = d > K ? d - K : 0, hi2 = d < K ? d : K;
 #pragma unroll
-      for (int s = 0; s < CH; ++s) {
-        int ltu[8];
-        bool inu[8];
-        int cnt = 0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          bool f = false;
-          int lt = 0;
-          if constexpr (CH == 1) {
-            lt = shfl_lower_bound<T, NC>(b[s][w], TR::valid(b[s][w]), ha, a[0], gbase, f);
-          } else {
-            if (TR::valid(b[s][w])) lt = sorted_lower_bound<T, NC>(b[s][w], ha, su, f);
-          }
-          ltu[w] = lt;
-          inu[w] = f;
-          cnt += f;
-        }
-        const int before = carry + group_excl_scan<G>(cnt, gl);
-        carry += group_sum<G>(cnt);
-        int run = 0;
-        const int c = s * G + gl;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          const int idx = c * 8 + w;
-          if (TR::valid(b[s][w]) && !inu[w] && idx + 1 + ltu[w] - (before + run) == T_) {
-            cand = b[s][w];
-            have = true;
-          }
-          run += inu[w];
-        }
+      for (int it = 0; it < LOG; ++it) {
+        const int mid = (lo2 + hi2) >> 1;
+        const bool go = lo2 < hi2;
+        const T x = su[sk(min(mid, K))];
+        const T y = sv[sk(max(d - 1 - mid, 0))];
+        const bool right = x <= y;
+        lo2 = (go && right) ? mid + 1 : lo2;
+        hi2 = (go && !right) ? mid : hi2;
       }
-      // the unique rank-T element, else merged[0] (reference argmax of all-False)
-      const unsigned gmask = ((G == 32) ? 0xffffffffu : ((1u << G) - 1u)) << gbase;
-      const unsigned hm = __ballot_sync(0xffffffffu, have) & gmask;
-      // shuffles are executed by every lane (hm differs between groups)
+      const T xa = su[sk(lo2)], xb = sv[sk(d - lo2)];
+      const T cand = xa <= xb ? xa : xb;
+      const unsigned hm = __ballot_sync(0xffffffffu, mine) & gmask;
       const uint64_t c1 = shfl64((uint64_t)cand, hm ? __ffs(hm) - 1 : gbase);
-      const uint64_t a0 = shfl64((uint64_t)a[0][0], gbase), b0 = shfl64((uint64_t)b[0][0], gbase);
-      st.kth = bitsd(hm ? c1 : (a0 < b0 ? a0 : b0));
+      const uint64_t u0 = shfl64((uint64_t)su[0], gbase), v0 = shfl64((uint64_t)sv[0], gbase);
+      st.kth = bitsd(hm ? c1 : (u0 < v0 ? u0 : v0));  // none: argmax of all-False -> merged[0]
     }
     if (valid && gl == 0) epi.edge(e, ul, vl, st);
     __syncwarp();
@@ -1102,10 +1195,16 @@ struct EpiKmv {
   }
 };
 
-template <int G, int CH, bool kKmv>
+template <int G, int CH>
 __host__ __device__ constexpr int sorted_warp_smem() {
-  // row copies for the shared-memory chunk search (CH > 1 only)
-  return CH == 1 ? 16 : (32 / G) * (kKmv ? 2 : 1) * G * CH * 8 * (kKmv ? 8 : 4);
+  // V-row copies for the shared-memory chunk search (CH > 1 only)
+  return CH == 1 ? 16 : (32 / G) * G * CH * 8 * 4;
+}
+
+template <int G, int CH, bool kKmv>
+__host__ __device__ constexpr int merge_warp_smem() {
+  // both (bank-skewed) rows of every edge of the warp's iteration
+  return (32 / G) * (2 * (G * CH * 9 + 1) + 1) * (kKmv ? 8 : 4);
 }
 
 template <int G, int CH, bool kFused>
@@ -1123,8 +1222,8 @@ __global__ void __launch_bounds__(kBlock) onehash_sorted_kernel(const int32_t* e
     __syncthreads();
   }
   EpiOnehash epi{k, sizes, out_count, out_est, kFused ? cnt_s : nullptr, slo_s, shi_s, 0};
-  sorted_edge_loop<G, CH, false>(ent, k, us, vs, e_begin, e_end,
-                                 smem_raw + (threadIdx.x >> 5) * sorted_warp_smem<G, CH, false>(), epi);
+  sorted_edge_loop<G, CH>(ent, k, us, vs, e_begin, e_end,
+                          smem_raw + (threadIdx.x >> 5) * sorted_warp_smem<G, CH>(), epi);
   if (kFused) {
     __syncthreads();
     for (int i = threadIdx.x; i <= k; i += blockDim.x) {
@@ -1150,8 +1249,8 @@ __global__ void __launch_bounds__(kBlock) kmv_sorted_kernel(const uint64_t* vals
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[kBlock / 32];
   EpiKmv epi{k, sizes, out_common, out_union, out_kth, out_est, kFused, 0.0};
-  sorted_edge_loop<G, 1, true>(vals, k, us, vs, e_begin, e_end,
-                               smem_raw + (threadIdx.x >> 5) * sorted_warp_smem<G, 1, true>(), epi);
+  merge_edge_loop<G, 1, true>(vals, k, us, vs, e_begin, e_end,
+                              smem_raw + (threadIdx.x >> 5) * merge_warp_smem<G, 1, true>(), epi);
   if (kFused) {
     double a = epi.acc;
     for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
@@ -1355,7 +1454,7 @@ static void launch_onehash_sorted(cudaStream_t s, const int32_t* ent, int k, con
                                   int32_t* out_count, double* out_est, int64_t* out_cnt,
                                   int64_t* out_ssum, int64_t* out_verbatim) {
   auto kern = onehash_sorted_kernel<G, CH, kFused>;
-  const size_t sm = (size_t)(kBlock / 32) * sorted_warp_smem<G, CH, false>();
+  const size_t sm = (size_t)(kBlock / 32) * sorted_warp_smem<G, CH>();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / G);
   kern<<<grid, kBlock, sm, s>>>(ent, k, sizes, us, vs, b, e, out_count, out_est, out_cnt, out_ssum,
@@ -1385,7 +1484,7 @@ static void launch_kmv_sorted(cudaStream_t s, const uint64_t* vals, int k, const
                               const int32_t* us, const int32_t* vs, int64_t b, int64_t e, int32_t* out_common,
                               int32_t* out_union, double* out_kth, double* out_est, double* out_sum) {
   auto kern = kmv_sorted_kernel<G, kFused>;
-  const size_t sm = (size_t)(kBlock / 32) * sorted_warp_smem<G, 1, true>();
+  const size_t sm = (size_t)(kBlock / 32) * merge_warp_smem<G, 1, true>();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / G);
   kern<<<grid, kBlock, sm, s>>>(vals, k, sizes, us, vs, b, e, out_common, out_union, out_kth, out_est, out_sum);
