@@ -66,6 +66,9 @@ PG_API int pg_device_sm_count(int* out_host);
 /* ---- a2: hash family  (hashing.py:78-111 HashFamily.__post_init__) --- */
 /* seed_i = mix64(base ^ mix64(i+1)), i < count; host-only, no device use */
 PG_API int pg_family_seeds(uint64_t base, int32_t count, uint64_t* out_host);
+/* the same seeds written to device memory on `stream` (no host transfer) */
+PG_API int pg_family_seeds_device(uint64_t base, int32_t count, uint64_t* out_dev,
+                                  void* stream);
 /* a1/a3 words: out[j] = mix64(seed ^ (uint64)keys[j])  (hashing.py:114-118) */
 PG_API int pg_hash_words(const int64_t* keys, int64_t count, uint64_t seed,
                   uint64_t* out, void* stream);
@@ -181,6 +184,16 @@ PG_API int pg_jaccard_count_khash(const int32_t* entries, int32_t k,
  * out_triples[0] = number of (u,v,w) triples. */
 PG_API int pg_4clique_bloom(const int64_t* dir_off, const int32_t* dir_adj,
                      const int32_t* src, int64_t e_begin, int64_t e_end,
+                     const uint64_t* rows_plus, int32_t bits, int32_t b,
+                     const uint64_t* seeds_dev, int32_t op,
+                     const int32_t* sizes, const double* lut,
+                     int64_t* out_hist, int64_t* out_sum_pos,
+                     int64_t* out_triples, void* stream);
+
+/* the same over a list of directed-edge indices (an edge sample): edge
+ * j = edge_ids[i] is (src[j], dir_adj[j]) */
+PG_API int pg_4clique_bloom_edges(const int64_t* dir_off, const int32_t* dir_adj,
+                     const int32_t* src, const int64_t* edge_ids, int64_t count,
                      const uint64_t* rows_plus, int32_t bits, int32_t b,
                      const uint64_t* seeds_dev, int32_t op,
                      const int32_t* sizes, const double* lut,

@@ -35,6 +35,7 @@ SIGNATURES = {
     "pg_last_error": [ctypes.c_char_p, c_size],
     "pg_device_sm_count": [ctypes.POINTER(ctypes.c_int)],
     "pg_family_seeds": [c_u64, c_i32, ctypes.POINTER(c_u64)],
+    "pg_family_seeds_device": [c_u64, c_i32, c_ptr, c_ptr],
     "pg_hash_words": [c_ptr, c_i64, c_u64, c_ptr, c_ptr],
     "pg_csr_upper_edges_workspace": [c_i64, c_i64, ctypes.POINTER(c_size)],
     "pg_csr_upper_edges": [c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i64,
@@ -67,6 +68,9 @@ SIGNATURES = {
     "pg_4clique_bloom": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i32,
                          c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr,
                          c_ptr, c_ptr],
+    "pg_4clique_bloom_edges": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_i32,
+                               c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr,
+                               c_ptr, c_ptr],
     "pg_4clique_exact": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr],
     "pg_pairs_exact": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
     "pg_l2_flush": [c_ptr, c_size, c_ptr],

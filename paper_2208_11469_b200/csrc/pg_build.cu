@@ -101,10 +101,10 @@ __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
       }
     }
     __syncwarp();
-    // the batch rows (hub rows are written by pass 2) and their ones
+    // the batch rows (hub rows are all-zero here; pass 2 ORs into them)
+    // and the non-hub ones
     const uint64_t* b64 = reinterpret_cast<const uint64_t*>(brows);
     for (int r = 0; r < nb; ++r) {
-      if (__shfl_sync(0xffffffffu, hub, r)) continue;
       for (uint32_t i = lane; i < words64; i += 32) rows[(vb + r) * words64 + i] = b64[r * words64 + i];
     }
     if (mine && !hub) {
@@ -116,51 +116,100 @@ __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
   }
 }
 
-// pass 2: one CTA per hub (grid-stride over the hub list)
+// pass 2: hub rows (zeroed by pass 1) are split into slices of
+// kHubSlice entries; the grid strides over the (hub, slice) items, each CTA
+// ORs its slice into a shared-memory row and then into the output row with
+// 64-bit global atomics.  Pass 3 counts the hubs' ones.
+constexpr int64_t kHubSlice = 2048;
+
 template <bool kPow2>
 __global__ void __launch_bounds__(kThreads) build_bloom_hubs_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, uint32_t bits, int b,
-    const uint64_t* __restrict__ seeds_dev, uint64_t* __restrict__ rows, int32_t* __restrict__ ones,
+    const uint64_t* __restrict__ seeds_dev, uint64_t* __restrict__ rows,
     const int32_t* __restrict__ hubs, const int32_t* __restrict__ hub_count) {
   extern __shared__ __align__(16) uint32_t smem[];
-  __shared__ int red[kWarps];
+  __shared__ int64_t s_v[kThreads], s_o[kThreads], s_d[kThreads], s_pre[kThreads + 1];
+  __shared__ int64_t s_wsum[kWarps];
   const uint32_t words32 = bits >> 5;
   const uint32_t words64 = bits >> 6;
   uint32_t* row = smem;
   uint64_t* seeds = reinterpret_cast<uint64_t*>(smem + words32 + (words32 & 1));
   for (int i = threadIdx.x; i < b; i += kThreads) seeds[i] = seeds_dev[i];
   const int nh = *hub_count;
-  const int lane = lane_id();
-  for (int hi = blockIdx.x; hi < nh; hi += gridDim.x) {
-    const int64_t v = hubs[hi];
-    const int64_t o = offsets[v];
-    const int64_t d = offsets[v + 1] - o;
-    for (uint32_t i = threadIdx.x; i < words32; i += kThreads) row[i] = 0u;
+  const int lane = lane_id(), wid = warp_id();
+  int64_t item_base = 0;  // (hub, slice) items before this batch of hubs
+  for (int h0 = 0; h0 < nh; h0 += kThreads) {
+    // stage kThreads hubs and the exclusive prefix of their slice counts
+    const int hi = h0 + threadIdx.x;
+    int64_t v = 0, o = 0, d = 0;
+    if (hi < nh) {
+      v = hubs[hi];
+      o = offsets[v];
+      d = offsets[v + 1] - o;
+    }
+    const int64_t ns = (d + kHubSlice - 1) / kHubSlice;
+    int64_t inc = ns;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const int64_t y = __shfl_up_sync(0xffffffffu, inc, off);
+      if (lane >= off) inc += y;
+    }
+    if (lane == 31) s_wsum[wid] = inc;
     __syncthreads();
-    for (int64_t j = threadIdx.x; j < d; j += kThreads) {
-      const int32_t x = adj[o + j];
-      for (int h = 0; h < b; ++h) {
-        const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x), bits);
-        atomicOr(&row[p >> 5], 1u << (p & 31));
+    int64_t wbase = 0;
+    for (int w = 0; w < wid; ++w) wbase += s_wsum[w];
+    s_v[threadIdx.x] = v;
+    s_o[threadIdx.x] = o;
+    s_d[threadIdx.x] = d;
+    s_pre[threadIdx.x] = wbase + inc - ns;
+    if (threadIdx.x == kThreads - 1) s_pre[kThreads] = wbase + inc;
+    __syncthreads();
+    const int64_t total = s_pre[kThreads];
+    int64_t t = ((int64_t)blockIdx.x - item_base) % (int64_t)gridDim.x;
+    if (t < 0) t += gridDim.x;
+    for (; t < total; t += gridDim.x) {
+      int lo = 0, hi2 = kThreads - 1;  // last hub j with s_pre[j] <= t
+      while (lo < hi2) {
+        const int mid = (lo + hi2 + 1) >> 1;
+        if (s_pre[mid] <= t) lo = mid;
+        else hi2 = mid - 1;
       }
+      const int64_t hv = s_v[lo], ho = s_o[lo], hd = s_d[lo];
+      const int64_t beg = (t - s_pre[lo]) * kHubSlice, end = min(hd, beg + kHubSlice);
+      for (uint32_t i = threadIdx.x; i < words32; i += kThreads) row[i] = 0u;
+      __syncthreads();
+      for (int64_t j = beg + threadIdx.x; j < end; j += kThreads) {
+        const int32_t x = adj[ho + j];
+        for (int h = 0; h < b; ++h) {
+          const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x), bits);
+          atomicOr(&row[p >> 5], 1u << (p & 31));
+        }
+      }
+      __syncthreads();
+      const uint64_t* row64 = reinterpret_cast<const uint64_t*>(row);
+      for (uint32_t i = threadIdx.x; i < words64; i += kThreads) {
+        const uint64_t w = row64[i];
+        if (w) atomicOr(reinterpret_cast<unsigned long long*>(rows + hv * words64 + i), (unsigned long long)w);
+      }
+      __syncthreads();
     }
+    item_base += total;
     __syncthreads();
-    int cnt = 0;
-    const uint64_t* row64 = reinterpret_cast<const uint64_t*>(row);
-    for (uint32_t i = threadIdx.x; i < words64; i += kThreads) {
-      const uint64_t w = row64[i];
-      cnt += __popcll(w);
-      rows[v * words64 + i] = w;
-    }
-    cnt = __reduce_add_sync(0xffffffffu, cnt);
-    if (lane == 0) red[warp_id()] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int t = 0;
-      for (int w = 0; w < kWarps; ++w) t += red[w];
-      ones[v] = t;
-    }
-    __syncthreads();
+  }
+}
+
+// pass 3: ones of the hub rows, one warp per hub
+__global__ void __launch_bounds__(kThreads) bloom_hub_ones_kernel(
+    const uint64_t* __restrict__ rows, uint32_t words64, int32_t* __restrict__ ones,
+    const int32_t* __restrict__ hubs, const int32_t* __restrict__ hub_count) {
+  const int nh = *hub_count;
+  const int lane = lane_id();
+  for (int hi = blockIdx.x * kWarps + warp_id(); hi < nh; hi += gridDim.x * kWarps) {
+    const int64_t v = hubs[hi];
+    int c = 0;
+    for (uint32_t i = lane; i < words64; i += 32) c += __popcll(rows[v * words64 + i]);
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) ones[v] = c;
   }
 }
 
@@ -510,6 +559,7 @@ struct HubList {
   int init(const int64_t* offsets, int64_t n, cudaStream_t st) {
     (void)offsets;
     s = st;
+    retain_default_pool();
     cudaError_t e = cudaMallocAsync(&buf, sizeof(int32_t) * (size_t)(n + 1), s);
     if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, sizeof(int32_t), s);
     if (e != cudaSuccess) return fail(PG_ERR_CUDA, "hub list: %s", cudaGetErrorString(e));
@@ -581,7 +631,8 @@ int pg_build_bloom(const int64_t* offsets, const int32_t* adj, int64_t n, int32_
     build_bloom_kernel<P2><<<grid, kThreads, smem, s>>>(offsets, adj, n, bits, b, R, seeds_dev, rows, ones, \
                                                         hubs.ids, hubs.count);                          \
     build_bloom_hubs_kernel<P2><<<hub_grid(), kThreads, smem_hub, s>>>(offsets, adj, bits, b, seeds_dev,  \
-                                                                       rows, ones, hubs.ids, hubs.count); \
+                                                                       rows, hubs.ids, hubs.count);       \
+    bloom_hub_ones_kernel<<<64, kThreads, 0, s>>>(rows, bits / 64, ones, hubs.ids, hubs.count);          \
   }
   if (pow2) PG_BB(true)
   else PG_BB(false)

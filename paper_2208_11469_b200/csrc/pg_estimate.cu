@@ -1284,7 +1284,8 @@ __global__ void __launch_bounds__(kBlock) clique4_bloom_kernel(
     const int64_t* __restrict__ off, const int32_t* __restrict__ adjp, const int32_t* __restrict__ src,
     int64_t e_begin, int64_t e_end, const uint64_t* __restrict__ rows, int bits, int b,
     const uint64_t* __restrict__ seeds_dev, int op, const int32_t* __restrict__ sizes,
-    const double* __restrict__ lut, int64_t* out_hist, int64_t* out_sum_pos, int64_t* out_triples) {
+    const double* __restrict__ lut, int64_t* out_hist, int64_t* out_sum_pos, int64_t* out_triples,
+    const int64_t* __restrict__ edge_ids) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int words32 = bits >> 5, words64 = bits >> 6;
   int* hist_s = reinterpret_cast<int*>(smem_raw);                                   // bits+1
@@ -1300,7 +1301,8 @@ __global__ void __launch_bounds__(kBlock) clique4_bloom_kernel(
   long long triples = 0, sum_pos = 0;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   for (int64_t j = e_begin + (int64_t)blockIdx.x * (blockDim.x >> 5) + w; j < e_end; j += nwarps) {
-    const int32_t u = src[j], v = adjp[j];
+    const int64_t jj = edge_ids ? edge_ids[j] : j;  // optional edge sample
+    const int32_t u = src[jj], v = adjp[jj];
     const int32_t* A = adjp + off[u];
     int64_t la = off[u + 1] - off[u];
     const int32_t* Bv = adjp + off[v];
@@ -1837,10 +1839,13 @@ int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k, const int
   return check_launch("tc_kmv");
 }
 
-int pg_4clique_bloom(const int64_t* dir_off, const int32_t* dir_adj, const int32_t* src, int64_t e_begin,
-                     int64_t e_end, const uint64_t* rows_plus, int32_t bits, int32_t b,
-                     const uint64_t* seeds_dev, int32_t op, const int32_t* sizes, const double* lut,
-                     int64_t* out_hist, int64_t* out_sum_pos, int64_t* out_triples, void* stream) {
+}  // extern "C"
+
+static int clique4_bloom(const int64_t* dir_off, const int32_t* dir_adj, const int32_t* src,
+                         const int64_t* edge_ids, int64_t e_begin, int64_t e_end, const uint64_t* rows_plus,
+                         int32_t bits, int32_t b, const uint64_t* seeds_dev, int32_t op, const int32_t* sizes,
+                         const double* lut, int64_t* out_hist, int64_t* out_sum_pos, int64_t* out_triples,
+                         void* stream) {
   PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
   if (bits > 16384) return fail(PG_ERR_UNSUPPORTED, "4-clique kernel supports Bloom widths up to 16384");
   PG_REQUIRE(b >= 1 && b <= 64, "Bloom hash count must be in [1, 64]");
@@ -1860,8 +1865,29 @@ int pg_4clique_bloom(const int64_t* dir_off, const int32_t* dir_adj, const int32
   const int grid = grid_cap(grid_for_kernel(clique4_bloom_kernel, smem), e_end - e_begin, kBlock / 32);
   clique4_bloom_kernel<<<grid, kBlock, smem, s>>>(dir_off, dir_adj, src, e_begin, e_end, rows_plus, bits, b,
                                                   seeds_dev, op, sizes, lut, out_hist, out_sum_pos,
-                                                  out_triples);
+                                                  out_triples, edge_ids);
   return check_launch("4clique_bloom");
+}
+
+extern "C" {
+
+int pg_4clique_bloom(const int64_t* dir_off, const int32_t* dir_adj, const int32_t* src, int64_t e_begin,
+                     int64_t e_end, const uint64_t* rows_plus, int32_t bits, int32_t b,
+                     const uint64_t* seeds_dev, int32_t op, const int32_t* sizes, const double* lut,
+                     int64_t* out_hist, int64_t* out_sum_pos, int64_t* out_triples, void* stream) {
+  return clique4_bloom(dir_off, dir_adj, src, nullptr, e_begin, e_end, rows_plus, bits, b, seeds_dev, op,
+                       sizes, lut, out_hist, out_sum_pos, out_triples, stream);
+}
+
+int pg_4clique_bloom_edges(const int64_t* dir_off, const int32_t* dir_adj, const int32_t* src,
+                           const int64_t* edge_ids, int64_t count, const uint64_t* rows_plus, int32_t bits,
+                           int32_t b, const uint64_t* seeds_dev, int32_t op, const int32_t* sizes,
+                           const double* lut, int64_t* out_hist, int64_t* out_sum_pos, int64_t* out_triples,
+                           void* stream) {
+  PG_REQUIRE(count >= 0, "count must be >= 0");
+  PG_REQUIRE(count == 0 || edge_ids, "null edge ids");
+  return clique4_bloom(dir_off, dir_adj, src, edge_ids, 0, count, rows_plus, bits, b, seeds_dev, op, sizes,
+                       lut, out_hist, out_sum_pos, out_triples, stream);
 }
 
 int pg_4clique_exact(const int64_t* dir_off, const int32_t* dir_adj, const int32_t* src, int64_t e_begin,

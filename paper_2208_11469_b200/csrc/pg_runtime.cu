@@ -43,6 +43,26 @@ __global__ void l2_flush_kernel(uint4* buf, size_t n16, uint32_t salt) {
   for (; i < n16; i += stride) buf[i] = make_uint4(salt, (uint32_t)i, salt, 0u);
 }
 
+__global__ void family_seeds_kernel(uint64_t base, int32_t count, uint64_t* out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < count) out[i] = mix64(base ^ mix64(static_cast<uint64_t>(i) + 1ull));
+}
+
+// Scratch allocations (cudaMallocAsync) come from the device's default pool;
+// keep its memory across synchronisations instead of releasing it at every
+// sync point and mapping it again on the next call.
+void retain_default_pool() {
+  static bool done[64] = {false};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64 || done[dev]) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    uint64_t keep = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  done[dev] = true;
+}
+
 }  // namespace pg
 
 extern "C" {
@@ -72,6 +92,13 @@ int pg_family_seeds(uint64_t base, int32_t count, uint64_t* out_host) {
   for (int32_t i = 0; i < count; ++i)
     out_host[i] = pg::mix64(base ^ pg::mix64(static_cast<uint64_t>(i) + 1ull));
   return PG_OK;
+}
+
+int pg_family_seeds_device(uint64_t base, int32_t count, uint64_t* out_dev, void* stream) {
+  if (count < 1) return pg::fail(PG_ERR_INVALID, "hash family needs at least one function");
+  if (!out_dev) return pg::fail(PG_ERR_INVALID, "null output");
+  pg::family_seeds_kernel<<<(count + 127) / 128, 128, 0, pg::as_stream(stream)>>>(base, count, out_dev);
+  return pg::check_launch("family_seeds");
 }
 
 int pg_l2_flush(void* buf, size_t bytes, void* stream) {

@@ -17,6 +17,7 @@ definitions are documented in DESIGN.md.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -38,8 +39,34 @@ def _to_device(a, dtype):
     return t.to("cuda", non_blocking=t.is_pinned()).to(dtype)
 
 
+_SIDE_STREAMS = {}
+
+
+def side_stream(name: str):
+    """Process-wide auxiliary CUDA stream (copy / build overlap)."""
+    import torch
+    dev = torch.cuda.current_device()
+    key = (name, dev)
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = torch.cuda.Stream()
+    return _SIDE_STREAMS[key]
+
+
+# pinned int32 adjacencies at least this large are uploaded in chunks
+# (PG_UPLOAD_CHUNKS=0 disables the chunked path)
+CHUNKED_UPLOAD_MIN_BYTES = 32 << 20
+UPLOAD_CHUNKS = int(os.environ.get("PG_UPLOAD_CHUNKS", "8"))
+
+
 class DeviceCsr:
-    """Device copy of a CSR (graph or directed view) and derived edge lists."""
+    """Device copy of a CSR (graph or directed view) and derived edge lists.
+
+    A pinned int32 adjacency of at least CHUNKED_UPLOAD_MIN_BYTES is uploaded
+    on a copy stream in UPLOAD_CHUNKS vertex-range chunks with one event each
+    (``upload_chunks``), so the first sketch build can start on a chunk as
+    soon as it lands (sketches._build_on_device); the current stream waits for
+    the whole upload, so every other consumer is ordered after it.
+    """
 
     def __init__(self, offsets: np.ndarray, adjacency: np.ndarray):
         import torch
@@ -47,14 +74,54 @@ class DeviceCsr:
             raise ValueError("vertex IDs must fit in int32 on the device")
         self.n = len(offsets) - 1
         self.nnz = len(adjacency)
-        # host arrays go up as they are (int64 in the reference contract) and
-        # are narrowed on the device: no host-side conversion pass
-        self.offsets = _to_device(offsets, torch.int64)
-        self.adj = _to_device(adjacency, torch.int32)
+        self.upload_chunks = []
+        adj_t = torch.from_numpy(np.ascontiguousarray(adjacency))
+        if (UPLOAD_CHUNKS > 0 and adj_t.dtype == torch.int32 and adj_t.is_pinned()
+                and adjacency.nbytes >= CHUNKED_UPLOAD_MIN_BYTES and self.n > 0):
+            self._chunked_upload(np.asarray(offsets), adj_t)
+        else:
+            # host arrays go up as they are (int64 in the reference contract)
+            # and are narrowed on the device: no host-side conversion pass
+            self.offsets = _to_device(offsets, torch.int64)
+            self.adj = _to_device(adjacency, torch.int32)
         self.degrees = (self.offsets[1:] - self.offsets[:-1]).to(torch.int32)
         self._upper = None
         self._src = None
         self._layouts = {}
+
+    def _chunked_upload(self, offsets: np.ndarray, adj_t) -> None:
+        import torch
+        cur = torch.cuda.current_stream()
+        cs = side_stream("copy")
+        self.offsets = torch.empty(self.n + 1, dtype=torch.int64, device="cuda")
+        self.adj = torch.empty(self.nnz, dtype=torch.int32, device="cuda")
+        off_t = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64))
+        # equal-volume chunks (tapered tails and per-chunk offsets slices
+        # measured slower: each extra DMA + build launch costs more than the
+        # shorter tail saves).  int64 needles: float needles would convert
+        # all of `offsets`.
+        targets = (np.arange(UPLOAD_CHUNKS + 1, dtype=np.int64) * self.nnz) // UPLOAD_CHUNKS
+        cuts = np.searchsorted(offsets, targets, side="left")
+        cuts[0], cuts[-1] = 0, self.n
+        cuts = np.unique(cuts)
+        cs.wait_stream(cur)  # the new blocks may still be in use on cur
+        with torch.cuda.stream(cs):
+            self.offsets.copy_(off_t, non_blocking=True)
+            for v0, v1 in zip(cuts[:-1].tolist(), cuts[1:].tolist()):
+                a, b = int(offsets[v0]), int(offsets[v1])
+                if b > a:
+                    self.adj[a:b].copy_(adj_t[a:b], non_blocking=True)
+                ev = torch.cuda.Event()
+                ev.record(cs)
+                self.upload_chunks.append((v0, v1, ev))
+        self.offsets.record_stream(cs)
+        self.adj.record_stream(cs)
+        cur.wait_stream(cs)
+
+    def take_upload_chunks(self):
+        """The pending (v0, v1, event) upload chunks, once (first consumer)."""
+        chunks, self.upload_chunks = self.upload_chunks, []
+        return chunks
 
     @classmethod
     def from_tensors(cls, offsets, adj) -> "DeviceCsr":
@@ -65,6 +132,7 @@ class DeviceCsr:
         self.nnz = adj.numel()
         self.offsets = offsets
         self.adj = adj
+        self.upload_chunks = []
         self.degrees = (offsets[1:] - offsets[:-1]).to(torch.int32)
         self._upper = None
         self._src = None

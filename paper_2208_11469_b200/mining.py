@@ -130,8 +130,10 @@ def four_clique_count(view: DirectedView, provider: IntersectionProvider,
 
 
 def four_clique_counts(view: DirectedView, provider: BloomProvider,
-                       e_begin: int, e_end: int):
-    """Device int64 [hist(B+1), sum_pos, triples] for directed edges range."""
+                       e_begin: int, e_end: int, edge_ids=None):
+    """Device int64 [hist(B+1), sum_pos, triples] for the directed edges
+    [e_begin, e_end), or for the directed-edge indices `edge_ids` (a sample;
+    host or device int64) when given."""
     import torch
     dev = view.device()
     sg = provider.sketched
@@ -140,11 +142,20 @@ def four_clique_counts(view: DirectedView, provider: BloomProvider,
     hist = torch.empty(bits + 1, dtype=torch.int64, device="cuda")
     spos = torch.empty(1, dtype=torch.int64, device="cuda")
     trip = torch.empty(1, dtype=torch.int64, device="cuda")
-    N.call("pg_4clique_bloom", N.ptr(dev.offsets), N.ptr(dev.adj),
-           N.ptr(dev.row_sources()), e_begin, e_end, N.ptr(d["rows"]), bits,
-           sg.hash_count, N.ptr(d["seeds"]), provider.op, N.ptr(d["sizes"]),
-           N.ptr(provider.lut_device()), N.ptr(hist), N.ptr(spos), N.ptr(trip),
-           N.stream_handle())
+    tail = (N.ptr(d["rows"]), bits, sg.hash_count, N.ptr(d["seeds"]), provider.op,
+            N.ptr(d["sizes"]), N.ptr(provider.lut_device()), N.ptr(hist), N.ptr(spos),
+            N.ptr(trip), N.stream_handle())
+    if edge_ids is None:
+        N.call("pg_4clique_bloom", N.ptr(dev.offsets), N.ptr(dev.adj),
+               N.ptr(dev.row_sources()), e_begin, e_end, *tail)
+    else:
+        ids = torch.as_tensor(np.asarray(edge_ids, dtype=np.int64)
+                              if not isinstance(edge_ids, torch.Tensor) else edge_ids)
+        ids = ids.to(device="cuda", dtype=torch.int64).contiguous()
+        if ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= dev.nnz):
+            raise ValueError("edge id out of range")
+        N.call("pg_4clique_bloom_edges", N.ptr(dev.offsets), N.ptr(dev.adj),
+               N.ptr(dev.row_sources()), N.ptr(ids), ids.numel(), *tail)
     return torch.cat([hist, spos, trip])
 
 

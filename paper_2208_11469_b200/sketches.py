@@ -200,7 +200,8 @@ class SketchedGraph:
 
     def __init__(self, kind, plan: BudgetPlan, family: HashFamily,
                  source: str, sizes, *, bit_matrix=None, ones=None,
-                 entries=None, lengths=None, values=None, device=None):
+                 entries=None, lengths=None, values=None, device=None,
+                 ready=None):
         self.kind = SketchKind(kind)
         self.plan = plan
         self.family = family
@@ -220,6 +221,14 @@ class SketchedGraph:
                       "entries": entries, "lengths": lengths,
                       "values": values}
         self._dev = dict(device) if device else {}
+        # CUDA event after which the device tensors are complete (builds on
+        # a side stream); consumers' streams wait on it at access time
+        self._ready = ready
+
+    def _wait_ready(self) -> None:
+        if self._ready is not None:
+            import torch
+            torch.cuda.current_stream().wait_event(self._ready)
 
     @property
     def sizes(self) -> np.ndarray:
@@ -246,6 +255,7 @@ class SketchedGraph:
         """Device buffers; uploads host arrays on first use if needed."""
         import torch
         from .graphs import _to_device
+        self._wait_ready()
         d = self._dev
         if "sizes" not in d:
             d["sizes"] = _to_device(self.sizes, torch.int32)
@@ -271,6 +281,7 @@ class SketchedGraph:
             t = self._dev.get({"bit_matrix": "rows"}.get(name, name))
             if t is None:
                 return None
+            self._wait_ready()
             a = t.cpu().numpy()
             if name == "bit_matrix":
                 a = a.view(np.uint64)
@@ -312,44 +323,95 @@ class SketchedGraph:
         return self.extra_bits_used() // 8
 
 
-def _build_on_device(dev: DeviceCsr, kind: SketchKind, plan: BudgetPlan,
-                     family: HashFamily, source: str,
-                     sizes: np.ndarray) -> SketchedGraph:
-    import torch
+def _launch_builders(dev: DeviceCsr, kind: SketchKind, plan: BudgetPlan, seeds, out,
+                     v0: int, v1: int, stream: int) -> None:
+    """Build the sketches of vertices [v0, v1) into the rows of `out`."""
     from . import _native as N
-    n = dev.n
-    st = N.stream_handle()
-    seeds = torch.from_numpy(family.seeds_array().view(np.int64)).cuda()
-    out = {"seeds": seeds, "sizes": dev.degrees}
+    n = v1 - v0
+    if n <= 0:
+        return
+    off = N.ptr(dev.offsets) + 8 * v0  # offsets stay absolute into adj
+
+    def row(t):
+        return N.ptr(t) + v0 * t.stride(0) * t.element_size()
+
+    if kind is SketchKind.BLOOM:
+        N.call("pg_build_bloom", off, N.ptr(dev.adj), n, plan.bits_per_vertex,
+               plan.hash_count, N.ptr(seeds), row(out["rows"]), row(out["ones"]), stream)
+        return
+    k = plan.entries_per_vertex
+    if kind is SketchKind.KHASH:
+        N.call("pg_build_khash", off, N.ptr(dev.adj), n, k, N.ptr(seeds),
+               row(out["entries"]), stream)
+    elif kind is SketchKind.ONEHASH:
+        N.call("pg_build_onehash", off, N.ptr(dev.adj), n, k, N.ptr(seeds),
+               row(out["entries"]), row(out["lengths"]), stream)
+    else:
+        N.call("pg_build_kmv", off, N.ptr(dev.adj), n, k, N.ptr(seeds),
+               row(out["values"]), row(out["lengths"]), stream)
+
+
+def _alloc_outputs(kind: SketchKind, plan: BudgetPlan, n: int) -> dict:
+    import torch
     alloc_n = max(n, 1)
     if kind is SketchKind.BLOOM:
         words = plan.bits_per_vertex // WORD_BITS
-        rows = torch.empty((alloc_n, words), dtype=torch.int64, device="cuda")
-        ones = torch.empty(alloc_n, dtype=torch.int32, device="cuda")
-        N.call("pg_build_bloom", N.ptr(dev.offsets), N.ptr(dev.adj), n,
-               plan.bits_per_vertex, plan.hash_count, N.ptr(seeds), N.ptr(rows),
-               N.ptr(ones), st)
-        out.update(rows=rows[:n], ones=ones[:n])
+        return {"rows": torch.empty((alloc_n, words), dtype=torch.int64, device="cuda"),
+                "ones": torch.empty(alloc_n, dtype=torch.int32, device="cuda")}
+    k = plan.entries_per_vertex
+    if kind is SketchKind.KHASH:
+        return {"entries": torch.empty((alloc_n, k), dtype=torch.int32, device="cuda")}
+    if kind is SketchKind.ONEHASH:
+        return {"entries": torch.empty((alloc_n, k), dtype=torch.int32, device="cuda"),
+                "lengths": torch.empty(alloc_n, dtype=torch.int32, device="cuda")}
+    return {"values": torch.empty((alloc_n, k), dtype=torch.float64, device="cuda"),
+            "lengths": torch.empty(alloc_n, dtype=torch.int32, device="cuda")}
+
+
+def _build_on_device(dev: DeviceCsr, kind: SketchKind, plan: BudgetPlan,
+                     family: HashFamily, source: str,
+                     sizes: np.ndarray) -> SketchedGraph:
+    """Launch the builders on the device.  If the CSR upload is still in
+    flight in chunks (DeviceCsr.upload_chunks), build each chunk on a side
+    stream as soon as it lands, overlapping the H2D copy with the build; the
+    result then carries a readiness event (SketchedGraph._wait_ready)."""
+    import torch
+    from . import _native as N
+    from .graphs import side_stream
+    n = dev.n
+
+    def device_seeds(stream):
+        # derived on the device: a host copy would queue behind the CSR upload
+        seeds = torch.empty(family.count, dtype=torch.int64, device="cuda")
+        N.call("pg_family_seeds_device", family.base_seed, family.count, N.ptr(seeds), stream)
+        return seeds
+
+    chunks = dev.take_upload_chunks()
+    if chunks:
+        cur = torch.cuda.current_stream()
+        bs = side_stream("build")
+        with torch.cuda.stream(bs):  # allocations ordered on bs
+            seeds = device_seeds(bs.cuda_stream)
+            out = _alloc_outputs(kind, plan, n)
+            for v0, v1, ev in chunks:
+                bs.wait_event(ev)
+                _launch_builders(dev, kind, plan, seeds, out, v0, v1, bs.cuda_stream)
+            ready = torch.cuda.Event()
+            ready.record(bs)
+        # consumers wait for `ready` when they touch the sketches
+        # (SketchedGraph._wait_ready), so work that only needs the CSR -- the
+        # edge-slot layout -- overlaps the last chunks' build
+        seeds.record_stream(cur)
+        for t in out.values():
+            t.record_stream(cur)
     else:
-        k = plan.entries_per_vertex
-        if kind is SketchKind.KHASH:
-            ent = torch.empty((alloc_n, k), dtype=torch.int32, device="cuda")
-            N.call("pg_build_khash", N.ptr(dev.offsets), N.ptr(dev.adj), n, k,
-                   N.ptr(seeds), N.ptr(ent), st)
-            out.update(entries=ent[:n])
-        elif kind is SketchKind.ONEHASH:
-            ent = torch.empty((alloc_n, k), dtype=torch.int32, device="cuda")
-            ln = torch.empty(alloc_n, dtype=torch.int32, device="cuda")
-            N.call("pg_build_onehash", N.ptr(dev.offsets), N.ptr(dev.adj), n, k,
-                   N.ptr(seeds), N.ptr(ent), N.ptr(ln), st)
-            out.update(entries=ent[:n], lengths=ln[:n])
-        else:
-            val = torch.empty((alloc_n, k), dtype=torch.float64, device="cuda")
-            ln = torch.empty(alloc_n, dtype=torch.int32, device="cuda")
-            N.call("pg_build_kmv", N.ptr(dev.offsets), N.ptr(dev.adj), n, k,
-                   N.ptr(seeds), N.ptr(val), N.ptr(ln), st)
-            out.update(values=val[:n], lengths=ln[:n])
-    return SketchedGraph(kind, plan, family, source, sizes, device=out)
+        ready = None
+        seeds = device_seeds(N.stream_handle())
+        out = _alloc_outputs(kind, plan, n)
+        _launch_builders(dev, kind, plan, seeds, out, 0, n, N.stream_handle())
+    out = {key: t[:n] for key, t in out.items()}
+    out.update(seeds=seeds, sizes=dev.degrees)
+    return SketchedGraph(kind, plan, family, source, sizes, device=out, ready=ready)
 
 
 def build_sketched_graph(graph: CsrGraph, kind, s: float, b: int = 1,

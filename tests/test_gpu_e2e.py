@@ -1,0 +1,97 @@
+"""The end-to-end host-input path: chunked pinned upload overlapped with the
+sketch build (graphs.DeviceCsr._chunked_upload, sketches._build_on_device)
+must give bit-identical sketches and estimates to the plain path."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _pinned(a):
+    import torch
+    t = torch.empty(a.shape, dtype=torch.from_numpy(a[:0]).dtype, pin_memory=True)
+    t.numpy()[...] = a
+    return t.numpy()
+
+
+def _device_arrays(sk):
+    return {k: v.cpu().numpy() for k, v in sk.device_tensors().items()}
+
+
+@pytest.mark.parametrize("kind,kw", [("bloom", {"bits_override": 1024, "b": 2}),
+                                     ("bloom", {"bits_override": 2048, "b": 1}),
+                                     ("khash", {"k_override": 32}),
+                                     ("onehash", {"k_override": 64}),
+                                     ("kmv", {"k_override": 64})])
+@pytest.mark.parametrize("chunks", [1, 3, 8, 64])
+def test_chunked_upload_build_identical(monkeypatch, kind, kw, chunks):
+    import paper_2208_11469_b200 as pg
+    from paper_2208_11469_b200 import graphs
+    g = pg.generate_kronecker(14, 16, 7)  # R-MAT hubs + isolated vertices
+    ref = pg.build_sketched_graph(g, kind, s=1.0, **kw)
+    want = _device_arrays(ref)
+    monkeypatch.setattr(graphs, "CHUNKED_UPLOAD_MIN_BYTES", 0)
+    monkeypatch.setattr(graphs, "UPLOAD_CHUNKS", chunks)
+    hg = pg.CsrGraph(_pinned(g.offsets), _pinned(g.adjacency.astype(np.int32)))
+    dev = hg.device()
+    assert dev.upload_chunks, "pinned int32 input must take the chunked path"
+    got_sk = pg.build_sketched_graph(hg, kind, s=1.0, **kw)
+    assert not dev.upload_chunks
+    got = _device_arrays(got_sk)
+    assert sorted(got) == sorted(want)
+    for key in want:
+        assert np.array_equal(got[key], want[key]), key
+    est_kind = {"bloom": "bf_and"}.get(kind, kind)
+    # integer reductions are exact; KMV's fp64 sum is order-dependent in the last bits
+    assert pg.tc_estimate(hg, got_sk, est_kind) == pytest.approx(
+        pg.tc_estimate(g, ref, est_kind), rel=1e-12)
+    # a second sketch of the same (already resident) graph uses the plain path
+    again = pg.build_sketched_graph(hg, kind, s=1.0, **kw)
+    for key, v in _device_arrays(again).items():
+        assert np.array_equal(v, want[key]), key
+
+
+def test_chunked_upload_csr_identical(monkeypatch):
+    import paper_2208_11469_b200 as pg
+    from paper_2208_11469_b200 import graphs
+    g = pg.generate_erdos_renyi_gnm(5000, 40000, 3)
+    monkeypatch.setattr(graphs, "CHUNKED_UPLOAD_MIN_BYTES", 0)
+    hg = pg.CsrGraph(_pinned(g.offsets), _pinned(g.adjacency.astype(np.int32)))
+    dev = hg.device()
+    assert np.array_equal(dev.offsets.cpu().numpy(), g.offsets)
+    assert np.array_equal(dev.adj.cpu().numpy(), g.adjacency)
+    us, vs = dev.upper_edges()
+    e = g.edges()
+    assert np.array_equal(us.cpu().numpy(), e[:, 0]) and np.array_equal(vs.cpu().numpy(), e[:, 1])
+
+
+def test_bloom_hub_slices_match_oracle():
+    """Rows of hub vertices (degree > 1024, built in 2048-entry slices by many
+    CTAs with global atomics) equal the oracle's rows."""
+    import paper_2208_11469_b200 as pg
+    from oracle import oracle as O
+    n = 9000
+    # vertex 0 adjacent to everything, vertex 1 to the even vertices, a ring
+    src = [np.zeros(n - 1, np.int64), np.ones(len(range(2, n, 2)), np.int64),
+           np.arange(2, n - 1, dtype=np.int64)]
+    dst = [np.arange(1, n, dtype=np.int64), np.arange(2, n, 2, dtype=np.int64),
+           np.arange(3, n, dtype=np.int64)]
+    g = pg.CsrGraph.from_edges(np.stack([np.concatenate(src), np.concatenate(dst)], 1), n)
+    assert g.degree(0) > 4 * 2048
+    for bits, b in ((1024, 2), (512, 3), (2048, 1)):
+        sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=b, bits_override=bits, seed=11)
+        rows, ones = O.C.build_bloom(g.offsets, g.adjacency, bits, b, seed=11)
+        assert np.array_equal(sk.bit_matrix, rows)
+        assert np.array_equal(sk.ones, ones)
+
+
+def test_device_seeds_match_host_family():
+    import torch
+    from paper_2208_11469_b200 import _native as N
+    from paper_2208_11469_b200.hashing import HashFamily
+    for base, count in ((0x9E3779B97F4A7C15, 1), (17, 64), (2 ** 64 - 1, 33)):
+        fam = HashFamily(base_seed=base, count=count)
+        out = torch.empty(count, dtype=torch.int64, device="cuda")
+        N.call("pg_family_seeds_device", fam.base_seed, count, N.ptr(out), N.stream_handle())
+        assert np.array_equal(out.cpu().numpy().view(np.uint64), fam.seeds_array())
