@@ -206,6 +206,15 @@ PG_API int pg_4clique_exact(const int64_t* dir_off, const int32_t* dir_adj,
                      const int32_t* src, int64_t e_begin, int64_t e_end,
                      int64_t* out_count, void* stream);
 
+/* Jarvis-Patrick clustering tail (mining.py:213-245): edge i = (us[i],
+ * vs[i]) is kept iff scores[i] > tau; out[0] = kept edges, out[1] =
+ * connected components of the kept-edge graph (ClusterResult.cluster_count),
+ * out[2] = vertices touched by a kept edge (singleton_count = n - out[2]);
+ * keep_out (nullable) receives each edge's 0/1 keep flag */
+PG_API int pg_jp_components(const int32_t* us, const int32_t* vs,
+                     const double* scores, int64_t count, double tau,
+                     int64_t n, uint8_t* keep_out, int64_t* out, void* stream);
+
 /* exact |N(u) & N(v)| per pair over a sorted CSR (providers.py:102-115
  * ExactProvider.pair_many; setops.py:23-51) */
 PG_API int pg_pairs_exact(const int64_t* offsets, const int32_t* adj,

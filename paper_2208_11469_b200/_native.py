@@ -73,6 +73,8 @@ SIGNATURES = {
                                c_ptr, c_ptr],
     "pg_4clique_exact": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr],
     "pg_pairs_exact": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
+    "pg_jp_components": [c_ptr, c_ptr, c_ptr, c_i64, c_dbl, c_i64, c_ptr,
+                         c_ptr, c_ptr],
     "pg_l2_flush": [c_ptr, c_size, c_ptr],
     "pg_rmat_pairs": [c_u64, c_u64, c_u64, c_u64, c_i32, c_i64, c_dbl, c_dbl,
                       c_dbl, c_ptr, c_ptr, c_ptr],

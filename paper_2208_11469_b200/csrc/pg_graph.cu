@@ -107,6 +107,82 @@ static size_t maxscan_temp_bytes(int64_t n) {
 
 static size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// ---- Jarvis-Patrick components (mining.py:213-245): lock-free union-find
+// over the kept edges.  Roots are hooked larger-index under smaller-index
+// with atomicCAS, so parent[x] <= x always and the find loop (with path
+// splitting) terminates; counting runs in a separate launch after every
+// union has completed.
+__device__ __forceinline__ int32_t cc_find(int32_t* parent, int32_t v) {
+  int32_t curr = __ldcg(parent + v);
+  if (curr != v) {
+    int32_t prev = v, next;
+    while (curr > (next = __ldcg(parent + curr))) {
+      parent[prev] = next;
+      prev = curr;
+      curr = next;
+    }
+  }
+  return curr;
+}
+
+__global__ void cc_init_kernel(int32_t* __restrict__ parent, uint8_t* __restrict__ touched, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    parent[i] = (int32_t)i;
+    touched[i] = 0;
+  }
+}
+
+__global__ void cc_union_kernel(const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
+                                const double* __restrict__ scores, int64_t count, double tau,
+                                int32_t* parent, uint8_t* __restrict__ touched, uint8_t* __restrict__ keep_out,
+                                unsigned long long* __restrict__ kept_total) {
+  unsigned long long kept = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const bool keep = scores[i] > tau;  // strict, as the reference
+    if (keep_out) keep_out[i] = keep;
+    if (!keep) continue;
+    ++kept;
+    const int32_t a = us[i], b = vs[i];
+    touched[a] = 1;
+    touched[b] = 1;
+    int32_t ra = cc_find(parent, a), rb = cc_find(parent, b);
+    while (ra != rb) {
+      if (ra < rb) {
+        const int32_t t = ra;
+        ra = rb;
+        rb = t;
+      }
+      // hook root ra (the larger) under rb; on failure ra gained a parent
+      const int32_t old = atomicCAS(parent + ra, ra, rb);
+      if (old == ra) break;
+      ra = cc_find(parent, old);
+      rb = cc_find(parent, rb);
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) kept += __shfl_xor_sync(0xffffffffu, kept, o);
+  if ((threadIdx.x & 31) == 0 && kept) atomicAdd(kept_total, kept);
+}
+
+__global__ void cc_count_kernel(int32_t* parent, const uint8_t* __restrict__ touched, int64_t n,
+                                unsigned long long* __restrict__ out /* [kept, clusters, touched] */) {
+  unsigned long long roots = 0, tv = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (touched[i]) {
+      ++tv;
+      roots += cc_find(parent, (int32_t)i) == (int32_t)i;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    roots += __shfl_xor_sync(0xffffffffu, roots, o);
+    tv += __shfl_xor_sync(0xffffffffu, tv, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (roots) atomicAdd(out + 1, roots);
+    if (tv) atomicAdd(out + 2, tv);
+  }
+}
+
 }  // namespace pg
 
 using namespace pg;
@@ -222,6 +298,33 @@ int pg_pairs_exact(const int64_t* offsets, const int32_t* adj, const int32_t* us
   PG_REQUIRE(offsets && us && vs && out_count, "null pointer");
   pairs_exact_kernel<<<sm_count() * 8, 256, 0, as_stream(stream)>>>(offsets, adj, us, vs, count, out_count);
   return check_launch("pairs_exact");
+}
+
+int pg_jp_components(const int32_t* us, const int32_t* vs, const double* scores, int64_t count, double tau,
+                     int64_t n, uint8_t* keep_out, int64_t* out, void* stream) {
+  PG_REQUIRE(count >= 0 && n >= 0, "bad sizes");
+  PG_REQUIRE(n < (int64_t(1) << 31), "vertex IDs must fit in int32");
+  PG_REQUIRE(out, "null output");
+  cudaStream_t s = as_stream(stream);
+  cudaError_t e = cudaMemsetAsync(out, 0, 3 * sizeof(int64_t), s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
+  if (n == 0) return PG_OK;
+  PG_REQUIRE(count == 0 || (us && vs && scores), "null pointer");
+  void* buf = nullptr;
+  e = cudaMallocAsync(&buf, align256(sizeof(int32_t) * n) + n, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "cudaMallocAsync: %s", cudaGetErrorString(e));
+  int32_t* parent = static_cast<int32_t*>(buf);
+  uint8_t* touched = static_cast<uint8_t*>(buf) + align256(sizeof(int32_t) * n);
+  auto* o = reinterpret_cast<unsigned long long*>(out);
+  const int grid = sm_count() * 8;
+  cc_init_kernel<<<grid, 256, 0, s>>>(parent, touched, n);
+  if (count > 0) cc_union_kernel<<<grid, 256, 0, s>>>(us, vs, scores, count, tau, parent, touched, keep_out, o);
+  cc_count_kernel<<<grid, 256, 0, s>>>(parent, touched, n, o);
+  e = cudaGetLastError();
+  const cudaError_t e2 = cudaFreeAsync(buf, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "jp_components: %s", cudaGetErrorString(e));
+  if (e2 != cudaSuccess) return fail(PG_ERR_CUDA, "cudaFreeAsync: %s", cudaGetErrorString(e2));
+  return PG_OK;
 }
 
 }  // extern "C"

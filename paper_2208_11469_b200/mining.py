@@ -201,23 +201,26 @@ class ClusterResult:
 
 def jarvis_patrick_cluster(graph: CsrGraph, provider: IntersectionProvider,
                            tau: float, threads: int = 1) -> ClusterResult:
-    """Keep edges whose score strictly exceeds tau; count components."""
+    """Keep edges whose score strictly exceeds tau; count components.
+
+    Scores, the keep test and the connected components of the kept-edge
+    graph (union-find) all run on the device (pg_jp_components); only the
+    kept edge list comes back to the host.
+    """
+    import torch
     us, vs = graph.device().upper_edges()
-    scores = provider._pairs_device(us, vs)
-    keep = scores > tau
-    ku = us[keep].cpu().numpy().astype(np.int64)
-    kv = vs[keep].cpu().numpy().astype(np.int64)
-    kept = np.stack([ku, kv], axis=1) if len(ku) else np.empty((0, 2), np.int64)
-    touched = np.unique(kept.reshape(-1))
-    if len(kept):
-        from scipy.sparse import coo_matrix
-        from scipy.sparse.csgraph import connected_components
-        a = coo_matrix((np.ones(len(ku)), (ku, kv)), shape=(graph.n, graph.n))
-        _, labels = connected_components(a, directed=False)
-        clusters = len(np.unique(labels[touched]))
+    scores = provider._pairs_device(us, vs).to(torch.float64)
+    keep = torch.empty(max(1, us.numel()), dtype=torch.uint8, device="cuda")
+    out = torch.empty(3, dtype=torch.int64, device="cuda")
+    N.call("pg_jp_components", N.ptr(us), N.ptr(vs), N.ptr(scores), us.numel(),
+           float(tau), graph.n, N.ptr(keep), N.ptr(out), N.stream_handle())
+    kept_n, clusters, touched = (int(x) for x in out.cpu().tolist())
+    if kept_n:
+        mask = keep[:us.numel()].bool()
+        kept = torch.stack([us[mask], vs[mask]], dim=1).cpu().numpy().astype(np.int64)
     else:
-        clusters = 0
-    return ClusterResult(kept, clusters, graph.n - len(touched))
+        kept = np.empty((0, 2), np.int64)
+    return ClusterResult(kept, clusters, graph.n - touched)
 
 
 @dataclass
