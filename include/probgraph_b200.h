@@ -215,6 +215,14 @@ PG_API int pg_jp_components(const int32_t* us, const int32_t* vs,
                      const double* scores, int64_t count, double tau,
                      int64_t n, uint8_t* keep_out, int64_t* out, void* stream);
 
+/* degree ordering (graphs.py:154-166 degree_order): rank[v] = position of
+ * (degree(v), v) in ascending order; the directed CSR keeps x in N+(v) iff
+ * rank[v] < rank[x], adjacency order preserved.  dir_off: n+1 entries,
+ * dir_adj: nnz/2 entries (each undirected edge once; nnz must be even). */
+PG_API int pg_degree_order(const int64_t* offsets, const int32_t* adj, int64_t n,
+                     int64_t nnz, int32_t* rank, int64_t* dir_off,
+                     int32_t* dir_adj, void* stream);
+
 /* exact |N(u) & N(v)| per pair over a sorted CSR (providers.py:102-115
  * ExactProvider.pair_many; setops.py:23-51) */
 PG_API int pg_pairs_exact(const int64_t* offsets, const int32_t* adj,

@@ -73,6 +73,7 @@ SIGNATURES = {
                                c_ptr, c_ptr],
     "pg_4clique_exact": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr],
     "pg_pairs_exact": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
+    "pg_degree_order": [c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr],
     "pg_jp_components": [c_ptr, c_ptr, c_ptr, c_i64, c_dbl, c_i64, c_ptr,
                          c_ptr, c_ptr],
     "pg_l2_flush": [c_ptr, c_size, c_ptr],

@@ -8,6 +8,8 @@
 // (affine-map exponentiation), so any slice of the stream is generated in
 // parallel and matches rng.random() element for element.
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_reduce.cuh>
 #include <cub/device/device_select.cuh>
 
 #include "pg_common.cuh"
@@ -164,6 +166,26 @@ static int key_bits(uint64_t n) {
 
 static size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
+// ---- degree ordering (graphs.py:154-166): rank by (degree, id), keep
+// x in N+(v) iff rank[v] < rank[x], adjacency order preserved
+__global__ void degree_keys_kernel(const int64_t* __restrict__ offsets, int64_t n, uint64_t* __restrict__ keys) {
+  for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n; v += (int64_t)gridDim.x * blockDim.x)
+    keys[v] = ((uint64_t)(offsets[v + 1] - offsets[v]) << 32) | (uint64_t)v;
+}
+
+__global__ void rank_scatter_kernel(const uint64_t* __restrict__ sorted, int64_t n, int32_t* __restrict__ rank) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    rank[(uint32_t)sorted[i]] = (int32_t)i;
+}
+
+__global__ void orient_flags_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ adj,
+                                    const int32_t* __restrict__ rank, int64_t nnz, int32_t* __restrict__ flags) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * blockDim.x)
+    flags[j] = rank[src[j]] < rank[adj[j]];
+}
+
+
+
 }  // namespace pg
 
 using namespace pg;
@@ -275,6 +297,76 @@ int pg_csr_from_pairs(const int64_t* a, const int64_t* b, int64_t count, int64_t
     if ((rc = check_launch("split_keys"))) break;
     offsets_kernel<<<grid, 256, 0, s>>>(srcv, 2 * m, n, offsets);
     rc = check_launch("offsets");
+  } while (false);
+  cudaFreeAsync(buf, s);
+  return rc;
+}
+
+int pg_degree_order(const int64_t* offsets, const int32_t* adj, int64_t n, int64_t nnz, int32_t* rank,
+                    int64_t* dir_off, int32_t* dir_adj, void* stream) {
+  PG_REQUIRE(n >= 0 && nnz >= 0, "bad sizes");
+  PG_REQUIRE(n < (int64_t(1) << 31), "vertex IDs must fit in int32");
+  PG_REQUIRE(nnz % 2 == 0, "a symmetric CSR has an even number of entries");
+  PG_REQUIRE(offsets && dir_off && (n == 0 || rank), "null pointer");
+  cudaStream_t s = as_stream(stream);
+  const int grid = sm_count() * 8;
+  if (n == 0) {
+    cudaError_t e = cudaMemsetAsync(dir_off, 0, sizeof(int64_t), s);
+    return e == cudaSuccess ? PG_OK : fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
+  }
+  PG_REQUIRE(nnz == 0 || (adj && dir_adj), "null pointer");
+  size_t t_sort = 0, t_sel = 0, t_red = 0, t_scan = 0;
+  cub::DeviceRadixSort::SortKeys(nullptr, t_sort, (const uint64_t*)nullptr, (uint64_t*)nullptr, n);
+  cub::DeviceSelect::Flagged(nullptr, t_sel, (const int32_t*)nullptr, (const int32_t*)nullptr, (int32_t*)nullptr,
+                             (int64_t*)nullptr, nnz);
+  cub::DeviceSegmentedReduce::Sum(nullptr, t_red, (const int32_t*)nullptr, (int64_t*)nullptr, n,
+                                  (const int64_t*)nullptr, (const int64_t*)nullptr);
+  cub::DeviceScan::ExclusiveSum(nullptr, t_scan, (const int64_t*)nullptr, (int64_t*)nullptr, n + 1);
+  size_t temp = t_sort;
+  for (size_t t : {t_sel, t_red, t_scan}) temp = t > temp ? t : temp;
+  temp = al256(temp);
+  // keys (2n u64) | src, flags (nnz i32 each) | counts (n+1 i64) | num | temp
+  const size_t kb = al256(sizeof(uint64_t) * 2 * n), eb = al256(sizeof(int32_t) * (nnz > 0 ? nnz : 1)),
+               cb = al256(sizeof(int64_t) * (n + 1));
+  void* buf = nullptr;
+  cudaError_t e = cudaMallocAsync(&buf, kb + 2 * eb + cb + 256 + temp, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "cudaMallocAsync: %s", cudaGetErrorString(e));
+  char* p = static_cast<char*>(buf);
+  uint64_t* k0 = reinterpret_cast<uint64_t*>(p);
+  uint64_t* k1 = k0 + n;
+  int32_t* src = reinterpret_cast<int32_t*>(p + kb);
+  int32_t* flags = reinterpret_cast<int32_t*>(p + kb + eb);
+  int64_t* counts = reinterpret_cast<int64_t*>(p + kb + 2 * eb);
+  int64_t* d_num = reinterpret_cast<int64_t*>(p + kb + 2 * eb + cb);
+  void* tmp = p + kb + 2 * eb + cb + 256;
+  int rc = PG_OK;
+  do {
+    degree_keys_kernel<<<grid, 256, 0, s>>>(offsets, n, k0);
+    if ((rc = check_launch("degree_keys"))) break;
+    size_t tb = temp;
+    e = cub::DeviceRadixSort::SortKeys(tmp, tb, k0, k1, n, 0, 64, s);
+    if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "sort: %s", cudaGetErrorString(e)); break; }
+    rank_scatter_kernel<<<grid, 256, 0, s>>>(k1, n, rank);
+    if ((rc = check_launch("rank_scatter"))) break;
+    e = cudaMemsetAsync(counts + n, 0, sizeof(int64_t), s);
+    if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(e)); break; }
+    if (nnz > 0) {
+      if ((rc = pg_csr_expand_rows(offsets, n, nnz, src, stream))) break;
+      orient_flags_kernel<<<grid, 256, 0, s>>>(src, adj, rank, nnz, flags);
+      if ((rc = check_launch("orient_flags"))) break;
+      tb = temp;
+      e = cub::DeviceSelect::Flagged(tmp, tb, adj, flags, dir_adj, d_num, nnz, s);
+      if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "select: %s", cudaGetErrorString(e)); break; }
+      tb = temp;
+      e = cub::DeviceSegmentedReduce::Sum(tmp, tb, flags, counts, n, offsets, offsets + 1, s);
+      if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "segmented sum: %s", cudaGetErrorString(e)); break; }
+    } else {
+      e = cudaMemsetAsync(counts, 0, sizeof(int64_t) * n, s);
+      if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(e)); break; }
+    }
+    tb = temp;
+    e = cub::DeviceScan::ExclusiveSum(tmp, tb, counts, dir_off, n + 1, s);
+    if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "scan: %s", cudaGetErrorString(e)); break; }
   } while (false);
   cudaFreeAsync(buf, s);
   return rc;

@@ -322,7 +322,38 @@ class DirectedView:
 
 
 def degree_order(graph: CsrGraph) -> DirectedView:
-    """Keep u in N+(v) iff (deg v, v) < (deg u, u)."""
+    """Keep u in N+(v) iff (deg v, v) < (deg u, u) (reference graphs.py:154-166).
+
+    On a CUDA machine the ranking and the directed CSR are built on the
+    device (pg_degree_order) and the view keeps them resident; host arrays
+    are copied back for the reference contract.
+    """
+    if graph.n > 0 and _cuda_available():
+        return _degree_order_device(graph)
+    return _degree_order_host(graph)
+
+
+def _degree_order_device(graph: CsrGraph) -> DirectedView:
+    import torch
+    from . import _native as N
+    dev = graph.device()
+    half = dev.nnz // 2
+    rank = torch.empty(graph.n, dtype=torch.int32, device="cuda")
+    off = torch.empty(graph.n + 1, dtype=torch.int64, device="cuda")
+    adj = torch.empty(max(1, half), dtype=torch.int32, device="cuda")
+    N.call("pg_degree_order", N.ptr(dev.offsets), N.ptr(dev.adj), graph.n, dev.nnz,
+           N.ptr(rank), N.ptr(off), N.ptr(adj), N.stream_handle())
+    adj = adj[:half]
+    host_adj = adj.cpu().numpy()
+    if graph.adjacency.dtype != np.int32:
+        host_adj = host_adj.astype(np.int64)
+    view = DirectedView(graph.n, graph.m, rank.cpu().numpy().astype(np.int64),
+                        off.cpu().numpy(), host_adj)
+    view._dev.append(DeviceCsr.from_tensors(off, adj))
+    return view
+
+
+def _degree_order_host(graph: CsrGraph) -> DirectedView:
     deg = graph.degrees()
     order = np.argsort(deg, kind="stable")  # ties -> ascending ID
     rank = np.empty(graph.n, dtype=np.int64)
