@@ -224,8 +224,15 @@ class CsrGraph:
 
     @classmethod
     def from_edges(cls, edges, n: int | None = None) -> "CsrGraph":
-        """Symmetrise, deduplicate and drop self loops."""
+        """Symmetrise, deduplicate and drop self loops (reference
+        graphs.py:57-89).  On a CUDA machine the pairs are canonicalised,
+        sorted and deduplicated on the device (pg_csr_from_pairs) and the
+        graph keeps its device mirror."""
         e = np.asarray(edges, dtype=np.int64).reshape(-1, 2)
+        if len(e) and int(e.min()) < 0:
+            raise ValueError("vertex IDs must be non-negative")
+        if len(e) and _cuda_available():
+            return cls._from_edges_device(e, n)
         lo = np.minimum(e[:, 0], e[:, 1])
         hi = np.maximum(e[:, 0], e[:, 1])
         proper = lo != hi
@@ -241,6 +248,30 @@ class CsrGraph:
         g = cls._from_canonical_keys(key, n)
         g.self_loops_dropped = loops
         g.duplicates_dropped = int(dups)
+        return g
+
+    @classmethod
+    def _from_edges_device(cls, e: np.ndarray, n: int | None) -> "CsrGraph":
+        import torch
+        t = torch.from_numpy(np.ascontiguousarray(e)).cuda()
+        a, b = t[:, 0].contiguous(), t[:, 1].contiguous()
+        proper = a != b
+        loops = int(e.shape[0] - int(proper.sum().item()))
+        hi_max = int(torch.where(proper, torch.maximum(a, b),
+                                 torch.full_like(a, -1)).max().item())
+        if n is None:
+            n = hi_max + 1 if hi_max >= 0 else 0
+        if hi_max >= n:
+            raise ValueError("edge endpoint exceeds vertex count")
+        if n >= 2 ** 31:
+            raise ValueError("vertex IDs must fit in int32 on the device")
+        if loops == e.shape[0]:  # nothing but self loops: the empty graph
+            g = cls._from_canonical_keys(np.empty(0, dtype=np.int64), n)
+        else:
+            g = _graph_from_device_pairs(a, b, n)
+            g.adjacency = g.adjacency.astype(np.int64)  # the reference's dtype
+        g.self_loops_dropped = loops
+        g.duplicates_dropped = int(e.shape[0] - loops - g.m)
         return g
 
     @classmethod

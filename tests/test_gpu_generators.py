@@ -63,3 +63,48 @@ def test_degree_order_device_matches_host(make):
     if g.m:
         ex = pg.make_provider("exact_merge", view=got)
         assert pg.triangle_count(got, ex) == pg.triangle_count(want, pg.make_provider("exact_merge", view=want))
+
+
+@pytest.mark.parametrize("edges,n", [
+    ([[0, 1], [1, 0], [2, 2], [3, 1], [1, 3], [1, 3]], None),
+    ([[4, 4], [4, 4]], None),
+    ([[4, 4], [1, 2]], 9),
+    ([[0, 5]], 6),
+])
+def test_from_edges_device_matches_host(edges, n):
+    import paper_2208_11469_b200 as pg
+    from paper_2208_11469_b200 import graphs
+    g = pg.CsrGraph.from_edges(edges, n)
+    assert g._dev is not None or g.m == 0
+    e = np.asarray(edges, dtype=np.int64)
+    # host restatement (the reference's algorithm): canonical unique pairs
+    lo, hi = np.minimum(e[:, 0], e[:, 1]), np.maximum(e[:, 0], e[:, 1])
+    keep = lo != hi
+    uv = np.unique(np.stack([lo[keep], hi[keep]], 1), axis=0)
+    nn = n if n is not None else (int(uv.max()) + 1 if len(uv) else 0)
+    want = graphs.CsrGraph._from_canonical_keys(uv[:, 0] * nn + uv[:, 1], nn) if len(uv) else None
+    assert g.n == nn
+    assert g.self_loops_dropped == int((~keep).sum())
+    assert g.duplicates_dropped == int(keep.sum()) - len(uv)
+    if want is not None:
+        assert np.array_equal(g.offsets, want.offsets)
+        assert np.array_equal(g.adjacency, want.adjacency)
+        assert g.adjacency.dtype == np.int64
+
+
+def test_from_edges_device_large_and_errors():
+    import paper_2208_11469_b200 as pg
+    from paper_2208_11469_b200 import graphs
+    rng = np.random.default_rng(11)
+    e = rng.integers(0, 50_000, size=(400_000, 2))
+    g = pg.CsrGraph.from_edges(e)
+    lo, hi = np.minimum(e[:, 0], e[:, 1]), np.maximum(e[:, 0], e[:, 1])
+    keep = lo != hi
+    key = np.unique(lo[keep] * g.n + hi[keep])
+    want = graphs.CsrGraph._from_canonical_keys(key, g.n)
+    assert np.array_equal(g.offsets, want.offsets) and np.array_equal(g.adjacency, want.adjacency)
+    assert np.array_equal(g.device().adj.cpu().numpy(), want.adjacency)
+    with pytest.raises(ValueError):
+        pg.CsrGraph.from_edges([[0, 7]], 5)
+    with pytest.raises(ValueError):
+        pg.CsrGraph.from_edges([[-1, 2]])
