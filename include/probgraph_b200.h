@@ -223,6 +223,31 @@ PG_API int pg_degree_order(const int64_t* offsets, const int32_t* adj, int64_t n
                      int64_t nnz, int32_t* rank, int64_t* dir_off,
                      int32_t* dir_adj, void* stream);
 
+/* ---- link prediction (mining.py:248-331) ---------
+ * two-hop candidates (_two_hop_candidates, :275-296): keys u*n+v (u < v),
+ * ascending, of non-adjacent pairs with a common neighbour.  keys_out NULL:
+ * *count_host = sum over w of C(deg w, 2), the capacity keys_out needs. */
+PG_API int pg_two_hop_candidates(const int64_t* offsets, const int32_t* adj,
+                     int64_t n, uint64_t* keys_out, int64_t capacity,
+                     int64_t* count_host, void* stream);
+/* vertex_similarity (:162-203) of every candidate.  measure: 0 JACCARD,
+ * 1 OVERLAP, 2 COMMON_NEIGHBORS, 3 TOTAL_NEIGHBORS (from est[i], the
+ * provider's pair estimate), 4 ADAMIC_ADAR, 5 RESOURCE_ALLOCATION (members
+ * from member_source 0 = CSR rows (rows = adj), 1 = 1-Hash entries [n][k]
+ * + lengths, 2 = k-Hash entries [n][k]; term[d] = the per-member term of a
+ * degree-d member, summed in ascending member order) */
+PG_API int pg_similarity_scores(int32_t measure, const uint64_t* keys,
+                     int64_t count, int64_t n, const int64_t* offsets,
+                     const double* est, int32_t member_source,
+                     const int32_t* rows, int32_t k, const int32_t* lengths,
+                     const double* term, double* scores, void* stream);
+/* link_prediction_eval's tail (:320-331): rank by (-score, u, v), take the
+ * first min(top, count), count those in removed_sorted -> out_hits[0] */
+PG_API int pg_rank_top_hits(const uint64_t* keys, const double* scores,
+                     int64_t count, int64_t top,
+                     const uint64_t* removed_sorted, int64_t n_removed,
+                     int64_t* out_hits, void* stream);
+
 /* exact |N(u) & N(v)| per pair over a sorted CSR (providers.py:102-115
  * ExactProvider.pair_many; setops.py:23-51) */
 PG_API int pg_pairs_exact(const int64_t* offsets, const int32_t* adj,

@@ -73,6 +73,11 @@ SIGNATURES = {
                                c_ptr, c_ptr],
     "pg_4clique_exact": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr],
     "pg_pairs_exact": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
+    "pg_two_hop_candidates": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, ctypes.POINTER(c_i64),
+                              c_ptr],
+    "pg_similarity_scores": [c_i32, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_i32, c_ptr,
+                             c_i32, c_ptr, c_ptr, c_ptr, c_ptr],
+    "pg_rank_top_hits": [c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i64, c_ptr, c_ptr],
     "pg_degree_order": [c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr],
     "pg_jp_components": [c_ptr, c_ptr, c_ptr, c_i64, c_dbl, c_i64, c_ptr,
                          c_ptr, c_ptr],

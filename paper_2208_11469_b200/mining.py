@@ -30,10 +30,11 @@ from .providers import (BloomProvider, ExactProvider, IntersectionProvider,
                         UnsupportedCombinationError, make_provider)
 from .sketches import SketchedGraph, SketchKind
 
-__all__ = ["SimilarityMeasure", "ClusterResult", "JaccardCount",
+__all__ = ["SimilarityMeasure", "ClusterResult", "JaccardCount", "LinkPredSplit",
            "triangle_count", "tc_estimate", "tc_counts", "four_clique_count",
            "vertex_similarity", "jarvis_patrick_cluster",
-           "jaccard_cluster_count", "jaccard_min_matches"]
+           "jaccard_cluster_count", "jaccard_min_matches",
+           "make_link_prediction_split", "link_prediction_eval"]
 
 
 class SimilarityMeasure(str, enum.Enum):
@@ -187,9 +188,18 @@ def vertex_similarity(u: int, v: int, measure, provider: IntersectionProvider,
         return du + dv - c
     members = provider.common_members(u, v)
     degs = graph.degrees()[members] if len(members) else np.empty(0)
+    # sequential sums in member (ascending ID) order, as the reference
+    # (mining.py:192-203) -- not fsum, whose rounding differs
+    total = 0.0
     if measure is SimilarityMeasure.ADAMIC_ADAR:
-        return math.fsum(1.0 / math.log(d) for d in degs.tolist() if d > 1)
-    return math.fsum(1.0 / d for d in degs.tolist() if d > 0)
+        for d in degs.tolist():
+            if d > 1:
+                total += 1.0 / math.log(d)
+        return total
+    for d in degs.tolist():
+        if d > 0:
+            total += 1.0 / d
+    return total
 
 
 @dataclass
@@ -267,3 +277,149 @@ def jaccard_cluster_count(graph: CsrGraph, sketched: SketchedGraph,
     c = jaccard_counts(graph, sketched, tau).cpu().numpy()
     return JaccardCount(int(c[0]), int(c[1]), c[2:].copy(),
                         jaccard_min_matches(sketched.capacity, tau))
+
+
+# ---------------------------------------------------------------------------
+# link prediction (reference mining.py:248-331)
+
+
+@dataclass
+class LinkPredSplit:
+    """A disjoint split E = E_sparse + E_removed for prediction testing."""
+
+    sparse_graph: CsrGraph
+    edges_sparse: np.ndarray
+    edges_removed: np.ndarray
+    fraction: float
+    seed: int
+
+
+def make_link_prediction_split(graph: CsrGraph, fraction: float,
+                               seed: int) -> LinkPredSplit:
+    """Remove round(fraction * m) random edges as the prediction targets.
+
+    The edge sample is the reference's own numpy draw (default_rng(seed)
+    .choice without replacement, :262-268) so splits are identical; the
+    sparse graph is rebuilt on the device (CsrGraph.from_edges).
+    """
+    if not 0 <= fraction <= 1:
+        raise ValueError("fraction must be in [0, 1]")
+    edges = graph.edges()
+    rng = np.random.default_rng(seed)
+    r = int(round(fraction * len(edges)))
+    removed_idx = np.sort(rng.choice(len(edges), size=r, replace=False))
+    mask = np.zeros(len(edges), dtype=bool)
+    mask[removed_idx] = True
+    removed = edges[mask]
+    sparse = edges[~mask]
+    sparse_graph = CsrGraph.from_edges(sparse, n=graph.n)
+    return LinkPredSplit(sparse_graph, sparse, removed, fraction, seed)
+
+
+def _two_hop_keys(graph: CsrGraph):
+    """Device uint64 keys u*n+v (ascending) of the non-adjacent 2-hop pairs."""
+    import ctypes
+    import torch
+    dev = graph.device()
+    total = ctypes.c_int64()
+    N.call("pg_two_hop_candidates", N.ptr(dev.offsets), N.ptr(dev.adj), graph.n, None, 0,
+           ctypes.byref(total), N.stream_handle())
+    keys = torch.empty(max(1, total.value), dtype=torch.int64, device="cuda")
+    got = ctypes.c_int64()
+    N.call("pg_two_hop_candidates", N.ptr(dev.offsets), N.ptr(dev.adj), graph.n,
+           N.ptr(keys), keys.numel(), ctypes.byref(got), N.stream_handle())
+    return keys[:got.value]
+
+
+def _two_hop_candidates(graph: CsrGraph) -> np.ndarray:
+    """Non-adjacent vertex pairs with at least one common neighbor, (u, v)
+    ascending (reference :275-296), computed on the device."""
+    if graph.n == 0:
+        return np.empty((0, 2), dtype=np.int64)
+    k = _two_hop_keys(graph).cpu().numpy()
+    return np.stack([k // graph.n, k % graph.n], axis=1).astype(np.int64) if len(k) \
+        else np.empty((0, 2), dtype=np.int64)
+
+
+_MEASURE_CODE = {SimilarityMeasure.JACCARD: 0, SimilarityMeasure.OVERLAP: 1,
+                 SimilarityMeasure.COMMON_NEIGHBORS: 2, SimilarityMeasure.TOTAL_NEIGHBORS: 3,
+                 SimilarityMeasure.ADAMIC_ADAR: 4, SimilarityMeasure.RESOURCE_ALLOCATION: 5}
+
+
+def _member_terms(graph: CsrGraph, measure: SimilarityMeasure) -> np.ndarray:
+    """term[d] of a degree-d common member, with the reference's expression
+    (math.log / float division on the host, so device sums match)."""
+    dmax = int(graph.degrees().max()) if graph.n else 0
+    t = np.zeros(dmax + 1, dtype=np.float64)
+    for d in range(1, dmax + 1):
+        if measure is SimilarityMeasure.ADAMIC_ADAR:
+            t[d] = 1.0 / math.log(d) if d > 1 else 0.0
+        else:
+            t[d] = 1.0 / d
+    return t
+
+
+def similarity_scores(graph: CsrGraph, keys, measure, provider: IntersectionProvider):
+    """vertex_similarity for a device batch of candidate keys u*n+v."""
+    import torch
+    from .providers import MinHashProvider
+    measure = SimilarityMeasure(measure)
+    dev = graph.device()
+    count = keys.numel()
+    scores = torch.empty(max(1, count), dtype=torch.float64, device="cuda")
+    code = _MEASURE_CODE[measure]
+    if measure in _COUNTING:
+        us = (keys // graph.n).to(torch.int32)
+        vs = (keys % graph.n).to(torch.int32)
+        est = provider._pairs_device(us, vs).to(torch.float64).contiguous()
+        N.call("pg_similarity_scores", code, N.ptr(keys), count, graph.n, N.ptr(dev.offsets),
+               N.ptr(est), 0, None, 0, None, None, N.ptr(scores), N.stream_handle())
+        return scores[:count]
+    term = torch.from_numpy(_member_terms(graph, measure)).cuda()
+    if isinstance(provider, ExactProvider):
+        src, rows, k, lengths = 0, dev.adj, 0, None
+    elif isinstance(provider, MinHashProvider):
+        d = provider.sketched.device_tensors()
+        rows, k = d["entries"], provider.sketched.capacity
+        src, lengths = (1, d["lengths"]) if provider.onehash else (2, None)
+    else:
+        raise UnsupportedCombinationError(
+            f"{provider.kind.value} cannot enumerate intersection members")
+    N.call("pg_similarity_scores", code, N.ptr(keys), count, graph.n, N.ptr(dev.offsets),
+           None, src, N.ptr(rows), k, N.ptr(lengths) if lengths is not None else None,
+           N.ptr(term), N.ptr(scores), N.stream_handle())
+    return scores[:count]
+
+
+def link_prediction_eval(graph: CsrGraph, split: LinkPredSplit,
+                         measure, provider: IntersectionProvider,
+                         top_count: int) -> int:
+    """How many of the top-scored candidate pairs are removed edges.
+
+    Candidates are the 2-hop pairs of the sparse graph; scores come from
+    vertex_similarity on the sparse graph; ties rank lexicographically by
+    (u, v); ``top_count`` is capped at the candidate count.  The bound
+    ``provider`` must be built over ``split.sparse_graph``.  Candidates,
+    scores, ranking and the hit count all run on the device.
+    """
+    import torch
+    if len(split.edges_sparse) + len(split.edges_removed) != graph.m:
+        raise ValueError("split does not cover the graph's edge set")
+    measure = SimilarityMeasure(measure)
+    if top_count <= 0:
+        return 0
+    sparse = split.sparse_graph
+    if sparse.n == 0:
+        return 0
+    keys = _two_hop_keys(sparse)
+    if keys.numel() == 0:
+        return 0
+    scores = similarity_scores(sparse, keys, measure, provider)
+    rem = np.asarray(split.edges_removed, dtype=np.int64).reshape(-1, 2)
+    removed = np.sort(rem[:, 0] * sparse.n + rem[:, 1])
+    removed_d = torch.from_numpy(removed).cuda() if len(removed) else \
+        torch.empty(1, dtype=torch.int64, device="cuda")
+    hits = torch.empty(1, dtype=torch.int64, device="cuda")
+    N.call("pg_rank_top_hits", N.ptr(keys), N.ptr(scores), keys.numel(), int(top_count),
+           N.ptr(removed_d), len(removed), N.ptr(hits), N.stream_handle())
+    return int(hits.item())
