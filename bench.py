@@ -340,6 +340,30 @@ def run_secondary():
         r.update(extra)
         return r
 
+    from oracle import oracle as O
+    port = O.NumpyPort(threads=len(os.sched_getaffinity(0)))
+
+    def cpu_leg(g, p, chunk, sample):
+        """The reference's per-edge strategy (numpy port, all host cores) on
+        a seeded edge sample, with the GPU's sum over the same sample."""
+        e = g.edges()
+        rng = np.random.default_rng(0)
+        idx = np.sort(rng.choice(len(e), size=min(sample, len(e)), replace=False))
+        us, vs = e[idx, 0], e[idx, 1]
+        t0 = time.perf_counter()
+        cpu = port.tc_sum(chunk, us, vs)
+        dt = time.perf_counter() - t0
+        gpu = float(np.sum(p.pair_many(us, vs)))
+        return {"cpu_edges_per_s": len(us) / dt, "cpu_sample_edges": int(len(us)),
+                "cpu_cores": port.threads, "cpu_kind": "port",
+                "speedup_vs_cpu": None,
+                "cpu_gpu_sample_rel_err": abs(cpu - gpu) / max(1.0, abs(cpu))}
+
+    def with_speedup(r, leg):
+        leg["speedup_vs_cpu"] = r["edge_intersections_per_s"] / leg["cpu_edges_per_s"]
+        r.update(leg)
+        return r
+
     out = {}
     try:
         # config 1: ER G(16384, 262144), Bloom 512/1
@@ -347,8 +371,11 @@ def run_secondary():
         sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=1, bits_override=512)
         p = pg.make_provider("bf_and", sketched=sk)
         ms, c = _time_device(lambda: tc_counts(p, g.device()), flush=flush)
-        out["c1_bloom512_tc"] = rec("ER n=16384 m=262144 seed 0", g, ms, 2 * 64 + 8,
-                                    {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0})
+        r = rec("ER n=16384 m=262144 seed 0", g, ms, 2 * 64 + 8,
+                {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0})
+        rows, sz = sk.bit_matrix, sk.sizes
+        out["c1_bloom512_tc"] = with_speedup(r, cpu_leg(
+            g, p, lambda a, b_: O.NumpyPort.bloom_chunk(rows, 512, 1, "bf_and", sz, a, b_), 1 << 22))
         # config 3: R-MAT s22 seed 2, 1-Hash k=64 and KMV k=64
         g = pg.generate_kronecker(22, 16, 2)
         for kind, bpe in (("onehash", 2 * 4 * 64 + 16), ("kmv", 2 * 8 * 64 + 24)):
@@ -358,27 +385,44 @@ def run_secondary():
             bms = (time.perf_counter() - t0) * 1e3
             p = pg.make_provider(kind, sketched=sk)
             ms, c = _time_device(lambda: tc_counts(p, g.device()), reps=3, flush=flush)
-            out[f"c3_{kind}64_tc"] = rec("R-MAT s22 ef16 seed 2", g, ms, bpe,
-                                         {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0,
-                                          "build_ms_wall": bms})
-            del sk, p
+            r = rec("R-MAT s22 ef16 seed 2", g, ms, bpe,
+                    {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0, "build_ms_wall": bms})
+            sz = sk.sizes
+            if kind == "onehash":
+                ent = sk.entries
+                chunk = lambda a, b_: O.NumpyPort.onehash_chunk(ent, 64, sz, a, b_)  # noqa: E731
+                sample = 1 << 20
+            else:
+                vals, lens = sk.values, sk.lengths
+                chunk = lambda a, b_: O.NumpyPort.kmv_chunk(vals, lens, 64, sz, a, b_)  # noqa: E731
+                sample = 1 << 21
+            out[f"c3_{kind}64_tc"] = with_speedup(r, cpu_leg(g, p, chunk, sample))
+            del sk, p, chunk
         # config 4: Chung-Lu 2^23, k-Hash k=32 Jaccard >= 0.1
         g = pg.generate_chung_lu(1 << 23, 32, 2.1, 3)
         sk = pg.build_sketched_graph(g, "khash", s=1.0, k_override=32)
         ms, c = _time_device(lambda: jaccard_counts(g, sk, 0.1), flush=flush)
         c = c.cpu().numpy()
-        out["c4_khash32_jaccard"] = rec("Chung-Lu n=2^23 avg 32 gamma 2.1 seed 3", g, ms, 2 * 4 * 32 + 8,
-                                        {"kept_jhat_ge_0.1": int(c[0]),
-                                         "kept_vertex_similarity_ge_0.1": int(c[1])})
-        del sk
+        r = rec("Chung-Lu n=2^23 avg 32 gamma 2.1 seed 3", g, ms, 2 * 4 * 32 + 8,
+                {"kept_jhat_ge_0.1": int(c[0]), "kept_vertex_similarity_ge_0.1": int(c[1])})
+        # CPU: the reference has no batch Jaccard; SURVEY 8(d) times its
+        # k-Hash gather + positional-match path (tc_estimate(khash))
+        ent, sz = sk.entries, sk.sizes
+        out["c4_khash32_jaccard"] = with_speedup(r, cpu_leg(
+            g, pg.make_provider("khash", sketched=sk),
+            lambda a, b_: O.NumpyPort.khash_chunk(ent, 32, sz, a, b_), 1 << 23))
+        del sk, ent
         # config 5: R-MAT s24 seed 4, Bloom 2048/2
         g = pg.generate_kronecker(24, 16, 4)
         sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=2, bits_override=2048)
         p = pg.make_provider("bf_and", sketched=sk)
         ms, c = _time_device(lambda: tc_counts(p, g.device()), flush=flush)
-        out["c5_bloom2048_tc"] = rec("R-MAT s24 ef16 seed 4", g, ms, 2 * 256 + 8,
-                                     {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0})
-        del sk, p, g
+        r = rec("R-MAT s24 ef16 seed 4", g, ms, 2 * 256 + 8,
+                {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0})
+        rows, sz = sk.bit_matrix, sk.sizes
+        out["c5_bloom2048_tc"] = with_speedup(r, cpu_leg(
+            g, p, lambda a, b_: O.NumpyPort.bloom_chunk(rows, 2048, 2, "bf_and", sz, a, b_), 1 << 23))
+        del sk, p, g, rows
         gc.collect()
         torch.cuda.empty_cache()
         # config 5b: 4-clique, R-MAT s18 seed 4, Bloom 2048/2 over N+
@@ -390,10 +434,22 @@ def run_secondary():
         nnz = view.device().nnz
         ms, c = _time_device(lambda: four_clique_counts(view, p, 0, nnz), reps=3)
         c = c.cpu().numpy()
-        out["c5b_4clique_bloom2048"] = {"graph": "R-MAT s18 ef16 seed 4", "ms": ms,
-                                        "triples": int(c[-1]),
-                                        "triples_per_s": int(c[-1]) / (ms / 1e3),
-                                        "estimate": p._tc_combine(c[:-1])}
+        r = {"graph": "R-MAT s18 ef16 seed 4", "ms": ms, "triples": int(c[-1]),
+             "triples_per_s": int(c[-1]) / (ms / 1e3), "estimate": p._tc_combine(c[:-1])}
+        # CPU: the C restatement (OpenMP, all host cores) over the fixed 1%
+        # directed-edge sample (seed 0) of SURVEY 8(d)
+        src = np.repeat(np.arange(view.n), view.out_degrees())
+        ids = np.sort(np.random.default_rng(0).choice(len(src), size=len(src) // 100,
+                                                      replace=False))
+        O.C.set_threads(len(os.sched_getaffinity(0)))
+        t0 = time.perf_counter()
+        _, trip = O.C.four_clique_bloom(view.offsets, view.adjacency, dsk.bit_matrix, 2048, 2,
+                                        edge_ids=ids)
+        dt = time.perf_counter() - t0
+        r.update({"cpu_triples_per_s": trip / dt, "cpu_sample_directed_edges": int(len(ids)),
+                  "cpu_cores": len(os.sched_getaffinity(0)), "cpu_kind": "port (C oracle)",
+                  "speedup_vs_cpu": r["triples_per_s"] / (trip / dt)})
+        out["c5b_4clique_bloom2048"] = r
     except Exception as exc:  # report, keep the headline line valid
         out["error"] = f"{type(exc).__name__}: {exc}"
     return out
