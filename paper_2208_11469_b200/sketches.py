@@ -228,7 +228,14 @@ class SketchedGraph:
     def _wait_ready(self) -> None:
         if self._ready is not None:
             import torch
+            if torch.cuda.is_current_stream_capturing():
+                # a capture cannot depend on an outside event: the build must
+                # be complete (it is after any earlier eager use)
+                self._ready.synchronize()
+                return
             torch.cuda.current_stream().wait_event(self._ready)
+            if self._ready.query():  # completed: later callers need no wait
+                self._ready = None
 
     @property
     def sizes(self) -> np.ndarray:
