@@ -1784,8 +1784,10 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
   PG_REQUIRE(out_hist, "null histogram");
   PG_REQUIRE(op != PG_BF_OR || (sizes && lut && out_sum_pos), "BF_OR needs sizes, table and sum output");
   cudaStream_t s = as_stream(stream);
-  cudaError_t ce = cudaMemsetAsync(out_hist, 0, sizeof(int64_t) * (bits + 1), s);
-  if (ce == cudaSuccess && out_sum_pos) ce = cudaMemsetAsync(out_sum_pos, 0, sizeof(int64_t), s);
+  // one memset when the sum slot directly follows the histogram
+  const bool adjacent = out_sum_pos == out_hist + bits + 1;
+  cudaError_t ce = cudaMemsetAsync(out_hist, 0, sizeof(int64_t) * (bits + 1 + (adjacent ? 1 : 0)), s);
+  if (ce == cudaSuccess && out_sum_pos && !adjacent) ce = cudaMemsetAsync(out_sum_pos, 0, sizeof(int64_t), s);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
   if (e_end == e_begin) return PG_OK;
   PG_REQUIRE(rows && us && vs, "null pointer");
@@ -1909,9 +1911,11 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
   PG_REQUIRE(out_cnt && out_ssum && out_verbatim && sizes, "null pointer");
   cudaStream_t s = as_stream(stream);
-  cudaError_t ce = cudaMemsetAsync(out_cnt, 0, sizeof(int64_t) * (k + 1), s);
-  if (ce == cudaSuccess) ce = cudaMemsetAsync(out_ssum, 0, sizeof(int64_t) * (k + 1), s);
-  if (ce == cudaSuccess) ce = cudaMemsetAsync(out_verbatim, 0, sizeof(int64_t), s);
+  // one memset when [cnt | ssum | verbatim] is one buffer
+  const bool adjacent = out_ssum == out_cnt + k + 1 && out_verbatim == out_ssum + k + 1;
+  cudaError_t ce = cudaMemsetAsync(out_cnt, 0, sizeof(int64_t) * (adjacent ? 2 * k + 3 : k + 1), s);
+  if (ce == cudaSuccess && !adjacent) ce = cudaMemsetAsync(out_ssum, 0, sizeof(int64_t) * (k + 1), s);
+  if (ce == cudaSuccess && !adjacent) ce = cudaMemsetAsync(out_verbatim, 0, sizeof(int64_t), s);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
   if (e_end == e_begin) return PG_OK;
   PG_REQUIRE(entries && us && vs, "null pointer");

@@ -213,13 +213,13 @@ class BloomProvider(_SketchProvider):
     def _tc_counts(self, us, vs, e_begin: int, e_end: int, padded: bool = False):
         import torch
         d, sg = self._dev(), self.sketched
-        hist = torch.empty(sg.bit_length + 1, dtype=torch.int64, device="cuda")
-        spos = torch.empty(1, dtype=torch.int64, device="cuda")
+        # [hist(B+1) | sum_pos]: one buffer, one memset, no concatenation
+        out = torch.empty(sg.bit_length + 2, dtype=torch.int64, device="cuda")
         N.call("pg_tc_bloom", N.ptr(d["rows"]), sg.bit_length, self.op,
                N.ptr(d["sizes"]), N.ptr(self.lut_device()), N.ptr(us), N.ptr(vs),
-               e_begin, e_end, int(padded), N.ptr(hist), N.ptr(spos),
+               e_begin, e_end, int(padded), N.ptr(out), N.ptr(out) + 8 * (sg.bit_length + 1),
                N.stream_handle())
-        return torch.cat([hist, spos])
+        return out
 
     def _tc_combine(self, counts: np.ndarray) -> float:
         """Sum of per-edge estimates from the exact integer outputs."""
@@ -299,13 +299,13 @@ class MinHashProvider(_SketchProvider):
         import torch
         d, sg = self._dev(), self.sketched
         k = sg.capacity
-        cnt = torch.empty(k + 1, dtype=torch.int64, device="cuda")
-        ssum = torch.empty(k + 1, dtype=torch.int64, device="cuda")
-        verb = torch.empty(1, dtype=torch.int64, device="cuda")
+        # [cnt(k+1) | ssum(k+1) | verbatim]: one buffer, one memset
+        out = torch.empty(2 * k + 3, dtype=torch.int64, device="cuda")
+        p0 = N.ptr(out)
         N.call("pg_tc_minhash", N.ptr(d["entries"]), k, int(self.onehash),
                N.ptr(d["sizes"]), N.ptr(us), N.ptr(vs), e_begin, e_end,
-               int(padded), N.ptr(cnt), N.ptr(ssum), N.ptr(verb), N.stream_handle())
-        return torch.cat([cnt, ssum, verb])
+               int(padded), p0, p0 + 8 * (k + 1), p0 + 16 * (k + 1), N.stream_handle())
+        return out
 
     def _tc_combine(self, counts: np.ndarray) -> float:
         k = self.sketched.capacity
