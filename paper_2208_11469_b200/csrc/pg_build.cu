@@ -23,7 +23,7 @@ namespace pg {
 constexpr int kWarps = 8;
 constexpr int kThreads = kWarps * 32;
 constexpr int kChunk = 64;      // vertices per CTA chunk
-constexpr int64_t kHub = 4096;  // degree above which the whole CTA builds
+constexpr int64_t kHub = 1024;  // degree above which the whole CTA builds
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 __device__ __forceinline__ int warp_id() { return threadIdx.x >> 5; }
@@ -244,7 +244,7 @@ template <int S>
 __global__ void __launch_bounds__(kThreads) build_khash_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n, int k,
     const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries, int32_t* __restrict__ hubs,
-    int32_t* __restrict__ hub_count) {
+    int32_t* __restrict__ hub_count, unsigned long long* __restrict__ vtx_work) {
   const int lane = lane_id();
   uint64_t seed[S];
 #pragma unroll
@@ -252,10 +252,14 @@ __global__ void __launch_bounds__(kThreads) build_khash_kernel(
     const int i = lane + 32 * s;
     seed[s] = i < k ? seeds_dev[i] : 0ull;
   }
-  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-  // each warp takes batches of 32 consecutive vertices; their offsets come in
-  // with one coalesced load and are broadcast by shuffles
-  for (int64_t vb = ((int64_t)blockIdx.x * kWarps + warp_id()) * 32; vb < n; vb += nwarps * 32) {
+  // warps take batches of 32 consecutive vertices from a global counter
+  // (degree-skewed rows make a static split leave most warps idle); the
+  // batch's offsets come in with one coalesced load, broadcast by shuffles
+  for (;;) {
+    unsigned long long vbu = 0;
+    if (lane_id() == 0) vbu = atomicAdd(vtx_work, 32ull);
+    const int64_t vb = (int64_t)__shfl_sync(0xffffffffu, vbu, 0);
+    if (vb >= n) break;
     const int64_t vl = vb + lane_id();
     const int64_t ol = vl < n ? offsets[vl] : 0;
     const int64_t el = vl < n ? offsets[vl + 1] : 0;
@@ -286,9 +290,10 @@ template <int S>
 __global__ void __launch_bounds__(kThreads) build_khash_hubs_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int k,
     const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries, const int32_t* __restrict__ hubs,
-    const int32_t* __restrict__ hub_count) {
+    const int32_t* __restrict__ hub_count, int32_t* __restrict__ hub_work) {
   __shared__ uint64_t red_h[kWarps][32 * S];
   __shared__ int32_t red_x[kWarps][32 * S];
+  __shared__ int s_hi;
   const int lane = lane_id();
   uint64_t seed[S];
 #pragma unroll
@@ -297,7 +302,12 @@ __global__ void __launch_bounds__(kThreads) build_khash_hubs_kernel(
     seed[s] = i < k ? seeds_dev[i] : 0ull;
   }
   const int nh = *hub_count;
-  for (int hi = blockIdx.x; hi < nh; hi += gridDim.x) {
+  for (;;) {  // hubs taken from a global counter (their degrees vary widely)
+    if (threadIdx.x == 0) s_hi = atomicAdd(hub_work, 1);
+    __syncthreads();
+    const int hi = s_hi;
+    __syncthreads();
+    if (hi >= nh) break;
     const int64_t v = hubs[hi];
     const int64_t o = offsets[v];
     const int64_t d = offsets[v + 1] - o;
@@ -464,14 +474,18 @@ __global__ void __launch_bounds__(kThreads) build_bottomk_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n, int k,
     const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries,
     double* __restrict__ values, int32_t* __restrict__ lengths, int32_t* __restrict__ hubs,
-    int32_t* __restrict__ hub_count) {
+    int32_t* __restrict__ hub_count, unsigned long long* __restrict__ vtx_work) {
   __shared__ int32_t scratch[kWarps][32 * P];
   const int lane = lane_id();
   const uint64_t seed0 = seeds_dev[0];
-  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-  // each warp takes batches of 32 consecutive vertices; their offsets come in
-  // with one coalesced load and are broadcast by shuffles
-  for (int64_t vb = ((int64_t)blockIdx.x * kWarps + warp_id()) * 32; vb < n; vb += nwarps * 32) {
+  // warps take batches of 32 consecutive vertices from a global counter
+  // (degree-skewed rows make a static split leave most warps idle); the
+  // batch's offsets come in with one coalesced load, broadcast by shuffles
+  for (;;) {
+    unsigned long long vbu = 0;
+    if (lane_id() == 0) vbu = atomicAdd(vtx_work, 32ull);
+    const int64_t vb = (int64_t)__shfl_sync(0xffffffffu, vbu, 0);
+    if (vb >= n) break;
     const int64_t vl = vb + lane_id();
     const int64_t ol = vl < n ? offsets[vl] : 0;
     const int64_t el = vl < n ? offsets[vl + 1] : 0;
@@ -502,14 +516,21 @@ template <int P, bool kKmv>
 __global__ void __launch_bounds__(kThreads) build_bottomk_hubs_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int k,
     const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries, double* __restrict__ values,
-    int32_t* __restrict__ lengths, const int32_t* __restrict__ hubs, const int32_t* __restrict__ hub_count) {
+    int32_t* __restrict__ lengths, const int32_t* __restrict__ hubs, const int32_t* __restrict__ hub_count,
+    int32_t* __restrict__ hub_work) {
   __shared__ int32_t scratch[32 * P];
   __shared__ uint64_t merge_keys[kWarps][32 * P];
   __shared__ int merge_cnt[kWarps];
+  __shared__ int s_hi;
   const int lane = lane_id();
   const uint64_t seed0 = seeds_dev[0];
   const int nh = *hub_count;
-  for (int hi = blockIdx.x; hi < nh; hi += gridDim.x) {
+  for (;;) {  // hubs taken from a global counter (their degrees vary widely)
+    if (threadIdx.x == 0) s_hi = atomicAdd(hub_work, 1);
+    __syncthreads();
+    const int hi = s_hi;
+    __syncthreads();
+    if (hi >= nh) break;
     const int64_t v = hubs[hi];
     const int64_t o = offsets[v];
     const int64_t d = offsets[v + 1] - o;
@@ -556,15 +577,20 @@ struct HubList {
   void* buf = nullptr;
   cudaStream_t s = nullptr;
   // capacity n + 1 (any vertex may be a hub): no host round trip for nnz
+  // header: [hub count i32 | hub work i32 | vertex-batch work u64], then ids
+  int32_t* hub_work = nullptr;
+  unsigned long long* vtx_work = nullptr;
   int init(const int64_t* offsets, int64_t n, cudaStream_t st) {
     (void)offsets;
     s = st;
     retain_default_pool();
-    cudaError_t e = cudaMallocAsync(&buf, sizeof(int32_t) * (size_t)(n + 1), s);
-    if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, sizeof(int32_t), s);
+    cudaError_t e = cudaMallocAsync(&buf, 16 + sizeof(int32_t) * (size_t)n, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, 16, s);
     if (e != cudaSuccess) return fail(PG_ERR_CUDA, "hub list: %s", cudaGetErrorString(e));
     count = static_cast<int32_t*>(buf);
-    ids = count + 1;
+    hub_work = count + 1;
+    vtx_work = reinterpret_cast<unsigned long long*>(static_cast<char*>(buf) + 8);
+    ids = reinterpret_cast<int32_t*>(static_cast<char*>(buf) + 16);
     return PG_OK;
   }
   ~HubList() {
@@ -589,10 +615,10 @@ static int launch_bottomk(const int64_t* offsets, const int32_t* adj, int64_t n,
   {                                                                                                      \
     const int grid = grid_for(build_bottomk_kernel<P, kKmv>, 0, n);                                     \
     build_bottomk_kernel<P, kKmv><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, \
-                                                            lengths, hubs.ids, hubs.count);              \
+                                                            lengths, hubs.ids, hubs.count, hubs.vtx_work); \
     build_bottomk_hubs_kernel<P, kKmv><<<hub_grid(), kThreads, 0, s>>>(offsets, adj, k, seeds_dev, entries, \
                                                                         values, lengths, hubs.ids,        \
-                                                                        hubs.count);                     \
+                                                                        hubs.count, hubs.hub_work);      \
   }
   if (k <= 32) PG_BK(1)
   else if (k <= 64) PG_BK(2)
@@ -654,9 +680,9 @@ int pg_build_khash(const int64_t* offsets, const int32_t* adj, int64_t n, int32_
   {                                                                                                      \
     const int grid = grid_for(build_khash_kernel<S>, 0, n);                                              \
     build_khash_kernel<S><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, hubs.ids,     \
-                                                    hubs.count);                                         \
+                                                    hubs.count, hubs.vtx_work);                          \
     build_khash_hubs_kernel<S><<<hub_grid(), kThreads, 0, s>>>(offsets, adj, k, seeds_dev, entries,       \
-                                                               hubs.ids, hubs.count);                    \
+                                                               hubs.ids, hubs.count, hubs.hub_work);     \
   }
   if (k <= 32) PG_KB(1)
   else if (k <= 64) PG_KB(2)
