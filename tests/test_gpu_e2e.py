@@ -95,3 +95,27 @@ def test_device_seeds_match_host_family():
         out = torch.empty(count, dtype=torch.int64, device="cuda")
         N.call("pg_family_seeds_device", fam.base_seed, count, N.ptr(out), N.stream_handle())
         assert np.array_equal(out.cpu().numpy().view(np.uint64), fam.seeds_array())
+
+
+@pytest.mark.parametrize("kind,sk_kind,kw", [("bf_and", "bloom", {"bits_override": 512, "b": 2}),
+                                             ("khash", "khash", {"k_override": 32}),
+                                             ("onehash", "onehash", {"k_override": 32}),
+                                             ("kmv", "kmv", {"k_override": 32})])
+def test_pair_many_reentrant_from_threads(kind, sk_kind, kw):
+    """providers are shared by thread-pool workers that call
+    pair_many on disjoint slices concurrently (reference mining.py:75-76)."""
+    from concurrent.futures import ThreadPoolExecutor
+    import paper_2208_11469_b200 as pg
+    g = pg.generate_kronecker(14, 16, 3)
+    sk = pg.build_sketched_graph(g, sk_kind, s=1.0, **kw)
+    p = pg.make_provider(kind, sketched=sk)
+    e = g.edges()
+    want = p.pair_many(e[:, 0], e[:, 1])
+    cuts = np.linspace(0, len(e), 33).astype(int)
+
+    def work(i):
+        return p.pair_many(e[cuts[i]:cuts[i + 1], 0], e[cuts[i]:cuts[i + 1], 1])
+
+    with ThreadPoolExecutor(max_workers=8) as pool:
+        parts = list(pool.map(work, range(32)))
+    assert np.array_equal(np.concatenate(parts), want)
