@@ -41,11 +41,29 @@ class UnsupportedCombinationError(ValueError):
     """Asked a provider for something its sketch kind cannot deliver."""
 
 
-def _as_device_ids(a):
+def _as_device_ids(a, n: int | None = None):
+    """int32 device vertex IDs.  With n given, indices follow numpy's rules
+    as the reference's row gathers do: -n <= i < 0 wraps, anything outside
+    [-n, n) raises IndexError -- the kernels never see an out-of-range row."""
     import torch
     if isinstance(a, torch.Tensor):
-        return a.to(device="cuda", dtype=torch.int32).contiguous(), True
+        t = a.to(device="cuda", dtype=torch.int64).reshape(-1)
+        if n is not None and t.numel():
+            lo, hi = int(t.min().item()), int(t.max().item())
+            if lo < -n or hi >= n:
+                bad = hi if hi >= n else lo
+                raise IndexError(f"index {bad} is out of bounds for axis 0 with size {n}")
+            if lo < 0:
+                t = torch.where(t < 0, t + n, t)
+        return t.to(torch.int32).contiguous(), True
     arr = np.asarray(a, dtype=np.int64).reshape(-1)
+    if n is not None and arr.size:
+        lo, hi = int(arr.min()), int(arr.max())
+        if lo < -n or hi >= n:
+            bad = hi if hi >= n else lo
+            raise IndexError(f"index {bad} is out of bounds for axis 0 with size {n}")
+        if lo < 0:
+            arr = np.where(arr < 0, arr + n, arr)
     return torch.from_numpy(arr.astype(np.int32)).cuda(), False
 
 
@@ -56,10 +74,13 @@ class IntersectionProvider:
     def pair(self, u: int, v: int) -> float:
         return float(self.pair_many(np.asarray([u]), np.asarray([v]))[0])
 
+    def _num_vertices(self) -> int:
+        raise NotImplementedError
+
     def pair_many(self, us, vs):
-        import torch
-        du, on_dev = _as_device_ids(us)
-        dv, _ = _as_device_ids(vs)
+        n = self._num_vertices()
+        du, on_dev = _as_device_ids(us, n)
+        dv, _ = _as_device_ids(vs, n)
         if du.shape != dv.shape:
             raise ValueError("us and vs must have the same length")
         out = self._pairs_device(du, dv)
@@ -109,6 +130,9 @@ class ExactProvider(IntersectionProvider):
             self._dev = DeviceCsr(self.offsets, self.adjacency)
         return self._dev
 
+    def _num_vertices(self) -> int:
+        return len(self.offsets) - 1
+
     def pair(self, u: int, v: int) -> int:
         return int(self.pair_many(np.asarray([u]), np.asarray([v]))[0])
 
@@ -156,6 +180,9 @@ class _SketchProvider(IntersectionProvider):
     def _dev(self) -> dict:
         return self.sketched.device_tensors()
 
+    def _num_vertices(self) -> int:
+        return self.sketched.n
+
 
 class BloomProvider(_SketchProvider):
     """Bloom estimates; ``kind`` picks the AND, limit or OR form."""
@@ -197,8 +224,8 @@ class BloomProvider(_SketchProvider):
     def pair_counts(self, us, vs):
         """Per-edge popcounts of AND (OR for BF_OR) -- the integer core."""
         import torch
-        du, on_dev = _as_device_ids(us)
-        dv, _ = _as_device_ids(vs)
+        du, on_dev = _as_device_ids(us, self.sketched.n)
+        dv, _ = _as_device_ids(vs, self.sketched.n)
         d, sg = self._dev(), self.sketched
         out = torch.empty(max(1, du.numel()), dtype=torch.int32, device="cuda")
         N.call("pg_pairs_bloom", N.ptr(d["rows"]), sg.bit_length,
@@ -285,8 +312,8 @@ class MinHashProvider(_SketchProvider):
     def pair_counts(self, us, vs):
         """Per-edge match counts (positional for k-Hash, set for 1-Hash)."""
         import torch
-        du, on_dev = _as_device_ids(us)
-        dv, _ = _as_device_ids(vs)
+        du, on_dev = _as_device_ids(us, self.sketched.n)
+        dv, _ = _as_device_ids(vs, self.sketched.n)
         d, sg = self._dev(), self.sketched
         out = torch.empty(max(1, du.numel()), dtype=torch.int32, device="cuda")
         N.call("pg_pairs_minhash", N.ptr(d["entries"]), sg.capacity,
@@ -350,8 +377,8 @@ class KmvProvider(_SketchProvider):
     def pair_stats(self, us, vs):
         """Per-edge (common, union) counts of the stored values."""
         import torch
-        du, _ = _as_device_ids(us)
-        dv, _ = _as_device_ids(vs)
+        du, _ = _as_device_ids(us, self.sketched.n)
+        dv, _ = _as_device_ids(vs, self.sketched.n)
         d, sg = self._dev(), self.sketched
         n = max(1, du.numel())
         com = torch.empty(n, dtype=torch.int32, device="cuda")

@@ -119,3 +119,23 @@ def test_pair_many_reentrant_from_threads(kind, sk_kind, kw):
     with ThreadPoolExecutor(max_workers=8) as pool:
         parts = list(pool.map(work, range(32)))
     assert np.array_equal(np.concatenate(parts), want)
+
+
+def test_pair_many_index_rules_match_numpy():
+    """Row gathers follow numpy's indexing as in the reference: negative IDs
+    wrap, IDs outside [-n, n) raise IndexError (never reach a kernel)."""
+    import paper_2208_11469_b200 as pg
+    g = pg.CsrGraph.from_edges([[0, 1], [1, 2], [2, 3]])
+    for kind, sk_kind in (("bf_and", "bloom"), ("khash", "khash"), ("kmv", "kmv")):
+        sk = pg.build_sketched_graph(g, sk_kind, s=1.0, b=1, bits_override=64, k_override=4)
+        p = pg.make_provider(kind, sketched=sk)
+        assert np.array_equal(p.pair_many(np.array([0, 1]), np.array([-1, -3])),
+                              p.pair_many(np.array([0, 1]), np.array([3, 1])))
+        for bad in ([4], [-5], [100]):
+            with pytest.raises(IndexError):
+                p.pair_many(np.array([0]), np.array(bad))
+    ex = pg.make_provider("exact_merge", graph=g)
+    with pytest.raises(IndexError):
+        ex.pair_many(np.array([0]), np.array([4]))
+    assert ex.pair_many(np.array([0]), np.array([-2])).tolist() == \
+        ex.pair_many(np.array([0]), np.array([2])).tolist()
