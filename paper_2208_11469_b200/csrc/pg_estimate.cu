@@ -479,6 +479,107 @@ __device__ __forceinline__ void sorted_edge_loop(const int32_t* __restrict__ R, 
   }
 }
 
+// ------------------------------------------------ 1-Hash hash-table engine
+// G = K/8 lanes per edge (8 IDs per lane), 32/G edges per warp iteration.
+// The u row's IDs are inserted once per run of edges sharing u (CSR order
+// keeps them consecutive) into a per-group shared-memory table of K buckets
+// x 4 slots (multiplicative hash of the ID; slots claimed with atomicCAS;
+// the rare fifth entry of a bucket goes to a stash).  Every v ID is then one
+// 16-byte bucket load + 4 compares (+ the stash when it is non-empty): one
+// LDS.128 per lookup where a binary search needs log2(K)+1 dependent loads.
+// Row lengths are min(size, K); the endpoints' sizes are prefetched with
+// the next edge's indices.  1-Hash needs only the number of common IDs
+// (providers.py:205-232 _matches_onehash).
+template <int K>
+__host__ __device__ constexpr int htab_group_ints() { return 4 * K + K + 4; }  // table | stash | count
+
+template <int K>
+__device__ __forceinline__ uint32_t htab_bucket(int32_t x) {
+  constexpr int kBits = K == 32 ? 5 : (K == 64 ? 6 : 7);
+  return ((uint32_t)x * 0x9E3779B1u) >> (32 - kBits);
+}
+
+template <int K, class Epi>
+__device__ __forceinline__ void htab_edge_loop(const int32_t* __restrict__ R, const int32_t* __restrict__ sizes,
+                                               const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
+                                               int64_t e_begin, int64_t e_end, int32_t* warp_smem, Epi& epi) {
+  constexpr int P = 8, G = K / P, E = 32 / G;
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
+  const unsigned gmask = ((G == 32) ? 0xffffffffu : ((1u << G) - 1u)) << (grp * G);
+  int32_t* T = warp_smem + grp * htab_group_ints<K>();  // 4K slots
+  int32_t* S = T + 4 * K;                                 // stash (K)
+  int* sc_p = reinterpret_cast<int*>(S + K);
+  int64_t wb, we;
+  warp_slice(e_begin, e_end, wb, we);
+  if (wb >= we) return;
+  int32_t ul = 0, vl = -1, szu = 0, szv = 0;
+  if (wb + grp < we) {
+    ul = us[wb + grp];
+    vl = vs[wb + grp];
+    szu = sizes[ul];
+    szv = vl < 0 ? 0 : sizes[vl];
+  }
+  uint32_t x[P];
+  ldg256_keep(R + (int64_t)(vl < 0 ? 0 : vl) * K + gl * P, x);
+  int32_t cur_u = -1;
+  int sc = 0;
+#pragma unroll 1
+  for (int64_t e0 = wb; e0 < we; e0 += E) {
+    const int64_t e = e0 + grp;
+    const bool valid = e < we && vl >= 0;
+    int32_t un = 0, vn = -1;
+    if (e + E < we) {
+      un = us[e + E];
+      vn = vs[e + E];
+    }
+    if (ul != cur_u) {  // uniform within the group: (re)build its table
+      uint32_t y[P];
+      ldg256_keep(R + (int64_t)ul * K + gl * P, y);
+      int4* T4 = reinterpret_cast<int4*>(T);
+#pragma unroll
+      for (int i = gl; i < K; i += G) T4[i] = make_int4(-1, -1, -1, -1);
+      if (gl == 0) *sc_p = 0;
+      __syncwarp(gmask);
+#pragma unroll
+      for (int p = 0; p < P; ++p) {
+        const int32_t q = (int32_t)y[p];
+        if (q < 0) continue;  // -1 pad
+        int32_t* bk = T + 4 * htab_bucket<K>(q);
+        bool placed = false;
+#pragma unroll
+        for (int sl = 0; sl < 4 && !placed; ++sl) placed = atomicCAS(bk + sl, -1, q) == -1;
+        if (!placed) S[atomicAdd(sc_p, 1)] = q;
+      }
+      __syncwarp(gmask);
+      sc = *reinterpret_cast<volatile int*>(sc_p);
+      cur_u = ul;
+    }
+    uint32_t xn[P];
+    ldg256_keep(R + (int64_t)(vn < 0 ? 0 : vn) * K + gl * P, xn);
+    const int32_t szun = un == ul ? szu : sizes[un];
+    const int32_t szvn = vn < 0 ? 0 : sizes[vn];
+    int m = 0;
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+      const int32_t q = (int32_t)x[p];
+      const int4 bk = reinterpret_cast<const int4*>(T)[htab_bucket<K>(q < 0 ? 0 : q)];
+      bool hit = (bk.x == q) | (bk.y == q) | (bk.z == q) | (bk.w == q);
+      for (int i = 0; i < sc; ++i) hit |= S[i] == q;
+      m += hit & (q >= 0);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+    if (valid && gl == 0) epi.edge_sized(e, szu, szv, m, min(szu, K), min(szv, K));
+#pragma unroll
+    for (int p = 0; p < P; ++p) x[p] = xn[p];
+    __syncwarp();
+    ul = un;
+    vl = vn;
+    szu = szun;
+    szv = szvn;
+  }
+}
+
 // ------------------------------------------------ merge-path group engine
 // KMV rows (k = 8*G*CH sorted elements, pads sort last).  G lanes
 // per edge; the 2k-element merge of the two rows is split into G equal
@@ -1152,8 +1253,10 @@ struct EpiOnehash {
   unsigned* shi_s;
   long long verb;
   __device__ __forceinline__ void edge(int64_t e, int32_t u, int32_t v, const SortedStats& st) {
-    const int m = st.common;
-    const int32_t su = sizes[u], sv = sizes[v];
+    edge_sized(e, sizes[u], sizes[v], st.common, st.lu, st.lv);
+  }
+  // the same with the endpoints' sizes already loaded (lengths unused)
+  __device__ __forceinline__ void edge_sized(int64_t e, int32_t su, int32_t sv, int m, int, int) {
     const bool verbatim = su <= k && sv <= k;
     if (cnt_s) {
       if (verbatim) verb += m;
@@ -1205,6 +1308,38 @@ template <int G, int CH, bool kKmv>
 __host__ __device__ constexpr int merge_warp_smem() {
   // both (bank-skewed) rows of every edge of the warp's iteration
   return (32 / G) * (2 * (G * CH * 9 + 1) + 1) * (kKmv ? 8 : 4);
+}
+
+template <int K, bool kFused>
+__global__ void __launch_bounds__(kBlock) onehash_htab_kernel(const int32_t* ent, const int32_t* sizes,
+                                                             const int32_t* us, const int32_t* vs,
+                                                             int64_t e_begin, int64_t e_end, int32_t* out_count,
+                                                             double* out_est, int64_t* out_cnt, int64_t* out_ssum,
+                                                             int64_t* out_verbatim) {
+  extern __shared__ __align__(16) int32_t htab_smem[];  // (kBlock/32) * (32/G) groups
+  __shared__ int cnt_s[K + 1];
+  __shared__ unsigned slo_s[K + 1], shi_s[K + 1];
+  if (kFused) {
+    for (int i = threadIdx.x; i <= K; i += blockDim.x) { cnt_s[i] = 0; slo_s[i] = 0; shi_s[i] = 0; }
+    __syncthreads();
+  }
+  constexpr int kWarpInts = (32 / (K / 8)) * htab_group_ints<K>();
+  EpiOnehash epi{K, sizes, out_count, out_est, kFused ? cnt_s : nullptr, slo_s, shi_s, 0};
+  htab_edge_loop<K>(ent, sizes, us, vs, e_begin, e_end, htab_smem + (threadIdx.x >> 5) * kWarpInts, epi);
+  if (kFused) {
+    __syncthreads();
+    for (int i = threadIdx.x; i <= K; i += blockDim.x) {
+      if (cnt_s[i]) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_cnt + i), (unsigned long long)cnt_s[i]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i),
+                  ((unsigned long long)shi_s[i] << 32) + slo_s[i]);
+      }
+    }
+    long long vb = epi.verb;
+    for (int o = 16; o > 0; o >>= 1) vb += __shfl_xor_sync(0xffffffffu, vb, o);
+    if ((threadIdx.x & 31) == 0 && vb)
+      atomicAdd(reinterpret_cast<unsigned long long*>(out_verbatim), (unsigned long long)vb);
+  }
 }
 
 template <int G, int CH, bool kFused>
@@ -1679,9 +1814,38 @@ static void launch_onehash_sorted(cudaStream_t s, const int32_t* ent, int k, con
                                 out_verbatim);
 }
 
+template <int K, bool kFused>
+static void launch_onehash_htab(cudaStream_t s, const int32_t* ent, const int32_t* sizes, const int32_t* us,
+                                const int32_t* vs, int64_t b, int64_t e, int32_t* out_count, double* out_est,
+                                int64_t* out_cnt, int64_t* out_ssum, int64_t* out_verbatim) {
+  auto kern = onehash_htab_kernel<K, kFused>;
+  const size_t sm = sizeof(int32_t) * (kBlock / 32) * (32 / (K / 8)) * htab_group_ints<K>();
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / 8));
+  kern<<<grid, kBlock, sm, s>>>(ent, sizes, us, vs, b, e, out_count, out_est, out_cnt, out_ssum, out_verbatim);
+}
+
 static bool onehash_sorted(cudaStream_t s, bool fused, const int32_t* ent, int k, const int32_t* sizes,
                            const int32_t* us, const int32_t* vs, int64_t b, int64_t e, int32_t* out_count,
                            double* out_est, int64_t* out_cnt, int64_t* out_ssum, int64_t* out_verbatim) {
+  static const bool lookup = [] {
+    const char* v = getenv("PG_ONEHASH_ENGINE");
+    return v && v[0] == 'l';
+  }();
+  if (!lookup) {
+#define PG_OT(K)                                                                                          \
+  {                                                                                                       \
+    if (fused) launch_onehash_htab<K, true>(s, ent, sizes, us, vs, b, e, out_count, out_est, out_cnt,    \
+                                            out_ssum, out_verbatim);                                      \
+    else launch_onehash_htab<K, false>(s, ent, sizes, us, vs, b, e, out_count, out_est, out_cnt,         \
+                                       out_ssum, out_verbatim);                                           \
+    return true;                                                                                          \
+  }
+    if (k == 32) PG_OT(32)
+    if (k == 64) PG_OT(64)
+    if (k == 128) PG_OT(128)
+#undef PG_OT
+  }
 #define PG_OS(G, CH)                                                                                     \
   {                                                                                                      \
     if (fused) launch_onehash_sorted<G, CH, true>(s, ent, k, sizes, us, vs, b, e, out_count, out_est,    \
