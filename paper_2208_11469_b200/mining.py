@@ -25,7 +25,7 @@ import numpy as np
 
 from . import _native as N
 from .estimators import EstimatorKind, swamidass_table
-from .graphs import CsrGraph, DirectedView
+from .graphs import CsrGraph, DirectedView, degree_order
 from .providers import (BloomProvider, ExactProvider, IntersectionProvider,
                         UnsupportedCombinationError, make_provider)
 from .sketches import SketchedGraph, SketchKind
@@ -34,7 +34,8 @@ __all__ = ["SimilarityMeasure", "ClusterResult", "JaccardCount", "LinkPredSplit"
            "triangle_count", "tc_estimate", "tc_counts", "four_clique_count",
            "vertex_similarity", "jarvis_patrick_cluster",
            "jaccard_cluster_count", "jaccard_min_matches",
-           "make_link_prediction_split", "link_prediction_eval"]
+           "make_link_prediction_split", "link_prediction_eval",
+           "doulion_tc", "reduced_execution_tc"]
 
 
 class SimilarityMeasure(str, enum.Enum):
@@ -423,3 +424,49 @@ def link_prediction_eval(graph: CsrGraph, split: LinkPredSplit,
     N.call("pg_rank_top_hits", N.ptr(keys), N.ptr(scores), keys.numel(), int(top_count),
            N.ptr(removed_d), len(removed), N.ptr(hits), N.stream_handle())
     return int(hits.item())
+
+
+# ---------------------------------------------------------------------------
+# sampling baselines for TC (reference mining.py:334-367)
+
+
+def doulion_tc(graph: CsrGraph, keep_prob: float, seed: int,
+               threads: int = 1) -> float:
+    """Keep each edge with probability p, count exactly, rescale by p^-3.
+
+    The edge sample is the reference's own draw (default_rng(seed).random
+    over graph.edges()); the subgraph, its degree ordering and the exact
+    count run on the device.
+    """
+    if not 0 < keep_prob <= 1:
+        raise ValueError("keep probability must be in (0, 1]")
+    edges = graph.edges()
+    rng = np.random.default_rng(seed)
+    kept = edges[rng.random(len(edges)) < keep_prob] if keep_prob < 1 else edges
+    sub = CsrGraph.from_edges(kept, n=graph.n)
+    view = degree_order(sub)
+    exact = ExactProvider.for_view(view)
+    return triangle_count(view, exact, threads) / keep_prob ** 3
+
+
+def reduced_execution_tc(view: DirectedView, fraction: float, seed: int,
+                         threads: int = 1) -> float:
+    """Node-iterator outer loop over a random vertex subset (the reference's
+    default_rng(seed).choice draw), rescaled by 1/fraction; the sampled
+    vertices' directed edges are selected and counted exactly on the device."""
+    import torch
+    if not 0 < fraction <= 1:
+        raise ValueError("fraction must be in (0, 1]")
+    rng = np.random.default_rng(seed)
+    count = max(1, int(round(fraction * view.n)))
+    sample = np.sort(rng.choice(view.n, size=count, replace=False))
+    dev = view.device()
+    if dev.nnz == 0:
+        return 0.0
+    picked = torch.zeros(view.n, dtype=torch.bool, device="cuda")
+    picked[torch.from_numpy(sample).cuda()] = True
+    src = dev.row_sources()
+    sel = picked[src.long()]
+    exact = ExactProvider.for_view(view)
+    total = exact._pairs_device(src[sel].contiguous(), dev.adj[sel].contiguous())
+    return float(int(total.sum().item()) if total.numel() else 0) / fraction
