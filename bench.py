@@ -311,7 +311,8 @@ def run_ours(args, cfg, rank, world, local):
             "data": "synthetic (seeded R-MAT, reference generator draw order)",
             "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "m": m,
                        "edges_per_rank": rank_edges,
-                       "edge_slots": slots, "row_padded_layout": padded,
+                       "edge_slots": slots, "row_padded_layout": bool(padded),
+                       "u_per_slot_group": padded == 2,
                        "sketch_bytes": g.n * bits // 8,
                        "l2": "flushed between timed steps (256 MiB write, outside the events)",
                        "parallelism": f"edge-range shards x{world}, replicated sketches, "

@@ -145,7 +145,9 @@ PG_API int pg_pairs_kmv(const double* values, const int32_t* lengths, int32_t k,
  * row-padded layout of pg_csr_upper_edges_padded with pad =
  * pg_group_pad(row bytes) and e_begin a multiple of pad (precondition, not
  * checked: every aligned group of pad slots holds one u).  Slots with
- * vs[j] < 0 are padding and skipped.
+ * vs[j] < 0 are padding and skipped.  pg_tc_bloom also takes 2 = the same
+ * layout with us[] holding one u per pad-slot group (us[j / pad], a pad-fold
+ * smaller u stream).
  * Bloom TC.
  * out_hist: int64[bits+1] histogram of per-edge popcounts
  * (for PG_BF_OR only edges with raw > 0 are counted, and out_sum_pos

@@ -185,10 +185,14 @@ __device__ __forceinline__ void ldg256_keep(const void* p, uint32_t (&r)[8]) {
                : "l"(p));
 }
 
-template <int W8, class Op, class Epi, bool kVCache = false, bool kPadded = false>
+// kLayout: 0 any edge list; 1 row-padded slots (every aligned group of G
+// slots shares one u; us[] per slot); 2 the same with us[] holding one u per
+// group (us[e / G]) -- a G-fold smaller u stream.
+template <int W8, class Op, class Epi, bool kVCache = false, int kLayout = 0>
 __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__ rows,
                                                const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
                                                int64_t e_begin, int64_t e_end, Epi& epi) {
+  constexpr bool kPadded = kLayout > 0;
   constexpr int G = W8 < 8 ? W8 : 8;  // lanes per edge
   constexpr int V = W8 / G;           // 32-byte chunks per lane per row
   constexpr int64_t kRowBytes = W8 * 32;
@@ -200,7 +204,7 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
   if (wb >= we) return;
   int32_t ul = 0, vl = 0;
   if (wb + lane < we) {
-    ul = us[wb + lane];
+    ul = kLayout == 2 ? us[(wb + lane) / G] : us[wb + lane];
     vl = vs[wb + lane];
   }
   int32_t ucur = -1;
@@ -215,7 +219,7 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
     const bool valid = e < we && vl >= 0;  // v < 0: padding slot
     int32_t un = 0, vn = 0;
     if (e + 32 < we) {
-      un = us[e + 32];
+      un = kLayout == 2 ? us[(e + 32) / G] : us[e + 32];
       vn = vs[e + 32];
     }
     uint32_t vr[G][V][8];
@@ -927,7 +931,7 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_bloom_kernel(const uint4* row
   }
 }
 
-template <int W8, class Op, int MINB, bool kVCache, bool kPadded>
+template <int W8, class Op, int MINB, bool kVCache, int kLayout>
 __global__ void __launch_bounds__(kBlock, MINB) tc_bloom_wide_kernel(const unsigned char* rows, int bits,
                                                                     const int32_t* us, const int32_t* vs,
                                                                     int64_t e_begin, int64_t e_end,
@@ -938,7 +942,7 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_bloom_wide_kernel(const unsig
   __syncthreads();
   epi.hist_s = hist_s;
   epi.sum_pos = 0;
-  wide_edge_loop<W8, Op, EpiBloomHist, kVCache, kPadded>(rows, us, vs, e_begin, e_end, epi);
+  wide_edge_loop<W8, Op, EpiBloomHist, kVCache, kLayout>(rows, us, vs, e_begin, e_end, epi);
   __syncthreads();
   for (int i = threadIdx.x; i <= bits; i += blockDim.x)
     if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_hist + i), (unsigned long long)hist_s[i]);
@@ -1941,7 +1945,7 @@ int pg_pairs_bloom(const uint64_t* rows, int32_t bits, int32_t b, int32_t op, co
 
 static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* sizes,
                          const double* lut, const int32_t* us, const int32_t* vs, int64_t e_begin,
-                         int64_t e_end, int64_t* out_hist, int64_t* out_sum_pos, void* stream, bool padded) {
+                         int64_t e_end, int64_t* out_hist, int64_t* out_sum_pos, void* stream, int padded) {
   PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
   PG_REQUIRE(op == PG_BF_AND || op == PG_BF_L || op == PG_BF_OR, "op is not a Bloom estimator");
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
@@ -1983,13 +1987,16 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
     k<<<grid, kBlock, smem, s>>>(rb, bits, us, vs, e_begin, e_end, epi, out_hist, out_sum_pos);      \
   }
 #define PG_WM(W8)                                                                  \
-  if (padded) {                                                                  \
-    if (vcache) PG_W(W8, 3, true, true)                                          \
-    else if (minb >= 4) PG_W(W8, 4, false, true)                                 \
-    else if (minb == 3) PG_W(W8, 3, false, true)                                 \
-    else PG_W(W8, 2, false, true)                                                \
+  if (padded == 2) {                                                             \
+    if (vcache) PG_W(W8, 3, true, 2)                                             \
+    else PG_W(W8, 3, false, 2)                                                   \
+  } else if (padded) {                                                           \
+    if (vcache) PG_W(W8, 3, true, 1)                                             \
+    else if (minb >= 4) PG_W(W8, 4, false, 1)                                    \
+    else if (minb == 3) PG_W(W8, 3, false, 1)                                    \
+    else PG_W(W8, 2, false, 1)                                                   \
   } else {                                                                       \
-    PG_W(W8, 2, false, false)                                                    \
+    PG_W(W8, 2, false, 0)                                                        \
   }
     if (w4 == 4) PG_WM(2)
     else if (w4 == 8) PG_WM(4)
@@ -2025,8 +2032,10 @@ int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* s
     pg_group_pad(bits / 8, &pad);
     PG_REQUIRE(e_begin % pad == 0, "e_begin must be a multiple of the layout pad %d", pad);
   }
+  PG_REQUIRE(padded >= 0 && padded <= 2, "padded must be 0, 1 or 2");
+  PG_REQUIRE(padded != 2 || pad > 1, "the group-u layout needs a padded row size");
   return tc_bloom_impl(rows, bits, op, sizes, lut, us, vs, e_begin, e_end, out_hist, out_sum_pos, stream,
-                       padded && pad > 1);
+                       pad > 1 ? padded : 0);
 }
 
 int pg_pairs_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int32_t* sizes,

@@ -185,6 +185,15 @@ class DeviceCsr:
             self._layouts[key] = (us[:k], vs[:k], k)
         return self._layouts[key]
 
+    def upper_edges_group_u(self, pad: int):
+        """(ug, vs, slots) of the row-padded layout with one u per group of
+        `pad` slots (ug[j // pad]), the group-u layout of pg_tc_bloom."""
+        key = ("group_u", pad)
+        if key not in self._layouts:
+            us, vs, slots = self.upper_edges_padded(pad)
+            self._layouts[key] = (us[::pad].contiguous(), vs, slots)
+        return self._layouts[key]
+
     def row_sources(self):
         """int32 device array src[j] = row of adjacency entry j."""
         if self._src is None:

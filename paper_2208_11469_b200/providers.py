@@ -237,6 +237,15 @@ class BloomProvider(_SketchProvider):
     def tc_pad(self) -> int:
         return N.group_pad(self.sketched.bit_length // 8)
 
+    def _tc_layout(self, dev):
+        """Bloom TC: the row-padded layout with one u per slot group
+        (padded mode 2 of pg_tc_bloom)."""
+        pad = self.tc_pad()
+        if pad > 1:
+            ug, vs, slots = dev.upper_edges_group_u(pad)
+            return ug, vs, slots, 2
+        return super()._tc_layout(dev)
+
     def _tc_counts(self, us, vs, e_begin: int, e_end: int, padded: bool = False):
         import torch
         d, sg = self._dev(), self.sketched
