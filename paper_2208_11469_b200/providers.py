@@ -184,6 +184,19 @@ class _SketchProvider(IntersectionProvider):
         return self.sketched.n
 
 
+_LUTS = {}
+
+
+def _device_lut(bits: int, b: int):
+    """The Swamidass table on the current device, uploaded once per (B, b):
+    a per-provider pageable upload would stall the host before every pass."""
+    import torch
+    key = (bits, b, torch.cuda.current_device())
+    if key not in _LUTS:
+        _LUTS[key] = torch.from_numpy(swamidass_table(bits, b).copy()).cuda()
+    return _LUTS[key]
+
+
 class BloomProvider(_SketchProvider):
     """Bloom estimates; ``kind`` picks the AND, limit or OR form."""
 
@@ -205,10 +218,7 @@ class BloomProvider(_SketchProvider):
 
     def lut_device(self):
         if self._lut is None:
-            import torch
-            sg = self.sketched
-            self._lut = torch.from_numpy(
-                swamidass_table(sg.bit_length, sg.hash_count).copy()).cuda()
+            self._lut = _device_lut(self.sketched.bit_length, self.sketched.hash_count)
         return self._lut
 
     def _pairs_device(self, us, vs):
