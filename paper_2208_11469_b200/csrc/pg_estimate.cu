@@ -305,6 +305,20 @@ struct SortedTraits<uint64_t> {
   __device__ static bool valid(uint64_t x) { return x < kInfBits; }
 };
 
+// KMV keys compared as doubles: the values are non-negative (or the +inf
+// pad), so IEEE order equals the bit order and one DSETP replaces a 64-bit
+// integer compare (two ISETPs)
+template <>
+struct SortedTraits<double> {
+  __device__ static double pad() { return __longlong_as_double((long long)kInfBits); }
+  __device__ static bool valid(double x) { return x < __longlong_as_double((long long)kInfBits); }
+};
+
+__device__ __forceinline__ double key_of(uint64_t bits) { return __longlong_as_double((long long)bits); }
+__device__ __forceinline__ int32_t key_of(int32_t x) { return x; }
+__device__ __forceinline__ uint64_t bits_of(double x) { return (uint64_t)__double_as_longlong(x); }
+__device__ __forceinline__ uint64_t bits_of(int32_t x) { return (uint64_t)(uint32_t)x; }
+
 template <class T, int CH, bool kKeep>
 __device__ __forceinline__ void load_sorted_chunks(const T* row, int G, int gl, T (&c)[CH][8]) {
 #pragma unroll
@@ -613,7 +627,8 @@ __device__ __forceinline__ void merge_edge_loop(const void* __restrict__ rows, i
                                                 const int32_t* __restrict__ us,
                                                 const int32_t* __restrict__ vs, int64_t e_begin,
                                                 int64_t e_end, unsigned char* warp_smem, Epi& epi) {
-  using T = typename std::conditional<kKmv, uint64_t, int32_t>::type;
+  using TL = typename std::conditional<kKmv, uint64_t, int32_t>::type;  // stored
+  using T = typename std::conditional<kKmv, double, int32_t>::type;     // compared
   using TR = SortedTraits<T>;
   constexpr int K = 8 * G * CH;  // row length
   constexpr int Q = 2 * K / G;   // merged outputs per lane
@@ -623,7 +638,7 @@ __device__ __forceinline__ void merge_edge_loop(const void* __restrict__ rows, i
   const int gl = lane & (G - 1);
   const int gbase = lane & ~(G - 1);
   const int grp = lane / G;
-  const T* R = reinterpret_cast<const T*>(rows);
+  const TL* R = reinterpret_cast<const TL*>(rows);
   // bank-skewed copies: element x at x + x/8 (lane diagonals start ~8 apart
   // in each row), a sentinel pad at K, groups offset by an odd element count
   constexpr int KP = K + K / 8 + 1;
@@ -652,19 +667,20 @@ __device__ __forceinline__ void merge_edge_loop(const void* __restrict__ rows, i
       un = us[e + E];
       vn = vs[e + E];
     }
-    T a[CH][8], b[CH][8];
-    load_sorted_chunks<T, CH, true>(R + (int64_t)ul * k, G, gl, a);
-    load_sorted_chunks<T, CH, false>(R + (int64_t)(vl < 0 ? 0 : vl) * k, G, gl, b);
+    TL a[CH][8], b[CH][8];
+    load_sorted_chunks<TL, CH, true>(R + (int64_t)ul * k, G, gl, a);
+    load_sorted_chunks<TL, CH, false>(R + (int64_t)(vl < 0 ? 0 : vl) * k, G, gl, b);
     int la = 0, lb = 0;
 #pragma unroll
     for (int s = 0; s < CH; ++s) {
       const int c = s * G + gl;
 #pragma unroll
       for (int w = 0; w < 8; ++w) {
-        su[c * 9 + w] = a[s][w];
-        sv[c * 9 + w] = b[s][w];
-        la += TR::valid(a[s][w]);
-        lb += TR::valid(b[s][w]);
+        const T ka = key_of(a[s][w]), kb = key_of(b[s][w]);
+        su[c * 9 + w] = ka;
+        sv[c * 9 + w] = kb;
+        la += TR::valid(ka);
+        lb += TR::valid(kb);
       }
     }
     la = group_sum<G>(la);
@@ -744,8 +760,8 @@ __device__ __forceinline__ void merge_edge_loop(const void* __restrict__ rows, i
       const T xa = su[sk(lo2)], xb = sv[sk(d - lo2)];
       const T cand = xa <= xb ? xa : xb;
       const unsigned hm = __ballot_sync(0xffffffffu, mine) & gmask;
-      const uint64_t c1 = shfl64((uint64_t)cand, hm ? __ffs(hm) - 1 : gbase);
-      const uint64_t u0 = shfl64((uint64_t)su[0], gbase), v0 = shfl64((uint64_t)sv[0], gbase);
+      const uint64_t c1 = shfl64(bits_of(cand), hm ? __ffs(hm) - 1 : gbase);
+      const uint64_t u0 = shfl64(bits_of(su[0]), gbase), v0 = shfl64(bits_of(sv[0]), gbase);
       st.kth = bitsd(hm ? c1 : (u0 < v0 ? u0 : v0));  // none: argmax of all-False -> merged[0]
     }
     if (valid && gl == 0) epi.edge(e, ul, vl, st);
