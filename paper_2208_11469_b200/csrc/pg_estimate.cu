@@ -1395,7 +1395,7 @@ __global__ void __launch_bounds__(kBlock) onehash_sorted_kernel(const int32_t* e
   }
 }
 
-template <int G, bool kFused>
+template <int G, int CH, bool kFused>
 __global__ void __launch_bounds__(kBlock) kmv_sorted_kernel(const uint64_t* vals, int k, const int32_t* sizes,
                                                            const int32_t* us, const int32_t* vs,
                                                            int64_t e_begin, int64_t e_end, int32_t* out_common,
@@ -1404,8 +1404,8 @@ __global__ void __launch_bounds__(kBlock) kmv_sorted_kernel(const uint64_t* vals
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[kBlock / 32];
   EpiKmv epi{k, sizes, out_common, out_union, out_kth, out_est, kFused, 0.0};
-  merge_edge_loop<G, 1, true>(vals, k, us, vs, e_begin, e_end,
-                              smem_raw + (threadIdx.x >> 5) * merge_warp_smem<G, 1, true>(), epi);
+  merge_edge_loop<G, CH, true>(vals, k, us, vs, e_begin, e_end,
+                               smem_raw + (threadIdx.x >> 5) * merge_warp_smem<G, CH, true>(), epi);
   if (kFused) {
     double a = epi.acc;
     for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
@@ -1881,12 +1881,12 @@ static bool onehash_sorted(cudaStream_t s, bool fused, const int32_t* ent, int k
   return false;
 }
 
-template <int G, bool kFused>
+template <int G, int CH, bool kFused>
 static void launch_kmv_sorted(cudaStream_t s, const uint64_t* vals, int k, const int32_t* sizes,
                               const int32_t* us, const int32_t* vs, int64_t b, int64_t e, int32_t* out_common,
                               int32_t* out_union, double* out_kth, double* out_est, double* out_sum) {
-  auto kern = kmv_sorted_kernel<G, kFused>;
-  const size_t sm = (size_t)(kBlock / 32) * merge_warp_smem<G, 1, true>();
+  auto kern = kmv_sorted_kernel<G, CH, kFused>;
+  const size_t sm = (size_t)(kBlock / 32) * merge_warp_smem<G, CH, true>();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / G);
   kern<<<grid, kBlock, sm, s>>>(vals, k, sizes, us, vs, b, e, out_common, out_union, out_kth, out_est, out_sum);
@@ -1895,16 +1895,31 @@ static void launch_kmv_sorted(cudaStream_t s, const uint64_t* vals, int k, const
 static bool kmv_sorted(cudaStream_t s, bool fused, const uint64_t* vals, int k, const int32_t* sizes,
                        const int32_t* us, const int32_t* vs, int64_t b, int64_t e, int32_t* out_common,
                        int32_t* out_union, double* out_kth, double* out_est, double* out_sum) {
-#define PG_KS(G)                                                                                        \
-  {                                                                                                     \
-    if (fused) launch_kmv_sorted<G, true>(s, vals, k, sizes, us, vs, b, e, out_common, out_union,      \
-                                          out_kth, out_est, out_sum);                                   \
-    else launch_kmv_sorted<G, false>(s, vals, k, sizes, us, vs, b, e, out_common, out_union, out_kth, \
-                                     out_est, out_sum);                                                 \
-    return true;                                                                                        \
+#define PG_KS(G, CH)                                                                                       \
+  {                                                                                                        \
+    if (fused) launch_kmv_sorted<G, CH, true>(s, vals, k, sizes, us, vs, b, e, out_common, out_union,     \
+                                              out_kth, out_est, out_sum);                                  \
+    else launch_kmv_sorted<G, CH, false>(s, vals, k, sizes, us, vs, b, e, out_common, out_union, out_kth, \
+                                         out_est, out_sum);                                                \
+    return true;                                                                                           \
   }
-  if (k == 32) PG_KS(4)
-  if (k == 64) PG_KS(8)
+  static const int lanes = [] {
+    const char* v = getenv("PG_KMV_LANES");
+    return v ? atoi(v) : 0;
+  }();
+  // 32 merge outputs per lane (two 8-element chunks of each row per lane):
+  // the two bisections per lane amortise over twice the outputs of the
+  // 16-output split (measured s20 k=64: 4.80 vs 5.85 ms); PG_KMV_LANES
+  // selects the 16-output split for comparison
+  if (k == 32) {
+    if (lanes == 4) PG_KS(4, 1)
+    PG_KS(2, 2)
+  }
+  if (k == 64) {
+    if (lanes == 8) PG_KS(8, 1)
+    PG_KS(4, 2)
+  }
+  if (k == 128) PG_KS(8, 2)
 #undef PG_KS
   return false;
 }

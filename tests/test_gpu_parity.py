@@ -173,3 +173,20 @@ def test_config2_full_parity(pg):
     assert parts.tolist() == counts.tolist()
     for kind, want in rec["tc"].items():
         assert pg.tc_estimate(g, sk, kind) == pytest.approx(want, rel=RTOL_SUM)
+
+
+@pytest.mark.parametrize("k", [16, 32, 64, 128])
+def test_kmv_pairs_all_widths_vs_oracle(pg, k):
+    """KMV per-edge estimates for every dispatch width (k = 32/64/128 take
+    the merge engine) equal the C oracle's restatement of
+    providers.py:266-301 (built from the same bit-identical sketches)."""
+    g = pg.generate_kronecker(12, 16, 5)
+    sk = pg.build_sketched_graph(g, "kmv", s=1.0, k_override=k)
+    vals, lens = O.C.build_kmv(g.offsets, g.adjacency, k)
+    assert np.array_equal(sk.values, vals) and np.array_equal(sk.lengths, lens)
+    e = g.edges()
+    p = pg.make_provider("kmv", sketched=sk)
+    com, uni, want = O.C.pairs_kmv(vals, lens, k, np.diff(g.offsets), e[:, 0], e[:, 1])
+    assert np.array_equal(p.pair_many(e[:, 0], e[:, 1]), want)
+    c, u = p.pair_stats(e[:, 0], e[:, 1])
+    assert np.array_equal(np.asarray(c), com) and np.array_equal(np.asarray(u), uni)
