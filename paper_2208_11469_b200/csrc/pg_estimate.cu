@@ -517,11 +517,23 @@ __device__ __forceinline__ uint32_t htab_bucket(int32_t x) {
   return ((uint32_t)x * 0x9E3779B1u) >> (32 - kBits);
 }
 
-template <int K, class Epi>
+// P consecutive 32-bit IDs of a row (P a multiple of 8, 32-byte aligned)
+template <int P>
+__device__ __forceinline__ void ldg_rowpart(const int32_t* p, uint32_t (&x)[P]) {
+#pragma unroll
+  for (int c = 0; c < P / 8; ++c) {
+    uint32_t r[8];
+    ldg256_keep(p + 8 * c, r);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[8 * c + i] = r[i];
+  }
+}
+
+template <int K, int P, class Epi>
 __device__ __forceinline__ void htab_edge_loop(const int32_t* __restrict__ R, const int32_t* __restrict__ sizes,
                                                const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
                                                int64_t e_begin, int64_t e_end, int32_t* warp_smem, Epi& epi) {
-  constexpr int P = 8, G = K / P, E = 32 / G;
+  constexpr int G = K / P, E = 32 / G;
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
   const unsigned gmask = ((G == 32) ? 0xffffffffu : ((1u << G) - 1u)) << (grp * G);
   int32_t* T = warp_smem + grp * htab_group_ints<K>();  // 4K slots
@@ -538,7 +550,7 @@ __device__ __forceinline__ void htab_edge_loop(const int32_t* __restrict__ R, co
     szv = vl < 0 ? 0 : sizes[vl];
   }
   uint32_t x[P];
-  ldg256_keep(R + (int64_t)(vl < 0 ? 0 : vl) * K + gl * P, x);
+  ldg_rowpart<P>(R + (int64_t)(vl < 0 ? 0 : vl) * K + gl * P, x);
   int32_t cur_u = -1;
   int sc = 0;
 #pragma unroll 1
@@ -552,7 +564,7 @@ __device__ __forceinline__ void htab_edge_loop(const int32_t* __restrict__ R, co
     }
     if (ul != cur_u) {  // uniform within the group: (re)build its table
       uint32_t y[P];
-      ldg256_keep(R + (int64_t)ul * K + gl * P, y);
+      ldg_rowpart<P>(R + (int64_t)ul * K + gl * P, y);
       int4* T4 = reinterpret_cast<int4*>(T);
 #pragma unroll
       for (int i = gl; i < K; i += G) T4[i] = make_int4(-1, -1, -1, -1);
@@ -573,7 +585,7 @@ __device__ __forceinline__ void htab_edge_loop(const int32_t* __restrict__ R, co
       cur_u = ul;
     }
     uint32_t xn[P];
-    ldg256_keep(R + (int64_t)(vn < 0 ? 0 : vn) * K + gl * P, xn);
+    ldg_rowpart<P>(R + (int64_t)(vn < 0 ? 0 : vn) * K + gl * P, xn);
     const int32_t szun = un == ul ? szu : sizes[un];
     const int32_t szvn = vn < 0 ? 0 : sizes[vn];
     int m = 0;
@@ -1330,7 +1342,7 @@ __host__ __device__ constexpr int merge_warp_smem() {
   return (32 / G) * (2 * (G * CH * 9 + 1) + 1) * (kKmv ? 8 : 4);
 }
 
-template <int K, bool kFused>
+template <int K, int P, bool kFused>
 __global__ void __launch_bounds__(kBlock) onehash_htab_kernel(const int32_t* ent, const int32_t* sizes,
                                                              const int32_t* us, const int32_t* vs,
                                                              int64_t e_begin, int64_t e_end, int32_t* out_count,
@@ -1343,9 +1355,9 @@ __global__ void __launch_bounds__(kBlock) onehash_htab_kernel(const int32_t* ent
     for (int i = threadIdx.x; i <= K; i += blockDim.x) { cnt_s[i] = 0; slo_s[i] = 0; shi_s[i] = 0; }
     __syncthreads();
   }
-  constexpr int kWarpInts = (32 / (K / 8)) * htab_group_ints<K>();
+  constexpr int kWarpInts = (32 / (K / P)) * htab_group_ints<K>();
   EpiOnehash epi{K, sizes, out_count, out_est, kFused ? cnt_s : nullptr, slo_s, shi_s, 0};
-  htab_edge_loop<K>(ent, sizes, us, vs, e_begin, e_end, htab_smem + (threadIdx.x >> 5) * kWarpInts, epi);
+  htab_edge_loop<K, P>(ent, sizes, us, vs, e_begin, e_end, htab_smem + (threadIdx.x >> 5) * kWarpInts, epi);
   if (kFused) {
     __syncthreads();
     for (int i = threadIdx.x; i <= K; i += blockDim.x) {
@@ -1834,14 +1846,14 @@ static void launch_onehash_sorted(cudaStream_t s, const int32_t* ent, int k, con
                                 out_verbatim);
 }
 
-template <int K, bool kFused>
+template <int K, int P, bool kFused>
 static void launch_onehash_htab(cudaStream_t s, const int32_t* ent, const int32_t* sizes, const int32_t* us,
                                 const int32_t* vs, int64_t b, int64_t e, int32_t* out_count, double* out_est,
                                 int64_t* out_cnt, int64_t* out_ssum, int64_t* out_verbatim) {
-  auto kern = onehash_htab_kernel<K, kFused>;
-  const size_t sm = sizeof(int32_t) * (kBlock / 32) * (32 / (K / 8)) * htab_group_ints<K>();
+  auto kern = onehash_htab_kernel<K, P, kFused>;
+  const size_t sm = sizeof(int32_t) * (kBlock / 32) * (32 / (K / P)) * htab_group_ints<K>();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / 8));
+  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / P));
   kern<<<grid, kBlock, sm, s>>>(ent, sizes, us, vs, b, e, out_count, out_est, out_cnt, out_ssum, out_verbatim);
 }
 
@@ -1853,17 +1865,21 @@ static bool onehash_sorted(cudaStream_t s, bool fused, const int32_t* ent, int k
     return v && v[0] == 'l';
   }();
   if (!lookup) {
-#define PG_OT(K)                                                                                          \
+#define PG_OT(K, P)                                                                                       \
   {                                                                                                       \
-    if (fused) launch_onehash_htab<K, true>(s, ent, sizes, us, vs, b, e, out_count, out_est, out_cnt,    \
-                                            out_ssum, out_verbatim);                                      \
-    else launch_onehash_htab<K, false>(s, ent, sizes, us, vs, b, e, out_count, out_est, out_cnt,         \
-                                       out_ssum, out_verbatim);                                           \
+    if (fused) launch_onehash_htab<K, P, true>(s, ent, sizes, us, vs, b, e, out_count, out_est, out_cnt, \
+                                               out_ssum, out_verbatim);                                   \
+    else launch_onehash_htab<K, P, false>(s, ent, sizes, us, vs, b, e, out_count, out_est, out_cnt,      \
+                                          out_ssum, out_verbatim);                                        \
     return true;                                                                                          \
   }
-    if (k == 32) PG_OT(32)
-    if (k == 64) PG_OT(64)
-    if (k == 128) PG_OT(128)
+    static const int per_lane = [] {
+      const char* v = getenv("PG_ONEHASH_IDS");
+      return v ? atoi(v) : 8;
+    }();
+    if (k == 32) { if (per_lane == 16) PG_OT(32, 16) PG_OT(32, 8) }
+    if (k == 64) { if (per_lane == 16) PG_OT(64, 16) PG_OT(64, 8) }
+    if (k == 128) { if (per_lane == 16) PG_OT(128, 16) PG_OT(128, 8) }
 #undef PG_OT
   }
 #define PG_OS(G, CH)                                                                                     \
