@@ -1408,7 +1408,7 @@ __global__ void __launch_bounds__(kBlock) onehash_sorted_kernel(const int32_t* e
 }
 
 template <int G, int CH, bool kFused>
-__global__ void __launch_bounds__(kBlock) kmv_sorted_kernel(const uint64_t* vals, int k, const int32_t* sizes,
+__global__ void __launch_bounds__(kBlock, 4) kmv_sorted_kernel(const uint64_t* vals, int k, const int32_t* sizes,
                                                            const int32_t* us, const int32_t* vs,
                                                            int64_t e_begin, int64_t e_end, int32_t* out_common,
                                                            int32_t* out_union, double* out_kth,
