@@ -1997,14 +1997,15 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
   PG_REQUIRE(op == PG_BF_AND || op == PG_BF_L || op == PG_BF_OR, "op is not a Bloom estimator");
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
   PG_REQUIRE(out_hist, "null histogram");
-  PG_REQUIRE(op != PG_BF_OR || (sizes && lut && out_sum_pos), "BF_OR needs sizes, table and sum output");
+  PG_REQUIRE(op != PG_BF_OR || out_sum_pos, "BF_OR needs the sum output");
   cudaStream_t s = as_stream(stream);
   // one memset when the sum slot directly follows the histogram
   const bool adjacent = out_sum_pos == out_hist + bits + 1;
   cudaError_t ce = cudaMemsetAsync(out_hist, 0, sizeof(int64_t) * (bits + 1 + (adjacent ? 1 : 0)), s);
   if (ce == cudaSuccess && out_sum_pos && !adjacent) ce = cudaMemsetAsync(out_sum_pos, 0, sizeof(int64_t), s);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
-  if (e_end == e_begin) return PG_OK;
+  if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
+  PG_REQUIRE(op != PG_BF_OR || (sizes && lut), "BF_OR needs sizes and the table");
   PG_REQUIRE(rows && us && vs, "null pointer");
   EpiBloomHist epi{op, sizes, lut, nullptr, 0};
   const size_t smem = sizeof(int) * (bits + 1);
@@ -2129,7 +2130,7 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
   PG_REQUIRE(k >= 1, "k must be >= 1");
   if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
-  PG_REQUIRE(out_cnt && out_ssum && out_verbatim && sizes, "null pointer");
+  PG_REQUIRE(out_cnt && out_ssum && out_verbatim, "null pointer");
   cudaStream_t s = as_stream(stream);
   // one memset when [cnt | ssum | verbatim] is one buffer
   const bool adjacent = out_ssum == out_cnt + k + 1 && out_verbatim == out_ssum + k + 1;
@@ -2137,8 +2138,8 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
   if (ce == cudaSuccess && !adjacent) ce = cudaMemsetAsync(out_ssum, 0, sizeof(int64_t) * (k + 1), s);
   if (ce == cudaSuccess && !adjacent) ce = cudaMemsetAsync(out_verbatim, 0, sizeof(int64_t), s);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
-  if (e_end == e_begin) return PG_OK;
-  PG_REQUIRE(entries && us && vs, "null pointer");
+  if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
+  PG_REQUIRE(entries && us && vs && sizes, "null pointer");
   if (onehash && onehash_sorted(s, true, entries, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, out_cnt,
                                 out_ssum, out_verbatim))
     return check_launch("tc_onehash_sorted");
@@ -2191,12 +2192,12 @@ int pg_jaccard_count_khash(const int32_t* entries, int32_t k, const int32_t* deg
   PG_REQUIRE(k >= 1, "k must be >= 1");
   if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
-  PG_REQUIRE(out_counts && degrees, "null pointer");
+  PG_REQUIRE(out_counts, "null pointer");
   cudaStream_t s = as_stream(stream);
   cudaError_t ce = cudaMemsetAsync(out_counts, 0, sizeof(int64_t) * (k + 3), s);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
-  if (e_end == e_begin) return PG_OK;
-  PG_REQUIRE(entries && us && vs, "null pointer");
+  if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
+  PG_REQUIRE(entries && us && vs && degrees, "null pointer");
   const int w4 = k % 4 == 0 ? k / 4 : 0;
   const uint4* e4 = reinterpret_cast<const uint4*>(entries);
   const int w8 = k % 8 == 0 ? k / 8 : 0;  // 32-byte chunks per row
@@ -2256,12 +2257,12 @@ int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k, const int
   PG_REQUIRE(k >= 1, "k must be >= 1");
   if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
-  PG_REQUIRE(out_sum && sizes, "null pointer");
+  PG_REQUIRE(out_sum, "null pointer");
   cudaStream_t s = as_stream(stream);
   cudaError_t ce = cudaMemsetAsync(out_sum, 0, sizeof(double), s);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
-  if (e_end == e_begin) return PG_OK;
-  PG_REQUIRE(values && us && vs, "null pointer");
+  if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
+  PG_REQUIRE(values && us && vs && sizes, "null pointer");
   const uint64_t* vb = reinterpret_cast<const uint64_t*>(values);
   if (kmv_sorted(s, true, vb, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, nullptr, nullptr, out_sum))
     return check_launch("tc_kmv_sorted");
