@@ -213,12 +213,15 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
   for (int i = 0; i < V; ++i)
 #pragma unroll
     for (int w = 0; w < 8; ++w) ur[i][w] = 0;
+  // 32-bit remaining-slot count instead of 64-bit bound checks (registers)
+  const int nslots = (int)(we - wb);
 #pragma unroll 1
-  for (int64_t e0 = wb; e0 < we; e0 += 32) {
-    const int64_t e = e0 + lane;
-    const bool valid = e < we && vl >= 0;  // v < 0: padding slot
+  for (int r0 = 0; r0 < nslots; r0 += 32) {
+    const int64_t e = wb + r0 + lane;
+    const int rem = nslots - r0;
+    const bool valid = lane < rem && vl >= 0;  // v < 0: padding slot
     int32_t un = 0, vn = 0;
-    if (e + 32 < we) {
+    if (lane + 32 < rem) {
       un = kLayout == 2 ? us[(e + 32) / G] : us[e + 32];
       vn = vs[e + 32];
     }
@@ -1803,6 +1806,7 @@ static int tc_minb(int w4, bool padded) {
   }();
   if (env >= 1 && env <= 4) return env;
   if (!padded) return 2;  // general layout: speculative u loads need ~110 regs
+  if (w4 >= 16) return 2;  // 256-byte rows: 8 rows of v in flight per lane group need > 80 regs
   return 3;
 }
 
@@ -2036,7 +2040,8 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
   }
 #define PG_WM(W8)                                                                  \
   if (padded == 2) {                                                             \
-    if (vcache) PG_W(W8, 3, true, 2)                                             \
+    if (vcache) { if (minb <= 2) PG_W(W8, 2, true, 2) else PG_W(W8, 3, true, 2) } \
+    else if (minb <= 2) PG_W(W8, 2, false, 2)                                    \
     else PG_W(W8, 3, false, 2)                                                   \
   } else if (padded) {                                                           \
     if (vcache) PG_W(W8, 3, true, 1)                                             \
