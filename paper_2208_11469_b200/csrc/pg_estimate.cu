@@ -2166,13 +2166,13 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
   const uint4* e4 = reinterpret_cast<const uint4*>(entries);
   const int w8 = k % 8 == 0 ? k / 8 : 0;  // 32-byte chunks per row
   if (padded && (w8 == 2 || w8 == 4 || w8 == 8)) {
-#define PG_KW(W8)                                                                        \
+#define PG_KW(W8, MB)                                                                    \
   {                                                                                      \
-    auto kern = tc_khash_kernel<W8, 1, 2, 3>;                                            \
+    auto kern = tc_khash_kernel<W8, 1, 2, MB>;                                           \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);        \
     kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum); \
   }
-    if (w8 == 2) PG_KW(2) else if (w8 == 4) PG_KW(4) else PG_KW(8)
+    if (w8 == 2) PG_KW(2, 3) else if (w8 == 4) PG_KW(4, 3) else PG_KW(8, 3)  // measured: 3 blocks beat the spill-free 2 (0.66 vs 0.72 ms, s20 k=64)
 #undef PG_KW
   } else if (!fast_w4(w4)) {
     auto kern = tc_khash_kernel<1, 1, 0>;
@@ -2207,13 +2207,13 @@ int pg_jaccard_count_khash(const int32_t* entries, int32_t k, const int32_t* deg
   const uint4* e4 = reinterpret_cast<const uint4*>(entries);
   const int w8 = k % 8 == 0 ? k / 8 : 0;  // 32-byte chunks per row
   if (padded && (w8 == 2 || w8 == 4 || w8 == 8)) {
-#define PG_JW(W8)                                                                                      \
+#define PG_JW(W8, MB)                                                                                  \
   {                                                                                                    \
-    auto kern = jaccard_khash_kernel<W8, 1, 2, 3>;                                                     \
+    auto kern = jaccard_khash_kernel<W8, 1, 2, MB>;                                                    \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);                      \
     kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts); \
   }
-    if (w8 == 2) PG_JW(2) else if (w8 == 4) PG_JW(4) else PG_JW(8)
+    if (w8 == 2) PG_JW(2, 3) else if (w8 == 4) PG_JW(4, 3) else PG_JW(8, 2)  // 256-B rows: 2 blocks (no spills)
 #undef PG_JW
   } else if (!fast_w4(w4)) {
     auto kern = jaccard_khash_kernel<1, 1, 0>;
