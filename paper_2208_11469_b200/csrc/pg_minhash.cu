@@ -1,0 +1,435 @@
+// k-Hash / 1-Hash per-edge estimates (providers.py:197-232 pair_many,
+// _matches_khash / _matches_onehash), their fused TC reductions and the
+// Jaccard threshold count (estimators.py:123-168, mining.py:157-186).
+#include "pg_engines.cuh"
+
+namespace pg {
+
+
+template <int V, int G, bool kScalar>
+__global__ void __launch_bounds__(kBlock) pairs_khash_kernel(const uint4* ent, int k, const int32_t* us,
+                                                            const int32_t* vs, int64_t count,
+                                                            EpiMinhashPairs epi) {
+  if (kScalar) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, 0, count, epi);
+  else group_edge_loop<V, G, OpEqPos>(ent, us, vs, 0, count, epi);
+}
+
+// kEngine: 0 scalar fallback, 1 group (128-bit) engine, 2 wide padded engine
+template <int V, int G, int kEngine, int MINB = 1>
+__global__ void __launch_bounds__(kBlock, MINB) tc_khash_kernel(const uint4* ent, int k, const int32_t* sizes,
+                                                               const int32_t* us, const int32_t* vs,
+                                                               int64_t e_begin, int64_t e_end,
+                                                               int64_t* out_cnt, int64_t* out_ssum) {
+  __shared__ int cnt_s[kMaxSketchK + 1];
+  __shared__ unsigned slo_s[kMaxSketchK + 1], shi_s[kMaxSketchK + 1];
+  for (int i = threadIdx.x; i <= k; i += blockDim.x) { cnt_s[i] = 0; slo_s[i] = 0; shi_s[i] = 0; }
+  __syncthreads();
+  EpiMinhashHist epi{sizes, cnt_s, slo_s, shi_s};
+  if (kEngine == 0) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
+  else if (kEngine == 1) group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
+  else wide_edge_loop<V, OpEqPos, EpiMinhashHist, false, true>(reinterpret_cast<const unsigned char*>(ent), us,
+                                                                vs, e_begin, e_end, epi);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+    if (cnt_s[i]) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(out_cnt + i), (unsigned long long)cnt_s[i]);
+      atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i),
+                ((unsigned long long)shi_s[i] << 32) + slo_s[i]);
+    }
+  }
+}
+
+template <int V, int G, int kEngine, int MINB = 1>
+__global__ void __launch_bounds__(kBlock, MINB) jaccard_khash_kernel(const uint4* ent, int k, const int32_t* deg,
+                                                                    const int32_t* us, const int32_t* vs,
+                                                                    int64_t e_begin, int64_t e_end,
+                                                                    int min_matches, double tau,
+                                                                    int64_t* out_counts) {
+  __shared__ int hist_s[kMaxSketchK + 1];
+  for (int i = threadIdx.x; i <= k; i += blockDim.x) hist_s[i] = 0;
+  __syncthreads();
+  EpiJaccard epi{k, min_matches, tau, deg, hist_s, 0, 0};
+  if (kEngine == 0) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
+  else if (kEngine == 1) group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
+  else wide_edge_loop<V, OpEqPos, EpiJaccard, false, true>(reinterpret_cast<const unsigned char*>(ent), us, vs,
+                                                            e_begin, e_end, epi);
+  __syncthreads();
+  for (int i = threadIdx.x; i <= k; i += blockDim.x)
+    if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_counts + 2 + i), (unsigned long long)hist_s[i]);
+  long long a = epi.n_hat, b = epi.n_sim;
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    b += __shfl_xor_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    if (a) atomicAdd(reinterpret_cast<unsigned long long*>(out_counts + 0), (unsigned long long)a);
+    if (b) atomicAdd(reinterpret_cast<unsigned long long*>(out_counts + 1), (unsigned long long)b);
+  }
+}
+
+// warp-per-edge match count of two ascending ID lists (-1 padded); returns
+// m and the two list lengths (warp-uniform)
+template <int P>
+__device__ __forceinline__ int onehash_matches(const int32_t* __restrict__ ent, int k, int32_t u, int32_t v,
+                                               int32_t* vbuf, int& lu, int& lv) {
+  const int lane = threadIdx.x & 31;
+  int32_t a[P], b[P];
+  lu = 0;
+  lv = 0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int idx = lane + 32 * s;
+    a[s] = idx < k ? ent[(int64_t)u * k + idx] : -1;
+    b[s] = idx < k ? ent[(int64_t)v * k + idx] : -1;
+    lu += __popc(__ballot_sync(0xffffffffu, a[s] >= 0));
+    lv += __popc(__ballot_sync(0xffffffffu, b[s] >= 0));
+  }
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int idx = lane + 32 * s;
+    if (idx < lv) vbuf[idx] = b[s];
+  }
+  __syncwarp();
+  int m = 0;
+#pragma unroll
+  for (int s = 0; s < P; ++s) {
+    const int idx = lane + 32 * s;
+    bool hit = false;
+    if (idx < lu) {
+      const int p = smem_lower_bound(vbuf, lv, a[s]);
+      hit = p < lv && vbuf[p] == a[s];
+    }
+    m += __popc(__ballot_sync(0xffffffffu, hit));
+  }
+  __syncwarp();
+  return m;
+}
+
+template <int P, bool kFused>
+__global__ void __launch_bounds__(kBlock) onehash_kernel(const int32_t* ent, int k, const int32_t* sizes,
+                                                        const int32_t* us, const int32_t* vs,
+                                                        int64_t e_begin, int64_t e_end,
+                                                        int32_t* out_count, double* out_est,
+                                                        int64_t* out_cnt, int64_t* out_ssum,
+                                                        int64_t* out_verbatim) {
+  __shared__ int32_t vbuf[kBlock / 32][32 * P];
+  __shared__ int cnt_s[kMaxSketchK + 1];
+  __shared__ unsigned slo_s[kMaxSketchK + 1], shi_s[kMaxSketchK + 1];
+  if (kFused) {
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) { cnt_s[i] = 0; slo_s[i] = 0; shi_s[i] = 0; }
+    __syncthreads();
+  }
+  const int lane = threadIdx.x & 31;
+  long long verb = 0;
+  int64_t wb, we;
+  warp_slice(e_begin, e_end, wb, we);
+  for (int64_t e = wb; e < we; ++e) {
+    const int32_t u = us[e], v = vs[e];
+    int lu, lv;
+    const int m = onehash_matches<P>(ent, k, u, v, vbuf[threadIdx.x >> 5], lu, lv);
+    if (lane == 0) {
+      const int32_t su = sizes[u], sv = sizes[v];
+      const bool verbatim = su <= k && sv <= k;
+      if (kFused) {
+        if (verbatim) verb += m;
+        else {
+          atomicAdd(cnt_s + m, 1);
+          smem_add64(slo_s + m, shi_s + m, (uint64_t)((int64_t)su + sv));
+        }
+      } else {
+        if (out_count) out_count[e] = m;
+        if (out_est) out_est[e] = verbatim ? (double)m : minhash_estimate(m, k, su, sv);
+      }
+    }
+  }
+  if (kFused) {
+    __syncthreads();
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+      if (cnt_s[i]) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_cnt + i), (unsigned long long)cnt_s[i]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i),
+                  ((unsigned long long)shi_s[i] << 32) + slo_s[i]);
+      }
+    }
+    if (lane == 0 && verb) atomicAdd(reinterpret_cast<unsigned long long*>(out_verbatim), (unsigned long long)verb);
+  }
+}
+
+template <int K, int P, bool kFused>
+__global__ void __launch_bounds__(kBlock) onehash_htab_kernel(const int32_t* ent, const int32_t* sizes,
+                                                             const int32_t* us, const int32_t* vs,
+                                                             int64_t e_begin, int64_t e_end, int32_t* out_count,
+                                                             double* out_est, int64_t* out_cnt, int64_t* out_ssum,
+                                                             int64_t* out_verbatim) {
+  extern __shared__ __align__(16) int32_t htab_smem[];  // (kBlock/32) * (32/G) groups
+  __shared__ int cnt_s[K + 1];
+  __shared__ unsigned slo_s[K + 1], shi_s[K + 1];
+  if (kFused) {
+    for (int i = threadIdx.x; i <= K; i += blockDim.x) { cnt_s[i] = 0; slo_s[i] = 0; shi_s[i] = 0; }
+    __syncthreads();
+  }
+  constexpr int kWarpInts = (32 / (K / P)) * htab_group_ints<K>();
+  EpiOnehash epi{K, sizes, out_count, out_est, kFused ? cnt_s : nullptr, slo_s, shi_s, 0};
+  htab_edge_loop<K, P>(ent, sizes, us, vs, e_begin, e_end, htab_smem + (threadIdx.x >> 5) * kWarpInts, epi);
+  if (kFused) {
+    __syncthreads();
+    for (int i = threadIdx.x; i <= K; i += blockDim.x) {
+      if (cnt_s[i]) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_cnt + i), (unsigned long long)cnt_s[i]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i),
+                  ((unsigned long long)shi_s[i] << 32) + slo_s[i]);
+      }
+    }
+    long long vb = epi.verb;
+    for (int o = 16; o > 0; o >>= 1) vb += __shfl_xor_sync(0xffffffffu, vb, o);
+    if ((threadIdx.x & 31) == 0 && vb)
+      atomicAdd(reinterpret_cast<unsigned long long*>(out_verbatim), (unsigned long long)vb);
+  }
+}
+
+template <int G, int CH, bool kFused>
+__global__ void __launch_bounds__(kBlock) onehash_sorted_kernel(const int32_t* ent, int k, const int32_t* sizes,
+                                                               const int32_t* us, const int32_t* vs,
+                                                               int64_t e_begin, int64_t e_end,
+                                                               int32_t* out_count, double* out_est,
+                                                               int64_t* out_cnt, int64_t* out_ssum,
+                                                               int64_t* out_verbatim) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int cnt_s[kMaxSketchK + 1];
+  __shared__ unsigned slo_s[kMaxSketchK + 1], shi_s[kMaxSketchK + 1];
+  if (kFused) {
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) { cnt_s[i] = 0; slo_s[i] = 0; shi_s[i] = 0; }
+    __syncthreads();
+  }
+  EpiOnehash epi{k, sizes, out_count, out_est, kFused ? cnt_s : nullptr, slo_s, shi_s, 0};
+  sorted_edge_loop<G, CH>(ent, k, us, vs, e_begin, e_end,
+                          smem_raw + (threadIdx.x >> 5) * sorted_warp_smem<G, CH>(), epi);
+  if (kFused) {
+    __syncthreads();
+    for (int i = threadIdx.x; i <= k; i += blockDim.x) {
+      if (cnt_s[i]) {
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_cnt + i), (unsigned long long)cnt_s[i]);
+        atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i),
+                  ((unsigned long long)shi_s[i] << 32) + slo_s[i]);
+      }
+    }
+    long long vb = epi.verb;
+    for (int o = 16; o > 0; o >>= 1) vb += __shfl_xor_sync(0xffffffffu, vb, o);
+    if ((threadIdx.x & 31) == 0 && vb)
+      atomicAdd(reinterpret_cast<unsigned long long*>(out_verbatim), (unsigned long long)vb);
+  }
+}
+
+// sorted-engine launchers; return false when k has no specialisation
+template <int G, int CH, bool kFused>
+static void launch_onehash_sorted(cudaStream_t s, const int32_t* ent, int k, const int32_t* sizes,
+                                  const int32_t* us, const int32_t* vs, int64_t b, int64_t e,
+                                  int32_t* out_count, double* out_est, int64_t* out_cnt,
+                                  int64_t* out_ssum, int64_t* out_verbatim) {
+  auto kern = onehash_sorted_kernel<G, CH, kFused>;
+  const size_t sm = (size_t)(kBlock / 32) * sorted_warp_smem<G, CH>();
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / G);
+  kern<<<grid, kBlock, sm, s>>>(ent, k, sizes, us, vs, b, e, out_count, out_est, out_cnt, out_ssum,
+                                out_verbatim);
+}
+
+template <int K, int P, bool kFused>
+static void launch_onehash_htab(cudaStream_t s, const int32_t* ent, const int32_t* sizes, const int32_t* us,
+                                const int32_t* vs, int64_t b, int64_t e, int32_t* out_count, double* out_est,
+                                int64_t* out_cnt, int64_t* out_ssum, int64_t* out_verbatim) {
+  auto kern = onehash_htab_kernel<K, P, kFused>;
+  const size_t sm = sizeof(int32_t) * (kBlock / 32) * (32 / (K / P)) * htab_group_ints<K>();
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / P));
+  kern<<<grid, kBlock, sm, s>>>(ent, sizes, us, vs, b, e, out_count, out_est, out_cnt, out_ssum, out_verbatim);
+}
+
+static bool onehash_sorted(cudaStream_t s, bool fused, const int32_t* ent, int k, const int32_t* sizes,
+                           const int32_t* us, const int32_t* vs, int64_t b, int64_t e, int32_t* out_count,
+                           double* out_est, int64_t* out_cnt, int64_t* out_ssum, int64_t* out_verbatim) {
+  static const bool lookup = [] {
+    const char* v = getenv("PG_ONEHASH_ENGINE");
+    return v && v[0] == 'l';
+  }();
+  if (!lookup) {
+#define PG_OT(K, P)                                                                                       \
+  {                                                                                                       \
+    if (fused) launch_onehash_htab<K, P, true>(s, ent, sizes, us, vs, b, e, out_count, out_est, out_cnt, \
+                                               out_ssum, out_verbatim);                                   \
+    else launch_onehash_htab<K, P, false>(s, ent, sizes, us, vs, b, e, out_count, out_est, out_cnt,      \
+                                          out_ssum, out_verbatim);                                        \
+    return true;                                                                                          \
+  }
+    static const int per_lane = [] {
+      const char* v = getenv("PG_ONEHASH_IDS");
+      return v ? atoi(v) : 8;
+    }();
+    if (k == 32) { if (per_lane == 16) PG_OT(32, 16) PG_OT(32, 8) }
+    if (k == 64) { if (per_lane == 16) PG_OT(64, 16) PG_OT(64, 8) }
+    if (k == 128) { if (per_lane == 16) PG_OT(128, 16) PG_OT(128, 8) }
+#undef PG_OT
+  }
+#define PG_OS(G, CH)                                                                                     \
+  {                                                                                                      \
+    if (fused) launch_onehash_sorted<G, CH, true>(s, ent, k, sizes, us, vs, b, e, out_count, out_est,    \
+                                                  out_cnt, out_ssum, out_verbatim);                      \
+    else launch_onehash_sorted<G, CH, false>(s, ent, k, sizes, us, vs, b, e, out_count, out_est,        \
+                                             out_cnt, out_ssum, out_verbatim);                           \
+    return true;                                                                                         \
+  }
+  if (k == 32) PG_OS(4, 1)
+  if (k == 64) PG_OS(8, 1)
+  if (k == 128) PG_OS(8, 2)
+#undef PG_OS
+  return false;
+}
+}  // namespace pg
+
+using namespace pg;
+
+extern "C" {
+
+
+int pg_pairs_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int32_t* sizes,
+                     const int32_t* us, const int32_t* vs, int64_t count, int32_t* out_count,
+                     double* out_est, void* stream) {
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(count >= 0, "count must be >= 0");
+  if (count == 0) return PG_OK;
+  PG_REQUIRE(entries && us && vs, "null pointer");
+  PG_REQUIRE(!out_est || sizes, "estimate needs sizes");
+  cudaStream_t s = as_stream(stream);
+  if (onehash) {
+    PG_REQUIRE(sizes, "1-Hash needs sizes");
+    if (onehash_sorted(s, false, entries, k, sizes, us, vs, 0, count, out_count, out_est, nullptr, nullptr,
+                       nullptr))
+      return check_launch("pairs_onehash_sorted");
+    const int grid = grid_cap(sm_count() * 8, count, kBlock / 32);
+#define PG_OH(P) onehash_kernel<P, false><<<grid, kBlock, 0, s>>>(entries, k, sizes, us, vs, 0, count, out_count, out_est, nullptr, nullptr, nullptr)
+    if (k <= 32) PG_OH(1);
+    else if (k <= 64) PG_OH(2);
+    else if (k <= 128) PG_OH(4);
+    else PG_OH(8);
+#undef PG_OH
+    return check_launch("pairs_onehash");
+  }
+  EpiMinhashPairs epi{k, sizes, out_count, out_est};
+  const int grid = grid_cap(sm_count() * 8, count, kBlock);
+  const int w4 = k % 4 == 0 ? k / 4 : 0;
+  const uint4* e4 = reinterpret_cast<const uint4*>(entries);
+  if (!fast_w4(w4)) {
+    pairs_khash_kernel<1, 1, true><<<grid, kBlock, 0, s>>>(e4, k, us, vs, count, epi);
+  } else {
+#define PG_L(V, G) pairs_khash_kernel<V, G, false><<<grid, kBlock, 0, s>>>(e4, k, us, vs, count, epi);
+    PG_ROW_DISPATCH(w4, PG_L)
+#undef PG_L
+  }
+  return check_launch("pairs_khash");
+}
+
+int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int32_t* sizes,
+                  const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end, int32_t padded,
+                  int64_t* out_cnt, int64_t* out_ssum, int64_t* out_verbatim, void* stream) {
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
+  PG_REQUIRE(out_cnt && out_ssum && out_verbatim, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  // one memset when [cnt | ssum | verbatim] is one buffer
+  const bool adjacent = out_ssum == out_cnt + k + 1 && out_verbatim == out_ssum + k + 1;
+  cudaError_t ce = cudaMemsetAsync(out_cnt, 0, sizeof(int64_t) * (adjacent ? 2 * k + 3 : k + 1), s);
+  if (ce == cudaSuccess && !adjacent) ce = cudaMemsetAsync(out_ssum, 0, sizeof(int64_t) * (k + 1), s);
+  if (ce == cudaSuccess && !adjacent) ce = cudaMemsetAsync(out_verbatim, 0, sizeof(int64_t), s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
+  PG_REQUIRE(entries && us && vs && sizes, "null pointer");
+  if (onehash && onehash_sorted(s, true, entries, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, out_cnt,
+                                out_ssum, out_verbatim))
+    return check_launch("tc_onehash_sorted");
+  if (onehash) {
+#define PG_OH(P)                                                                                  \
+  {                                                                                               \
+    auto kern = onehash_kernel<P, true>;                                                          \
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock / 32);            \
+    kern<<<grid, kBlock, 0, s>>>(entries, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, out_cnt, out_ssum, out_verbatim); \
+  }
+    if (k <= 32) PG_OH(1)
+    else if (k <= 64) PG_OH(2)
+    else if (k <= 128) PG_OH(4)
+    else PG_OH(8)
+#undef PG_OH
+    return check_launch("tc_onehash");
+  }
+  const int w4 = k % 4 == 0 ? k / 4 : 0;
+  const uint4* e4 = reinterpret_cast<const uint4*>(entries);
+  const int w8 = k % 8 == 0 ? k / 8 : 0;  // 32-byte chunks per row
+  if (padded && (w8 == 2 || w8 == 4 || w8 == 8)) {
+#define PG_KW(W8, MB)                                                                    \
+  {                                                                                      \
+    auto kern = tc_khash_kernel<W8, 1, 2, MB>;                                           \
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);        \
+    kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum); \
+  }
+    if (w8 == 2) PG_KW(2, 3) else if (w8 == 4) PG_KW(4, 3) else PG_KW(8, 3)  // measured: 3 blocks beat the spill-free 2 (0.66 vs 0.72 ms, s20 k=64)
+#undef PG_KW
+  } else if (!fast_w4(w4)) {
+    auto kern = tc_khash_kernel<1, 1, 0>;
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);
+    kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum);
+  } else {
+#define PG_L(V, G)                                                                       \
+  {                                                                                      \
+    auto kern = tc_khash_kernel<V, G, 1>;                                                \
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);        \
+    kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum); \
+  }
+    PG_ROW_DISPATCH(w4, PG_L)
+#undef PG_L
+  }
+  return check_launch("tc_khash");
+}
+
+int pg_jaccard_count_khash(const int32_t* entries, int32_t k, const int32_t* degrees, const int32_t* us,
+                           const int32_t* vs, int64_t e_begin, int64_t e_end, int32_t padded,
+                           int32_t min_matches, double tau, int64_t* out_counts, void* stream) {
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
+  PG_REQUIRE(out_counts, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  cudaError_t ce = cudaMemsetAsync(out_counts, 0, sizeof(int64_t) * (k + 3), s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
+  PG_REQUIRE(entries && us && vs && degrees, "null pointer");
+  const int w4 = k % 4 == 0 ? k / 4 : 0;
+  const uint4* e4 = reinterpret_cast<const uint4*>(entries);
+  const int w8 = k % 8 == 0 ? k / 8 : 0;  // 32-byte chunks per row
+  if (padded && (w8 == 2 || w8 == 4 || w8 == 8)) {
+#define PG_JW(W8, MB)                                                                                  \
+  {                                                                                                    \
+    auto kern = jaccard_khash_kernel<W8, 1, 2, MB>;                                                    \
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);                      \
+    kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts); \
+  }
+    if (w8 == 2) PG_JW(2, 3) else if (w8 == 4) PG_JW(4, 3) else PG_JW(8, 2)  // 256-B rows: 2 blocks (no spills)
+#undef PG_JW
+  } else if (!fast_w4(w4)) {
+    auto kern = jaccard_khash_kernel<1, 1, 0>;
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);
+    kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts);
+  } else {
+#define PG_L(V, G)                                                                                         \
+  {                                                                                                        \
+    auto kern = jaccard_khash_kernel<V, G, 1>;                                                             \
+    const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);                          \
+    kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts);    \
+  }
+    PG_ROW_DISPATCH(w4, PG_L)
+#undef PG_L
+  }
+  return check_launch("jaccard_khash");
+}
+
+}  // extern "C"
