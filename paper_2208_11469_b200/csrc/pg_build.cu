@@ -87,7 +87,8 @@ __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
     meta->pref[lane] = incl - (int)d;
     meta->off[lane] = o;
     if (lane == 31) meta->pref[32] = incl;
-    for (uint32_t i = lane; i < (uint32_t)R * words32; i += 32) brows[i] = 0u;
+    uint4* brows4 = reinterpret_cast<uint4*>(brows);
+    for (uint32_t i = lane; i < (uint32_t)R * words32 / 4; i += 32) brows4[i] = make_uint4(0u, 0u, 0u, 0u);
     __syncwarp();
     const int total = meta->pref[32];
     int j = 0;  // batch vertex of the lane's current entry (non-decreasing)
@@ -101,15 +102,16 @@ __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
       }
     }
     __syncwarp();
-    // the batch rows (hub rows are all-zero here; pass 2 ORs into them)
-    // and the non-hub ones
+    // the batch rows -- consecutive vertices, so one contiguous block of the
+    // output, copied with 128-bit stores by all lanes (hub rows are all-zero
+    // here; pass 2 ORs into them) -- and the non-hub ones (each lane its own
+    // row, words read in a lane-rotated order to spread the banks)
     const uint64_t* b64 = reinterpret_cast<const uint64_t*>(brows);
-    for (int r = 0; r < nb; ++r) {
-      for (uint32_t i = lane; i < words64; i += 32) rows[(vb + r) * words64 + i] = b64[r * words64 + i];
-    }
+    uint4* out4 = reinterpret_cast<uint4*>(rows + vb * words64);
+    for (uint32_t i = lane; i < (uint32_t)nb * words64 / 2; i += 32) out4[i] = brows4[i];
     if (mine && !hub) {
       int c = 0;
-      for (uint32_t i = 0; i < words64; ++i) c += __popcll(b64[lane * words64 + i]);
+      for (uint32_t i = 0; i < words64; ++i) c += __popcll(b64[lane * words64 + (i + lane) % words64]);
       ones[v] = c;
     }
     __syncwarp();
