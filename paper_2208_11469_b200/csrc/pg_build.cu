@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n,
     uint32_t bits, int b, int R, const uint64_t* __restrict__ seeds_dev,
     uint64_t* __restrict__ rows, int32_t* __restrict__ ones, int32_t* __restrict__ hubs,
-    int32_t* __restrict__ hub_count) {
+    int32_t* __restrict__ hub_count, unsigned long long* __restrict__ vtx_work) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t words32 = bits >> 5;
   const uint32_t words64 = bits >> 6;
@@ -66,8 +66,13 @@ __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
   for (int i = threadIdx.x; i < b; i += kThreads) seeds[i] = seeds_dev[i];
   __syncthreads();
   const int lane = lane_id();
-  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-  for (int64_t vb = ((int64_t)blockIdx.x * kWarps + warp_id()) * R; vb < n; vb += nwarps * R) {
+  // warps take R-vertex batches from a global counter (row costs vary
+  // widely: a static split left most warps idle, 15% achieved occupancy)
+  for (;;) {
+    unsigned long long vbu = 0;
+    if (lane == 0) vbu = atomicAdd(vtx_work, (unsigned long long)R);
+    const int64_t vb = (int64_t)__shfl_sync(0xffffffffu, vbu, 0);
+    if (vb >= n) break;
     const int nb = (int)((n - vb) < R ? (n - vb) : R);
     const int64_t v = vb + lane;
     const bool mine = lane < nb;
@@ -657,7 +662,7 @@ int pg_build_bloom(const int64_t* offsets, const int32_t* adj, int64_t n, int32_
                          (int)smem_hub);                                                                \
     const int grid = grid_for(build_bloom_kernel<P2>, smem, (n + R - 1) / R * 32);                      \
     build_bloom_kernel<P2><<<grid, kThreads, smem, s>>>(offsets, adj, n, bits, b, R, seeds_dev, rows, ones, \
-                                                        hubs.ids, hubs.count);                          \
+                                                        hubs.ids, hubs.count, hubs.vtx_work);           \
     build_bloom_hubs_kernel<P2><<<hub_grid(), kThreads, smem_hub, s>>>(offsets, adj, bits, b, seeds_dev,  \
                                                                        rows, hubs.ids, hubs.count);       \
     bloom_hub_ones_kernel<<<64, kThreads, 0, s>>>(rows, bits / 64, ones, hubs.ids, hubs.count);          \
