@@ -104,6 +104,37 @@ __device__ __forceinline__ void warp_slice(int64_t e_begin, int64_t e_end, int64
   if (wb > e_end) wb = e_end;
 }
 
+// Dynamic edge chunks: a warp takes the next `chunk`-edge range of
+// [e_begin, e_end) from a per-launch global counter (zeroed by the launcher).
+// Per-edge cost varies (row lengths, u-run rebuilds), and a static split
+// left warps idle at the block's final barrier.
+__device__ __forceinline__ bool next_chunk(unsigned long long* ctr, int64_t e_begin, int64_t e_end,
+                                           int64_t chunk, int64_t& wb, int64_t& we) {
+  unsigned long long c = 0;
+  if ((threadIdx.x & 31) == 0) c = atomicAdd(ctr, 1ull);
+  c = __shfl_sync(0xffffffffu, c, 0);
+  wb = e_begin + (int64_t)c * chunk;
+  if (wb >= e_end) return false;
+  we = min(wb + chunk, e_end);
+  return true;
+}
+
+// host: one zeroed 64-bit chunk counter per launch (stream-ordered scratch)
+struct ChunkCounter {
+  unsigned long long* p = nullptr;
+  cudaStream_t s = nullptr;
+  cudaError_t init(cudaStream_t st) {
+    s = st;
+    retain_default_pool();
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(unsigned long long), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, sizeof(unsigned long long), s);
+    return e;
+  }
+  ~ChunkCounter() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
 // Group engine: calls epi.edge(e, u, v, count) once per edge of the warp's
 // slice, from the lane that loaded the edge.
 //
@@ -541,81 +572,85 @@ __device__ __forceinline__ void ldg_rowpart(const int32_t* p, uint32_t (&x)[P]) 
 template <int K, int P, class Epi>
 __device__ __forceinline__ void htab_edge_loop(const int32_t* __restrict__ R, const int32_t* __restrict__ sizes,
                                                const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
-                                               int64_t e_begin, int64_t e_end, int32_t* warp_smem, Epi& epi) {
+                                               int64_t e_begin, int64_t e_end, unsigned long long* ctr,
+                                               int32_t* warp_smem, Epi& epi) {
   constexpr int G = K / P, E = 32 / G;
+  constexpr int64_t kChunk = 64 * E;
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
   const unsigned gmask = ((G == 32) ? 0xffffffffu : ((1u << G) - 1u)) << (grp * G);
   int32_t* T = warp_smem + grp * htab_group_ints<K>();  // 4K slots
   int32_t* S = T + 4 * K;                                 // stash (K)
   int* sc_p = reinterpret_cast<int*>(S + K);
-  int64_t wb, we;
-  warp_slice(e_begin, e_end, wb, we);
-  if (wb >= we) return;
-  int32_t ul = 0, vl = -1, szu = 0, szv = 0;
-  if (wb + grp < we) {
-    ul = us[wb + grp];
-    vl = vs[wb + grp];
-    szu = sizes[ul];
-    szv = vl < 0 ? 0 : sizes[vl];
-  }
-  uint32_t x[P];
-  ldg_rowpart<P>(R + (int64_t)(vl < 0 ? 0 : vl) * K + gl * P, x);
-  int32_t cur_u = -1;
+  int32_t cur_u = -1;  // the group's table survives chunk boundaries
   int sc = 0;
-#pragma unroll 1
-  for (int64_t e0 = wb; e0 < we; e0 += E) {
-    const int64_t e = e0 + grp;
-    const bool valid = e < we && vl >= 0;
-    int32_t un = 0, vn = -1;
-    if (e + E < we) {
-      un = us[e + E];
-      vn = vs[e + E];
+  int64_t wb, we;
+  while (next_chunk(ctr, e_begin, e_end, kChunk, wb, we)) {
+    int32_t ul = 0, vl = -1, szu = 0, szv = 0;
+    if (wb + grp < we) {
+      ul = us[wb + grp];
+      vl = vs[wb + grp];
+      szu = sizes[ul];
+      szv = vl < 0 ? 0 : sizes[vl];
     }
-    if (ul != cur_u) {  // uniform within the group: (re)build its table
-      uint32_t y[P];
-      ldg_rowpart<P>(R + (int64_t)ul * K + gl * P, y);
-      int4* T4 = reinterpret_cast<int4*>(T);
+    uint32_t x[P];
+    ldg_rowpart<P>(R + (int64_t)(vl < 0 ? 0 : vl) * K + gl * P, x);
+#pragma unroll 1
+    for (int64_t e0 = wb; e0 < we; e0 += E) {
+      const int64_t e = e0 + grp;
+      const bool valid = e < we && vl >= 0;
+      int32_t un = 0, vn = -1;
+      if (e + E < we) {
+        un = us[e + E];
+        vn = vs[e + E];
+      }
+      if (ul != cur_u) {  // uniform within the group: (re)build its table
+        uint32_t y[P];
+        ldg_rowpart<P>(R + (int64_t)ul * K + gl * P, y);
+        int4* T4 = reinterpret_cast<int4*>(T);
 #pragma unroll
-      for (int i = gl; i < K; i += G) T4[i] = make_int4(-1, -1, -1, -1);
-      if (gl == 0) *sc_p = 0;
-      __syncwarp(gmask);
+        for (int i = gl; i < K; i += G) T4[i] = make_int4(-1, -1, -1, -1);
+        if (gl == 0) *sc_p = 0;
+        __syncwarp(gmask);
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const int32_t q = (int32_t)y[p];
+          if (q < 0) continue;  // -1 pad
+          int32_t* bk = T + 4 * htab_bucket<K>(q);
+          bool placed = false;
+#pragma unroll
+          for (int sl = 0; sl < 4 && !placed; ++sl) placed = atomicCAS(bk + sl, -1, q) == -1;
+          if (!placed) S[atomicAdd(sc_p, 1)] = q;
+        }
+        __syncwarp(gmask);
+        sc = *reinterpret_cast<volatile int*>(sc_p);
+        cur_u = ul;
+      }
+      uint32_t xn[P];
+      ldg_rowpart<P>(R + (int64_t)(vn < 0 ? 0 : vn) * K + gl * P, xn);
+      const int32_t szun = un == ul ? szu : sizes[un];
+      const int32_t szvn = vn < 0 ? 0 : sizes[vn];
+      int m = 0;
 #pragma unroll
       for (int p = 0; p < P; ++p) {
-        const int32_t q = (int32_t)y[p];
-        if (q < 0) continue;  // -1 pad
-        int32_t* bk = T + 4 * htab_bucket<K>(q);
-        bool placed = false;
-#pragma unroll
-        for (int sl = 0; sl < 4 && !placed; ++sl) placed = atomicCAS(bk + sl, -1, q) == -1;
-        if (!placed) S[atomicAdd(sc_p, 1)] = q;
+        const int32_t q = (int32_t)x[p];
+        if (q >= 0) {  // pads (-1) cost no shared-memory wavefront
+          const int4 bk = reinterpret_cast<const int4*>(T)[htab_bucket<K>(q)];
+          bool hit = (bk.x == q) | (bk.y == q) | (bk.z == q) | (bk.w == q);
+          for (int i = 0; i < sc; ++i) hit |= S[i] == q;
+          m += hit;
+        }
       }
-      __syncwarp(gmask);
-      sc = *reinterpret_cast<volatile int*>(sc_p);
-      cur_u = ul;
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+      if (valid && gl == 0) epi.edge_sized(e, szu, szv, m, min(szu, K), min(szv, K));
+#pragma unroll
+      for (int p = 0; p < P; ++p) x[p] = xn[p];
+      __syncwarp();
+      ul = un;
+      vl = vn;
+      szu = szun;
+      szv = szvn;
     }
-    uint32_t xn[P];
-    ldg_rowpart<P>(R + (int64_t)(vn < 0 ? 0 : vn) * K + gl * P, xn);
-    const int32_t szun = un == ul ? szu : sizes[un];
-    const int32_t szvn = vn < 0 ? 0 : sizes[vn];
-    int m = 0;
-#pragma unroll
-    for (int p = 0; p < P; ++p) {
-      const int32_t q = (int32_t)x[p];
-      const int4 bk = reinterpret_cast<const int4*>(T)[htab_bucket<K>(q < 0 ? 0 : q)];
-      bool hit = (bk.x == q) | (bk.y == q) | (bk.z == q) | (bk.w == q);
-      for (int i = 0; i < sc; ++i) hit |= S[i] == q;
-      m += hit & (q >= 0);
-    }
-#pragma unroll
-    for (int o = G / 2; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
-    if (valid && gl == 0) epi.edge_sized(e, szu, szv, m, min(szu, K), min(szv, K));
-#pragma unroll
-    for (int p = 0; p < P; ++p) x[p] = xn[p];
-    __syncwarp();
-    ul = un;
-    vl = vn;
-    szu = szun;
-    szv = szvn;
   }
 }
 

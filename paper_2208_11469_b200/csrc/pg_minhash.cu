@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kBlock) onehash_htab_kernel(const int32_t* ent
                                                              const int32_t* us, const int32_t* vs,
                                                              int64_t e_begin, int64_t e_end, int32_t* out_count,
                                                              double* out_est, int64_t* out_cnt, int64_t* out_ssum,
-                                                             int64_t* out_verbatim) {
+                                                             int64_t* out_verbatim, unsigned long long* ctr) {
   extern __shared__ __align__(16) int32_t htab_smem[];  // (kBlock/32) * (32/G) groups
   __shared__ int cnt_s[K + 1];
   __shared__ unsigned slo_s[K + 1], shi_s[K + 1];
@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kBlock) onehash_htab_kernel(const int32_t* ent
   }
   constexpr int kWarpInts = (32 / (K / P)) * htab_group_ints<K>();
   EpiOnehash epi{K, sizes, out_count, out_est, kFused ? cnt_s : nullptr, slo_s, shi_s, 0};
-  htab_edge_loop<K, P>(ent, sizes, us, vs, e_begin, e_end, htab_smem + (threadIdx.x >> 5) * kWarpInts, epi);
+  htab_edge_loop<K, P>(ent, sizes, us, vs, e_begin, e_end, ctr, htab_smem + (threadIdx.x >> 5) * kWarpInts, epi);
   if (kFused) {
     __syncthreads();
     for (int i = threadIdx.x; i <= K; i += blockDim.x) {
@@ -242,7 +242,10 @@ static void launch_onehash_htab(cudaStream_t s, const int32_t* ent, const int32_
   const size_t sm = sizeof(int32_t) * (kBlock / 32) * (32 / (K / P)) * htab_group_ints<K>();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / P));
-  kern<<<grid, kBlock, sm, s>>>(ent, sizes, us, vs, b, e, out_count, out_est, out_cnt, out_ssum, out_verbatim);
+  ChunkCounter ctr;
+  if (ctr.init(s) != cudaSuccess) return;  // reported by check_launch
+  kern<<<grid, kBlock, sm, s>>>(ent, sizes, us, vs, b, e, out_count, out_est, out_cnt, out_ssum, out_verbatim,
+                                ctr.p);
 }
 
 static bool onehash_sorted(cudaStream_t s, bool fused, const int32_t* ent, int k, const int32_t* sizes,
