@@ -116,6 +116,18 @@ PG_API int pg_build_onehash(const int64_t* offsets, const int32_t* adj, int64_t 
 PG_API int pg_build_kmv(const int64_t* offsets, const int32_t* adj, int64_t n,
                  int32_t k, const uint64_t* seeds_dev, double* values,
                  int32_t* lengths, void* stream);
+/* KMV value ranks (a device layout of sketches.py:375-396, not a reference
+ * interface): rank_of[x] = dense rank of unit_value(h_0(x)) among all x in
+ * [0, n) (hashing.py:146-153), rank_values[r] = the value of rank r.  Equal
+ * values share a rank, so ranks order and compare exactly like the values. */
+PG_API int pg_kmv_rank_table(int64_t n, const uint64_t* seeds_dev, int32_t* rank_of,
+                      double* rank_values, void* stream);
+/* pg_build_kmv plus ranks[n][k] (int32 ascending, INT32_MAX pad): the same
+ * selection made on ranks; values = rank_values[ranks] (bit-identical). */
+PG_API int pg_build_kmv_ranked(const int64_t* offsets, const int32_t* adj, int64_t n,
+                        int32_t k, const uint64_t* seeds_dev, const int32_t* rank_of,
+                        const double* rank_values, double* values, int32_t* ranks,
+                        int32_t* lengths, void* stream);
 
 /* ---- (2) per-edge estimators, parity path
  *      (providers.py:150-162 BloomProvider.pair_many,
@@ -164,10 +176,20 @@ PG_API int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash,
                   const int32_t* sizes, const int32_t* us, const int32_t* vs,
                   int64_t e_begin, int64_t e_end, int32_t padded, int64_t* out_cnt,
                   int64_t* out_ssum, int64_t* out_verbatim, void* stream);
-/* KMV TC: out_sum[0] = sum of per-edge estimates (fixed-order fp64) */
+/* KMV TC: out_sum[0] = sum of per-edge estimates (fp64; block sums added
+ * atomically, so the last bits depend on the order) */
 PG_API int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k,
               const int32_t* sizes, const int32_t* us, const int32_t* vs,
               int64_t e_begin, int64_t e_end, double* out_sum, void* stream);
+/* KMV TC over rank rows (pg_build_kmv_ranked) and the row-padded edge slots
+ * of pad = pg_kmv_ranked_pad(k) (256/k for k = 32, 64, 128; 0 = no
+ * rank-directory engine for k): the same per-edge estimates as pg_tc_kmv
+ * (providers.py:266-301), out_sum[0] = their sum. */
+PG_API int pg_kmv_ranked_pad(int32_t k, int32_t* pad_host);
+PG_API int pg_tc_kmv_ranked(const int32_t* ranks, const double* rank_values,
+                     const int32_t* lengths, int32_t k, const int32_t* sizes,
+                     const int32_t* us, const int32_t* vs, int64_t e_begin,
+                     int64_t e_end, double* out_sum, void* stream);
 /* Jaccard clustering count (config 4; estimators.py:123-131 + 148-154 and
  * mining.py:157-186).  out_counts[0] = #edges with matches >= min_matches
  * (J-hat = m/k >= tau), out_counts[1] = #edges whose vertex_similarity

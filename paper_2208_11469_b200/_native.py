@@ -51,6 +51,9 @@ SIGNATURES = {
     "pg_build_onehash": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr,
                          c_ptr],
     "pg_build_kmv": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr, c_ptr],
+    "pg_kmv_rank_table": [c_i64, c_ptr, c_ptr, c_ptr, c_ptr],
+    "pg_build_kmv_ranked": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr, c_ptr,
+                            c_ptr, c_ptr, c_ptr, c_ptr],
     "pg_pairs_bloom": [c_ptr, c_i32, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr,
                        c_i64, c_ptr, c_ptr, c_ptr],
     "pg_pairs_minhash": [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
@@ -63,6 +66,9 @@ SIGNATURES = {
                       c_i32, c_ptr, c_ptr, c_ptr, c_ptr],
     "pg_tc_kmv": [c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64, c_i64,
                   c_ptr, c_ptr],
+    "pg_kmv_ranked_pad": [c_i32, ctypes.POINTER(c_i32)],
+    "pg_tc_kmv_ranked": [c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
+                         c_i64, c_ptr, c_ptr],
     "pg_jaccard_count_khash": [c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
                                c_i64, c_i32, c_i32, c_dbl, c_ptr, c_ptr],
     "pg_4clique_bloom": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i32,
@@ -166,6 +172,13 @@ def group_pad(row_bytes: int) -> int:
     """Lane-group size of the fused row kernels = pad of their slot layout."""
     pad = ctypes.c_int32()
     check(load_library().pg_group_pad(int(row_bytes), ctypes.byref(pad)), "pg_group_pad")
+    return pad.value
+
+
+def kmv_ranked_pad(k: int) -> int:
+    """Slot pad of the rank-directory KMV engine for k (0: no such engine)."""
+    pad = ctypes.c_int32()
+    check(load_library().pg_kmv_ranked_pad(int(k), ctypes.byref(pad)), "pg_kmv_ranked_pad")
     return pad.value
 
 

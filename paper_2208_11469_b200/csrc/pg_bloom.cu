@@ -48,13 +48,13 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_bloom_wide_kernel(const unsig
                                                                     const int32_t* us, const int32_t* vs,
                                                                     int64_t e_begin, int64_t e_end,
                                                                     EpiBloomHist epi, int64_t* out_hist,
-                                                                    int64_t* out_sum_pos) {
+                                                                    int64_t* out_sum_pos, unsigned long long* ctr) {
   extern __shared__ int hist_s[];
   for (int i = threadIdx.x; i <= bits; i += blockDim.x) hist_s[i] = 0;
   __syncthreads();
   epi.hist_s = hist_s;
   epi.sum_pos = 0;
-  wide_edge_loop<W8, Op, EpiBloomHist, kVCache, kLayout>(rows, us, vs, e_begin, e_end, epi);
+  wide_edge_loop<W8, Op, EpiBloomHist, kVCache, kLayout>(rows, us, vs, e_begin, e_end, epi, ctr);
   __syncthreads();
   for (int i = threadIdx.x; i <= bits; i += blockDim.x)
     if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_hist + i), (unsigned long long)hist_s[i]);
@@ -160,6 +160,14 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
     const int minb = tc_minb(w4, padded);
     const unsigned char* rb = reinterpret_cast<const unsigned char*>(rows);
     cudaError_t le = cudaSuccess;
+    static const bool dyn = [] {
+      const char* v = getenv("PG_TC_DYNAMIC");
+      return !(v && v[0] == '0');
+    }();
+    // dynamic chunks pay off on large edge sets (c4/c5: 3-5%); below ~32 M
+    // slots the per-launch counter costs more than the balance gains
+    ChunkCounter ctr;
+    if (dyn && e_end - e_begin >= kDynamicMinSlots && (le = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(le));
 #define PG_W(W8, MB, VC, PD)                                                                          \
   {                                                                                                  \
     auto k = op == PG_BF_OR ? tc_bloom_wide_kernel<W8, OpOr, MB, VC, PD>                             \
@@ -167,7 +175,7 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
     le = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
     if (le != cudaSuccess) return fail(PG_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(le));  \
     const int grid = grid_cap(grid_for_kernel(k, smem), e_end - e_begin, kBlock);                    \
-    k<<<grid, kBlock, smem, s>>>(rb, bits, us, vs, e_begin, e_end, epi, out_hist, out_sum_pos);      \
+    k<<<grid, kBlock, smem, s>>>(rb, bits, us, vs, e_begin, e_end, epi, out_hist, out_sum_pos, ctr.p); \
   }
 #define PG_WM(W8)                                                                  \
   if (padded == 2) {                                                             \

@@ -16,6 +16,9 @@
 // serialise on one warp.  The adjacency row is read once, coalesced.
 #include <algorithm>
 
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
+
 #include "pg_common.cuh"
 
 namespace pg {
@@ -418,34 +421,56 @@ struct WarpBottomK {
   }
 };
 
-template <bool kKmv>
-__device__ __forceinline__ uint64_t bottomk_key(uint64_t seed0, int32_t x) {
+// Bottom-k modes: 0 1-Hash (key = hash word), 1 KMV (key = the unit value's
+// IEEE bits), 2 KMV on global value ranks (key = rank_of[x], the dense rank
+// of x's unit value among all vertices: same order and ties as the value
+// bits, so the same selection; see pg_kmv_rank_table).
+struct BottomKRank {
+  const int32_t* rank_of = nullptr;       // mode 2
+  const double* rank_values = nullptr;    // mode 2: value of each rank
+  int32_t* ranks = nullptr;               // mode 2 output rows (INT32_MAX pad)
+};
+
+template <int kMode>
+__device__ __forceinline__ uint64_t bottomk_key(uint64_t seed0, int32_t x, const BottomKRank& rk) {
+  if (kMode == 2) return (uint64_t)(uint32_t)__ldg(rk.rank_of + x);
   const uint64_t w = hash_word(seed0, x);
-  return kKmv ? dbits(unit_value(w)) : w;
+  return kMode == 1 ? dbits(unit_value(w)) : w;
 }
 
-template <int P, bool kKmv>
-__device__ __forceinline__ void bottomk_scan(WarpBottomK<P, kKmv>& L, const int32_t* __restrict__ row,
-                                             int64_t beg, int64_t end, int64_t step, uint64_t seed0) {
+template <int P, int kMode>
+__device__ __forceinline__ void bottomk_scan(WarpBottomK<P, kMode != 0>& L, const int32_t* __restrict__ row,
+                                             int64_t beg, int64_t end, int64_t step, uint64_t seed0,
+                                             const BottomKRank& rk) {
   const int lane = lane_id();
   for (int64_t base = beg; base < end; base += step) {
     const int64_t j = base + lane;
     const bool valid = j < end;
-    const uint64_t c = valid ? bottomk_key<kKmv>(seed0, row[j]) : ~0ull;
+    const uint64_t c = valid ? bottomk_key<kMode>(seed0, row[j], rk) : ~0ull;
     L.offer(c, valid);
   }
 }
 
 // write the final list of vertex v.  1-Hash: IDs ascending (rank sort in
 // the warp's smem scratch), -1 pad; KMV: values ascending, +inf pad.
-template <int P, bool kKmv>
-__device__ __forceinline__ void bottomk_emit(const WarpBottomK<P, kKmv>& L, int64_t v, int k,
+template <int P, int kMode>
+__device__ __forceinline__ void bottomk_emit(const WarpBottomK<P, kMode != 0>& L, int64_t v, int k,
                                              uint64_t seed0, int32_t* scratch,
                                              int32_t* __restrict__ entries, double* __restrict__ values,
-                                             int32_t* __restrict__ lengths) {
+                                             int32_t* __restrict__ lengths, const BottomKRank& rk) {
   const int lane = lane_id();
   const int cnt = L.cnt;
-  if (kKmv) {
+  if (kMode == 2) {
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const int idx = lane + 32 * s;
+      if (idx < k) {
+        const bool in = idx < cnt;
+        values[v * k + idx] = in ? __ldg(rk.rank_values + (uint32_t)L.key[s]) : bitsd(kInfBits);
+        rk.ranks[v * k + idx] = in ? (int32_t)L.key[s] : INT32_MAX;
+      }
+    }
+  } else if (kMode == 1) {
 #pragma unroll
     for (int s = 0; s < P; ++s) {
       const int idx = lane + 32 * s;
@@ -476,12 +501,13 @@ __device__ __forceinline__ void bottomk_emit(const WarpBottomK<P, kKmv>& L, int6
   if (lane == 0) lengths[v] = cnt;
 }
 
-template <int P, bool kKmv>
+template <int P, int kMode>
 __global__ void __launch_bounds__(kThreads) build_bottomk_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n, int k,
     const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries,
     double* __restrict__ values, int32_t* __restrict__ lengths, int32_t* __restrict__ hubs,
-    int32_t* __restrict__ hub_count, unsigned long long* __restrict__ vtx_work) {
+    int32_t* __restrict__ hub_count, unsigned long long* __restrict__ vtx_work, BottomKRank rk) {
+  constexpr bool kKmv = kMode != 0;
   __shared__ int32_t scratch[kWarps][32 * P];
   const int lane = lane_id();
   const uint64_t seed0 = seeds_dev[0];
@@ -513,18 +539,19 @@ __global__ void __launch_bounds__(kThreads) build_bottomk_kernel(
       }
       WarpBottomK<P, kKmv> L;
       L.init(k);
-      bottomk_scan<P, kKmv>(L, adj + o, 0, d, 32, seed0);
-      bottomk_emit<P, kKmv>(L, v, k, seed0, scratch[warp_id()], entries, values, lengths);
+      bottomk_scan<P, kMode>(L, adj + o, 0, d, 32, seed0, rk);
+      bottomk_emit<P, kMode>(L, v, k, seed0, scratch[warp_id()], entries, values, lengths, rk);
     }
   }
 }
 
-template <int P, bool kKmv>
+template <int P, int kMode>
 __global__ void __launch_bounds__(kThreads) build_bottomk_hubs_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int k,
     const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries, double* __restrict__ values,
     int32_t* __restrict__ lengths, const int32_t* __restrict__ hubs, const int32_t* __restrict__ hub_count,
-    int32_t* __restrict__ hub_work) {
+    int32_t* __restrict__ hub_work, BottomKRank rk) {
+  constexpr bool kKmv = kMode != 0;
   __shared__ int32_t scratch[32 * P];
   __shared__ uint64_t merge_keys[kWarps][32 * P];
   __shared__ int merge_cnt[kWarps];
@@ -543,7 +570,7 @@ __global__ void __launch_bounds__(kThreads) build_bottomk_hubs_kernel(
     const int64_t d = offsets[v + 1] - o;
     WarpBottomK<P, kKmv> L;
     L.init(k);
-    bottomk_scan<P, kKmv>(L, adj + o, 32 * warp_id(), d, kThreads, seed0);
+    bottomk_scan<P, kMode>(L, adj + o, 32 * warp_id(), d, kThreads, seed0, rk);
 #pragma unroll
     for (int s = 0; s < P; ++s) merge_keys[warp_id()][lane + 32 * s] = L.key[s];
     if (lane == 0) merge_cnt[warp_id()] = L.cnt;
@@ -559,7 +586,7 @@ __global__ void __launch_bounds__(kThreads) build_bottomk_hubs_kernel(
           M.offer(valid ? merge_keys[w][idx] : ~0ull, valid);
         }
       }
-      bottomk_emit<P, kKmv>(M, v, k, seed0, scratch, entries, values, lengths);
+      bottomk_emit<P, kMode>(M, v, k, seed0, scratch, entries, values, lengths, rk);
     }
     __syncthreads();
   }
@@ -611,28 +638,52 @@ int hub_grid() { return sm_count() * 4; }
 
 using namespace pg;
 
-template <bool kKmv>
+template <int kMode>
 static int launch_bottomk(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t k,
                           const uint64_t* seeds_dev, int32_t* entries, double* values, int32_t* lengths,
-                          void* stream) {
+                          void* stream, BottomKRank rk = BottomKRank()) {
   cudaStream_t s = as_stream(stream);
   HubList hubs;
   if (int rc = hubs.init(offsets, n, s)) return rc;
-#define PG_BK(P)                                                                                         \
-  {                                                                                                      \
-    const int grid = grid_for(build_bottomk_kernel<P, kKmv>, 0, n);                                     \
-    build_bottomk_kernel<P, kKmv><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, \
-                                                            lengths, hubs.ids, hubs.count, hubs.vtx_work); \
-    build_bottomk_hubs_kernel<P, kKmv><<<hub_grid(), kThreads, 0, s>>>(offsets, adj, k, seeds_dev, entries, \
-                                                                        values, lengths, hubs.ids,        \
-                                                                        hubs.count, hubs.hub_work);      \
+#define PG_BK(P)                                                                                          \
+  {                                                                                                       \
+    const int grid = grid_for(build_bottomk_kernel<P, kMode>, 0, n);                                     \
+    build_bottomk_kernel<P, kMode><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, \
+                                                             lengths, hubs.ids, hubs.count, hubs.vtx_work, rk); \
+    build_bottomk_hubs_kernel<P, kMode><<<hub_grid(), kThreads, 0, s>>>(offsets, adj, k, seeds_dev, entries, \
+                                                                         values, lengths, hubs.ids,        \
+                                                                         hubs.count, hubs.hub_work, rk);   \
   }
   if (k <= 32) PG_BK(1)
   else if (k <= 64) PG_BK(2)
   else if (k <= 128) PG_BK(4)
   else PG_BK(8)
 #undef PG_BK
-  return check_launch(kKmv ? "build_kmv" : "build_onehash");
+  return check_launch(kMode == 0 ? "build_onehash" : "build_kmv");
+}
+
+// ---------------------------------------------------- KMV value ranks ----
+// unit-value bits of every vertex ID (the KMV key of x as a neighbour)
+__global__ void kmv_universe_kernel(int64_t n, const uint64_t* __restrict__ seeds_dev, uint64_t* __restrict__ keys,
+                                    int32_t* __restrict__ ids) {
+  const uint64_t seed0 = seeds_dev[0];
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+    keys[x] = dbits(unit_value(hash_word(seed0, (int32_t)x)));
+    ids[x] = (int32_t)x;
+  }
+}
+__global__ void kmv_rank_flags_kernel(int64_t n, const uint64_t* __restrict__ keys, int32_t* __restrict__ flags) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    flags[i] = (i > 0 && keys[i] != keys[i - 1]) ? 1 : 0;
+}
+__global__ void kmv_rank_scatter_kernel(int64_t n, const uint64_t* __restrict__ keys,
+                                        const int32_t* __restrict__ ids, const int32_t* __restrict__ dense,
+                                        int32_t* __restrict__ rank_of, double* __restrict__ rank_values) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t r = dense[i];
+    rank_of[ids[i]] = r;
+    if (i == 0 || keys[i] != keys[i - 1]) rank_values[r] = bitsd(keys[i]);
+  }
 }
 
 extern "C" {
@@ -706,7 +757,7 @@ int pg_build_onehash(const int64_t* offsets, const int32_t* adj, int64_t n, int3
   if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(offsets && seeds_dev && entries && lengths, "null pointer");
   if (n == 0) return PG_OK;
-  return launch_bottomk<false>(offsets, adj, n, k, seeds_dev, entries, nullptr, lengths, stream);
+  return launch_bottomk<0>(offsets, adj, n, k, seeds_dev, entries, nullptr, lengths, stream);
 }
 
 int pg_build_kmv(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t k,
@@ -716,7 +767,60 @@ int pg_build_kmv(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t 
   if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(offsets && seeds_dev && values && lengths, "null pointer");
   if (n == 0) return PG_OK;
-  return launch_bottomk<true>(offsets, adj, n, k, seeds_dev, nullptr, values, lengths, stream);
+  return launch_bottomk<1>(offsets, adj, n, k, seeds_dev, nullptr, values, lengths, stream);
+}
+
+int pg_kmv_rank_table(int64_t n, const uint64_t* seeds_dev, int32_t* rank_of, double* rank_values,
+                      void* stream) {
+  PG_REQUIRE(n >= 0 && n <= INT32_MAX, "n must be in [0, 2^31)");
+  if (n == 0) return PG_OK;
+  PG_REQUIRE(seeds_dev && rank_of && rank_values, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  retain_default_pool();
+  size_t t_sort = 0, t_scan = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t_sort, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, n, 0, 64);
+  cub::DeviceScan::InclusiveSum(nullptr, t_scan, (const int32_t*)nullptr, (int32_t*)nullptr, n);
+  const size_t tb = std::max(t_sort, t_scan);
+  const size_t bytes = 2 * 8 * (size_t)n + 3 * 4 * (size_t)n + tb + 64;
+  char* buf = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&buf), bytes, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "rank table scratch: %s", cudaGetErrorString(e));
+  uint64_t* k0 = reinterpret_cast<uint64_t*>(buf);
+  uint64_t* k1 = k0 + n;
+  int32_t* i0 = reinterpret_cast<int32_t*>(k1 + n);
+  int32_t* i1 = i0 + n;
+  int32_t* fl = i1 + n;
+  void* tmp = fl + n + 8;
+  const int grid = sm_count() * 8;
+  kmv_universe_kernel<<<grid, 256, 0, s>>>(n, seeds_dev, k0, i0);
+  // unit values lie in (0, 1]: their IEEE bits are below 2^62
+  size_t t = tb;
+  e = cub::DeviceRadixSort::SortPairs(tmp, t, k0, k1, i0, i1, n, 0, 62, s);
+  if (e == cudaSuccess) {
+    kmv_rank_flags_kernel<<<grid, 256, 0, s>>>(n, k1, fl);
+    t = tb;
+    e = cub::DeviceScan::InclusiveSum(tmp, t, fl, i0, n, s);
+  }
+  if (e == cudaSuccess) kmv_rank_scatter_kernel<<<grid, 256, 0, s>>>(n, k1, i1, i0, rank_of, rank_values);
+  cudaFreeAsync(buf, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "rank table: %s", cudaGetErrorString(e));
+  return check_launch("kmv_rank_table");
+}
+
+int pg_build_kmv_ranked(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t k,
+                        const uint64_t* seeds_dev, const int32_t* rank_of, const double* rank_values,
+                        double* values, int32_t* ranks, int32_t* lengths, void* stream) {
+  PG_REQUIRE(n >= 0, "n must be >= 0");
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(offsets && seeds_dev && rank_of && rank_values && values && ranks && lengths, "null pointer");
+  if (n == 0) return PG_OK;
+  BottomKRank rk;
+  rk.rank_of = rank_of;
+  rk.rank_values = rank_values;
+  rk.ranks = ranks;
+  return launch_bottomk<2>(offsets, adj, n, k, seeds_dev, nullptr, values, lengths, stream, rk);
 }
 
 }  // extern "C"

@@ -119,6 +119,9 @@ __device__ __forceinline__ bool next_chunk(unsigned long long* ctr, int64_t e_be
   return true;
 }
 
+// edge sets from which the fixed-row engines take dynamic chunks
+constexpr int64_t kDynamicMinSlots = int64_t(1) << 25;
+
 // host: one zeroed 64-bit chunk counter per launch (stream-ordered scratch)
 struct ChunkCounter {
   unsigned long long* p = nullptr;
@@ -228,7 +231,8 @@ __device__ __forceinline__ void ldg256_keep(const void* p, uint32_t (&r)[8]) {
 template <int W8, class Op, class Epi, bool kVCache = false, int kLayout = 0>
 __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__ rows,
                                                const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
-                                               int64_t e_begin, int64_t e_end, Epi& epi) {
+                                               int64_t e_begin, int64_t e_end, Epi& epi,
+                                               unsigned long long* ctr = nullptr) {
   constexpr bool kPadded = kLayout > 0;
   constexpr int G = W8 < 8 ? W8 : 8;  // lanes per edge
   constexpr int V = W8 / G;           // 32-byte chunks per lane per row
@@ -236,20 +240,30 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   const int gbase = lane & ~(G - 1);
-  int64_t wb, we;
-  warp_slice(e_begin, e_end, wb, we);
-  if (wb >= we) return;
-  int32_t ul = 0, vl = 0;
-  if (wb + lane < we) {
-    ul = kLayout == 2 ? us[(wb + lane) / G] : us[wb + lane];
-    vl = vs[wb + lane];
-  }
   int32_t ucur = -1;
   uint32_t ur[V][8];
 #pragma unroll
   for (int i = 0; i < V; ++i)
 #pragma unroll
     for (int w = 0; w < 8; ++w) ur[i][w] = 0;
+  // ranges: dynamic 512-slot chunks when the launcher passes a counter,
+  // else one static per-warp slice (the cached u row survives chunk ends)
+  int64_t wb, we;
+  bool first = true;
+  for (;;) {
+  if (ctr) {
+    if (!next_chunk(ctr, e_begin, e_end, 512, wb, we)) return;
+  } else {
+    if (!first) return;
+    warp_slice(e_begin, e_end, wb, we);
+    if (wb >= we) return;
+  }
+  first = false;
+  int32_t ul = 0, vl = 0;
+  if (wb + lane < we) {
+    ul = kLayout == 2 ? us[(wb + lane) / G] : us[wb + lane];
+    vl = vs[wb + lane];
+  }
   // 32-bit remaining-slot count instead of 64-bit bound checks (registers)
   const int nslots = (int)(we - wb);
 #pragma unroll 1
@@ -317,6 +331,7 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
     if (valid) epi.edge(e, ul, vl, cnt);
     ul = un;
     vl = vn;
+  }
   }
 }
 

@@ -223,6 +223,237 @@ static bool kmv_sorted(cudaStream_t s, bool fused, const uint64_t* vals, int k, 
 #undef PG_KS
   return false;
 }
+
+// ------------------------------------------ KMV rank-directory engine ----
+// Rows hold global value ranks (int32 ascending, INT32_MAX pad; built by
+// pg_build_kmv_ranked from pg_kmv_rank_table): the same order and ties as
+// the values, in half the bytes, with 32-bit compares.  The edge slots are
+// row-padded to E = 32/G (pg_csr_upper_edges_padded), so every warp
+// iteration holds E edges of one u.  When u changes, the warp builds a
+// directory of u's row A in shared memory: NB = 2K buckets over
+// [A[0], A[lu-1]] (monotone map: one IMAD.HI), each an int4 record
+// {the bucket's three smallest elements (INT32_MAX pad), first index |
+// count << 8}.  A probe of x is one LDS.128: lt = |A < x|, hit = x in A (a
+// bucket with more than three elements finishes from the sorted copy of A).
+// For the v row B (G lanes, 8 ranks each) the reference's merged-row
+// quantities (providers.py:266-301) follow without merging:
+//   common = sum(hit);  dist_j = |A <= b_j| + (j+1) - C_j, the number of
+//   distinct union values <= b_j (C_j = inclusive prefix of hit);  the
+//   T-th distinct union value (T = k_eff) is min(A[R + T - D - 1], b_{j*+1})
+//   with j* the last j with dist_j < T, R = |A <= b_j*|, D = dist_j*
+//   (R = D = 0 when there is none; b_lv = +inf).
+template <int K>
+struct RankDir {
+  static constexpr int NB = 2 * K;
+  int4 rec[NB];
+  int32_t a[K + 4];
+  int32_t dir[NB + 4];
+};
+
+__device__ __forceinline__ uint32_t rd_bucket(int32_t x, int32_t lo, int32_t spanm1, uint32_t mul) {
+  return __umulhi((uint32_t)min(max(x - lo, 0), spanm1), mul);
+}
+
+template <int K>
+__device__ __forceinline__ void rd_build(RankDir<K>& W, const int32_t* __restrict__ arow, int lu, int32_t& lo,
+                                         int32_t& spanm1, uint32_t& mul) {
+  constexpr int NB = RankDir<K>::NB;
+  const int lane = threadIdx.x & 31;
+#pragma unroll
+  for (int s = 0; s < K / 32; ++s) W.a[lane + 32 * s] = __ldg(arow + lane + 32 * s);
+  __syncwarp();
+  lo = lu > 0 ? W.a[0] : 0;
+  const int32_t hi = lu > 0 ? W.a[lu - 1] : 0;
+  spanm1 = hi - lo;
+  const uint32_t span = (uint32_t)spanm1 + 1u;
+  mul = span > (uint32_t)NB ? (uint32_t)(((uint64_t)NB << 32) / span) : 0xFFFFFFFFu;
+  // dir[b] = |{i : bucket(a_i) < b}| for b in [0, NB]: element i writes i
+  // over the buckets (bucket(a_{i-1}), bucket(a_i)], the last one lu over
+  // (bucket(a_{lu-1}), NB]
+  if (lu == 0) {
+    for (int b = lane; b <= NB; b += 32) W.dir[b] = 0;
+  }
+#pragma unroll
+  for (int s = 0; s < K / 32; ++s) {
+    const int i = lane + 32 * s;
+    if (i < lu) {
+      const int bk = (int)rd_bucket(W.a[i], lo, spanm1, mul);
+      const int bp = i == 0 ? -1 : (int)rd_bucket(W.a[i - 1], lo, spanm1, mul);
+      for (int b = bp + 1; b <= bk; ++b) W.dir[b] = i;
+      if (i == lu - 1)
+        for (int b = bk + 1; b <= NB; ++b) W.dir[b] = lu;
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int t = 0; t < NB / 32; ++t) {
+    const int b = lane + 32 * t;
+    const int d = W.dir[b], c = W.dir[b + 1] - d;
+    int4 r;
+    r.x = c > 0 ? W.a[d] : INT32_MAX;
+    r.y = c > 1 ? W.a[d + 1] : INT32_MAX;
+    r.z = c > 2 ? W.a[d + 2] : INT32_MAX;
+    r.w = d | (c << 8);
+    W.rec[b] = r;
+  }
+  __syncwarp();
+}
+
+template <int K>
+__device__ __forceinline__ int rd_probe(const RankDir<K>& W, int32_t x, int32_t lo, int32_t spanm1, uint32_t mul,
+                                        bool& hit) {
+  const int4 r = W.rec[rd_bucket(x, lo, spanm1, mul)];
+  int lt = (r.x < x) + (r.y < x) + (r.z < x);
+  hit = (r.x == x) | (r.y == x) | (r.z == x);
+  const int d = r.w & 0xff, c = r.w >> 8;
+  if (c > 3) {
+    for (int i = 3; i < c; ++i) {
+      const int32_t y = W.a[d + i];
+      lt += y < x;
+      hit |= y == x;
+    }
+  }
+  return d + lt;
+}
+
+template <int K>
+__global__ void __launch_bounds__(kBlock) kmv_ranked_kernel(const int32_t* __restrict__ R,
+                                                            const double* __restrict__ rank_values,
+                                                            const int32_t* __restrict__ lengths,
+                                                            const int32_t* __restrict__ sizes,
+                                                            const int32_t* __restrict__ us,
+                                                            const int32_t* __restrict__ vs, int64_t e_begin,
+                                                            int64_t e_end, double* out_sum,
+                                                            unsigned long long* ctr) {
+  constexpr int P = 8, G = K / P, E = 32 / G;
+  constexpr int64_t kChunk = 64 * E;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double red[kBlock / 32];
+  RankDir<K>& W = reinterpret_cast<RankDir<K>*>(smem_raw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
+  double acc = 0.0;
+  int32_t cur_u = -1, lo = 0, spanm1 = 0, lu = 0, su = 0;
+  uint32_t mul = 0;
+  int64_t wb, we;
+  while (next_chunk(ctr, e_begin, e_end, kChunk, wb, we)) {
+    int32_t vl = -1, lvl = 0, svl = 0;
+    if (wb + grp < we) {
+      vl = vs[wb + grp];
+      if (vl >= 0) {
+        lvl = lengths[vl];
+        svl = sizes[vl];
+      }
+    }
+    uint32_t x[P];
+    ldg_rowpart<P>(R + (int64_t)(vl < 0 ? 0 : vl) * K + gl * P, x);
+#pragma unroll 1
+    for (int64_t e0 = wb; e0 < we; e0 += E) {
+      const int64_t e = e0 + grp;
+      const bool valid = e < we && vl >= 0;
+      const int32_t u = us[e0];  // one u per padded group of E slots
+      if (u != cur_u) {
+        cur_u = u;
+        lu = lengths[u];
+        su = sizes[u];
+        rd_build<K>(W, R + (int64_t)u * K, lu, lo, spanm1, mul);
+      }
+      int32_t vn = -1, lvn = 0, svn = 0;
+      if (e + E < we) {
+        vn = vs[e + E];
+        if (vn >= 0) {
+          lvn = lengths[vn];
+          svn = sizes[vn];
+        }
+      }
+      uint32_t xn[P];
+      ldg_rowpart<P>(R + (int64_t)(vn < 0 ? 0 : vn) * K + gl * P, xn);
+      // per element: le = |A <= b_j|, hit = b_j in A
+      int le[P];
+      unsigned hits = 0;
+#pragma unroll
+      for (int t = 0; t < P; ++t) {
+        const int32_t q = (int32_t)x[t];
+        le[t] = 0;
+        if (valid && q != INT32_MAX) {
+          bool h;
+          le[t] = rd_probe<K>(W, q, lo, spanm1, mul, h) + h;
+          hits |= (unsigned)h << t;
+        }
+      }
+      // C_j: group exclusive scan of the per-lane hit counts
+      const int mc = __popc(hits);
+      int incl = mc;
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (gl >= o) incl += y;
+      }
+      const int common = __shfl_sync(0xffffffffu, incl, (grp + 1) * G - 1);
+      const int T = min(lu, lvl);
+      int C = incl - mc, less = 0, dist[P];
+#pragma unroll
+      for (int t = 0; t < P; ++t) {
+        const int j = gl * P + t;
+        C += (hits >> t) & 1;
+        dist[t] = le[t] + (j + 1) - C;
+        less += (j < lvl) && dist[t] < T;
+      }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) less += __shfl_xor_sync(0xffffffffu, less, o);
+      const int js = less - 1;  // last j with dist_j < T (dist is nondecreasing)
+      int pk = 0;
+#pragma unroll
+      for (int t = 0; t < P; ++t)
+        if (gl * P + t == js) pk = le[t] | (dist[t] << 16);
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) pk += __shfl_xor_sync(0xffffffffu, pk, o);
+      if (valid && gl == 0) {
+        // KMV estimate (providers.py:266-301; kmv_estimate restates it)
+        KmvEdge r;
+        r.common = common;
+        r.uni = lu + lvl - common;
+        r.k_eff = T;
+        r.kth = 0.0;
+        if (!(su <= K && svl <= K) && T >= 2) {
+          const int Rr = pk & 0xffff, D = pk >> 16;
+          const int32_t ka = W.a[Rr + T - D - 1];
+          const int32_t kb = js + 1 < lvl ? __ldg(R + (int64_t)vl * K + js + 1) : INT32_MAX;
+          r.kth = __ldg(rank_values + min(ka, kb));
+        }
+        acc = __dadd_rn(acc, kmv_estimate(r, K, su, svl));
+      }
+#pragma unroll
+      for (int t = 0; t < P; ++t) x[t] = xn[t];
+      vl = vn;
+      lvl = lvn;
+      svl = svn;
+    }
+  }
+  double a = acc;
+  for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+  if (lane == 0) red[threadIdx.x >> 5] = a;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < kBlock / 32; ++i) t = __dadd_rn(t, red[i]);
+    if (t != 0.0) atomicAdd(out_sum, t);
+  }
+}
+
+template <int K>
+static int launch_kmv_ranked(cudaStream_t s, const int32_t* ranks, const double* rank_values,
+                             const int32_t* lengths, const int32_t* sizes, const int32_t* us, const int32_t* vs,
+                             int64_t b, int64_t e, double* out_sum) {
+  auto kern = kmv_ranked_kernel<K>;
+  const size_t sm = (size_t)(kBlock / 32) * sizeof(RankDir<K>);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / 8));
+  ChunkCounter ctr;
+  const cudaError_t ce = ctr.init(s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce));
+  kern<<<grid, kBlock, sm, s>>>(ranks, rank_values, lengths, sizes, us, vs, b, e, out_sum, ctr.p);
+  return check_launch("tc_kmv_ranked");
+}
 }  // namespace pg
 
 using namespace pg;
@@ -281,6 +512,31 @@ int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k, const int
   else PG_KM(8)
 #undef PG_KM
   return check_launch("tc_kmv");
+}
+
+int pg_kmv_ranked_pad(int32_t k, int32_t* pad_host) {
+  PG_REQUIRE(pad_host, "null output");
+  *pad_host = (k == 32 || k == 64 || k == 128) ? 256 / k : 0;
+  return PG_OK;
+}
+
+int pg_tc_kmv_ranked(const int32_t* ranks, const double* rank_values, const int32_t* lengths, int32_t k,
+                     const int32_t* sizes, const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end,
+                     double* out_sum, void* stream) {
+  if (k != 32 && k != 64 && k != 128)
+    return fail(PG_ERR_UNSUPPORTED, "the rank-directory KMV engine supports k = 32, 64, 128 (got %d)", k);
+  const int pad = 256 / k;
+  PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
+  PG_REQUIRE(e_begin % pad == 0, "e_begin must be a multiple of the layout pad %d", pad);
+  PG_REQUIRE(out_sum, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  cudaError_t ce = cudaMemsetAsync(out_sum, 0, sizeof(double), s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
+  PG_REQUIRE(ranks && rank_values && lengths && sizes && us && vs, "null pointer");
+  if (k == 32) return launch_kmv_ranked<32>(s, ranks, rank_values, lengths, sizes, us, vs, e_begin, e_end, out_sum);
+  if (k == 64) return launch_kmv_ranked<64>(s, ranks, rank_values, lengths, sizes, us, vs, e_begin, e_end, out_sum);
+  return launch_kmv_ranked<128>(s, ranks, rank_values, lengths, sizes, us, vs, e_begin, e_end, out_sum);
 }
 
 }  // extern "C"

@@ -19,7 +19,8 @@ template <int V, int G, int kEngine, int MINB = 1>
 __global__ void __launch_bounds__(kBlock, MINB) tc_khash_kernel(const uint4* ent, int k, const int32_t* sizes,
                                                                const int32_t* us, const int32_t* vs,
                                                                int64_t e_begin, int64_t e_end,
-                                                               int64_t* out_cnt, int64_t* out_ssum) {
+                                                               int64_t* out_cnt, int64_t* out_ssum,
+                                                               unsigned long long* ctr = nullptr) {
   __shared__ int cnt_s[kMaxSketchK + 1];
   __shared__ unsigned slo_s[kMaxSketchK + 1], shi_s[kMaxSketchK + 1];
   for (int i = threadIdx.x; i <= k; i += blockDim.x) { cnt_s[i] = 0; slo_s[i] = 0; shi_s[i] = 0; }
@@ -28,7 +29,7 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_khash_kernel(const uint4* ent
   if (kEngine == 0) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
   else if (kEngine == 1) group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
   else wide_edge_loop<V, OpEqPos, EpiMinhashHist, false, true>(reinterpret_cast<const unsigned char*>(ent), us,
-                                                                vs, e_begin, e_end, epi);
+                                                                vs, e_begin, e_end, epi, ctr);
   __syncthreads();
   for (int i = threadIdx.x; i <= k; i += blockDim.x) {
     if (cnt_s[i]) {
@@ -44,7 +45,8 @@ __global__ void __launch_bounds__(kBlock, MINB) jaccard_khash_kernel(const uint4
                                                                     const int32_t* us, const int32_t* vs,
                                                                     int64_t e_begin, int64_t e_end,
                                                                     int min_matches, double tau,
-                                                                    int64_t* out_counts) {
+                                                                    int64_t* out_counts,
+                                                                    unsigned long long* ctr = nullptr) {
   __shared__ int hist_s[kMaxSketchK + 1];
   for (int i = threadIdx.x; i <= k; i += blockDim.x) hist_s[i] = 0;
   __syncthreads();
@@ -52,7 +54,7 @@ __global__ void __launch_bounds__(kBlock, MINB) jaccard_khash_kernel(const uint4
   if (kEngine == 0) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
   else if (kEngine == 1) group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
   else wide_edge_loop<V, OpEqPos, EpiJaccard, false, true>(reinterpret_cast<const unsigned char*>(ent), us, vs,
-                                                            e_begin, e_end, epi);
+                                                            e_begin, e_end, epi, ctr);
   __syncthreads();
   for (int i = threadIdx.x; i <= k; i += blockDim.x)
     if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_counts + 2 + i), (unsigned long long)hist_s[i]);
@@ -373,20 +375,22 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
   {                                                                                      \
     auto kern = tc_khash_kernel<W8, 1, 2, MB>;                                           \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);        \
-    kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum); \
+    ChunkCounter ctr;                                                                    \
+    if (e_end - e_begin >= kDynamicMinSlots && (ce = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce)); \
+    kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, ctr.p); \
   }
     if (w8 == 2) PG_KW(2, 3) else if (w8 == 4) PG_KW(4, 3) else PG_KW(8, 3)  // measured: 3 blocks beat the spill-free 2 (0.66 vs 0.72 ms, s20 k=64)
 #undef PG_KW
   } else if (!fast_w4(w4)) {
     auto kern = tc_khash_kernel<1, 1, 0>;
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);
-    kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum);
+    kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, nullptr);
   } else {
 #define PG_L(V, G)                                                                       \
   {                                                                                      \
     auto kern = tc_khash_kernel<V, G, 1>;                                                \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);        \
-    kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum); \
+    kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, nullptr); \
   }
     PG_ROW_DISPATCH(w4, PG_L)
 #undef PG_L
@@ -414,20 +418,22 @@ int pg_jaccard_count_khash(const int32_t* entries, int32_t k, const int32_t* deg
   {                                                                                                    \
     auto kern = jaccard_khash_kernel<W8, 1, 2, MB>;                                                    \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);                      \
-    kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts); \
+    ChunkCounter ctr;                                                                                  \
+    if (e_end - e_begin >= kDynamicMinSlots && (ce = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce)); \
+    kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts, ctr.p); \
   }
     if (w8 == 2) PG_JW(2, 3) else if (w8 == 4) PG_JW(4, 3) else PG_JW(8, 2)  // 256-B rows: 2 blocks (no spills)
 #undef PG_JW
   } else if (!fast_w4(w4)) {
     auto kern = jaccard_khash_kernel<1, 1, 0>;
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);
-    kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts);
+    kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts, nullptr);
   } else {
 #define PG_L(V, G)                                                                                         \
   {                                                                                                        \
     auto kern = jaccard_khash_kernel<V, G, 1>;                                                             \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);                          \
-    kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts);    \
+    kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts, nullptr);    \
   }
     PG_ROW_DISPATCH(w4, PG_L)
 #undef PG_L

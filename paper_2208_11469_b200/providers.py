@@ -408,10 +408,23 @@ class KmvProvider(_SketchProvider):
         return (com[:du.numel()].cpu().numpy().astype(np.int64),
                 uni[:du.numel()].cpu().numpy().astype(np.int64))
 
+    def _ranked(self) -> bool:
+        """Rank rows built with the sketches (device builds) and a
+        rank-directory engine for this k."""
+        return "ranks" in self._dev() and N.kmv_ranked_pad(self.sketched.capacity) > 0
+
+    def tc_pad(self) -> int:
+        return N.kmv_ranked_pad(self.sketched.capacity) if self._ranked() else 1
+
     def _tc_counts(self, us, vs, e_begin: int, e_end: int, padded: bool = False):
         import torch
         d, sg = self._dev(), self.sketched
         out = torch.empty(1, dtype=torch.float64, device="cuda")
+        if padded and self._ranked():
+            N.call("pg_tc_kmv_ranked", N.ptr(d["ranks"]), N.ptr(d["rank_values"]),
+                   N.ptr(d["lengths"]), sg.capacity, N.ptr(d["sizes"]), N.ptr(us),
+                   N.ptr(vs), e_begin, e_end, N.ptr(out), N.stream_handle())
+            return out
         N.call("pg_tc_kmv", N.ptr(d["values"]), N.ptr(d["lengths"]),
                sg.capacity, N.ptr(d["sizes"]), N.ptr(us), N.ptr(vs), e_begin,
                e_end, N.ptr(out), N.stream_handle())

@@ -354,8 +354,10 @@ def _launch_builders(dev: DeviceCsr, kind: SketchKind, plan: BudgetPlan, seeds, 
         N.call("pg_build_onehash", off, N.ptr(dev.adj), n, k, N.ptr(seeds),
                row(out["entries"]), row(out["lengths"]), stream)
     else:
-        N.call("pg_build_kmv", off, N.ptr(dev.adj), n, k, N.ptr(seeds),
-               row(out["values"]), row(out["lengths"]), stream)
+        # values plus their global-rank rows (the KMV TC engine's layout)
+        N.call("pg_build_kmv_ranked", off, N.ptr(dev.adj), n, k, N.ptr(seeds),
+               N.ptr(out["rank_of"]), N.ptr(out["rank_values"]),
+               row(out["values"]), row(out["ranks"]), row(out["lengths"]), stream)
 
 
 def _alloc_outputs(kind: SketchKind, plan: BudgetPlan, n: int) -> dict:
@@ -372,7 +374,18 @@ def _alloc_outputs(kind: SketchKind, plan: BudgetPlan, n: int) -> dict:
         return {"entries": torch.empty((alloc_n, k), dtype=torch.int32, device="cuda"),
                 "lengths": torch.empty(alloc_n, dtype=torch.int32, device="cuda")}
     return {"values": torch.empty((alloc_n, k), dtype=torch.float64, device="cuda"),
+            "ranks": torch.empty((alloc_n, k), dtype=torch.int32, device="cuda"),
+            "rank_of": torch.empty(alloc_n, dtype=torch.int32, device="cuda"),
+            "rank_values": torch.empty(alloc_n, dtype=torch.float64, device="cuda"),
             "lengths": torch.empty(alloc_n, dtype=torch.int32, device="cuda")}
+
+
+def _prepare_builders(kind: SketchKind, n: int, seeds, out, stream: int) -> None:
+    """Whole-graph tables the per-chunk builders read (KMV value ranks)."""
+    from . import _native as N
+    if kind is SketchKind.KMV:
+        N.call("pg_kmv_rank_table", n, N.ptr(seeds), N.ptr(out["rank_of"]),
+               N.ptr(out["rank_values"]), stream)
 
 
 def _build_on_device(dev: DeviceCsr, kind: SketchKind, plan: BudgetPlan,
@@ -400,6 +413,7 @@ def _build_on_device(dev: DeviceCsr, kind: SketchKind, plan: BudgetPlan,
         with torch.cuda.stream(bs):  # allocations ordered on bs
             seeds = device_seeds(bs.cuda_stream)
             out = _alloc_outputs(kind, plan, n)
+            _prepare_builders(kind, n, seeds, out, bs.cuda_stream)
             for v0, v1, ev in chunks:
                 bs.wait_event(ev)
                 _launch_builders(dev, kind, plan, seeds, out, v0, v1, bs.cuda_stream)
@@ -415,6 +429,7 @@ def _build_on_device(dev: DeviceCsr, kind: SketchKind, plan: BudgetPlan,
         ready = None
         seeds = device_seeds(N.stream_handle())
         out = _alloc_outputs(kind, plan, n)
+        _prepare_builders(kind, n, seeds, out, N.stream_handle())
         _launch_builders(dev, kind, plan, seeds, out, 0, n, N.stream_handle())
     out = {key: t[:n] for key, t in out.items()}
     out.update(seeds=seeds, sizes=dev.degrees)
