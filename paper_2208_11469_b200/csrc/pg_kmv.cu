@@ -316,8 +316,19 @@ __device__ __forceinline__ int rd_probe(const RankDir<K>& W, int32_t x, int32_t 
   return d + lt;
 }
 
+// Slot blocks: a warp walks its chunk 32 slots at a time; lane l holds slot
+// l's u, v, sizes and lengths (loaded one block ahead, so no iteration waits
+// on an index -> row chain), the groups take E slots per iteration (v by
+// shuffle), and after the block every lane finishes one slot's estimate
+// (the fp64 tail runs with all 32 lanes instead of one lane per group).
 template <int K>
-__global__ void __launch_bounds__(kBlock) kmv_ranked_kernel(const int32_t* __restrict__ R,
+struct RankWarp {
+  RankDir<K> dir;
+  int2 buf[32];  // per slot of the block: {common | (j*+1) << 8, A[R+T-D-1]}
+};
+
+template <int K>
+__global__ void __launch_bounds__(kBlock, 4) kmv_ranked_kernel(const int32_t* __restrict__ R,
                                                             const double* __restrict__ rank_values,
                                                             const int32_t* __restrict__ lengths,
                                                             const int32_t* __restrict__ sizes,
@@ -325,108 +336,142 @@ __global__ void __launch_bounds__(kBlock) kmv_ranked_kernel(const int32_t* __res
                                                             const int32_t* __restrict__ vs, int64_t e_begin,
                                                             int64_t e_end, double* out_sum,
                                                             unsigned long long* ctr) {
-  constexpr int P = 8, G = K / P, E = 32 / G;
-  constexpr int64_t kChunk = 64 * E;
+  constexpr int P = 8, G = K / P, E = 32 / G, IT = 32 / E;
+  constexpr int64_t kChunk = 512;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[kBlock / 32];
-  RankDir<K>& W = reinterpret_cast<RankDir<K>*>(smem_raw)[threadIdx.x >> 5];
+  RankWarp<K>& Wp = reinterpret_cast<RankWarp<K>*>(smem_raw)[threadIdx.x >> 5];
+  RankDir<K>& W = Wp.dir;
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
   double acc = 0.0;
   int32_t cur_u = -1, lo = 0, spanm1 = 0, lu = 0, su = 0;
   uint32_t mul = 0;
   int64_t wb, we;
   while (next_chunk(ctr, e_begin, e_end, kChunk, wb, we)) {
-    int32_t vl = -1, lvl = 0, svl = 0;
-    if (wb + grp < we) {
-      vl = vs[wb + grp];
-      if (vl >= 0) {
-        lvl = lengths[vl];
-        svl = sizes[vl];
-      }
+    // this block's slot of lane l (u, v) and the gathers of its endpoints
+    int32_t ul = 0, vl = -1;
+    if (wb + lane < we) {
+      ul = us[wb + lane];
+      vl = vs[wb + lane];
     }
+    int32_t svl = 0, lvl = 0, sul = sizes[ul], lul = lengths[ul];
+    if (vl >= 0) {
+      svl = sizes[vl];
+      lvl = lengths[vl];
+    }
+    int32_t vq = __shfl_sync(0xffffffffu, vl, grp);
     uint32_t x[P];
-    ldg_rowpart<P>(R + (int64_t)(vl < 0 ? 0 : vl) * K + gl * P, x);
+    ldg_rowpart<P>(R + (int64_t)(vq < 0 ? 0 : vq) * K + gl * P, x);
 #pragma unroll 1
-    for (int64_t e0 = wb; e0 < we; e0 += E) {
-      const int64_t e = e0 + grp;
-      const bool valid = e < we && vl >= 0;
-      const int32_t u = us[e0];  // one u per padded group of E slots
-      if (u != cur_u) {
-        cur_u = u;
-        lu = lengths[u];
-        su = sizes[u];
-        rd_build<K>(W, R + (int64_t)u * K, lu, lo, spanm1, mul);
+    for (int64_t b0 = wb; b0 < we; b0 += 32) {
+      // next block's slots (consumed 8 iterations later)
+      int32_t un = 0, vn = -1, sun = 0, lun = 0, svn = 0, lvn = 0;
+      if (b0 + 32 + lane < we) {
+        un = us[b0 + 32 + lane];
+        vn = vs[b0 + 32 + lane];
       }
-      int32_t vn = -1, lvn = 0, svn = 0;
-      if (e + E < we) {
-        vn = vs[e + E];
-        if (vn >= 0) {
-          lvn = lengths[vn];
-          svn = sizes[vn];
+#pragma unroll 1
+      for (int it = 0; it < IT; ++it) {
+        const int slot = it * E + grp;
+        const int32_t u = __shfl_sync(0xffffffffu, ul, it * E);  // one u per padded group
+        const int lv = __shfl_sync(0xffffffffu, lvl, slot);
+        const bool valid = b0 + slot < we && vq >= 0;
+        if (it == IT / 2) {  // the next block's endpoint gathers, off the critical path
+          sun = sizes[un];
+          lun = lengths[un];
+          if (vn >= 0) {
+            svn = sizes[vn];
+            lvn = lengths[vn];
+          }
         }
-      }
-      uint32_t xn[P];
-      ldg_rowpart<P>(R + (int64_t)(vn < 0 ? 0 : vn) * K + gl * P, xn);
-      // per element: le = |A <= b_j|, hit = b_j in A
-      int le[P];
-      unsigned hits = 0;
-#pragma unroll
-      for (int t = 0; t < P; ++t) {
-        const int32_t q = (int32_t)x[t];
-        le[t] = 0;
-        if (valid && q != INT32_MAX) {
-          bool h;
-          le[t] = rd_probe<K>(W, q, lo, spanm1, mul, h) + h;
-          hits |= (unsigned)h << t;
+        if (u != cur_u) {
+          cur_u = u;
+          lu = __shfl_sync(0xffffffffu, lul, it * E);
+          su = __shfl_sync(0xffffffffu, sul, it * E);
+          rd_build<K>(W, R + (int64_t)u * K, lu, lo, spanm1, mul);
         }
+        // the next iteration's v row (the next block's first at the end)
+        const int32_t vqn = __shfl_sync(0xffffffffu, it + 1 < IT ? vl : vn, it + 1 < IT ? slot + E : grp);
+        uint32_t xn[P];
+        ldg_rowpart<P>(R + (int64_t)(vqn < 0 ? 0 : vqn) * K + gl * P, xn);
+        // le_t = |A <= b_t| (<= K <= 128) packed four per register
+        uint32_t le[P / 4];
+        unsigned hits = 0;
+#pragma unroll
+        for (int t = 0; t < P; ++t) {
+          const int32_t q = (int32_t)x[t];
+          if (t % 4 == 0) le[t / 4] = 0;
+          if (valid && q != INT32_MAX) {
+            bool h;
+            const int l = rd_probe<K>(W, q, lo, spanm1, mul, h) + h;
+            le[t / 4] |= (uint32_t)l << (8 * (t % 4));
+            hits |= (unsigned)h << t;
+          }
+        }
+        const int mc = __popc(hits);
+        int incl = mc;
+#pragma unroll
+        for (int o = 1; o < G; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (gl >= o) incl += y;
+        }
+        const int common = __shfl_sync(0xffffffffu, incl, (grp + 1) * G - 1);
+        const int T = min(lu, lv);
+        // less = #t with dist_t < T (a prefix: dist is nondecreasing);
+        // cand = (|A <= b|, dist) of this lane's last such element
+        int C = incl - mc, less = 0, cand = 0;
+#pragma unroll
+        for (int t = 0; t < P; ++t) {
+          const int j = gl * P + t;
+          C += (hits >> t) & 1;
+          const int let = (le[t / 4] >> (8 * (t % 4))) & 0xff;
+          const int dist = let + (j + 1) - C;
+          if (j < lv && dist < T) {
+            ++less;
+            cand = let | (dist << 16);
+          }
+        }
+        int tot = less;
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+        const int js = tot - 1;  // last j with dist_j < T
+        const int pk = __shfl_sync(0xffffffffu, cand, grp * G + (js < 0 ? 0 : js / P));
+        if (valid && gl == 0) {
+          int ka = 0;
+          if (T >= 2) {
+            const int Rr = js < 0 ? 0 : (pk & 0xffff), D = js < 0 ? 0 : (pk >> 16);
+            ka = W.a[Rr + T - D - 1];
+          }
+          Wp.buf[slot] = make_int2(common | ((js + 1) << 8), ka);
+        }
+#pragma unroll
+        for (int t = 0; t < P; ++t) x[t] = xn[t];
+        vq = vqn;
       }
-      // C_j: group exclusive scan of the per-lane hit counts
-      const int mc = __popc(hits);
-      int incl = mc;
-#pragma unroll
-      for (int o = 1; o < G; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (gl >= o) incl += y;
-      }
-      const int common = __shfl_sync(0xffffffffu, incl, (grp + 1) * G - 1);
-      const int T = min(lu, lvl);
-      int C = incl - mc, less = 0, dist[P];
-#pragma unroll
-      for (int t = 0; t < P; ++t) {
-        const int j = gl * P + t;
-        C += (hits >> t) & 1;
-        dist[t] = le[t] + (j + 1) - C;
-        less += (j < lvl) && dist[t] < T;
-      }
-#pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1) less += __shfl_xor_sync(0xffffffffu, less, o);
-      const int js = less - 1;  // last j with dist_j < T (dist is nondecreasing)
-      int pk = 0;
-#pragma unroll
-      for (int t = 0; t < P; ++t)
-        if (gl * P + t == js) pk = le[t] | (dist[t] << 16);
-#pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1) pk += __shfl_xor_sync(0xffffffffu, pk, o);
-      if (valid && gl == 0) {
-        // KMV estimate (providers.py:266-301; kmv_estimate restates it)
+      __syncwarp();
+      // every lane finishes its slot: KMV estimate (providers.py:266-301)
+      if (b0 + lane < we && vl >= 0) {
+        const int2 bf = Wp.buf[lane];
+        const int common = bf.x & 0xff, jn = bf.x >> 8;
         KmvEdge r;
         r.common = common;
-        r.uni = lu + lvl - common;
-        r.k_eff = T;
+        r.uni = lul + lvl - common;
+        r.k_eff = min(lul, lvl);
         r.kth = 0.0;
-        if (!(su <= K && svl <= K) && T >= 2) {
-          const int Rr = pk & 0xffff, D = pk >> 16;
-          const int32_t ka = W.a[Rr + T - D - 1];
-          const int32_t kb = js + 1 < lvl ? __ldg(R + (int64_t)vl * K + js + 1) : INT32_MAX;
-          r.kth = __ldg(rank_values + min(ka, kb));
+        if (!(sul <= K && svl <= K) && r.k_eff >= 2) {
+          const int32_t kb = jn < lvl ? __ldg(R + (int64_t)vl * K + jn) : INT32_MAX;
+          r.kth = __ldg(rank_values + min(bf.y, kb));
         }
-        acc = __dadd_rn(acc, kmv_estimate(r, K, su, svl));
+        acc = __dadd_rn(acc, kmv_estimate(r, K, sul, svl));
       }
-#pragma unroll
-      for (int t = 0; t < P; ++t) x[t] = xn[t];
+      __syncwarp();
+      // rotate to the next block: its endpoint gathers
+      ul = un;
       vl = vn;
-      lvl = lvn;
+      sul = sun;
+      lul = lun;
       svl = svn;
+      lvl = lvn;
     }
   }
   double a = acc;
@@ -445,7 +490,7 @@ static int launch_kmv_ranked(cudaStream_t s, const int32_t* ranks, const double*
                              const int32_t* lengths, const int32_t* sizes, const int32_t* us, const int32_t* vs,
                              int64_t b, int64_t e, double* out_sum) {
   auto kern = kmv_ranked_kernel<K>;
-  const size_t sm = (size_t)(kBlock / 32) * sizeof(RankDir<K>);
+  const size_t sm = (size_t)(kBlock / 32) * sizeof(RankWarp<K>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / 8));
   ChunkCounter ctr;
