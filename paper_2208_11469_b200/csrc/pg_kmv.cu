@@ -225,6 +225,13 @@ static bool kmv_sorted(cudaStream_t s, bool fused, const uint64_t* vals, int k, 
 }
 
 // ------------------------------------------ KMV rank-directory engine ----
+#ifndef PG_RANKED_MINB
+#define PG_RANKED_MINB 3
+#endif
+#ifndef PG_RANKED_PER_LANE
+#define PG_RANKED_PER_LANE 8
+#endif
+constexpr int kRankedPerLane = PG_RANKED_PER_LANE;  // v-row ranks per lane
 // Rows hold global value ranks (int32 ascending, INT32_MAX pad; built by
 // pg_build_kmv_ranked from pg_kmv_rank_table): the same order and ties as
 // the values, in half the bytes, with 32-bit compares.  The edge slots are
@@ -299,21 +306,31 @@ __device__ __forceinline__ void rd_build(RankDir<K>& W, const int32_t* __restric
   __syncwarp();
 }
 
+// le = |A <= x| and hit = (x in A) from the bucket record alone (exact when
+// the bucket holds at most three elements; `ovf` flags the others)
 template <int K>
 __device__ __forceinline__ int rd_probe(const RankDir<K>& W, int32_t x, int32_t lo, int32_t spanm1, uint32_t mul,
-                                        bool& hit) {
-  const int4 r = W.rec[rd_bucket(x, lo, spanm1, mul)];
-  int lt = (r.x < x) + (r.y < x) + (r.z < x);
+                                        bool ok, bool& hit, bool& ovf) {
+  int4 r = make_int4(INT32_MAX, INT32_MAX, INT32_MAX, 0);
+  if (ok) r = W.rec[rd_bucket(x, lo, spanm1, mul)];
   hit = (r.x == x) | (r.y == x) | (r.z == x);
-  const int d = r.w & 0xff, c = r.w >> 8;
-  if (c > 3) {
-    for (int i = 3; i < c; ++i) {
-      const int32_t y = W.a[d + i];
-      lt += y < x;
-      hit |= y == x;
-    }
+  ovf = r.w >= (4 << 8);
+  return (r.w & 0xff) + (r.x <= x) + (r.y <= x) + (r.z <= x);
+}
+// the same for an overflowing bucket, from the sorted copy of A
+template <int K>
+__device__ __noinline__ int rd_probe_slow(const RankDir<K>& W, int32_t x, int32_t lo, int32_t spanm1, uint32_t mul,
+                                          bool& hit) {
+  const int w = W.rec[rd_bucket(x, lo, spanm1, mul)].w;
+  const int d = w & 0xff, c = w >> 8;
+  int le = d;
+  hit = false;
+  for (int i = 0; i < c; ++i) {
+    const int32_t y = W.a[d + i];
+    le += y <= x;
+    hit |= y == x;
   }
-  return d + lt;
+  return le;
 }
 
 // Slot blocks: a warp walks its chunk 32 slots at a time; lane l holds slot
@@ -327,16 +344,18 @@ struct RankWarp {
   int2 buf[32];  // per slot of the block: {common | (j*+1) << 8, A[R+T-D-1]}
 };
 
-template <int K>
-__global__ void __launch_bounds__(kBlock, 4) kmv_ranked_kernel(const int32_t* __restrict__ R,
-                                                            const double* __restrict__ rank_values,
-                                                            const int32_t* __restrict__ lengths,
-                                                            const int32_t* __restrict__ sizes,
-                                                            const int32_t* __restrict__ us,
-                                                            const int32_t* __restrict__ vs, int64_t e_begin,
-                                                            int64_t e_end, double* out_sum,
-                                                            unsigned long long* ctr) {
-  constexpr int P = 8, G = K / P, E = 32 / G, IT = 32 / E;
+// P ranks of each v row per lane (G = K/P lanes per edge, E = 32/G edges per
+// iteration; the slot layout is padded to E)
+template <int K, int P>
+__global__ void __launch_bounds__(kBlock, PG_RANKED_MINB) kmv_ranked_kernel(const int32_t* __restrict__ R,
+                                                               const double* __restrict__ rank_values,
+                                                               const int32_t* __restrict__ lengths,
+                                                               const int32_t* __restrict__ sizes,
+                                                               const int32_t* __restrict__ us,
+                                                               const int32_t* __restrict__ vs, int64_t e_begin,
+                                                               int64_t e_end, double* out_sum,
+                                                               unsigned long long* ctr) {
+  constexpr int G = K / P, E = 32 / G, IT = 32 / E;
   constexpr int64_t kChunk = 512;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double red[kBlock / 32];
@@ -344,7 +363,7 @@ __global__ void __launch_bounds__(kBlock, 4) kmv_ranked_kernel(const int32_t* __
   RankDir<K>& W = Wp.dir;
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
   double acc = 0.0;
-  int32_t cur_u = -1, lo = 0, spanm1 = 0, lu = 0, su = 0;
+  int32_t cur_u = -1, lo = 0, spanm1 = 0, lu = 0;
   uint32_t mul = 0;
   int64_t wb, we;
   while (next_chunk(ctr, e_begin, e_end, kChunk, wb, we)) {
@@ -364,7 +383,7 @@ __global__ void __launch_bounds__(kBlock, 4) kmv_ranked_kernel(const int32_t* __
     ldg_rowpart<P>(R + (int64_t)(vq < 0 ? 0 : vq) * K + gl * P, x);
 #pragma unroll 1
     for (int64_t b0 = wb; b0 < we; b0 += 32) {
-      // next block's slots (consumed 8 iterations later)
+      // next block's slots (consumed IT iterations later)
       int32_t un = 0, vn = -1, sun = 0, lun = 0, svn = 0, lvn = 0;
       if (b0 + 32 + lane < we) {
         un = us[b0 + 32 + lane];
@@ -387,7 +406,6 @@ __global__ void __launch_bounds__(kBlock, 4) kmv_ranked_kernel(const int32_t* __
         if (u != cur_u) {
           cur_u = u;
           lu = __shfl_sync(0xffffffffu, lul, it * E);
-          su = __shfl_sync(0xffffffffu, sul, it * E);
           rd_build<K>(W, R + (int64_t)u * K, lu, lo, spanm1, mul);
         }
         // the next iteration's v row (the next block's first at the end)
@@ -396,16 +414,27 @@ __global__ void __launch_bounds__(kBlock, 4) kmv_ranked_kernel(const int32_t* __
         ldg_rowpart<P>(R + (int64_t)(vqn < 0 ? 0 : vqn) * K + gl * P, xn);
         // le_t = |A <= b_t| (<= K <= 128) packed four per register
         uint32_t le[P / 4];
-        unsigned hits = 0;
+        unsigned hits = 0, ovf = 0;
 #pragma unroll
         for (int t = 0; t < P; ++t) {
           const int32_t q = (int32_t)x[t];
+          const bool ok = valid && q != INT32_MAX;
+          bool h, o;
+          const int l = rd_probe<K>(W, q, lo, spanm1, mul, ok, h, o);
           if (t % 4 == 0) le[t / 4] = 0;
-          if (valid && q != INT32_MAX) {
-            bool h;
-            const int l = rd_probe<K>(W, q, lo, spanm1, mul, h) + h;
-            le[t / 4] |= (uint32_t)l << (8 * (t % 4));
-            hits |= (unsigned)h << t;
+          le[t / 4] |= (uint32_t)(ok ? l : 0) << (8 * (t % 4));
+          hits |= (unsigned)(ok && h) << t;
+          ovf |= (unsigned)(ok && o) << t;
+        }
+        if (__any_sync(0xffffffffu, ovf != 0)) {  // buckets of four or more elements
+#pragma unroll
+          for (int t = 0; t < P; ++t) {
+            if ((ovf >> t) & 1) {
+              bool h;
+              const int l = rd_probe_slow<K>(W, (int32_t)x[t], lo, spanm1, mul, h);
+              le[t / 4] = (le[t / 4] & ~(0xffu << (8 * (t % 4)))) | ((uint32_t)l << (8 * (t % 4)));
+              hits = (hits & ~(1u << t)) | ((unsigned)h << t);
+            }
           }
         }
         const int mc = __popc(hits);
@@ -465,7 +494,6 @@ __global__ void __launch_bounds__(kBlock, 4) kmv_ranked_kernel(const int32_t* __
         acc = __dadd_rn(acc, kmv_estimate(r, K, sul, svl));
       }
       __syncwarp();
-      // rotate to the next block: its endpoint gathers
       ul = un;
       vl = vn;
       sul = sun;
@@ -489,10 +517,11 @@ template <int K>
 static int launch_kmv_ranked(cudaStream_t s, const int32_t* ranks, const double* rank_values,
                              const int32_t* lengths, const int32_t* sizes, const int32_t* us, const int32_t* vs,
                              int64_t b, int64_t e, double* out_sum) {
-  auto kern = kmv_ranked_kernel<K>;
+  constexpr int P = kRankedPerLane;
+  auto kern = kmv_ranked_kernel<K, P>;
   const size_t sm = (size_t)(kBlock / 32) * sizeof(RankWarp<K>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / 8));
+  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / P));
   ChunkCounter ctr;
   const cudaError_t ce = ctr.init(s);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce));
@@ -561,7 +590,7 @@ int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k, const int
 
 int pg_kmv_ranked_pad(int32_t k, int32_t* pad_host) {
   PG_REQUIRE(pad_host, "null output");
-  *pad_host = (k == 32 || k == 64 || k == 128) ? 256 / k : 0;
+  *pad_host = (k == 32 || k == 64 || k == 128) ? 32 * kRankedPerLane / k : 0;
   return PG_OK;
 }
 
@@ -570,7 +599,7 @@ int pg_tc_kmv_ranked(const int32_t* ranks, const double* rank_values, const int3
                      double* out_sum, void* stream) {
   if (k != 32 && k != 64 && k != 128)
     return fail(PG_ERR_UNSUPPORTED, "the rank-directory KMV engine supports k = 32, 64, 128 (got %d)", k);
-  const int pad = 256 / k;
+  const int pad = 32 * kRankedPerLane / k;
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
   PG_REQUIRE(e_begin % pad == 0, "e_begin must be a multiple of the layout pad %d", pad);
   PG_REQUIRE(out_sum, "null pointer");
