@@ -48,6 +48,7 @@ __device__ __forceinline__ uint32_t bloom_pos(uint64_t w, uint32_t bits) {
 // that vertex's row in shared memory; the R rows are then one contiguous block
 // of the output.  Vertices with d > kHubBloom are left to pass 2.
 constexpr int64_t kHubBloom = 1024;
+constexpr int64_t kMidBloom = 64;  // rows above this take pass 1b (a warp each)
 
 struct BloomBatchSmem {
   int64_t off[32];
@@ -59,7 +60,8 @@ __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n,
     uint32_t bits, int b, int R, const uint64_t* __restrict__ seeds_dev,
     uint64_t* __restrict__ rows, int32_t* __restrict__ ones, int32_t* __restrict__ hubs,
-    int32_t* __restrict__ hub_count, unsigned long long* __restrict__ vtx_work) {
+    int32_t* __restrict__ hub_count, unsigned long long* __restrict__ vtx_work, int32_t* __restrict__ mids,
+    int32_t* __restrict__ mid_count) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const uint32_t words32 = bits >> 5;
   const uint32_t words64 = bits >> 6;
@@ -81,9 +83,12 @@ __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
     const bool mine = lane < nb;
     const int64_t o = mine ? offsets[v] : 0;
     int64_t d = mine ? offsets[v + 1] - o : 0;
-    const bool hub = d > kHubBloom;
-    if (hub) {
+    const bool hub = d > kMidBloom;  // built by pass 1b (mid) or pass 2 (hub)
+    if (d > kHubBloom) {
       hubs[atomicAdd(hub_count, 1)] = (int32_t)v;
+      d = 0;
+    } else if (hub) {
+      mids[atomicAdd(mid_count, 1)] = (int32_t)v;
       d = 0;
     }
     int incl = (int)d;  // exclusive prefix of the batch's (non-hub) degrees
@@ -122,6 +127,54 @@ __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
       for (uint32_t i = 0; i < words64; ++i) c += __popcll(b64[lane * words64 + (i + lane) % words64]);
       ones[v] = c;
     }
+    __syncwarp();
+  }
+}
+
+// pass 1b: mid-degree vertices (kMidBloom < d <= kHubBloom), one warp each,
+// taken from a counter: a 32-vertex batch of such rows would hold up to 32K
+// entries on one warp, and that tail set the duration of every chunked build
+// (17% active warps).  The row is built in the warp's shared-memory slot and
+// written whole (pass 1 wrote it as zeros).
+template <bool kPow2>
+__global__ void __launch_bounds__(kThreads) build_bloom_mid_kernel(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, uint32_t bits, int b,
+    const uint64_t* __restrict__ seeds_dev, uint64_t* __restrict__ rows, int32_t* __restrict__ ones,
+    const int32_t* __restrict__ mids, const int32_t* __restrict__ mid_count, int32_t* __restrict__ mid_work) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t words32 = bits >> 5, words64 = bits >> 6;
+  uint64_t* seeds = reinterpret_cast<uint64_t*>(smem_raw);
+  uint32_t* row = reinterpret_cast<uint32_t*>(seeds + 64) + (size_t)warp_id() * words32;
+  for (int i = threadIdx.x; i < b; i += kThreads) seeds[i] = seeds_dev[i];
+  __syncthreads();
+  const int nm = *mid_count;
+  const int lane = lane_id();
+  for (;;) {
+    int mi = 0;
+    if (lane == 0) mi = atomicAdd(mid_work, 1);
+    mi = __shfl_sync(0xffffffffu, mi, 0);
+    if (mi >= nm) break;
+    const int64_t v = mids[mi];
+    const int64_t o = offsets[v], d = offsets[v + 1] - o;
+    for (uint32_t i = lane; i < words32; i += 32) row[i] = 0u;
+    __syncwarp();
+    for (int64_t t = lane; t < d; t += 32) {
+      const int32_t x = adj[o + t];
+      for (int h = 0; h < b; ++h) {
+        const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x), bits);
+        atomicOr(&row[p >> 5], 1u << (p & 31));
+      }
+    }
+    __syncwarp();
+    const uint64_t* r64 = reinterpret_cast<const uint64_t*>(row);
+    int c = 0;
+    for (uint32_t i = lane; i < words64; i += 32) {
+      const uint64_t w = r64[i];
+      rows[v * words64 + i] = w;
+      c += __popcll(w);
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if (lane == 0) ones[v] = c;
     __syncwarp();
   }
 }
@@ -614,17 +667,30 @@ struct HubList {
   // header: [hub count i32 | hub work i32 | vertex-batch work u64], then ids
   int32_t* hub_work = nullptr;
   unsigned long long* vtx_work = nullptr;
-  int init(const int64_t* offsets, int64_t n, cudaStream_t st) {
+  // optional second list (Bloom: mid-degree vertices, one warp each):
+  // header [mid count i32 | mid work i32], then up to n ids
+  int32_t* mid_count = nullptr;
+  int32_t* mid_work = nullptr;
+  int32_t* mids = nullptr;
+  int init(const int64_t* offsets, int64_t n, cudaStream_t st, bool with_mid = false) {
     (void)offsets;
     s = st;
     retain_default_pool();
-    cudaError_t e = cudaMallocAsync(&buf, 16 + sizeof(int32_t) * (size_t)n, s);
+    const size_t list = sizeof(int32_t) * (size_t)n;
+    const size_t bytes = 16 + list + (with_mid ? 16 + list : 0);
+    cudaError_t e = cudaMallocAsync(&buf, bytes, s);
     if (e == cudaSuccess) e = cudaMemsetAsync(buf, 0, 16, s);
+    if (e == cudaSuccess && with_mid) e = cudaMemsetAsync(static_cast<char*>(buf) + 16 + list, 0, 16, s);
     if (e != cudaSuccess) return fail(PG_ERR_CUDA, "hub list: %s", cudaGetErrorString(e));
     count = static_cast<int32_t*>(buf);
     hub_work = count + 1;
     vtx_work = reinterpret_cast<unsigned long long*>(static_cast<char*>(buf) + 8);
     ids = reinterpret_cast<int32_t*>(static_cast<char*>(buf) + 16);
+    if (with_mid) {
+      mid_count = reinterpret_cast<int32_t*>(static_cast<char*>(buf) + 16 + list);
+      mid_work = mid_count + 1;
+      mids = mid_count + 4;
+    }
     return PG_OK;
   }
   ~HubList() {
@@ -699,12 +765,13 @@ int pg_build_bloom(const int64_t* offsets, const int32_t* adj, int64_t n, int32_
   if (n == 0) return PG_OK;
   cudaStream_t s = as_stream(stream);
   HubList hubs;
-  if (int rc = hubs.init(offsets, n, s)) return rc;
+  if (int rc = hubs.init(offsets, n, s, true)) return rc;
   // batch size: 32 vertices per warp while the rows fit ~96 KB per CTA
   int R = 32;
   while (R > 1 && (size_t)kWarps * R * (bits / 8) > 96 * 1024) R >>= 1;
   const size_t smem = kWarps * sizeof(BloomBatchSmem) + 64 * sizeof(uint64_t) + (size_t)kWarps * R * (bits / 8);
   const size_t smem_hub = (size_t)(bits / 8) + 8 + 64 * sizeof(uint64_t);
+  const size_t smem_mid = 64 * sizeof(uint64_t) + (size_t)kWarps * (bits / 8);
   const bool pow2 = (bits & (bits - 1)) == 0;
 #define PG_BB(P2)                                                                                       \
   {                                                                                                     \
@@ -713,7 +780,12 @@ int pg_build_bloom(const int64_t* offsets, const int32_t* adj, int64_t n, int32_
                          (int)smem_hub);                                                                \
     const int grid = grid_for(build_bloom_kernel<P2>, smem, (n + R - 1) / R * 32);                      \
     build_bloom_kernel<P2><<<grid, kThreads, smem, s>>>(offsets, adj, n, bits, b, R, seeds_dev, rows, ones, \
-                                                        hubs.ids, hubs.count, hubs.vtx_work);           \
+                                                        hubs.ids, hubs.count, hubs.vtx_work, hubs.mids,  \
+                                                        hubs.mid_count);                                \
+    cudaFuncSetAttribute(build_bloom_mid_kernel<P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                         (int)smem_mid);                                                                \
+    build_bloom_mid_kernel<P2><<<grid_for(build_bloom_mid_kernel<P2>, smem_mid, n), kThreads, smem_mid, s>>>( \
+        offsets, adj, bits, b, seeds_dev, rows, ones, hubs.mids, hubs.mid_count, hubs.mid_work);        \
     build_bloom_hubs_kernel<P2><<<hub_grid(), kThreads, smem_hub, s>>>(offsets, adj, bits, b, seeds_dev,  \
                                                                        rows, hubs.ids, hubs.count);       \
     bloom_hub_ones_kernel<<<64, kThreads, 0, s>>>(rows, bits / 64, ones, hubs.ids, hubs.count);          \
