@@ -94,6 +94,22 @@ PG_API int pg_csr_upper_edges_padded(const int64_t* offsets, const int32_t* adj,
                               int32_t pad, int32_t* us, int32_t* vs, int64_t capacity,
                               int64_t* slots_host, void* workspace, size_t workspace_bytes,
                               void* stream);
+/* The same padded slots for the rows of [v0, v1) only -- their lower
+ * (lower = 1: neighbours < u) or upper (0: > u) entries -- appended at the
+ * device cursor cursor_dev[0] with no host sync; range_dev receives the
+ * appended [begin, end) and cursor_dev[0] advances to end; us is the
+ * group-u array (one u per pad slots, padded mode 2).  cursor_dev[1] is set
+ * to 1 if the range's slots exceed max_slots (a host bound on them, e.g.
+ * its entries + (pad-1) rows) or `capacity` (they are then dropped).  Used
+ * to lay out each upload chunk as it lands (CsrGraph.edges(),
+ * graphs.py:101-105, restricted to a vertex range; the lower triangle holds
+ * every undirected edge once as well). */
+PG_API int pg_csr_range_slots_workspace(int64_t rows, int64_t max_slots, size_t* bytes);
+PG_API int pg_csr_range_slots_append(const int64_t* offsets, const int32_t* adj, int64_t v0,
+                              int64_t v1, int32_t pad, int32_t lower, int64_t max_slots,
+                              int32_t* ug, int32_t* vs, int64_t capacity, int64_t* cursor_dev,
+                              int64_t* range_dev, void* workspace, size_t workspace_bytes,
+                              void* stream);
 /* lanes-per-edge group size of the fused kernels for rows of `row_bytes`
  * (Bloom: bits/8, k-Hash: 4k) = the pad of the layout above (1: no pad) */
 PG_API int pg_group_pad(int32_t row_bytes, int32_t* pad_host);
@@ -169,6 +185,15 @@ PG_API int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op,
                 const int32_t* sizes, const double* lut, const int32_t* us,
                 const int32_t* vs, int64_t e_begin, int64_t e_end, int32_t padded,
                 int64_t* out_hist, int64_t* out_sum_pos, void* stream);
+/* pg_tc_bloom (padded mode 2) over the slots [range_dev[0], range_dev[1])
+ * read on the device (a pg_csr_range_slots_append range); the launch is
+ * sized for max_slots.  accumulate = 1 adds into out_hist / out_sum_pos
+ * instead of overwriting them (one histogram over several ranges). */
+PG_API int pg_tc_bloom_range(const uint64_t* rows, int32_t bits, int32_t op,
+                      const int32_t* sizes, const double* lut, const int32_t* ug,
+                      const int32_t* vs, const int64_t* range_dev, int64_t max_slots,
+                      int32_t accumulate, int64_t* out_hist, int64_t* out_sum_pos,
+                      void* stream);
 /* k-/1-Hash TC: out_cnt[m], out_ssum[m] (m = 0..k): number of edges and
  * int64 sum of (s_u+s_v) of non-verbatim edges with m matches;
  * out_verbatim[0] = sum of matches over verbatim 1-Hash edges. */

@@ -48,8 +48,13 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_bloom_wide_kernel(const unsig
                                                                     const int32_t* us, const int32_t* vs,
                                                                     int64_t e_begin, int64_t e_end,
                                                                     EpiBloomHist epi, int64_t* out_hist,
-                                                                    int64_t* out_sum_pos, unsigned long long* ctr) {
+                                                                    int64_t* out_sum_pos, unsigned long long* ctr,
+                                                                    const int64_t* range_dev) {
   extern __shared__ int hist_s[];
+  if (range_dev) {  // [begin, end) computed on the device (appended slot ranges)
+    e_begin = range_dev[0];
+    e_end = range_dev[1];
+  }
   for (int i = threadIdx.x; i <= bits; i += blockDim.x) hist_s[i] = 0;
   __syncthreads();
   epi.hist_s = hist_s;
@@ -127,7 +132,8 @@ int pg_pairs_bloom(const uint64_t* rows, int32_t bits, int32_t b, int32_t op, co
 
 static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* sizes,
                          const double* lut, const int32_t* us, const int32_t* vs, int64_t e_begin,
-                         int64_t e_end, int64_t* out_hist, int64_t* out_sum_pos, void* stream, int padded) {
+                         int64_t e_end, int64_t* out_hist, int64_t* out_sum_pos, void* stream, int padded,
+                         const int64_t* range_dev = nullptr, bool accumulate = false) {
   PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
   PG_REQUIRE(op == PG_BF_AND || op == PG_BF_L || op == PG_BF_OR, "op is not a Bloom estimator");
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
@@ -136,8 +142,11 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
   cudaStream_t s = as_stream(stream);
   // one memset when the sum slot directly follows the histogram
   const bool adjacent = out_sum_pos == out_hist + bits + 1;
-  cudaError_t ce = cudaMemsetAsync(out_hist, 0, sizeof(int64_t) * (bits + 1 + (adjacent ? 1 : 0)), s);
-  if (ce == cudaSuccess && out_sum_pos && !adjacent) ce = cudaMemsetAsync(out_sum_pos, 0, sizeof(int64_t), s);
+  cudaError_t ce = cudaSuccess;
+  if (!accumulate) {
+    ce = cudaMemsetAsync(out_hist, 0, sizeof(int64_t) * (bits + 1 + (adjacent ? 1 : 0)), s);
+    if (ce == cudaSuccess && out_sum_pos && !adjacent) ce = cudaMemsetAsync(out_sum_pos, 0, sizeof(int64_t), s);
+  }
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
   if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
   PG_REQUIRE(op != PG_BF_OR || (sizes && lut), "BF_OR needs sizes and the table");
@@ -175,7 +184,8 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
     le = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
     if (le != cudaSuccess) return fail(PG_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(le));  \
     const int grid = grid_cap(grid_for_kernel(k, smem), e_end - e_begin, kBlock);                    \
-    k<<<grid, kBlock, smem, s>>>(rb, bits, us, vs, e_begin, e_end, epi, out_hist, out_sum_pos, ctr.p); \
+    k<<<grid, kBlock, smem, s>>>(rb, bits, us, vs, e_begin, e_end, epi, out_hist, out_sum_pos, ctr.p,  \
+                                 range_dev);                                                          \
   }
 #define PG_WM(W8)                                                                  \
   if (padded == 2) {                                                             \
@@ -231,6 +241,22 @@ int pg_tc_bloom(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* s
 }
 
 }  // extern "C"
+
+extern "C" int pg_tc_bloom_range(const uint64_t* rows, int32_t bits, int32_t op, const int32_t* sizes,
+                                 const double* lut, const int32_t* ug, const int32_t* vs, const int64_t* range_dev,
+                                 int64_t max_slots, int32_t accumulate, int64_t* out_hist, int64_t* out_sum_pos,
+                                 void* stream) {
+  int32_t pad = 1;
+  PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
+  pg_group_pad(bits / 8, &pad);
+  if (pad <= 1) return fail(PG_ERR_UNSUPPORTED, "device slot ranges need a group-u Bloom row size (got %d bits)", bits);
+  PG_REQUIRE(range_dev, "null range");
+  PG_REQUIRE(max_slots >= 0, "max_slots must be >= 0");
+  // the wide engine's group-u layout; the launch is sized for max_slots and
+  // the kernel reads the actual [begin, end) from range_dev
+  return tc_bloom_impl(rows, bits, op, sizes, lut, ug, vs, 0, max_slots, out_hist, out_sum_pos, stream, 2,
+                       range_dev, accumulate != 0);
+}
 
 extern "C" int pg_group_pad(int32_t row_bytes, int32_t* pad_host) {
   PG_REQUIRE(pad_host, "null output");

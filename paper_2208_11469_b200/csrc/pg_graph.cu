@@ -50,6 +50,75 @@ __global__ void upper_gather_kernel(const int64_t* __restrict__ offsets, const i
   }
 }
 
+// ---- edge slots of a vertex range, appended on the device (no host sync) ----
+// Row u of [v0, v1) contributes its lower (< u) or upper (> u) neighbours,
+// padded to a multiple of `pad` with v = -1, at a running device cursor.
+// The TC of an upload chunk can then run as soon as the chunk and its
+// sketches are on the device (the lower triangle of chunk c needs sketches
+// of chunks <= c only).
+__global__ void range_slot_count_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj,
+                                        int64_t v0, int64_t v1, int lower, int64_t* __restrict__ first,
+                                        int64_t* __restrict__ lens, int64_t* __restrict__ cnt, int64_t pad) {
+  for (int64_t u = v0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < v1;
+       u += (int64_t)gridDim.x * blockDim.x) {
+    int64_t lo = offsets[u], hi = offsets[u + 1];
+    const int64_t beg = lo, end = hi;
+    while (lo < hi) {  // first neighbour > u (the CSR is loop-free)
+      const int64_t mid = (lo + hi) >> 1;
+      if (adj[mid] <= u) lo = mid + 1;
+      else hi = mid;
+    }
+    const int64_t f = lower ? beg : lo, len = lower ? lo - beg : end - lo;
+    first[u - v0] = f;
+    lens[u - v0] = len;
+    cnt[u - v0] = (len + pad - 1) / pad * pad;
+  }
+}
+
+// marks[start[r]] = r + 1 for the range's non-empty rows (0 elsewhere); the
+// inclusive max-scan of the marks gives every slot its row (load-balanced:
+// a thread per slot, whatever the row lengths)
+__global__ void range_slot_mark_kernel(const int64_t* __restrict__ cnt, const int64_t* __restrict__ start,
+                                       int64_t rows, int32_t* __restrict__ marks) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < rows; r += (int64_t)gridDim.x * blockDim.x)
+    if (cnt[r] > 0) marks[start[r]] = (int32_t)(r + 1);
+}
+
+// slot o of the range (o < its device-side total): row r = rowof[o] - 1,
+// the (o - start[r])-th lower/upper neighbour or -1 (padding); a group-u
+// entry per `pad` slots.  Slots past `capacity` are dropped and flagged.
+__global__ void range_slot_gather_kernel(const int32_t* __restrict__ adj, int64_t v0, int64_t rows,
+                                         const int64_t* __restrict__ first, const int64_t* __restrict__ lens,
+                                         const int64_t* __restrict__ cnt, const int64_t* __restrict__ start,
+                                         const int32_t* __restrict__ rowof, int64_t max_slots, int lg_pad,
+                                         int64_t capacity, const int64_t* __restrict__ cursor,
+                                         int64_t* __restrict__ overflow, int32_t* __restrict__ ug,
+                                         int32_t* __restrict__ vs) {
+  const int64_t base = cursor[0];
+  const int64_t total = start[rows - 1] + cnt[rows - 1];
+  const int64_t lim = min(total, max_slots);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (total > max_slots || base + total > capacity)) *overflow = 1;
+  const int64_t pad_mask = (int64_t(1) << lg_pad) - 1;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < lim; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t slot = base + o;
+    if (slot >= capacity) break;
+    const int32_t r = rowof[o] - 1;
+    const int64_t k = o - start[r];
+    vs[slot] = k < lens[r] ? adj[first[r] + k] : -1;
+    if ((k & pad_mask) == 0) ug[slot >> lg_pad] = (int32_t)(v0 + r);
+  }
+}
+
+// advance the cursor past the range and record [begin, end) of its slots
+__global__ void range_slot_finish_kernel(const int64_t* __restrict__ cnt, const int64_t* __restrict__ start,
+                                         int64_t rows, int64_t* __restrict__ cursor, int64_t* __restrict__ range) {
+  const int64_t base = cursor[0];
+  const int64_t total = rows > 0 ? start[rows - 1] + cnt[rows - 1] : 0;
+  range[0] = base;
+  range[1] = base + total;
+  cursor[0] = base + total;
+}
+
 __global__ void mark_csr_rows_kernel(const int64_t* __restrict__ offsets, int64_t n, int32_t* __restrict__ marks) {
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
        u += (int64_t)gridDim.x * blockDim.x)
@@ -255,6 +324,61 @@ int pg_csr_upper_edges_padded(const int64_t* offsets, const int32_t* adj, int64_
   PG_REQUIRE(pad >= 1 && pad <= 32 && (pad & (pad - 1)) == 0, "pad must be a power of two <= 32");
   return upper_edges_impl(offsets, adj, n, us, vs, capacity, slots_host, workspace, workspace_bytes, stream,
                           pad);
+}
+
+int pg_csr_range_slots_workspace(int64_t rows, int64_t max_slots, size_t* bytes) {
+  PG_REQUIRE(bytes && rows >= 0 && max_slots >= 0, "bad arguments");
+  size_t t1 = 0, t2 = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, t1, (const int64_t*)nullptr, (int64_t*)nullptr, rows > 0 ? rows : 1);
+  cub::DeviceScan::InclusiveScan(nullptr, t2, (const int32_t*)nullptr, (int32_t*)nullptr, ::cuda::maximum<>{},
+                                 max_slots > 0 ? max_slots : 1);
+  *bytes = 4 * align256(sizeof(int64_t) * (size_t)(rows + 1)) + 2 * align256(sizeof(int32_t) * (size_t)(max_slots + 1)) +
+           align256(t1 > t2 ? t1 : t2);
+  return PG_OK;
+}
+
+int pg_csr_range_slots_append(const int64_t* offsets, const int32_t* adj, int64_t v0, int64_t v1, int32_t pad,
+                              int32_t lower, int64_t max_slots, int32_t* ug, int32_t* vs, int64_t capacity,
+                              int64_t* cursor_dev, int64_t* range_dev, void* workspace, size_t workspace_bytes,
+                              void* stream) {
+  PG_REQUIRE(0 <= v0 && v0 <= v1, "bad vertex range");
+  PG_REQUIRE(pad >= 1 && pad <= 32 && (pad & (pad - 1)) == 0, "pad must be a power of two <= 32");
+  PG_REQUIRE(cursor_dev && range_dev && workspace, "null pointer");
+  const int64_t rows = v1 - v0;
+  size_t need = 0;
+  pg_csr_range_slots_workspace(rows, max_slots, &need);
+  PG_REQUIRE(workspace_bytes >= need, "workspace too small (%zu < %zu)", workspace_bytes, need);
+  cudaStream_t s = as_stream(stream);
+  const size_t arr = align256(sizeof(int64_t) * (size_t)(rows + 1));
+  const size_t sarr = align256(sizeof(int32_t) * (size_t)(max_slots + 1));
+  char* ws = static_cast<char*>(workspace);
+  int64_t* first = reinterpret_cast<int64_t*>(ws);
+  int64_t* cnt = reinterpret_cast<int64_t*>(ws + arr);
+  int64_t* start = reinterpret_cast<int64_t*>(ws + 2 * arr);
+  int64_t* lens = reinterpret_cast<int64_t*>(ws + 3 * arr);
+  int32_t* marks = reinterpret_cast<int32_t*>(ws + 4 * arr);
+  int32_t* rowof = reinterpret_cast<int32_t*>(ws + 4 * arr + sarr);
+  void* temp = ws + 4 * arr + 2 * sarr;
+  size_t temp_bytes = workspace_bytes - 4 * arr - 2 * sarr;
+  const int grid = sm_count() * 8;
+  if (rows > 0 && max_slots > 0) {
+    PG_REQUIRE(offsets && adj && ug && vs, "null pointer");
+    range_slot_count_kernel<<<grid, 256, 0, s>>>(offsets, adj, v0, v1, lower, first, lens, cnt, pad);
+    if (int rc = check_launch("range_slot_count")) return rc;
+    cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, cnt, start, rows, s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(marks, 0, sizeof(int32_t) * (size_t)max_slots, s);
+    if (e != cudaSuccess) return fail(PG_ERR_CUDA, "scan: %s", cudaGetErrorString(e));
+    range_slot_mark_kernel<<<grid, 256, 0, s>>>(cnt, start, rows, marks);
+    if (int rc = check_launch("range_slot_mark")) return rc;
+    size_t tb = temp_bytes;
+    e = cub::DeviceScan::InclusiveScan(temp, tb, marks, rowof, ::cuda::maximum<>{}, max_slots, s);
+    if (e != cudaSuccess) return fail(PG_ERR_CUDA, "max-scan: %s", cudaGetErrorString(e));
+    range_slot_gather_kernel<<<grid, 256, 0, s>>>(adj, v0, rows, first, lens, cnt, start, rowof, max_slots,
+                                                  __builtin_ctz(pad), capacity, cursor_dev, cursor_dev + 1, ug, vs);
+    if (int rc = check_launch("range_slot_gather")) return rc;
+  }
+  range_slot_finish_kernel<<<1, 1, 0, s>>>(cnt, start, rows > 0 && max_slots > 0 ? rows : 0, cursor_dev, range_dev);
+  return check_launch("range_slot_finish");
 }
 
 int pg_csr_expand_rows(const int64_t* offsets, int64_t n, int64_t nnz, int32_t* src, void* stream) {

@@ -75,6 +75,7 @@ class DeviceCsr:
         self.n = len(offsets) - 1
         self.nnz = len(adjacency)
         self.upload_chunks = []
+        self.chunk_bounds = []  # (v0, v1, nnz_before) of every upload chunk
         adj_t = torch.from_numpy(np.ascontiguousarray(adjacency))
         if (UPLOAD_CHUNKS > 0 and adj_t.dtype == torch.int32 and adj_t.is_pinned()
                 and adjacency.nbytes >= CHUNKED_UPLOAD_MIN_BYTES and self.n > 0):
@@ -107,13 +108,18 @@ class DeviceCsr:
         cs.wait_stream(cur)  # the new blocks may still be in use on cur
         with torch.cuda.stream(cs):
             self.offsets.copy_(off_t, non_blocking=True)
-            for v0, v1 in zip(cuts[:-1].tolist(), cuts[1:].tolist()):
+            # highest vertex range first: once chunk c has landed, every
+            # range above it is on the device, so a chunk's upper-triangle
+            # edges (u < v) can be estimated as soon as its own sketches are
+            # built (mining._tc_counts_chunked)
+            for v0, v1 in reversed(list(zip(cuts[:-1].tolist(), cuts[1:].tolist()))):
                 a, b = int(offsets[v0]), int(offsets[v1])
                 if b > a:
                     self.adj[a:b].copy_(adj_t[a:b], non_blocking=True)
                 ev = torch.cuda.Event()
                 ev.record(cs)
                 self.upload_chunks.append((v0, v1, ev))
+                self.chunk_bounds.append((v0, v1, a, b))
         self.offsets.record_stream(cs)
         self.adj.record_stream(cs)
         cur.wait_stream(cs)
@@ -133,6 +139,7 @@ class DeviceCsr:
         self.offsets = offsets
         self.adj = adj
         self.upload_chunks = []
+        self.chunk_bounds = []
         self.degrees = (offsets[1:] - offsets[:-1]).to(torch.int32)
         self._upper = None
         self._src = None

@@ -88,9 +88,82 @@ def tc_counts(provider, dev, rank: int = 0, world: int = 1):
         part = provider._pairs_device(us[b:e], vs[b:e])
         return part.sum().reshape(1) if part.numel() else torch.zeros(
             1, dtype=torch.int64, device="cuda")
+    if world == 1 and _chunk_pipelined(provider, dev):
+        return _tc_counts_chunked(provider, dev)
     us, vs, slots, padded = provider._tc_layout(dev)
     b, e = edge_range(slots, rank, world, align=32 if padded else 1)
     return provider._tc_counts(us, vs, b, e, padded)
+
+
+def _chunk_pipelined(provider, dev) -> bool:
+    """A Bloom TC whose CSR is still arriving in upload chunks with per-chunk
+    sketch builds (the host-CSR path): it can run chunk by chunk."""
+    sg = getattr(provider, "sketched", None)
+    return (isinstance(provider, BloomProvider) and provider.kind is not EstimatorKind.BF_OR
+            and sg is not None and bool(sg._chunk_ready) and sg._chunk_dev is dev
+            and provider.tc_pad() > 1 and not dev._layouts)
+
+
+def _tc_counts_chunked(provider, dev):
+    """The fused Bloom TC of a chunk-uploaded graph, pipelined with the
+    upload.  Chunks arrive highest vertex range first (DeviceCsr), so the
+    upper-triangle slots of chunk c (rows [v0, v1), neighbours > u, whose
+    sketches are all built once c's are) are laid out on a side stream as
+    soon as the chunk lands, and its TC runs on another as soon as its
+    sketches are built, with device-side slot ranges (no host sync).  The
+    slots are the whole-graph layout's, range by range: the same per-edge
+    popcounts, so the same histogram."""
+    import ctypes
+    import torch
+    from .graphs import side_stream
+    sg = provider.sketched
+    # the raw device buffers: device_tensors() would order the current
+    # stream after the whole build; here each chunk waits for its own events
+    d = sg._dev
+    pad = provider.tc_pad()
+    bits = sg.bit_length
+    cur = torch.cuda.current_stream()
+    ls, ts = side_stream("layout"), side_stream("tc")
+    chunks = sg._chunk_ready
+    cap = dev.nnz + (pad - 1) * dev.n + pad  # lower entries <= nnz: no overflow
+    nnz_of = {(v0, v1): b - a for v0, v1, a, b in dev.chunk_bounds}
+
+    def bound(v0, v1):  # host bound on a range's padded slots
+        return nnz_of.get((v0, v1), dev.nnz) + (pad - 1) * (v1 - v0)
+
+    max_rows = max(v1 - v0 for v0, v1, _, _ in chunks)
+    ws_bytes = ctypes.c_size_t()
+    N.call("pg_csr_range_slots_workspace", max_rows,
+           max(bound(v0, v1) for v0, v1, _, _ in chunks), ctypes.byref(ws_bytes))
+    with torch.cuda.stream(ls):
+        ug = torch.empty(cap // pad + 1, dtype=torch.int32, device="cuda")
+        vs = torch.empty(cap, dtype=torch.int32, device="cuda")
+        ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device="cuda")
+        cur_rng = torch.zeros(2 + 2 * len(chunks), dtype=torch.int64, device="cuda")
+    with torch.cuda.stream(ts):
+        out = torch.zeros(bits + 2, dtype=torch.int64, device="cuda")
+    hl, h = N.stream_handle(ls), N.stream_handle(ts)
+    for c, (v0, v1, copied, built) in enumerate(chunks):
+        ls.wait_event(copied)
+        rng = N.ptr(cur_rng) + 8 * (2 + 2 * c)
+        max_slots = bound(v0, v1)
+        N.call("pg_csr_range_slots_append", N.ptr(dev.offsets), N.ptr(dev.adj), v0, v1,
+               pad, 0, max_slots, N.ptr(ug), N.ptr(vs), cap, N.ptr(cur_rng), rng,
+               N.ptr(ws), ws_bytes.value, hl)
+        laid = torch.cuda.Event()
+        laid.record(ls)
+        ts.wait_event(laid)
+        ts.wait_event(built)
+        # AND / L histograms need neither sizes nor the table (BF_OR does;
+        # it takes the whole-graph path)
+        N.call("pg_tc_bloom_range", N.ptr(d["rows"]), bits, provider.op,
+               None, None, N.ptr(ug), N.ptr(vs), rng, max_slots, 1,
+               N.ptr(out), N.ptr(out) + 8 * (bits + 1), h)
+    for t in (ug, vs, cur_rng):  # read on ts after their last use on ls
+        t.record_stream(ts)
+    cur.wait_stream(ts)
+    out.record_stream(cur)
+    return out
 
 
 def tc_combine(provider, counts: np.ndarray) -> float:

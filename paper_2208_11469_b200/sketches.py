@@ -224,6 +224,8 @@ class SketchedGraph:
         # CUDA event after which the device tensors are complete (builds on
         # a side stream); consumers' streams wait on it at access time
         self._ready = ready
+        self._chunk_ready = []  # per upload chunk (v0, v1, copy event, build event)
+        self._chunk_dev = None
 
     def _wait_ready(self) -> None:
         if self._ready is not None:
@@ -414,9 +416,15 @@ def _build_on_device(dev: DeviceCsr, kind: SketchKind, plan: BudgetPlan,
             seeds = device_seeds(bs.cuda_stream)
             out = _alloc_outputs(kind, plan, n)
             _prepare_builders(kind, n, seeds, out, bs.cuda_stream)
+            chunk_ready = []
             for v0, v1, ev in chunks:
                 bs.wait_event(ev)
                 _launch_builders(dev, kind, plan, seeds, out, v0, v1, bs.cuda_stream)
+                built = torch.cuda.Event()
+                built.record(bs)
+                # (copy event, build event): a consumer may start on the
+                # vertex range once both passed (mining.tc_counts)
+                chunk_ready.append((v0, v1, ev, built))
             ready = torch.cuda.Event()
             ready.record(bs)
         # consumers wait for `ready` when they touch the sketches
@@ -427,13 +435,17 @@ def _build_on_device(dev: DeviceCsr, kind: SketchKind, plan: BudgetPlan,
             t.record_stream(cur)
     else:
         ready = None
+        chunk_ready = []
         seeds = device_seeds(N.stream_handle())
         out = _alloc_outputs(kind, plan, n)
         _prepare_builders(kind, n, seeds, out, N.stream_handle())
         _launch_builders(dev, kind, plan, seeds, out, 0, n, N.stream_handle())
     out = {key: t[:n] for key, t in out.items()}
     out.update(seeds=seeds, sizes=dev.degrees)
-    return SketchedGraph(kind, plan, family, source, sizes, device=out, ready=ready)
+    sg = SketchedGraph(kind, plan, family, source, sizes, device=out, ready=ready)
+    sg._chunk_ready = chunk_ready
+    sg._chunk_dev = dev if chunk_ready else None
+    return sg
 
 
 def build_sketched_graph(graph: CsrGraph, kind, s: float, b: int = 1,
