@@ -158,11 +158,22 @@ __global__ void __launch_bounds__(kThreads) build_bloom_mid_kernel(
     const int64_t o = offsets[v], d = offsets[v + 1] - o;
     for (uint32_t i = lane; i < words32; i += 32) row[i] = 0u;
     __syncwarp();
-    for (int64_t t = lane; t < d; t += 32) {
-      const int32_t x = adj[o + t];
-      for (int h = 0; h < b; ++h) {
-        const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x), bits);
-        atomicOr(&row[p >> 5], 1u << (p & 31));
+    // four entries per lane in flight (the row is in L2/HBM: one dependent
+    // load per 32 entries left the warp latency-bound)
+    for (int64_t t0 = 0; t0 < d; t0 += 128) {
+      int32_t x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t t = t0 + 32 * q + lane;
+        x[q] = t < d ? adj[o + t] : -1;
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (x[q] < 0) continue;
+        for (int h = 0; h < b; ++h) {
+          const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x[q]), bits);
+          atomicOr(&row[p >> 5], 1u << (p & 31));
+        }
       }
     }
     __syncwarp();
@@ -241,11 +252,20 @@ __global__ void __launch_bounds__(kThreads) build_bloom_hubs_kernel(
       const int64_t beg = (t - s_pre[lo]) * kHubSlice, end = min(hd, beg + kHubSlice);
       for (uint32_t i = threadIdx.x; i < words32; i += kThreads) row[i] = 0u;
       __syncthreads();
-      for (int64_t j = beg + threadIdx.x; j < end; j += kThreads) {
-        const int32_t x = adj[ho + j];
-        for (int h = 0; h < b; ++h) {
-          const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x), bits);
-          atomicOr(&row[p >> 5], 1u << (p & 31));
+      for (int64_t j0 = beg; j0 < end; j0 += 4 * kThreads) {  // four loads in flight per thread
+        int32_t x[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int64_t j = j0 + q * kThreads + threadIdx.x;
+          x[q] = j < end ? adj[ho + j] : -1;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (x[q] < 0) continue;
+          for (int h = 0; h < b; ++h) {
+            const uint32_t p = bloom_pos<kPow2>(hash_word(seeds[h], x[q]), bits);
+            atomicOr(&row[p >> 5], 1u << (p & 31));
+          }
         }
       }
       __syncthreads();
