@@ -542,8 +542,9 @@ def run_e2e(pg, g, sk, steps, bits, b, m):
     return {"value": m / t, "unit": "edge-intersections/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": 8 * (bits + 2), "ms_per_step": t * 1e3,
             "path": "CsrGraph(pinned int32 CSR) -> build_sketched_graph(bloom, device) -> "
-                    "tc_estimate(bf_and): H2D of the CSR, device sketch build, device edge "
-                    "slots, fused kernel, histogram D2H, host combine",
+                    "tc_estimate(bf_and): H2D of the CSR in 8 vertex-range chunks (highest "
+                    "first), per-chunk device sketch build, per-chunk device edge slots and "
+                    "fused kernel as each chunk's sketches land, histogram D2H, host combine",
             "estimate": est}
 
 

@@ -94,9 +94,14 @@ class DeviceCsr:
         import torch
         cur = torch.cuda.current_stream()
         cs = side_stream("copy")
+        # the offsets go first (every chunk's build needs them), issued
+        # before the rest of the setup: the copy engine is the critical path
         self.offsets = torch.empty(self.n + 1, dtype=torch.int64, device="cuda")
-        self.adj = torch.empty(self.nnz, dtype=torch.int32, device="cuda")
         off_t = torch.from_numpy(np.ascontiguousarray(offsets, dtype=np.int64))
+        cs.wait_stream(cur)  # the new blocks may still be in use on cur
+        with torch.cuda.stream(cs):
+            self.offsets.copy_(off_t, non_blocking=True)
+        self.adj = torch.empty(self.nnz, dtype=torch.int32, device="cuda")
         # equal-volume chunks (tapered tails and per-chunk offsets slices
         # measured slower: each extra DMA + build launch costs more than the
         # shorter tail saves).  int64 needles: float needles would convert
@@ -105,9 +110,8 @@ class DeviceCsr:
         cuts = np.searchsorted(offsets, targets, side="left")
         cuts[0], cuts[-1] = 0, self.n
         cuts = np.unique(cuts)
-        cs.wait_stream(cur)  # the new blocks may still be in use on cur
+        cs.wait_stream(cur)
         with torch.cuda.stream(cs):
-            self.offsets.copy_(off_t, non_blocking=True)
             # highest vertex range first: once chunk c has landed, every
             # range above it is on the device, so a chunk's upper-triangle
             # edges (u < v) can be estimated as soon as its own sketches are
