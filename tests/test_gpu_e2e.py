@@ -139,3 +139,80 @@ def test_pair_many_index_rules_match_numpy():
         ex.pair_many(np.array([0]), np.array([4]))
     assert ex.pair_many(np.array([0]), np.array([-2])).tolist() == \
         ex.pair_many(np.array([0]), np.array([2])).tolist()
+
+
+@pytest.mark.parametrize("pad", [1, 2, 4, 8])
+@pytest.mark.parametrize("lower", [0, 1])
+def test_range_slots_append_matches_whole_layout(pad, lower):
+    """pg_csr_range_slots_append over consecutive vertex ranges (device
+    cursor, no host sync) reproduces the whole-graph padded layout range by
+    range; lower = 1 gives the mirrored (v < u) slots."""
+    import ctypes
+    import torch
+    import paper_2208_11469_b200 as pg
+    from paper_2208_11469_b200 import _native as N
+    g = pg.generate_kronecker(13, 16, 11)
+    dev = g.device()
+    off, adj = g.offsets, g.adjacency
+    # expected: rows in order, each row's upper (or lower) entries padded to pad
+    want_v, want_u = [], []
+    for u in range(g.n):
+        row = adj[off[u]:off[u + 1]]
+        part = row[row < u] if lower else row[row > u]
+        c = -(-len(part) // pad) * pad
+        want_v += list(part) + [-1] * (c - len(part))
+        want_u += [u] * (c // pad)
+    cuts = [0, 3, 100, 2000, 2001, 5000, g.n]
+    cap = g.offsets[-1] + (pad - 1) * g.n + pad
+    ug = torch.full((cap // pad + 1,), -7, dtype=torch.int32, device="cuda")
+    vs = torch.full((cap,), -7, dtype=torch.int32, device="cuda")
+    cursor = torch.zeros(2 + 2 * len(cuts), dtype=torch.int64, device="cuda")
+    for i, (v0, v1) in enumerate(zip(cuts[:-1], cuts[1:])):
+        bound = int(off[v1] - off[v0]) + (pad - 1) * (v1 - v0)
+        ws_bytes = ctypes.c_size_t()
+        N.call("pg_csr_range_slots_workspace", v1 - v0, bound, ctypes.byref(ws_bytes))
+        ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device="cuda")
+        N.call("pg_csr_range_slots_append", N.ptr(dev.offsets), N.ptr(dev.adj), v0, v1, pad, lower,
+               bound, N.ptr(ug), N.ptr(vs), cap, N.ptr(cursor), N.ptr(cursor) + 8 * (2 + 2 * i),
+               N.ptr(ws), ws_bytes.value, N.stream_handle())
+    c = cursor.cpu().numpy()
+    total = len(want_v)
+    assert c[0] == total and c[1] == 0
+    rng = c[2:2 + 2 * (len(cuts) - 1)].reshape(-1, 2)
+    assert rng[0, 0] == 0 and rng[-1, 1] == total and np.all(rng[1:, 0] == rng[:-1, 1])
+    assert np.array_equal(vs[:total].cpu().numpy(), np.array(want_v, dtype=np.int32))
+    assert np.array_equal(ug[:total // pad].cpu().numpy(), np.array(want_u, dtype=np.int32))
+
+
+def test_tc_bloom_range_accumulates_to_whole():
+    """pg_tc_bloom_range over appended ranges, accumulating, gives the
+    whole-graph pg_tc_bloom histogram (same integers)."""
+    import ctypes
+    import torch
+    import paper_2208_11469_b200 as pg
+    from paper_2208_11469_b200 import _native as N
+    g = pg.generate_kronecker(13, 16, 12)
+    sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=2, bits_override=1024)
+    p = pg.make_provider("bf_and", sketched=sk)
+    from paper_2208_11469_b200.mining import tc_counts
+    want = tc_counts(p, g.device()).cpu().numpy()
+    dev, d = g.device(), sk.device_tensors()
+    pad = p.tc_pad()
+    cuts = [0, 17, 900, 4000, g.n]
+    cap = g.offsets[-1] + (pad - 1) * g.n + pad
+    ug = torch.empty(cap // pad + 1, dtype=torch.int32, device="cuda")
+    vs = torch.empty(cap, dtype=torch.int32, device="cuda")
+    cursor = torch.zeros(2 + 2 * len(cuts), dtype=torch.int64, device="cuda")
+    out = torch.zeros(1024 + 2, dtype=torch.int64, device="cuda")
+    for i, (v0, v1) in enumerate(zip(cuts[:-1], cuts[1:])):
+        bound = int(g.offsets[v1] - g.offsets[v0]) + (pad - 1) * (v1 - v0)
+        ws_bytes = ctypes.c_size_t()
+        N.call("pg_csr_range_slots_workspace", v1 - v0, bound, ctypes.byref(ws_bytes))
+        ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device="cuda")
+        rng = N.ptr(cursor) + 8 * (2 + 2 * i)
+        N.call("pg_csr_range_slots_append", N.ptr(dev.offsets), N.ptr(dev.adj), v0, v1, pad, 0,
+               bound, N.ptr(ug), N.ptr(vs), cap, N.ptr(cursor), rng, N.ptr(ws), ws_bytes.value,
+               N.stream_handle())
+        N.call("pg_tc_bloom_range", N.ptr(d["rows"]), 1024, p.op, None, None, N.ptr(ug), N.ptr(vs),
+               rng, bound, 1, N.ptr(out), N.ptr(out) + 8 * 1025, N.stream_handle())
+    assert np.array_equal(out.cpu().numpy(), want)
