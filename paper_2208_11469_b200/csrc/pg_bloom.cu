@@ -43,7 +43,9 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_bloom_kernel(const uint4* row
   }
 }
 
-template <int W8, class Op, int MINB, bool kVCache, int kLayout>
+// kSched: 0 static per-warp slices, 1 dynamic chunks (ctr), 2 static slices
+// of the device-side range [range_dev[0], range_dev[1]) (appended slots)
+template <int W8, class Op, int MINB, bool kVCache, int kLayout, int kSched = 0>
 __global__ void __launch_bounds__(kBlock, MINB) tc_bloom_wide_kernel(const unsigned char* rows, int bits,
                                                                     const int32_t* us, const int32_t* vs,
                                                                     int64_t e_begin, int64_t e_end,
@@ -51,7 +53,7 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_bloom_wide_kernel(const unsig
                                                                     int64_t* out_sum_pos, unsigned long long* ctr,
                                                                     const int64_t* range_dev) {
   extern __shared__ int hist_s[];
-  if (range_dev) {  // [begin, end) computed on the device (appended slot ranges)
+  if (kSched == 2) {
     e_begin = range_dev[0];
     e_end = range_dev[1];
   }
@@ -59,7 +61,7 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_bloom_wide_kernel(const unsig
   __syncthreads();
   epi.hist_s = hist_s;
   epi.sum_pos = 0;
-  wide_edge_loop<W8, Op, EpiBloomHist, kVCache, kLayout>(rows, us, vs, e_begin, e_end, epi, ctr);
+  wide_edge_loop<W8, Op, EpiBloomHist, kVCache, kLayout, kSched == 1>(rows, us, vs, e_begin, e_end, epi, ctr);
   __syncthreads();
   for (int i = threadIdx.x; i <= bits; i += blockDim.x)
     if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_hist + i), (unsigned long long)hist_s[i]);
@@ -176,11 +178,15 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
     // dynamic chunks pay off on large edge sets (c4/c5: 3-5%); below ~32 M
     // slots the per-launch counter costs more than the balance gains
     ChunkCounter ctr;
-    if (dyn && e_end - e_begin >= kDynamicMinSlots && (le = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(le));
+    if (dyn && !range_dev && e_end - e_begin >= kDynamicMinSlots && (le = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(le));
 #define PG_W(W8, MB, VC, PD)                                                                          \
   {                                                                                                  \
     auto k = op == PG_BF_OR ? tc_bloom_wide_kernel<W8, OpOr, MB, VC, PD>                             \
                             : tc_bloom_wide_kernel<W8, OpAnd, MB, VC, PD>;                           \
+    if (range_dev) k = op == PG_BF_OR ? tc_bloom_wide_kernel<W8, OpOr, MB, VC, PD, 2>               \
+                                      : tc_bloom_wide_kernel<W8, OpAnd, MB, VC, PD, 2>;             \
+    else if (ctr.p) k = op == PG_BF_OR ? tc_bloom_wide_kernel<W8, OpOr, MB, VC, PD, 1>              \
+                                       : tc_bloom_wide_kernel<W8, OpAnd, MB, VC, PD, 1>;            \
     le = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
     if (le != cudaSuccess) return fail(PG_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(le));  \
     const int grid = grid_cap(grid_for_kernel(k, smem), e_end - e_begin, kBlock);                    \

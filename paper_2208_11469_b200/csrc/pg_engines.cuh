@@ -228,7 +228,7 @@ __device__ __forceinline__ void ldg256_keep(const void* p, uint32_t (&r)[8]) {
 // kLayout: 0 any edge list; 1 row-padded slots (every aligned group of G
 // slots shares one u; us[] per slot); 2 the same with us[] holding one u per
 // group (us[e / G]) -- a G-fold smaller u stream.
-template <int W8, class Op, class Epi, bool kVCache = false, int kLayout = 0>
+template <int W8, class Op, class Epi, bool kVCache = false, int kLayout = 0, bool kDyn = false>
 __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__ rows,
                                                const int32_t* __restrict__ us, const int32_t* __restrict__ vs,
                                                int64_t e_begin, int64_t e_end, Epi& epi,
@@ -246,12 +246,12 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
   for (int i = 0; i < V; ++i)
 #pragma unroll
     for (int w = 0; w < 8; ++w) ur[i][w] = 0;
-  // ranges: dynamic 512-slot chunks when the launcher passes a counter,
+  // ranges: dynamic 512-slot chunks (kDyn: the launcher passes a counter),
   // else one static per-warp slice (the cached u row survives chunk ends)
   int64_t wb, we;
   bool first = true;
   for (;;) {
-  if (ctr) {
+  if (kDyn) {
     if (!next_chunk(ctr, e_begin, e_end, 512, wb, we)) return;
   } else {
     if (!first) return;

@@ -15,7 +15,7 @@ __global__ void __launch_bounds__(kBlock) pairs_khash_kernel(const uint4* ent, i
 }
 
 // kEngine: 0 scalar fallback, 1 group (128-bit) engine, 2 wide padded engine
-template <int V, int G, int kEngine, int MINB = 1>
+template <int V, int G, int kEngine, int MINB = 1, bool kDyn = false>
 __global__ void __launch_bounds__(kBlock, MINB) tc_khash_kernel(const uint4* ent, int k, const int32_t* sizes,
                                                                const int32_t* us, const int32_t* vs,
                                                                int64_t e_begin, int64_t e_end,
@@ -28,8 +28,8 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_khash_kernel(const uint4* ent
   EpiMinhashHist epi{sizes, cnt_s, slo_s, shi_s};
   if (kEngine == 0) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
   else if (kEngine == 1) group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
-  else wide_edge_loop<V, OpEqPos, EpiMinhashHist, false, true>(reinterpret_cast<const unsigned char*>(ent), us,
-                                                                vs, e_begin, e_end, epi, ctr);
+  else wide_edge_loop<V, OpEqPos, EpiMinhashHist, false, true, kDyn>(reinterpret_cast<const unsigned char*>(ent),
+                                                                      us, vs, e_begin, e_end, epi, ctr);
   __syncthreads();
   for (int i = threadIdx.x; i <= k; i += blockDim.x) {
     if (cnt_s[i]) {
@@ -40,7 +40,7 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_khash_kernel(const uint4* ent
   }
 }
 
-template <int V, int G, int kEngine, int MINB = 1>
+template <int V, int G, int kEngine, int MINB = 1, bool kDyn = false>
 __global__ void __launch_bounds__(kBlock, MINB) jaccard_khash_kernel(const uint4* ent, int k, const int32_t* deg,
                                                                     const int32_t* us, const int32_t* vs,
                                                                     int64_t e_begin, int64_t e_end,
@@ -53,8 +53,8 @@ __global__ void __launch_bounds__(kBlock, MINB) jaccard_khash_kernel(const uint4
   EpiJaccard epi{k, min_matches, tau, deg, hist_s, 0, 0};
   if (kEngine == 0) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
   else if (kEngine == 1) group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
-  else wide_edge_loop<V, OpEqPos, EpiJaccard, false, true>(reinterpret_cast<const unsigned char*>(ent), us, vs,
-                                                            e_begin, e_end, epi, ctr);
+  else wide_edge_loop<V, OpEqPos, EpiJaccard, false, true, kDyn>(reinterpret_cast<const unsigned char*>(ent), us,
+                                                                  vs, e_begin, e_end, epi, ctr);
   __syncthreads();
   for (int i = threadIdx.x; i <= k; i += blockDim.x)
     if (hist_s[i]) atomicAdd(reinterpret_cast<unsigned long long*>(out_counts + 2 + i), (unsigned long long)hist_s[i]);
@@ -374,6 +374,7 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
 #define PG_KW(W8, MB)                                                                    \
   {                                                                                      \
     auto kern = tc_khash_kernel<W8, 1, 2, MB>;                                           \
+    if (e_end - e_begin >= kDynamicMinSlots) kern = tc_khash_kernel<W8, 1, 2, MB, true>; \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);        \
     ChunkCounter ctr;                                                                    \
     if (e_end - e_begin >= kDynamicMinSlots && (ce = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce)); \
@@ -417,6 +418,7 @@ int pg_jaccard_count_khash(const int32_t* entries, int32_t k, const int32_t* deg
 #define PG_JW(W8, MB)                                                                                  \
   {                                                                                                    \
     auto kern = jaccard_khash_kernel<W8, 1, 2, MB>;                                                    \
+    if (e_end - e_begin >= kDynamicMinSlots) kern = jaccard_khash_kernel<W8, 1, 2, MB, true>;          \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);                      \
     ChunkCounter ctr;                                                                                  \
     if (e_end - e_begin >= kDynamicMinSlots && (ce = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce)); \
