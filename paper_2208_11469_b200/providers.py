@@ -276,7 +276,8 @@ class BloomProvider(_SketchProvider):
                          / sg.hash_count)
         lut = swamidass_table(sg.bit_length, sg.hash_count)
         nz = np.nonzero(hist)[0]
-        weighted = math.fsum(float(hist[o]) * float(lut[o]) for o in nz)
+        # float(hist[o]) * lut[o] per bin (vectorised), exactly-rounded sum
+        weighted = math.fsum((hist[nz].astype(np.float64) * lut[nz]).tolist())
         if self.kind is EstimatorKind.BF_AND:
             return weighted
         return float(spos) - weighted

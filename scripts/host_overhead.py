@@ -34,9 +34,6 @@ for rep in range(4):
     sk = pg.build_sketched_graph(graph, "bloom", s=1.0, b=2, bits_override=1024)
     T["build"] = time.perf_counter() - t
     p = pg.make_provider("bf_and", sketched=sk)
-    t = time.perf_counter()
-    lay = p._tc_layout(dev)
-    T["layout(sync)"] = time.perf_counter() - t
     from paper_2208_11469_b200.mining import tc_counts
     t = time.perf_counter()
     c = tc_counts(p, dev)
