@@ -223,6 +223,148 @@ __global__ void __launch_bounds__(kBlock) onehash_sorted_kernel(const int32_t* e
 }
 
 // sorted-engine launchers; return false when k has no specialisation
+// ---------------------------------- 1-Hash, per-warp table, slot blocks
+// The row-padded slot layout with pad E = 256/k (pg_csr_upper_edges_padded)
+// gives every warp iteration E edges of one u, so the u table is one per
+// warp (built by all 32 lanes: k/32 IDs each, against k/8 per lane in the
+// per-group engine, and a quarter of its shared memory) and survives across
+// the whole u run.  Slot blocks as in the KMV rank engine: lane l holds slot
+// l's endpoints one block ahead; after each 32-slot block every lane files
+// its slot's statistics.  Same bucket table and probe as htab_edge_loop.
+template <int K>
+struct alignas(16) OnehashWarp {
+  int32_t tab[4 * K];  // K buckets x 4 slots
+  int32_t stash[K];
+  int32_t mbuf[32];    // per slot of the block: matches
+  int sc;
+};
+
+template <int K>
+__global__ void __launch_bounds__(kBlock, 5) onehash_block_kernel(const int32_t* __restrict__ R,
+                                                               const int32_t* __restrict__ sizes,
+                                                               const int32_t* __restrict__ us,
+                                                               const int32_t* __restrict__ vs, int64_t e_begin,
+                                                               int64_t e_end, int64_t* out_cnt, int64_t* out_ssum,
+                                                               int64_t* out_verbatim, unsigned long long* ctr) {
+  constexpr int P = 8, G = K / P, E = 32 / G, IT = 32 / E;
+  constexpr int64_t kChunk = 512;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ int cnt_s[K + 1];
+  __shared__ unsigned slo_s[K + 1], shi_s[K + 1];
+  for (int i = threadIdx.x; i <= K; i += blockDim.x) { cnt_s[i] = 0; slo_s[i] = 0; shi_s[i] = 0; }
+  __syncthreads();
+  OnehashWarp<K>& W = reinterpret_cast<OnehashWarp<K>*>(smem_raw)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
+  EpiOnehash epi{K, sizes, nullptr, nullptr, cnt_s, slo_s, shi_s, 0};
+  int32_t cur_u = -1;
+  int sc = 0;
+  int64_t wb, we;
+  while (next_chunk(ctr, e_begin, e_end, kChunk, wb, we)) {
+    int32_t ul = 0, vl = -1;
+    if (wb + lane < we) {
+      ul = us[wb + lane];
+      vl = vs[wb + lane];
+    }
+    int32_t sul = sizes[ul], svl = vl >= 0 ? sizes[vl] : 0;
+    int32_t vq = __shfl_sync(0xffffffffu, vl, grp);
+    uint32_t x[P];
+    ldg_rowpart<P>(R + (int64_t)(vq < 0 ? 0 : vq) * K + gl * P, x);
+#pragma unroll 1
+    for (int64_t b0 = wb; b0 < we; b0 += 32) {
+      int32_t un = 0, vn = -1, sun = 0, svn = 0;
+      if (b0 + 32 + lane < we) {
+        un = us[b0 + 32 + lane];
+        vn = vs[b0 + 32 + lane];
+      }
+#pragma unroll 1
+      for (int it = 0; it < IT; ++it) {
+        const int slot = it * E + grp;
+        const int32_t u = __shfl_sync(0xffffffffu, ul, it * E);
+        const bool valid = b0 + slot < we && vq >= 0;
+        if (it == IT / 2) {  // the next block's sizes, off the critical path
+          sun = sizes[un];
+          svn = vn >= 0 ? sizes[vn] : 0;
+        }
+        if (u != cur_u) {  // warp-uniform: rebuild the warp's table
+          cur_u = u;
+          int32_t y[K / 32];
+#pragma unroll
+          for (int q = 0; q < K / 32; ++q) y[q] = __ldg(R + (int64_t)u * K + lane + 32 * q);
+          int4* T4 = reinterpret_cast<int4*>(W.tab);
+#pragma unroll
+          for (int i = lane; i < K; i += 32) T4[i] = make_int4(-1, -1, -1, -1);
+          if (lane == 0) W.sc = 0;
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < K / 32; ++q) {
+            if (y[q] < 0) continue;  // -1 pad
+            int32_t* bk = W.tab + 4 * htab_bucket<K>(y[q]);
+            bool placed = false;
+#pragma unroll
+            for (int sl = 0; sl < 4 && !placed; ++sl) placed = atomicCAS(bk + sl, -1, y[q]) == -1;
+            if (!placed) W.stash[atomicAdd(&W.sc, 1)] = y[q];
+          }
+          __syncwarp();
+          sc = *reinterpret_cast<volatile int*>(&W.sc);
+        }
+        const int32_t vqn = __shfl_sync(0xffffffffu, it + 1 < IT ? vl : vn, it + 1 < IT ? slot + E : grp);
+        uint32_t xn[P];
+        ldg_rowpart<P>(R + (int64_t)(vqn < 0 ? 0 : vqn) * K + gl * P, xn);
+        int m = 0;
+#pragma unroll
+        for (int p = 0; p < P; ++p) {
+          const int32_t q = (int32_t)x[p];
+          if (valid && q >= 0) {
+            const int4 bk = reinterpret_cast<const int4*>(W.tab)[htab_bucket<K>(q)];
+            bool hit = (bk.x == q) | (bk.y == q) | (bk.z == q) | (bk.w == q);
+            for (int i = 0; i < sc; ++i) hit |= W.stash[i] == q;
+            m += hit;
+          }
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+        if (gl == 0) W.mbuf[slot] = m;
+#pragma unroll
+        for (int p = 0; p < P; ++p) x[p] = xn[p];
+        vq = vqn;
+      }
+      __syncwarp();
+      if (b0 + lane < we && vl >= 0) epi.edge_sized(b0 + lane, sul, svl, W.mbuf[lane], 0, 0);
+      __syncwarp();
+      ul = un;
+      vl = vn;
+      sul = sun;
+      svl = svn;
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i <= K; i += blockDim.x) {
+    if (cnt_s[i]) {
+      atomicAdd(reinterpret_cast<unsigned long long*>(out_cnt + i), (unsigned long long)cnt_s[i]);
+      atomicAdd(reinterpret_cast<unsigned long long*>(out_ssum + i), ((unsigned long long)shi_s[i] << 32) + slo_s[i]);
+    }
+  }
+  long long vb = epi.verb;
+  for (int o = 16; o > 0; o >>= 1) vb += __shfl_xor_sync(0xffffffffu, vb, o);
+  if ((threadIdx.x & 31) == 0 && vb)
+    atomicAdd(reinterpret_cast<unsigned long long*>(out_verbatim), (unsigned long long)vb);
+}
+
+template <int K>
+static int launch_onehash_block(cudaStream_t s, const int32_t* ent, const int32_t* sizes, const int32_t* us,
+                                const int32_t* vs, int64_t b, int64_t e, int64_t* out_cnt, int64_t* out_ssum,
+                                int64_t* out_verbatim) {
+  auto kern = onehash_block_kernel<K>;
+  const size_t sm = sizeof(OnehashWarp<K>) * (kBlock / 32);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / 8));
+  ChunkCounter ctr;
+  const cudaError_t ce = ctr.init(s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce));
+  kern<<<grid, kBlock, sm, s>>>(ent, sizes, us, vs, b, e, out_cnt, out_ssum, out_verbatim, ctr.p);
+  return check_launch("tc_onehash_block");
+}
+
 template <int G, int CH, bool kFused>
 static void launch_onehash_sorted(cudaStream_t s, const int32_t* ent, int k, const int32_t* sizes,
                                   const int32_t* us, const int32_t* vs, int64_t b, int64_t e,
@@ -350,6 +492,13 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
   if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
   PG_REQUIRE(entries && us && vs && sizes, "null pointer");
+  if (onehash && padded && (k == 32 || k == 64 || k == 128)) {
+    // the row-padded layout of pad 256/k: one u per warp iteration
+    PG_REQUIRE(e_begin % (256 / k) == 0, "e_begin must be a multiple of the layout pad %d", 256 / k);
+    if (k == 32) return launch_onehash_block<32>(s, entries, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim);
+    if (k == 64) return launch_onehash_block<64>(s, entries, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim);
+    return launch_onehash_block<128>(s, entries, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim);
+  }
   if (onehash && onehash_sorted(s, true, entries, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, out_cnt,
                                 out_ssum, out_verbatim))
     return check_launch("tc_onehash_sorted");

@@ -318,7 +318,10 @@ class MinHashProvider(_SketchProvider):
         return self.kind is EstimatorKind.ONEHASH
 
     def tc_pad(self) -> int:
-        return 1 if self.onehash else N.group_pad(4 * self.sketched.capacity)
+        k = self.sketched.capacity
+        if self.onehash:  # per-warp-table engine: one u per 256/k slots
+            return 256 // k if k in (32, 64, 128) else 1
+        return N.group_pad(4 * k)
 
     def _pairs_device(self, us, vs):
         import torch
