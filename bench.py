@@ -139,12 +139,12 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(config: str):
-    """dram bytes per launch of the TC kernel from the committed ncu summary."""
+def load_traffic(config: str, key: str = "dram_bytes_per_launch"):
+    """Per-launch bytes of the TC kernel from the committed ncu summary."""
     path = os.path.join(REPO, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(config, {}).get("dram_bytes_per_launch")
+            return json.load(fh).get(config, {}).get(key)
     except Exception:
         return None
 
@@ -320,7 +320,11 @@ def run_ours(args, cfg, rank, world, local):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "bytes_per_edge": bytes_per_edge, "kernel_ms": kern_ms_avg,
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         # physical picture from the same ncu capture: bytes the
+                         # L2 delivered to the SMs per launch (u rows stay in
+                         # registers across u runs; traffic = what L2 missed)
+                         "l2_to_sm_bytes": load_traffic(args.config, "l2_to_sm_bytes") if world == 1 else None},
             "clocks": clk.summary(),
             "gpu_launches": args.steps,
             "cuda_graph": graph_note or "one graph replay per step",
