@@ -155,10 +155,15 @@ def load_traffic(config: str, key: str = "dram_bytes_per_launch"):
 
 def run_ours(args, cfg, rank, world, local):
     import torch
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # PG_BENCH_BACKEND=gloo: a functional check of the sharded path with
+        # several ranks on one GPU (host-side all-reduce; not a measurement)
+        backend = os.environ.get("PG_BENCH_BACKEND", "nccl")
+        dist.init_process_group(backend, **({"device_id": torch.device("cuda", local)}
+                                            if backend == "nccl" else {}))
     import paper_2208_11469_b200 as pg
     from paper_2208_11469_b200 import _native as N
     from paper_2208_11469_b200.sharding import allreduce_counts, edge_range
