@@ -194,6 +194,10 @@ PG_API int pg_tc_bloom_range(const uint64_t* rows, int32_t bits, int32_t op,
                       const int32_t* vs, const int64_t* range_dev, int64_t max_slots,
                       int32_t accumulate, int64_t* out_hist, int64_t* out_sum_pos,
                       void* stream);
+/* slot pad of the 1-Hash per-warp-table TC engine for k (the layout pad
+ * pg_tc_minhash expects with onehash = 1 and padded = 1; 1 = no such engine
+ * for k, padded slots are then not needed) */
+PG_API int pg_onehash_block_pad(int32_t k, int32_t* pad_host);
 /* k-/1-Hash TC: out_cnt[m], out_ssum[m] (m = 0..k): number of edges and
  * int64 sum of (s_u+s_v) of non-verbatim edges with m matches;
  * out_verbatim[0] = sum of matches over verbatim 1-Hash edges. */

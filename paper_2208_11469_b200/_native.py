@@ -72,6 +72,7 @@ SIGNATURES = {
     "pg_tc_kmv": [c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64, c_i64,
                   c_ptr, c_ptr],
     "pg_kmv_ranked_pad": [c_i32, ctypes.POINTER(c_i32)],
+    "pg_onehash_block_pad": [c_i32, ctypes.POINTER(c_i32)],
     "pg_tc_kmv_ranked": [c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
                          c_i64, c_ptr, c_ptr],
     "pg_jaccard_count_khash": [c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
@@ -184,6 +185,13 @@ def kmv_ranked_pad(k: int) -> int:
     """Slot pad of the rank-directory KMV engine for k (0: no such engine)."""
     pad = ctypes.c_int32()
     check(load_library().pg_kmv_ranked_pad(int(k), ctypes.byref(pad)), "pg_kmv_ranked_pad")
+    return pad.value
+
+
+def onehash_block_pad(k: int) -> int:
+    """Slot pad of the per-warp-table 1-Hash TC engine for k (1: none)."""
+    pad = ctypes.c_int32()
+    check(load_library().pg_onehash_block_pad(int(k), ctypes.byref(pad)), "pg_onehash_block_pad")
     return pad.value
 
 

@@ -231,6 +231,11 @@ __global__ void __launch_bounds__(kBlock) onehash_sorted_kernel(const int32_t* e
 // the whole u run.  Slot blocks as in the KMV rank engine: lane l holds slot
 // l's endpoints one block ahead; after each 32-slot block every lane files
 // its slot's statistics.  Same bucket table and probe as htab_edge_loop.
+#ifndef PG_OH_PER_LANE
+#define PG_OH_PER_LANE 8
+#endif
+constexpr int kOnehashPerLane = PG_OH_PER_LANE;  // v-row IDs per lane (pad = 32 * this / k)
+
 template <int K>
 struct alignas(16) OnehashWarp {
   int32_t tab[4 * K];  // K buckets x 4 slots
@@ -246,7 +251,7 @@ __global__ void __launch_bounds__(kBlock, 5) onehash_block_kernel(const int32_t*
                                                                const int32_t* __restrict__ vs, int64_t e_begin,
                                                                int64_t e_end, int64_t* out_cnt, int64_t* out_ssum,
                                                                int64_t* out_verbatim, unsigned long long* ctr) {
-  constexpr int P = 8, G = K / P, E = 32 / G, IT = 32 / E;
+  constexpr int P = kOnehashPerLane, G = K / P, E = 32 / G, IT = 32 / E;
   constexpr int64_t kChunk = 512;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ int cnt_s[K + 1];
@@ -357,7 +362,7 @@ static int launch_onehash_block(cudaStream_t s, const int32_t* ent, const int32_
   auto kern = onehash_block_kernel<K>;
   const size_t sm = sizeof(OnehashWarp<K>) * (kBlock / 32);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / 8));
+  const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / kOnehashPerLane));
   ChunkCounter ctr;
   const cudaError_t ce = ctr.init(s);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce));
@@ -476,6 +481,12 @@ int pg_pairs_minhash(const int32_t* entries, int32_t k, int32_t onehash, const i
   return check_launch("pairs_khash");
 }
 
+int pg_onehash_block_pad(int32_t k, int32_t* pad_host) {
+  PG_REQUIRE(pad_host, "null output");
+  *pad_host = (k == 32 || k == 64 || k == 128) ? 32 * kOnehashPerLane / k : 1;
+  return PG_OK;
+}
+
 int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int32_t* sizes,
                   const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end, int32_t padded,
                   int64_t* out_cnt, int64_t* out_ssum, int64_t* out_verbatim, void* stream) {
@@ -493,8 +504,9 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
   if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
   PG_REQUIRE(entries && us && vs && sizes, "null pointer");
   if (onehash && padded && (k == 32 || k == 64 || k == 128)) {
-    // the row-padded layout of pad 256/k: one u per warp iteration
-    PG_REQUIRE(e_begin % (256 / k) == 0, "e_begin must be a multiple of the layout pad %d", 256 / k);
+    // the row-padded layout of pad 32 * kOnehashPerLane / k: one u per warp iteration
+    const int pad = 32 * kOnehashPerLane / k;
+    PG_REQUIRE(e_begin % pad == 0, "e_begin must be a multiple of the layout pad %d", pad);
     if (k == 32) return launch_onehash_block<32>(s, entries, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim);
     if (k == 64) return launch_onehash_block<64>(s, entries, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim);
     return launch_onehash_block<128>(s, entries, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim);

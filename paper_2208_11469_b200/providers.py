@@ -319,8 +319,8 @@ class MinHashProvider(_SketchProvider):
 
     def tc_pad(self) -> int:
         k = self.sketched.capacity
-        if self.onehash:  # per-warp-table engine: one u per 256/k slots
-            return 256 // k if k in (32, 64, 128) else 1
+        if self.onehash:  # per-warp-table engine: one u per warp iteration
+            return N.onehash_block_pad(k)
         return N.group_pad(4 * k)
 
     def _pairs_device(self, us, vs):

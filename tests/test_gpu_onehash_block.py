@@ -37,7 +37,7 @@ def test_onehash_block_tc_vs_oracle(pg, k):
         ent, ln = O.C.build_onehash(g.offsets, g.adjacency, k)
         assert np.array_equal(sk.entries, ent) and np.array_equal(sk.lengths, ln)
         p = pg.make_provider("onehash", sketched=sk)
-        assert p.tc_pad() == 256 // k
+        assert p.tc_pad() == N.onehash_block_pad(k)
         counts = tc_counts(p, g.device()).cpu().numpy()
         e = g.edges()
         m = O.C.pairs_minhash(ent, k, True, e[:, 0], e[:, 1])
