@@ -448,8 +448,14 @@ def run_secondary():
                                    reps=1, flush=flush)
             p = pg.make_provider(kind, sketched=sk)
             ms, c = _time_device(lambda: tc_counts(p, g.device()), reps=3, flush=flush)
-            r = rec("R-MAT s22 ef16 seed 2", g, ms, bpe,
-                    {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0, "build_ms": bms})
+            extra = {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0, "build_ms": bms}
+            if kind == "kmv":
+                # the rank-directory kernel reads 4-byte global value ranks,
+                # not the 8-byte values the algorithmic figure counts
+                kb = 2 * 4 * 64 + 24
+                extra.update(kernel_bytes_per_edge=kb,
+                             frac_at_kernel_bytes=g.m * kb / (ms / 1e3) / 1e9 / peak)
+            r = rec("R-MAT s22 ef16 seed 2", g, ms, bpe, extra)
             sz = sk.sizes
             if kind == "onehash":
                 ent = sk.entries
