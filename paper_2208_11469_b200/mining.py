@@ -125,7 +125,7 @@ def _tc_counts_chunked(provider, dev):
     cur = torch.cuda.current_stream()
     ls, ts = side_stream("layout"), side_stream("tc")
     chunks = sg._chunk_ready
-    cap = dev.nnz + (pad - 1) * dev.n + pad  # lower entries <= nnz: no overflow
+    cap = dev.nnz + (pad - 1) * dev.n + pad  # upper entries <= nnz: never overflows
     nnz_of = {(v0, v1): b - a for v0, v1, a, b in dev.chunk_bounds}
 
     def bound(v0, v1):  # host bound on a range's padded slots
