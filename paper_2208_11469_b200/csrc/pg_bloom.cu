@@ -176,7 +176,10 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
       return !(v && v[0] == '0');
     }();
     // dynamic chunks pay off on large edge sets (c4/c5: 3-5%); below ~32 M
-    // slots the per-launch counter costs more than the balance gains
+    // slots the per-launch counter costs more than the balance gains.  The
+    // dynamic variant of the 256-byte-row kernel fits 3 CTAs/SM in 80
+    // registers without spills (c5: 5.48 vs 6.09 ms at 2 CTAs/SM); the static
+    // one spills 216 bytes there and keeps 2
     ChunkCounter ctr;
     if (dyn && !range_dev && e_end - e_begin >= kDynamicMinSlots && (le = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(le));
 #define PG_W(W8, MB, VC, PD)                                                                          \
@@ -195,7 +198,7 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
   }
 #define PG_WM(W8)                                                                  \
   if (padded == 2) {                                                             \
-    if (vcache) { if (minb <= 2) PG_W(W8, 2, true, 2) else PG_W(W8, 3, true, 2) } \
+    if (vcache) { if (minb <= 2 && !ctr.p) PG_W(W8, 2, true, 2) else PG_W(W8, 3, true, 2) } \
     else if (minb <= 2) PG_W(W8, 2, false, 2)                                    \
     else PG_W(W8, 3, false, 2)                                                   \
   } else if (padded) {                                                           \

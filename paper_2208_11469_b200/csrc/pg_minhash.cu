@@ -14,6 +14,11 @@ __global__ void __launch_bounds__(kBlock) pairs_khash_kernel(const uint4* ent, i
   else group_edge_loop<V, G, OpEqPos>(ent, us, vs, 0, count, epi);
 }
 
+// CTAs/SM of the wide k-Hash engine for 128-byte rows (k = 32): 4 (64
+// registers) measured 3.70 vs 4.04 ms at c4 over 3 -- the random row gathers
+// are latency-bound, more warps in flight win
+constexpr int kKhash128Minb = 4;
+
 // kEngine: 0 scalar fallback, 1 group (128-bit) engine, 2 wide padded engine
 template <int V, int G, int kEngine, int MINB = 1, bool kDyn = false>
 __global__ void __launch_bounds__(kBlock, MINB) tc_khash_kernel(const uint4* ent, int k, const int32_t* sizes,
@@ -541,7 +546,7 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
     if (e_end - e_begin >= kDynamicMinSlots && (ce = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce)); \
     kern<<<grid, kBlock, 0, s>>>(e4, k, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, ctr.p); \
   }
-    if (w8 == 2) PG_KW(2, 3) else if (w8 == 4) PG_KW(4, 3) else PG_KW(8, 3)  // measured: 3 blocks beat the spill-free 2 (0.66 vs 0.72 ms, s20 k=64)
+    if (w8 == 2) PG_KW(2, 3) else if (w8 == 4) PG_KW(4, kKhash128Minb) else PG_KW(8, 3)  // measured: 3 blocks beat the spill-free 2 (0.66 vs 0.72 ms, s20 k=64)
 #undef PG_KW
   } else if (!fast_w4(w4)) {
     auto kern = tc_khash_kernel<1, 1, 0>;
@@ -585,7 +590,7 @@ int pg_jaccard_count_khash(const int32_t* entries, int32_t k, const int32_t* deg
     if (e_end - e_begin >= kDynamicMinSlots && (ce = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce)); \
     kern<<<grid, kBlock, 0, s>>>(e4, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts, ctr.p); \
   }
-    if (w8 == 2) PG_JW(2, 3) else if (w8 == 4) PG_JW(4, 3) else PG_JW(8, 2)  // 256-B rows: 2 blocks (no spills)
+    if (w8 == 2) PG_JW(2, 3) else if (w8 == 4) PG_JW(4, kKhash128Minb) else PG_JW(8, 2)  // 256-B rows: 2 blocks (no spills)
 #undef PG_JW
   } else if (!fast_w4(w4)) {
     auto kern = jaccard_khash_kernel<1, 1, 0>;
