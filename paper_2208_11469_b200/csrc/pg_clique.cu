@@ -133,6 +133,9 @@ __global__ void __launch_bounds__(kBlock) clique4_bloom_kernel(
 // processed 32/G at a time: G lanes per member, one 256-bit load of BF+(w)
 // each, popcount of AND (OR) with the slice, G-lane reduction.  Edges whose
 // shorter list exceeds kC4Cap take the global path.
+#ifndef PG_C4_MINB
+#define PG_C4_MINB 5  // 46 registers, no spills: 5.23 vs 5.39 ms at c5b (shared memory also caps at 5)
+#endif
 constexpr int kC4Cap = 512;
 
 __device__ __forceinline__ bool smem_contains(const int32_t* a, int len, int32_t x) {
@@ -146,7 +149,7 @@ __device__ __forceinline__ bool smem_contains(const int32_t* a, int len, int32_t
 }
 
 template <int G>
-__global__ void __launch_bounds__(kBlock) clique4_bloom_staged_kernel(
+__global__ void __launch_bounds__(kBlock, PG_C4_MINB) clique4_bloom_staged_kernel(
     const int64_t* __restrict__ off, const int32_t* __restrict__ adjp, const int32_t* __restrict__ src,
     int64_t e_begin, int64_t e_end, const uint64_t* __restrict__ rows, int b,
     const uint64_t* __restrict__ seeds_dev, int op, const int32_t* __restrict__ sizes,
