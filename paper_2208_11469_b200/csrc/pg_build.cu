@@ -47,6 +47,9 @@ __device__ __forceinline__ uint32_t bloom_pos(uint64_t w, uint32_t bits) {
 // in the batch's degree prefix (monotone per lane), and OR its b bits into
 // that vertex's row in shared memory; the R rows are then one contiguous block
 // of the output.  Vertices with d > kHubBloom are left to pass 2.
+#ifndef PG_BB_MINB
+#define PG_BB_MINB 6  // 40 registers: whole s20 build 327 -> 311 us
+#endif
 constexpr int64_t kHubBloom = 1024;
 constexpr int64_t kMidBloom = 64;  // rows above this take pass 1b (a warp each)
 
@@ -56,7 +59,7 @@ struct BloomBatchSmem {
 };
 
 template <bool kPow2>
-__global__ void __launch_bounds__(kThreads) build_bloom_kernel(
+__global__ void __launch_bounds__(kThreads, PG_BB_MINB) build_bloom_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n,
     uint32_t bits, int b, int R, const uint64_t* __restrict__ seeds_dev,
     uint64_t* __restrict__ rows, int32_t* __restrict__ ones, int32_t* __restrict__ hubs,
@@ -137,7 +140,7 @@ __global__ void __launch_bounds__(kThreads) build_bloom_kernel(
 // (17% active warps).  The row is built in the warp's shared-memory slot and
 // written whole (pass 1 wrote it as zeros).
 template <bool kPow2>
-__global__ void __launch_bounds__(kThreads) build_bloom_mid_kernel(
+__global__ void __launch_bounds__(kThreads, PG_BB_MINB) build_bloom_mid_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, uint32_t bits, int b,
     const uint64_t* __restrict__ seeds_dev, uint64_t* __restrict__ rows, int32_t* __restrict__ ones,
     const int32_t* __restrict__ mids, const int32_t* __restrict__ mid_count, int32_t* __restrict__ mid_work) {
