@@ -134,7 +134,8 @@ __global__ void __launch_bounds__(kThreads, PG_BB_MINB) build_bloom_kernel(
   }
 }
 
-// pass 1b: mid-degree vertices (kMidBloom < d <= kHubBloom), one warp each,
+// pass 1b: mid-degree vertices (kMidBloom < d <= kHubBloom), one warp each
+// (the grid is sized for a warp per vertex of the range, not per batch),
 // taken from a counter: a 32-vertex batch of such rows would hold up to 32K
 // entries on one warp, and that tail set the duration of every chunked build
 // (17% active warps).  The row is built in the warp's shared-memory slot and
@@ -807,7 +808,7 @@ int pg_build_bloom(const int64_t* offsets, const int32_t* adj, int64_t n, int32_
                                                         hubs.mid_count);                                \
     cudaFuncSetAttribute(build_bloom_mid_kernel<P2>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
                          (int)smem_mid);                                                                \
-    build_bloom_mid_kernel<P2><<<grid_for(build_bloom_mid_kernel<P2>, smem_mid, n), kThreads, smem_mid, s>>>( \
+    build_bloom_mid_kernel<P2><<<grid_for(build_bloom_mid_kernel<P2>, smem_mid, 32 * (int64_t)n), kThreads, smem_mid, s>>>( \
         offsets, adj, bits, b, seeds_dev, rows, ones, hubs.mids, hubs.mid_count, hubs.mid_work);        \
     build_bloom_hubs_kernel<P2><<<hub_grid(), kThreads, smem_hub, s>>>(offsets, adj, bits, b, seeds_dev,  \
                                                                        rows, hubs.ids, hubs.count);       \
