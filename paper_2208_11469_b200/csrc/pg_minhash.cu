@@ -18,6 +18,10 @@ __global__ void __launch_bounds__(kBlock) pairs_khash_kernel(const uint4* ent, i
 // registers) measured 3.70 vs 4.04 ms at c4 over 3 -- the random row gathers
 // are latency-bound, more warps in flight win
 constexpr int kKhash128Minb = 4;
+#ifndef PG_KHASH_VCACHE
+#define PG_KHASH_VCACHE 0
+#endif
+constexpr bool kKhashVCache = PG_KHASH_VCACHE;  // L1-allocated v rows in the wide k-Hash engine
 
 // kEngine: 0 scalar fallback, 1 group (128-bit) engine, 2 wide padded engine
 template <int V, int G, int kEngine, int MINB = 1, bool kDyn = false>
@@ -33,7 +37,7 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_khash_kernel(const uint4* ent
   EpiMinhashHist epi{sizes, cnt_s, slo_s, shi_s};
   if (kEngine == 0) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
   else if (kEngine == 1) group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
-  else wide_edge_loop<V, OpEqPos, EpiMinhashHist, false, true, kDyn>(reinterpret_cast<const unsigned char*>(ent),
+  else wide_edge_loop<V, OpEqPos, EpiMinhashHist, kKhashVCache, true, kDyn>(reinterpret_cast<const unsigned char*>(ent),
                                                                       us, vs, e_begin, e_end, epi, ctr);
   __syncthreads();
   for (int i = threadIdx.x; i <= k; i += blockDim.x) {
@@ -58,7 +62,7 @@ __global__ void __launch_bounds__(kBlock, MINB) jaccard_khash_kernel(const uint4
   EpiJaccard epi{k, min_matches, tau, deg, hist_s, 0, 0};
   if (kEngine == 0) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
   else if (kEngine == 1) group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
-  else wide_edge_loop<V, OpEqPos, EpiJaccard, false, true, kDyn>(reinterpret_cast<const unsigned char*>(ent), us,
+  else wide_edge_loop<V, OpEqPos, EpiJaccard, kKhashVCache, true, kDyn>(reinterpret_cast<const unsigned char*>(ent), us,
                                                                   vs, e_begin, e_end, epi, ctr);
   __syncthreads();
   for (int i = threadIdx.x; i <= k; i += blockDim.x)
