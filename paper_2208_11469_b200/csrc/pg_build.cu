@@ -578,6 +578,84 @@ __device__ __forceinline__ void bottomk_emit(const WarpBottomK<P, kMode != 0>& L
   if (lane == 0) lengths[v] = cnt;
 }
 
+// KMV row of d <= 32 R neighbours (R = 1, 2): element i = lane + 32 r of a
+// 32R-key warp bitonic sort (pad keys ~0 sort last), then the distinct keys
+// in order (key i kept when it differs from key i-1), the first k written:
+// values ascending, +inf pad; mode 2 also the rank row.  Rows shorter than
+// kShortSortMin keep the list insertions (cheaper below ~a dozen keys).
+constexpr int kShortSortMin = 12;
+
+template <int kMode, int R>
+__device__ __forceinline__ void kmv_short_row_r(const int32_t* __restrict__ row, int d, int64_t v, int k,
+                                                uint64_t seed0, double* __restrict__ values,
+                                                int32_t* __restrict__ lengths, const BottomKRank& rk) {
+  const int lane = lane_id();
+  uint64_t key[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = lane + 32 * r;
+    key[r] = i < d ? bottomk_key<kMode>(seed0, row[i], rk) : ~0ull;
+  }
+#pragma unroll
+  for (int size = 2; size <= 32 * R; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      uint64_t old[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) old[r] = key[r];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        const bool up = (i & size) == 0;  // ascending block
+        const uint64_t other = stride == 32 ? old[r ^ 1] : shfl64(old[r], lane ^ stride);
+        const bool lower = (i & stride) == 0;
+        const uint64_t mn = old[r] < other ? old[r] : other, mx = old[r] < other ? other : old[r];
+        key[r] = (lower == up) ? mn : mx;
+      }
+    }
+  }
+  const unsigned lt = (1u << lane) - 1u;
+  int before = 0, total = 0;
+  uint64_t carry = ~0ull;  // key 32 r - 1 (the last of the previous register)
+  bool keep[R];
+  int pos[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const uint64_t prev = shfl_up64(key[r], 1);
+    keep[r] = key[r] != ~0ull && key[r] != (lane == 0 ? (r ? carry : ~0ull) : prev);
+    const unsigned b = __ballot_sync(0xffffffffu, keep[r]);
+    pos[r] = before + __popc(b & lt);
+    before += __popc(b);
+    carry = shfl64(key[r], 31);
+  }
+  total = before;
+  const int cnt = min(total, k);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (keep[r] && pos[r] < k) {
+      if (kMode == 2) {
+        values[v * k + pos[r]] = __ldg(rk.rank_values + (uint32_t)key[r]);
+        rk.ranks[v * k + pos[r]] = (int32_t)key[r];
+      } else {
+        values[v * k + pos[r]] = bitsd(key[r]);
+      }
+    }
+  }
+  for (int i = cnt + lane; i < k; i += 32) {
+    values[v * k + i] = bitsd(kInfBits);
+    if (kMode == 2) rk.ranks[v * k + i] = INT32_MAX;
+  }
+  if (lane == 0) lengths[v] = cnt;
+}
+
+template <int kMode>
+__device__ __forceinline__ void kmv_short_row(const int32_t* __restrict__ row, int d, int64_t v, int k,
+                                              uint64_t seed0, double* __restrict__ values,
+                                              int32_t* __restrict__ lengths, const BottomKRank& rk) {
+  if (d <= 32) kmv_short_row_r<kMode, 1>(row, d, v, k, seed0, values, lengths, rk);
+  else kmv_short_row_r<kMode, 2>(row, d, v, k, seed0, values, lengths, rk);
+}
+
 template <int P, int kMode>
 __global__ void __launch_bounds__(kThreads) build_bottomk_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n, int k,
@@ -612,6 +690,13 @@ __global__ void __launch_bounds__(kThreads) build_bottomk_kernel(
         // every neighbour is kept and the CSR row is already ID-sorted
         for (int j = lane; j < k; j += 32) entries[v * k + j] = j < d ? adj[o + j] : -1;
         if (lane == 0) lengths[v] = (int32_t)d;
+        continue;
+      }
+      if (kMode != 0 && d > kShortSortMin && d <= 64) {
+        // KMV rows of at most 64 neighbours: one warp bitonic sort of the
+        // keys, first copies of equal keys kept (the reference's distinct
+        // values), the first k written -- instead of d list insertions
+        kmv_short_row<kMode>(adj + o, (int)d, v, k, seed0, values, lengths, rk);
         continue;
       }
       WarpBottomK<P, kKmv> L;
