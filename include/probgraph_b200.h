@@ -303,6 +303,11 @@ PG_API int pg_rank_top_hits(const uint64_t* keys, const double* scores,
 
 /* exact |N(u) & N(v)| per pair over a sorted CSR (providers.py:102-115
  * ExactProvider.pair_many; setops.py:23-51) */
+/* sum over the edges (us[e], vs[e]) of |N(u) & N(v)| in the CSR -- the
+ * exact triangle count of a degree-ordered view (mining.py:88-102
+ * triangle_count with the exact provider) without per-edge outputs */
+PG_API int pg_tc_exact(const int64_t* offsets, const int32_t* adj, const int32_t* us,
+                const int32_t* vs, int64_t count, int64_t* out_sum, void* stream);
 PG_API int pg_pairs_exact(const int64_t* offsets, const int32_t* adj,
                    const int32_t* us, const int32_t* vs, int64_t count,
                    int64_t* out_count, void* stream);

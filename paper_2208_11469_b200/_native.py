@@ -85,6 +85,7 @@ SIGNATURES = {
                                c_ptr, c_ptr],
     "pg_4clique_exact": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr],
     "pg_pairs_exact": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
+    "pg_tc_exact": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
     "pg_two_hop_candidates": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, ctypes.POINTER(c_i64),
                               c_ptr],
     "pg_similarity_scores": [c_i32, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_i32, c_ptr,

@@ -3,6 +3,8 @@
 // (mining.py:83-85 _directed_edge_arrays), exact pair intersection counts
 // (providers.py:102-115, setops.py:23-51) and raw hash words
 // (hashing.py:114-118).
+#include <algorithm>
+
 #include <cub/device/device_scan.cuh>
 #include <cuda/functional>
 
@@ -117,6 +119,72 @@ __global__ void range_slot_finish_kernel(const int64_t* __restrict__ cnt, const 
   range[0] = base;
   range[1] = base + total;
   cursor[0] = base + total;
+}
+
+// Fused exact triangle count: sum over the edges (us[e], vs[e]) of
+// |N(u) & N(v)| in the CSR (offsets, adj) -- pairs_exact_kernel plus the sum,
+// without the per-edge int64 output.  Warp per edge; the longer row is staged
+// in the warp's shared memory when it fits (kTcStage ints) and every element
+// of the shorter row is binary-searched there.
+constexpr int kTcStage = 512;
+
+__device__ __forceinline__ bool staged_contains(const int32_t* a, int len, int32_t x) {
+  int lo = 0, hi = len;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1;
+    else hi = mid;
+  }
+  return lo < len && a[lo] == x;
+}
+
+// G lanes per edge (32/G edges per warp iteration), each group with its
+// own stage of kTcStage * G / 32 ints
+template <int G>
+__global__ void __launch_bounds__(256) tc_exact_kernel(const int64_t* __restrict__ offsets,
+                                                       const int32_t* __restrict__ adj,
+                                                       const int32_t* __restrict__ us,
+                                                       const int32_t* __restrict__ vs, int64_t count,
+                                                       unsigned long long* __restrict__ out) {
+  constexpr int E = 32 / G, kCap = kTcStage / E;
+  __shared__ int32_t stage[8][kTcStage];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, gl = lane % G, grp = lane / G;
+  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (grp * G);
+  int32_t* sB = stage[w] + grp * kCap;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  unsigned long long hits = 0;
+  for (int64_t e0 = ((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) * E; e0 < count; e0 += warps * E) {
+    const int64_t e = e0 + grp;
+    int64_t ab = 0, ae = 0, bb = 0, be = 0;
+    if (e < count) {
+      const int32_t u = us[e], v = vs[e];
+      ab = offsets[u]; ae = offsets[u + 1]; bb = offsets[v]; be = offsets[v + 1];
+      if (ae - ab > be - bb) {
+        int64_t t = ab; ab = bb; bb = t;
+        t = ae; ae = be; be = t;
+      }
+    }
+    const int64_t la = ae - ab, lb = be - bb;
+    if (lb <= kCap) {
+      for (int i = gl; i < lb; i += G) sB[i] = adj[bb + i];
+      __syncwarp(gmask);
+      for (int64_t j = gl; j < la; j += G) hits += staged_contains(sB, (int)lb, adj[ab + j]);
+      __syncwarp(gmask);
+    } else {
+      for (int64_t j = ab + gl; j < ae; j += G) {
+        const int32_t x = adj[j];
+        int64_t lo = bb, hi = be;
+        while (lo < hi) {
+          const int64_t mid = (lo + hi) >> 1;
+          if (adj[mid] < x) lo = mid + 1;
+          else hi = mid;
+        }
+        hits += (lo < be && adj[lo] == x);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) hits += __shfl_xor_sync(0xffffffffu, hits, o);
+  if (lane == 0 && hits) atomicAdd(out, hits);
 }
 
 __global__ void mark_csr_rows_kernel(const int64_t* __restrict__ offsets, int64_t n, int32_t* __restrict__ marks) {
@@ -413,6 +481,37 @@ int pg_hash_words(const int64_t* keys, int64_t count, uint64_t seed, uint64_t* o
   PG_REQUIRE(keys && out, "null pointer");
   hash_words_kernel<<<sm_count() * 4, 256, 0, as_stream(stream)>>>(keys, count, seed, out);
   return check_launch("hash_words");
+}
+
+int pg_tc_exact(const int64_t* offsets, const int32_t* adj, const int32_t* us, const int32_t* vs, int64_t count,
+                int64_t* out_sum, void* stream) {
+  PG_REQUIRE(count >= 0, "count must be >= 0");
+  PG_REQUIRE(out_sum, "null output");
+  cudaStream_t s = as_stream(stream);
+  cudaError_t e = cudaMemsetAsync(out_sum, 0, sizeof(int64_t), s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
+  if (count == 0) return PG_OK;
+  PG_REQUIRE(offsets && adj && us && vs, "null pointer");
+  static const int G = [] {
+    const char* v = getenv("PG_TC_EXACT_LANES");
+    return v ? atoi(v) : 32;
+  }();
+#define PG_TE(GG)                                                                                       \
+  {                                                                                                     \
+    int per_sm = 0;                                                                                     \
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc_exact_kernel<GG>, 256, 0) != cudaSuccess || \
+        per_sm < 1)                                                                                     \
+      per_sm = 1;                                                                                       \
+    const int64_t need = (count + 8 * (32 / GG) - 1) / (8 * (32 / GG));                                 \
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sm_count() * per_sm)); \
+    tc_exact_kernel<GG><<<grid, 256, 0, s>>>(offsets, adj, us, vs, count,                              \
+                                             reinterpret_cast<unsigned long long*>(out_sum));           \
+  }
+  if (G == 8) PG_TE(8)
+  else if (G == 16) PG_TE(16)
+  else PG_TE(32)
+#undef PG_TE
+  return check_launch("tc_exact");
 }
 
 int pg_pairs_exact(const int64_t* offsets, const int32_t* adj, const int32_t* us, const int32_t* vs,

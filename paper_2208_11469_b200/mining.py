@@ -59,6 +59,14 @@ def triangle_count(view: DirectedView, provider: IntersectionProvider,
                    threads: int = 1):
     """Sum of |N+v & N+u| over directed edges (exact int for exact providers)."""
     dev = view.device()
+    if isinstance(provider, ExactProvider):
+        # fused intersections + sum over the provider's CSR
+        import torch
+        d = provider.device()
+        out = torch.empty(1, dtype=torch.int64, device="cuda")
+        N.call("pg_tc_exact", N.ptr(d.offsets), N.ptr(d.adj), N.ptr(dev.row_sources()),
+               N.ptr(dev.adj), dev.nnz, N.ptr(out), N.stream_handle())
+        return int(out.item())
     part = provider._pairs_device(dev.row_sources(), dev.adj)
     if provider.is_exact:
         return int(part.sum().item()) if part.numel() else 0
