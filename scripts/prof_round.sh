@@ -6,6 +6,6 @@ ncu -i /tmp/tc.ncu-rep --page details > gpurun_out/r01d_ncu_tc_c2.txt 2>&1
 ncu -i /tmp/tc.ncu-rep --page raw --csv > gpurun_out/r01d_ncu_tc_c2_raw.csv 2>&1
 ncu -f --set full --clock-control none --import-source on -k regex:kmv_ranked -s 1 -c 1 -o /tmp/kmv python scripts/prof_sorted_once.py kmv > gpurun_out/ncu_kmv.log 2>&1
 ncu -i /tmp/kmv.ncu-rep --page details > gpurun_out/r01d_ncu_kmv_ranked_s20.txt 2>&1
-ncu -f --set full --clock-control none --import-source on -k regex:onehash_htab -s 1 -c 1 -o /tmp/oh python scripts/prof_sorted_once.py onehash > gpurun_out/ncu_oh.log 2>&1
-ncu -i /tmp/oh.ncu-rep --page details > gpurun_out/r01d_ncu_onehash_htab_s20.txt 2>&1
+ncu -f --set full --clock-control none --import-source on -k regex:onehash_block -s 1 -c 1 -o /tmp/oh python scripts/prof_sorted_once.py onehash > gpurun_out/ncu_oh.log 2>&1
+ncu -i /tmp/oh.ncu-rep --page details > gpurun_out/r01d_ncu_onehash_block_s20.txt 2>&1
 ls -la gpurun_out
