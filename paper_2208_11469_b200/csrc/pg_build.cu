@@ -528,6 +528,60 @@ __device__ __forceinline__ void bottomk_scan(WarpBottomK<P, kMode != 0>& L, cons
   }
 }
 
+// ascending warp bitonic sort of 32 R keys; element i = lane + 32 r (R <= 2)
+template <int R>
+__device__ __forceinline__ void warp_bitonic_sort(uint64_t (&key)[R]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int size = 2; size <= 32 * R; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      uint64_t old[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) old[r] = key[r];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        const bool up = (i & size) == 0;  // ascending block
+        const uint64_t other = stride == 32 ? old[r ^ 1] : shfl64(old[r], lane ^ stride);
+        const bool lower = (i & stride) == 0;
+        const uint64_t mn = old[r] < other ? old[r] : other, mx = old[r] < other ? other : old[r];
+        key[r] = (lower == up) ? mn : mx;
+      }
+    }
+  }
+}
+
+// Fill a bottom-k list of k = 32 P (P <= 2) keys from k candidates at
+// row[b0 + lane + stride * r] by one bitonic sort instead of k insertions.
+// KMV lists hold distinct values: a repeated key (equal values of two
+// neighbours) makes it return false and the caller inserts one by one.
+template <int P, int kMode>
+__device__ __forceinline__ bool bottomk_fill_sorted(WarpBottomK<P, kMode != 0>& L, const int32_t* __restrict__ row,
+                                                    int64_t b0, int64_t stride, uint64_t seed0, const BottomKRank& rk) {
+  constexpr int R = P <= 2 ? P : 1;
+  const int lane = lane_id();
+  uint64_t key[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) key[r] = bottomk_key<kMode>(seed0, row[b0 + lane + stride * r], rk);
+  warp_bitonic_sort<R>(key);
+  if (kMode != 0) {
+    bool dup = false;
+    uint64_t carry = ~0ull;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const uint64_t prev = shfl_up64(key[r], 1);
+      dup |= key[r] == (lane == 0 ? carry : prev);
+      carry = shfl64(key[r], 31);
+    }
+    if (__any_sync(0xffffffffu, dup)) return false;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) L.key[r] = key[r];
+  L.cnt = 32 * R;
+  return true;
+}
+
 // write the final list of vertex v.  1-Hash: IDs ascending (rank sort in
 // the warp's smem scratch), -1 pad; KMV: values ascending, +inf pad.
 template <int P, int kMode>
@@ -596,24 +650,7 @@ __device__ __forceinline__ void kmv_short_row_r(const int32_t* __restrict__ row,
     const int i = lane + 32 * r;
     key[r] = i < d ? bottomk_key<kMode>(seed0, row[i], rk) : ~0ull;
   }
-#pragma unroll
-  for (int size = 2; size <= 32 * R; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      uint64_t old[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) old[r] = key[r];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = lane + 32 * r;
-        const bool up = (i & size) == 0;  // ascending block
-        const uint64_t other = stride == 32 ? old[r ^ 1] : shfl64(old[r], lane ^ stride);
-        const bool lower = (i & stride) == 0;
-        const uint64_t mn = old[r] < other ? old[r] : other, mx = old[r] < other ? other : old[r];
-        key[r] = (lower == up) ? mn : mx;
-      }
-    }
-  }
+  warp_bitonic_sort<R>(key);
   const unsigned lt = (1u << lane) - 1u;
   int before = 0, total = 0;
   uint64_t carry = ~0ull;  // key 32 r - 1 (the last of the previous register)
@@ -701,7 +738,10 @@ __global__ void __launch_bounds__(kThreads) build_bottomk_kernel(
       }
       WarpBottomK<P, kKmv> L;
       L.init(k);
-      bottomk_scan<P, kMode>(L, adj + o, 0, d, 32, seed0, rk);
+      int64_t first = 0;
+      if (P <= 2 && k == 32 * P && d >= k && bottomk_fill_sorted<P, kMode>(L, adj + o, 0, 32, seed0, rk))
+        first = k;  // the first k keys by one sort; the rest are offered as usual
+      bottomk_scan<P, kMode>(L, adj + o, first, d, 32, seed0, rk);
       bottomk_emit<P, kMode>(L, v, k, seed0, scratch[warp_id()], entries, values, lengths, rk);
     }
   }
@@ -732,7 +772,12 @@ __global__ void __launch_bounds__(kThreads) build_bottomk_hubs_kernel(
     const int64_t d = offsets[v + 1] - o;
     WarpBottomK<P, kKmv> L;
     L.init(k);
-    bottomk_scan<P, kMode>(L, adj + o, 32 * warp_id(), d, kThreads, seed0, rk);
+    // each warp's first k strided candidates fill its list by one sort
+    int64_t first = 32 * warp_id();
+    if (P <= 2 && k == 32 * P && d >= 32 * warp_id() + (int64_t)kThreads * (P - 1) + 32 &&
+        bottomk_fill_sorted<P, kMode>(L, adj + o, 32 * warp_id(), kThreads, seed0, rk))
+      first += (int64_t)kThreads * P;
+    bottomk_scan<P, kMode>(L, adj + o, first, d, kThreads, seed0, rk);
 #pragma unroll
     for (int s = 0; s < P; ++s) merge_keys[warp_id()][lane + 32 * s] = L.key[s];
     if (lane == 0) merge_cnt[warp_id()] = L.cnt;
