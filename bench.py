@@ -49,7 +49,7 @@ def parse():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=sorted(WORKLOAD), default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=15)
     ap.add_argument("--no-busy", action="store_true",
                     help="skip the untimed clock-sampling tail (for ncu runs)")
     ap.add_argument("--no-secondary", action="store_true",
