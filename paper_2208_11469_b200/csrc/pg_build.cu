@@ -785,7 +785,12 @@ __global__ void __launch_bounds__(kThreads) build_bottomk_hubs_kernel(
     if (warp_id() == 0) {
       WarpBottomK<P, kKmv> M;
       M.init(k);
-      for (int w = 0; w < kWarps; ++w) {
+      // warp 0's list is already a sorted, distinct bottom-k: it starts the
+      // merge as is (k insertions saved per hub); the others are offered
+#pragma unroll
+      for (int r = 0; r < P; ++r) M.key[r] = merge_keys[0][lane + 32 * r];
+      M.cnt = merge_cnt[0];
+      for (int w = 1; w < kWarps; ++w) {
         const int cw = merge_cnt[w];
         for (int base = 0; base < cw; base += 32) {
           const int idx = base + lane;
