@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kBlock, PG_RANKED_MINB) kmv_ranked_kernel(cons
         uint32_t xn[P];
         ldg_rowpart<P>(R + (int64_t)(vqn < 0 ? 0 : vqn) * K + gl * P, xn);
         // le_t = |A <= b_t| (<= K <= 128) packed four per register
-        uint32_t le[P / 4];
+        int le[P];
         unsigned hits = 0, ovf = 0;
 #pragma unroll
         for (int t = 0; t < P; ++t) {
@@ -421,8 +421,7 @@ __global__ void __launch_bounds__(kBlock, PG_RANKED_MINB) kmv_ranked_kernel(cons
           const bool ok = valid && q != INT32_MAX;
           bool h, o;
           const int l = rd_probe<K>(W, q, lo, spanm1, mul, ok, h, o);
-          if (t % 4 == 0) le[t / 4] = 0;
-          le[t / 4] |= (uint32_t)(ok ? l : 0) << (8 * (t % 4));
+          le[t] = ok ? l : 0;
           hits |= (unsigned)(ok && h) << t;
           ovf |= (unsigned)(ok && o) << t;
         }
@@ -432,7 +431,7 @@ __global__ void __launch_bounds__(kBlock, PG_RANKED_MINB) kmv_ranked_kernel(cons
             if ((ovf >> t) & 1) {
               bool h;
               const int l = rd_probe_slow<K>(W, (int32_t)x[t], lo, spanm1, mul, h);
-              le[t / 4] = (le[t / 4] & ~(0xffu << (8 * (t % 4)))) | ((uint32_t)l << (8 * (t % 4)));
+              le[t] = l;
               hits = (hits & ~(1u << t)) | ((unsigned)h << t);
             }
           }
@@ -453,7 +452,7 @@ __global__ void __launch_bounds__(kBlock, PG_RANKED_MINB) kmv_ranked_kernel(cons
         for (int t = 0; t < P; ++t) {
           const int j = gl * P + t;
           C += (hits >> t) & 1;
-          const int let = (le[t / 4] >> (8 * (t % 4))) & 0xff;
+          const int let = le[t];
           const int dist = let + (j + 1) - C;
           if (j < lv && dist < T) {
             ++less;
