@@ -244,10 +244,23 @@ __global__ void __launch_bounds__(kBlock) onehash_sorted_kernel(const int32_t* e
 #define PG_OH_PER_LANE 8
 #endif
 constexpr int kOnehashPerLane = PG_OH_PER_LANE;  // v-row IDs per lane (pad = 32 * this / k)
+#ifndef PG_OH_SLOTS
+#define PG_OH_SLOTS 4
+#endif
+// slots per bucket of the per-warp table: 4 (K buckets, one LDS.128 per
+// probe) or 2 (2K buckets, one LDS.64: half the shared-memory wavefronts)
+constexpr int kOnehashSlots = PG_OH_SLOTS;
+
+template <int K>
+__device__ __forceinline__ uint32_t oh_bucket(int32_t x) {
+  constexpr int kB = 4 * K / kOnehashSlots;  // buckets
+  constexpr int kBits = kB == 32 ? 5 : kB == 64 ? 6 : kB == 128 ? 7 : kB == 256 ? 8 : 9;
+  return ((uint32_t)x * 0x9E3779B1u) >> (32 - kBits);
+}
 
 template <int K>
 struct alignas(16) OnehashWarp {
-  int32_t tab[4 * K];  // K buckets x 4 slots
+  int32_t tab[4 * K];  // K buckets x 4 slots, or 2K buckets x 2 (kOnehashSlots)
   int32_t stash[K];
   int32_t mbuf[32];    // per slot of the block: matches
   int sc;
@@ -312,10 +325,10 @@ __global__ void __launch_bounds__(kBlock, 5) onehash_block_kernel(const int32_t*
 #pragma unroll
           for (int q = 0; q < K / 32; ++q) {
             if (y[q] < 0) continue;  // -1 pad
-            int32_t* bk = W.tab + 4 * htab_bucket<K>(y[q]);
+            int32_t* bk = W.tab + kOnehashSlots * oh_bucket<K>(y[q]);
             bool placed = false;
 #pragma unroll
-            for (int sl = 0; sl < 4 && !placed; ++sl) placed = atomicCAS(bk + sl, -1, y[q]) == -1;
+            for (int sl = 0; sl < kOnehashSlots && !placed; ++sl) placed = atomicCAS(bk + sl, -1, y[q]) == -1;
             if (!placed) W.stash[atomicAdd(&W.sc, 1)] = y[q];
           }
           __syncwarp();
@@ -329,8 +342,14 @@ __global__ void __launch_bounds__(kBlock, 5) onehash_block_kernel(const int32_t*
         for (int p = 0; p < P; ++p) {
           const int32_t q = (int32_t)x[p];
           if (valid && q >= 0) {
-            const int4 bk = reinterpret_cast<const int4*>(W.tab)[htab_bucket<K>(q)];
-            bool hit = (bk.x == q) | (bk.y == q) | (bk.z == q) | (bk.w == q);
+            bool hit;
+            if constexpr (kOnehashSlots == 2) {
+              const int2 bk = reinterpret_cast<const int2*>(W.tab)[oh_bucket<K>(q)];
+              hit = (bk.x == q) | (bk.y == q);
+            } else {
+              const int4 bk = reinterpret_cast<const int4*>(W.tab)[oh_bucket<K>(q)];
+              hit = (bk.x == q) | (bk.y == q) | (bk.z == q) | (bk.w == q);
+            }
             for (int i = 0; i < sc; ++i) hit |= W.stash[i] == q;
             m += hit;
           }
