@@ -50,6 +50,9 @@ __device__ __forceinline__ uint32_t bloom_pos(uint64_t w, uint32_t bits) {
 #ifndef PG_BB_MINB
 #define PG_BB_MINB 6  // 40 registers: whole s20 build 327 -> 311 us
 #endif
+#ifndef PG_BH_MINB
+#define PG_BH_MINB 4  // 62 registers (84 unbounded): whole s20 build 313 -> 257 us
+#endif
 constexpr int64_t kHubBloom = 1024;
 constexpr int64_t kMidBloom = 64;  // rows above this take pass 1b (a warp each)
 
@@ -201,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, PG_BB_MINB) build_bloom_mid_kernel(
 constexpr int64_t kHubSlice = 2048;
 
 template <bool kPow2>
-__global__ void __launch_bounds__(kThreads) build_bloom_hubs_kernel(
+__global__ void __launch_bounds__(kThreads, PG_BH_MINB) build_bloom_hubs_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, uint32_t bits, int b,
     const uint64_t* __restrict__ seeds_dev, uint64_t* __restrict__ rows,
     const int32_t* __restrict__ hubs, const int32_t* __restrict__ hub_count) {
