@@ -53,6 +53,18 @@ __device__ __forceinline__ uint32_t bloom_pos(uint64_t w, uint32_t bits) {
 #ifndef PG_BH_MINB
 #define PG_BH_MINB 4  // 62 registers (84 unbounded): whole s20 build 313 -> 257 us
 #endif
+#ifndef PG_BK_MINB
+#define PG_BK_MINB 1
+#endif
+#ifndef PG_BKH_MINB
+#define PG_BKH_MINB 1
+#endif
+#ifndef PG_KB_MINB
+#define PG_KB_MINB 1
+#endif
+#ifndef PG_KBH_MINB
+#define PG_KBH_MINB 1
+#endif
 constexpr int64_t kHubBloom = 1024;
 constexpr int64_t kMidBloom = 64;  // rows above this take pass 1b (a warp each)
 
@@ -305,33 +317,39 @@ __global__ void __launch_bounds__(kThreads) bloom_hub_ones_kernel(
 
 // ============================================================= k-Hash ====
 // Lane = hash function (i = lane + 32*s).  Each lane keeps the running
-// lexicographic minimum of (h_i(x), x) over the neighbour row, which is
-// exactly argmin with the smaller-ID tie-break of the reference.
+// minimum of h_i(x) over the neighbour row.  For a fixed seed, h_i(x) =
+// mix64(seed_i ^ x) is a bijection of x, so equal hashes mean the same ID:
+// the reference's smaller-ID tie-break never fires, and the argmin is
+// recovered from the minimum itself (x = unmix64(h) ^ seed_i) after the
+// scan -- the loop carries one 64-bit register pair per function and a
+// 64-bit compare, and IDs zero-extend so seed_i's high word stays constant.
 template <int S>
 __device__ __forceinline__ void khash_scan(const int32_t* __restrict__ row, int64_t beg, int64_t end,
                                            int64_t step, const uint64_t (&seed)[S],
-                                           uint64_t (&best_h)[S], int32_t (&best_x)[S]) {
+                                           uint64_t (&best_h)[S]) {
   const int lane = lane_id();
   for (int64_t base = beg; base < end; base += step) {
     const int64_t j = base + lane;
-    const int32_t xl = j < end ? row[j] : 0;
+    const uint32_t xl = j < end ? (uint32_t)row[j] : 0u;
     const int cnt = (end - base) < 32 ? (int)(end - base) : 32;
     for (int t = 0; t < cnt; ++t) {
-      const int32_t x = __shfl_sync(0xffffffffu, xl, t);
+      const uint32_t x = __shfl_sync(0xffffffffu, xl, t);
 #pragma unroll
       for (int s = 0; s < S; ++s) {
-        const uint64_t h = hash_word(seed[s], x);
-        if (h < best_h[s] || (h == best_h[s] && x < best_x[s])) {
-          best_h[s] = h;
-          best_x[s] = x;
-        }
+        const uint64_t h = mix64(seed[s] ^ (uint64_t)x);
+        best_h[s] = h < best_h[s] ? h : best_h[s];
       }
     }
   }
 }
 
+// the ID whose hash is h under `seed` (IDs are non-negative int32)
+__device__ __forceinline__ int32_t khash_arg(uint64_t seed, uint64_t h) {
+  return (int32_t)(uint32_t)(unmix64(h) ^ seed);
+}
+
 template <int S>
-__global__ void __launch_bounds__(kThreads) build_khash_kernel(
+__global__ void __launch_bounds__(kThreads, PG_KB_MINB) build_khash_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n, int k,
     const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries, int32_t* __restrict__ hubs,
     int32_t* __restrict__ hub_count, unsigned long long* __restrict__ vtx_work) {
@@ -363,26 +381,24 @@ __global__ void __launch_bounds__(kThreads) build_khash_kernel(
         continue;
       }
       uint64_t bh[S];
-      int32_t bx[S];
 #pragma unroll
-      for (int s = 0; s < S; ++s) { bh[s] = ~0ull; bx[s] = 0x7fffffff; }
-      khash_scan<S>(adj + o, 0, d, 32, seed, bh, bx);
+      for (int s = 0; s < S; ++s) bh[s] = ~0ull;
+      khash_scan<S>(adj + o, 0, d, 32, seed, bh);
 #pragma unroll
       for (int s = 0; s < S; ++s) {
         const int i = lane + 32 * s;
-        if (i < k) entries[v * k + i] = d > 0 ? bx[s] : -1;
+        if (i < k) entries[v * k + i] = d > 0 ? khash_arg(seed[s], bh[s]) : -1;
       }
     }
   }
 }
 
 template <int S>
-__global__ void __launch_bounds__(kThreads) build_khash_hubs_kernel(
+__global__ void __launch_bounds__(kThreads, PG_KBH_MINB) build_khash_hubs_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int k,
     const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries, const int32_t* __restrict__ hubs,
     const int32_t* __restrict__ hub_count, int32_t* __restrict__ hub_work) {
   __shared__ uint64_t red_h[kWarps][32 * S];
-  __shared__ int32_t red_x[kWarps][32 * S];
   __shared__ int s_hi;
   const int lane = lane_id();
   uint64_t seed[S];
@@ -402,25 +418,16 @@ __global__ void __launch_bounds__(kThreads) build_khash_hubs_kernel(
     const int64_t o = offsets[v];
     const int64_t d = offsets[v + 1] - o;
     uint64_t bh[S];
-    int32_t bx[S];
 #pragma unroll
-    for (int s = 0; s < S; ++s) { bh[s] = ~0ull; bx[s] = 0x7fffffff; }
-    khash_scan<S>(adj + o, 32 * warp_id(), d, kThreads, seed, bh, bx);
+    for (int s = 0; s < S; ++s) bh[s] = ~0ull;
+    khash_scan<S>(adj + o, 32 * warp_id(), d, kThreads, seed, bh);
 #pragma unroll
-    for (int s = 0; s < S; ++s) {
-      red_h[warp_id()][lane + 32 * s] = bh[s];
-      red_x[warp_id()][lane + 32 * s] = bx[s];
-    }
+    for (int s = 0; s < S; ++s) red_h[warp_id()][lane + 32 * s] = bh[s];
     __syncthreads();
     for (int i = threadIdx.x; i < k; i += kThreads) {
       uint64_t h = red_h[0][i];
-      int32_t x = red_x[0][i];
-      for (int w = 1; w < kWarps; ++w) {
-        const uint64_t h2 = red_h[w][i];
-        const int32_t x2 = red_x[w][i];
-        if (h2 < h || (h2 == h && x2 < x)) { h = h2; x = x2; }
-      }
-      entries[v * k + i] = x;
+      for (int w = 1; w < kWarps; ++w) h = red_h[w][i] < h ? red_h[w][i] : h;
+      entries[v * k + i] = khash_arg(seeds_dev[i], h);  // hubs have d > 1024
     }
     __syncthreads();
   }
@@ -697,7 +704,7 @@ __device__ __forceinline__ void kmv_short_row(const int32_t* __restrict__ row, i
 }
 
 template <int P, int kMode>
-__global__ void __launch_bounds__(kThreads) build_bottomk_kernel(
+__global__ void __launch_bounds__(kThreads, PG_BK_MINB) build_bottomk_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int64_t n, int k,
     const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries,
     double* __restrict__ values, int32_t* __restrict__ lengths, int32_t* __restrict__ hubs,
@@ -751,7 +758,7 @@ __global__ void __launch_bounds__(kThreads) build_bottomk_kernel(
 }
 
 template <int P, int kMode>
-__global__ void __launch_bounds__(kThreads) build_bottomk_hubs_kernel(
+__global__ void __launch_bounds__(kThreads, PG_BKH_MINB) build_bottomk_hubs_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int k,
     const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries, double* __restrict__ values,
     int32_t* __restrict__ lengths, const int32_t* __restrict__ hubs, const int32_t* __restrict__ hub_count,

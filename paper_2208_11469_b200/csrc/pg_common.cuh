@@ -47,9 +47,11 @@ __host__ __device__ __forceinline__ uint64_t unmix64(uint64_t x) {
 }
 
 // word(i, key) = mix64(seed_i ^ uint64(key))  (hashing.py:114-118);
-// a non-negative int32 vertex ID zero-extends exactly like int64 -> uint64
+// keys are vertex IDs (non-negative int32), whose int64 -> uint64 cast is a
+// zero extension: the high word of seed_i ^ key is seed_i's, which the
+// compiler hoists out of the neighbour loops
 __device__ __forceinline__ uint64_t hash_word(uint64_t seed, int32_t key) {
-  return mix64(seed ^ static_cast<uint64_t>(static_cast<int64_t>(key)));
+  return mix64(seed ^ static_cast<uint64_t>(static_cast<uint32_t>(key)));
 }
 
 // unit value (word+1)*2^-64 in (0,1]; all-ones word -> 1.0 (hashing.py:148-153).
