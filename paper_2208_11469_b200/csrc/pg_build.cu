@@ -53,6 +53,12 @@ __device__ __forceinline__ uint32_t bloom_pos(uint64_t w, uint32_t bits) {
 #ifndef PG_BH_MINB
 #define PG_BH_MINB 4  // 62 registers (84 unbounded): whole s20 build 313 -> 257 us
 #endif
+#ifndef PG_BK_HUB_KERNEL
+#define PG_BK_HUB_KERNEL build_bottomk_hubs_buffered_kernel
+#endif
+#ifndef PG_BK_HUB
+#define PG_BK_HUB 1024
+#endif
 #ifndef PG_BK_MINB
 #define PG_BK_MINB 1
 #endif
@@ -538,6 +544,35 @@ __device__ __forceinline__ void bottomk_scan(WarpBottomK<P, kMode != 0>& L, cons
   }
 }
 
+// bottomk_scan for the CTAs that share one hub row: a warp whose list is
+// full publishes its k-th key T to the CTA (shared atomicMin), and every
+// warp drops candidates >= the smallest published T -- that warp already
+// holds k distinct keys <= T, so none of them can reach the row's bottom-k
+// (KMV: a candidate equal to T is a duplicate of a listed value).  Without
+// it each warp keeps its own bottom-k of its 1/8 of the row, inserting
+// ~k ln(n/8k) candidates instead of the row's ~k ln(n/k) / 8.
+template <int P, int kMode>
+__device__ __forceinline__ void bottomk_scan_shared(WarpBottomK<P, kMode != 0>& L,
+                                                    const int32_t* __restrict__ row, int64_t beg,
+                                                    int64_t end, int64_t step, uint64_t seed0,
+                                                    const BottomKRank& rk, unsigned long long* s_thr) {
+  const int lane = lane_id();
+  uint64_t mine = ~0ull;
+  for (int64_t base = beg; base < end; base += step) {
+    const int64_t j = base + lane;
+    const uint64_t c = j < end ? bottomk_key<kMode>(seed0, row[j], rk) : ~0ull;
+    const uint64_t cta = *(volatile unsigned long long*)s_thr;
+    L.offer(c, j < end && c < cta);
+    if (L.full()) {
+      const uint64_t t = L.threshold();
+      if (t < mine) {
+        mine = t;
+        if (lane == 0) atomicMin(s_thr, (unsigned long long)t);
+      }
+    }
+  }
+}
+
 // ascending warp bitonic sort of 32 R keys; element i = lane + 32 r (R <= 2)
 template <int R>
 __device__ __forceinline__ void warp_bitonic_sort(uint64_t (&key)[R]) {
@@ -729,7 +764,7 @@ __global__ void __launch_bounds__(kThreads, PG_BK_MINB) build_bottomk_kernel(
       const int64_t v = vb + t;
       const int64_t o = __shfl_sync(0xffffffffu, ol, t);
       const int64_t d = __shfl_sync(0xffffffffu, el, t) - o;
-      if (d > kHub) {
+      if (d > PG_BK_HUB) {
         if (lane == 0) hubs[atomicAdd(hub_count, 1)] = (int32_t)v;
         continue;
       }
@@ -757,6 +792,145 @@ __global__ void __launch_bounds__(kThreads, PG_BK_MINB) build_bottomk_kernel(
   }
 }
 
+// ascending CTA bitonic sort of buf[0, n) in shared memory, n a power of two
+// (>= 2); every thread of the CTA calls it; ends with a barrier
+__device__ __forceinline__ void cta_bitonic_sort(uint64_t* buf, int n) {
+  for (int size = 2; size <= n; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int t = threadIdx.x; t < (n >> 1); t += kThreads) {
+        const int i = 2 * t - (t & (stride - 1));
+        const int j = i + stride;
+        const uint64_t x = buf[i], y = buf[j];
+        if ((x > y) == ((i & size) == 0)) {
+          buf[i] = y;
+          buf[j] = x;
+        }
+      }
+    }
+  }
+  __syncthreads();
+}
+
+// Hub rows (d > PG_BK_HUB) by a buffered threshold filter, one CTA per hub:
+// every thread hashes kHubU entries per round and appends the keys below the
+// CTA threshold T to a shared buffer (one shared atomic per warp); when the
+// next round could overflow it, the CTA sorts the buffer and keeps the first
+// k distinct keys, and T becomes the k-th of them.  T is the k-th distinct
+// key of everything seen so far, so a later key > T cannot reach the row's
+// bottom-k and a key == T is a repeat of a listed one.  A row of d entries
+// costs about log_{1+B/k}(d/B) compactions and no per-key list insertions;
+// the eight per-warp lists it replaces inserted ~8 k ln(d/8k) keys and were
+// merged by one warp while the other seven waited (1-Hash k=64 at c3: 9.9M
+// insertions for 46.5M hub entries, 1.4 ms).
+#ifndef PG_HUB_U
+#define PG_HUB_U 2
+#endif
+constexpr int kHubU = PG_HUB_U;                  // entries per thread per round
+constexpr int kHubRound = kHubU * kThreads;
+constexpr int kHubBuf = 2 * kHubRound;           // shared keys (8 KB)
+static_assert(kHubRound >= 256, "a compaction (<= k <= 256 keys) plus one round fits");
+
+// sort buf[0, n), keep its first min(k, distinct) distinct keys in buf[0, ..);
+// returns that count (CTA-uniform via s_out)
+template <bool kDedup>
+__device__ __forceinline__ int hub_compact(uint64_t* buf, int n, int k, int* s_out) {
+  int np = 64;
+  while (np < n) np <<= 1;
+  for (int i = n + threadIdx.x; i < np; i += kThreads) buf[i] = ~0ull;
+  cta_bitonic_sort(buf, np);
+  if (warp_id() == 0) {
+    const int lane = lane_id();
+    int got = 0;
+    uint64_t last = 0;
+    for (int base = 0; base < n && got < k; base += 32) {
+      const int i = base + lane;
+      const uint64_t x = i < n ? buf[i] : ~0ull;
+      const uint64_t prev = shfl_up64(x, 1);
+      const uint64_t before = lane == 0 ? last : prev;
+      const bool isnew = i < n && (!kDedup || i == 0 || x != before);
+      last = shfl64(x, 31);
+      const unsigned m = __ballot_sync(0xffffffffu, isnew);
+      const int pos = got + __popc(m & ((1u << lane) - 1u));
+      __syncwarp();
+      if (isnew && pos < k) buf[pos] = x;  // pos <= i: only slots already read
+      got += __popc(m);
+    }
+    if (lane == 0) *s_out = got < k ? got : k;
+  }
+  __syncthreads();
+  return *s_out;
+}
+
+template <int P, int kMode>
+__global__ void __launch_bounds__(kThreads, PG_BKH_MINB) build_bottomk_hubs_buffered_kernel(
+    const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int k,
+    const uint64_t* __restrict__ seeds_dev, int32_t* __restrict__ entries, double* __restrict__ values,
+    int32_t* __restrict__ lengths, const int32_t* __restrict__ hubs, const int32_t* __restrict__ hub_count,
+    int32_t* __restrict__ hub_work, BottomKRank rk) {
+  constexpr bool kKmv = kMode != 0;
+  __shared__ uint64_t buf[kHubBuf];
+  __shared__ int32_t scratch[32 * P];
+  __shared__ int s_hi, s_n, s_out;
+  const int lane = lane_id();
+  const uint64_t seed0 = seeds_dev[0];
+  const int nh = *hub_count;
+  for (;;) {  // hubs taken from a global counter (their degrees vary widely)
+    if (threadIdx.x == 0) {
+      s_hi = atomicAdd(hub_work, 1);
+      s_n = 0;
+    }
+    __syncthreads();
+    const int hi = s_hi;
+    if (hi >= nh) break;
+    const int64_t v = hubs[hi];
+    const int64_t o = offsets[v];
+    const int64_t d = offsets[v + 1] - o;
+    const int32_t* __restrict__ row = adj + o;
+    uint64_t T = ~0ull;  // CTA-uniform
+    for (int64_t j0 = 0; j0 < d; j0 += kHubRound) {
+      __syncthreads();
+      int n = s_n;
+      if (n >= kHubBuf - kHubRound) {  // compact as soon as a round's worth is buffered
+        n = hub_compact<kKmv>(buf, n, k, &s_out);
+        if (threadIdx.x == 0) s_n = n;
+        T = n >= k ? buf[k - 1] : ~0ull;
+        __syncthreads();
+      }
+      uint64_t c[kHubU];
+      bool pass[kHubU];
+#pragma unroll
+      for (int u = 0; u < kHubU; ++u) {
+        const int64_t j = j0 + u * kThreads + threadIdx.x;
+        c[u] = j < d ? bottomk_key<kMode>(seed0, row[j], rk) : ~0ull;
+        pass[u] = j < d && (c[u] < T || T == ~0ull);
+      }
+#pragma unroll
+      for (int u = 0; u < kHubU; ++u) {
+        const unsigned m = __ballot_sync(0xffffffffu, pass[u]);
+        int base = 0;
+        if (lane == 0 && m) base = atomicAdd(&s_n, __popc(m));
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (pass[u]) buf[base + __popc(m & ((1u << lane) - 1u))] = c[u];
+      }
+    }
+    __syncthreads();
+    const int cnt = hub_compact<kKmv>(buf, s_n, k, &s_out);
+    if (warp_id() == 0) {
+      WarpBottomK<P, kKmv> M;
+      M.init(k);
+#pragma unroll
+      for (int r = 0; r < P; ++r) {
+        const int idx = lane + 32 * r;
+        if (idx < cnt) M.key[r] = buf[idx];
+      }
+      M.cnt = cnt;
+      bottomk_emit<P, kMode>(M, v, k, seed0, scratch, entries, values, lengths, rk);
+    }
+    __syncthreads();
+  }
+}
+
 template <int P, int kMode>
 __global__ void __launch_bounds__(kThreads, PG_BKH_MINB) build_bottomk_hubs_kernel(
     const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj, int k,
@@ -768,11 +942,15 @@ __global__ void __launch_bounds__(kThreads, PG_BKH_MINB) build_bottomk_hubs_kern
   __shared__ uint64_t merge_keys[kWarps][32 * P];
   __shared__ int merge_cnt[kWarps];
   __shared__ int s_hi;
+  __shared__ unsigned long long s_thr;
   const int lane = lane_id();
   const uint64_t seed0 = seeds_dev[0];
   const int nh = *hub_count;
   for (;;) {  // hubs taken from a global counter (their degrees vary widely)
-    if (threadIdx.x == 0) s_hi = atomicAdd(hub_work, 1);
+    if (threadIdx.x == 0) {
+      s_hi = atomicAdd(hub_work, 1);
+      s_thr = ~0ull;
+    }
     __syncthreads();
     const int hi = s_hi;
     __syncthreads();
@@ -787,7 +965,7 @@ __global__ void __launch_bounds__(kThreads, PG_BKH_MINB) build_bottomk_hubs_kern
     if (P <= 2 && k == 32 * P && d >= 32 * warp_id() + (int64_t)kThreads * (P - 1) + 32 &&
         bottomk_fill_sorted<P, kMode>(L, adj + o, 32 * warp_id(), kThreads, seed0, rk))
       first += (int64_t)kThreads * P;
-    bottomk_scan<P, kMode>(L, adj + o, first, d, kThreads, seed0, rk);
+    bottomk_scan_shared<P, kMode>(L, adj + o, first, d, kThreads, seed0, rk, &s_thr);
 #pragma unroll
     for (int s = 0; s < P; ++s) merge_keys[warp_id()][lane + 32 * s] = L.key[s];
     if (lane == 0) merge_cnt[warp_id()] = L.cnt;
@@ -885,7 +1063,7 @@ static int launch_bottomk(const int64_t* offsets, const int32_t* adj, int64_t n,
     const int grid = grid_for(build_bottomk_kernel<P, kMode>, 0, n);                                     \
     build_bottomk_kernel<P, kMode><<<grid, kThreads, 0, s>>>(offsets, adj, n, k, seeds_dev, entries, values, \
                                                              lengths, hubs.ids, hubs.count, hubs.vtx_work, rk); \
-    build_bottomk_hubs_kernel<P, kMode><<<hub_grid(), kThreads, 0, s>>>(offsets, adj, k, seeds_dev, entries, \
+    PG_BK_HUB_KERNEL<P, kMode><<<hub_grid(), kThreads, 0, s>>>(offsets, adj, k, seeds_dev, entries, \
                                                                          values, lengths, hubs.ids,        \
                                                                          hubs.count, hubs.hub_work, rk);   \
   }
