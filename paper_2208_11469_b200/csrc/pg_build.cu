@@ -53,6 +53,9 @@ __device__ __forceinline__ uint32_t bloom_pos(uint64_t w, uint32_t bits) {
 #ifndef PG_BH_MINB
 #define PG_BH_MINB 4  // 62 registers (84 unbounded): whole s20 build 313 -> 257 us
 #endif
+#ifndef PG_MERGE_MIN
+#define PG_MERGE_MIN 4
+#endif
 #ifndef PG_BK_HUB_KERNEL
 #define PG_BK_HUB_KERNEL build_bottomk_hubs_buffered_kernel
 #endif
@@ -444,6 +447,30 @@ __global__ void __launch_bounds__(kThreads, PG_KBH_MINB) build_khash_hubs_kernel
 // L owns slots L, L+32, ...  `cnt` (warp-uniform) slots are valid.  Keys are
 // unique (1-Hash: mix64 is a bijection, so distinct IDs hash apart; KMV:
 // duplicates are rejected on insertion, which is the reference's dedup).
+// ascending warp bitonic sort of 32 R keys; element i = lane + 32 r (R <= 2)
+template <int R>
+__device__ __forceinline__ void warp_bitonic_sort(uint64_t (&key)[R]) {
+  const int lane = lane_id();
+#pragma unroll
+  for (int size = 2; size <= 32 * R; size <<= 1) {
+#pragma unroll
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      uint64_t old[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) old[r] = key[r];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int i = lane + 32 * r;
+        const bool up = (i & size) == 0;  // ascending block
+        const uint64_t other = stride == 32 ? old[r ^ 1] : shfl64(old[r], lane ^ stride);
+        const bool lower = (i & stride) == 0;
+        const uint64_t mn = old[r] < other ? old[r] : other, mx = old[r] < other ? other : old[r];
+        key[r] = (lower == up) ? mn : mx;
+      }
+    }
+  }
+}
+
 template <int P, bool kDedup>
 struct WarpBottomK {
   uint64_t key[P];
@@ -496,6 +523,72 @@ struct WarpBottomK {
     cnt = min(cnt + 1, k);
   }
 
+  // offer_merge: offer() for a full list of k = 32 P keys (P <= 2).  A
+  // chunk with more than PG_MERGE_MIN keys below the threshold is merged in
+  // one step instead of key by key: the chunk is warp-sorted, and with A the
+  // list and C the sorted chunk padded to 32 P, min(A[i], C[32P-1-i]) holds
+  // the 32 P smallest of both as a bitonic sequence, sorted by log2(32 P)
+  // half-cleaner stages.  KMV lists hold distinct values: a repeat in the
+  // result puts the chunk back through insert(), which rejects it.
+  __device__ __forceinline__ void offer_merge(uint64_t c, bool valid) {
+    const uint64_t thr = threshold();
+    const bool pass = valid && c < thr;
+    const unsigned mask = __ballot_sync(0xffffffffu, pass);
+    if (__popc(mask) <= PG_MERGE_MIN) {
+      offer_masked(c, mask);
+      return;
+    }
+    const int lane = lane_id();
+    uint64_t srt[1] = {pass ? c : ~0ull};
+    warp_bitonic_sort<1>(srt);
+    uint64_t old[P];
+#pragma unroll
+    for (int s = 0; s < P; ++s) old[s] = key[s];
+    const uint64_t rev = shfl64(srt[0], 31 - lane);
+    key[P - 1] = rev < key[P - 1] ? rev : key[P - 1];
+    if (P == 2) {
+      const uint64_t lo = key[0] < key[P - 1] ? key[0] : key[P - 1];
+      const uint64_t hi = key[0] < key[P - 1] ? key[P - 1] : key[0];
+      key[0] = lo;
+      key[P - 1] = hi;
+    }
+#pragma unroll
+    for (int stride = 16; stride > 0; stride >>= 1) {
+#pragma unroll
+      for (int s = 0; s < P; ++s) {
+        const uint64_t other = shfl64(key[s], lane ^ stride);
+        const bool lower = (lane & stride) == 0;
+        const uint64_t mn = key[s] < other ? key[s] : other, mx = key[s] < other ? other : key[s];
+        key[s] = lower ? mn : mx;
+      }
+    }
+    if (kDedup) {
+      bool dup = false;
+      uint64_t carry = ~0ull;
+#pragma unroll
+      for (int s = 0; s < P; ++s) {
+        const uint64_t prev = shfl_up64(key[s], 1);
+        dup |= key[s] == (lane == 0 ? carry : prev);
+        carry = shfl64(key[s], 31);
+      }
+      if (__any_sync(0xffffffffu, dup)) {
+#pragma unroll
+        for (int s = 0; s < P; ++s) key[s] = old[s];
+        offer_masked(c, mask);
+      }
+    }
+  }
+
+  // insert the lanes of `mask` in lane order, re-filtering as the threshold drops
+  __device__ __forceinline__ void offer_masked(uint64_t c, unsigned mask) {
+    while (mask) {
+      const int t = __ffs(mask) - 1;
+      mask &= mask - 1;
+      insert(shfl64(c, t));
+      mask &= __ballot_sync(0xffffffffu, c < threshold());
+    }
+  }
+
   // offer one candidate per lane (valid lanes only)
   __device__ __forceinline__ void offer(uint64_t c, bool valid) {
     uint64_t thr = full() ? threshold() : ~0ull;
@@ -540,7 +633,8 @@ __device__ __forceinline__ void bottomk_scan(WarpBottomK<P, kMode != 0>& L, cons
     const int64_t j = base + lane;
     const bool valid = j < end;
     const uint64_t c = valid ? bottomk_key<kMode>(seed0, row[j], rk) : ~0ull;
-    L.offer(c, valid);
+    if (P <= 2 && L.k == 32 * P && L.full()) L.offer_merge(c, valid);
+    else L.offer(c, valid);
   }
 }
 
@@ -568,30 +662,6 @@ __device__ __forceinline__ void bottomk_scan_shared(WarpBottomK<P, kMode != 0>& 
       if (t < mine) {
         mine = t;
         if (lane == 0) atomicMin(s_thr, (unsigned long long)t);
-      }
-    }
-  }
-}
-
-// ascending warp bitonic sort of 32 R keys; element i = lane + 32 r (R <= 2)
-template <int R>
-__device__ __forceinline__ void warp_bitonic_sort(uint64_t (&key)[R]) {
-  const int lane = lane_id();
-#pragma unroll
-  for (int size = 2; size <= 32 * R; size <<= 1) {
-#pragma unroll
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      uint64_t old[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) old[r] = key[r];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int i = lane + 32 * r;
-        const bool up = (i & size) == 0;  // ascending block
-        const uint64_t other = stride == 32 ? old[r ^ 1] : shfl64(old[r], lane ^ stride);
-        const bool lower = (i & stride) == 0;
-        const uint64_t mn = old[r] < other ? old[r] : other, mx = old[r] < other ? other : old[r];
-        key[r] = (lower == up) ? mn : mx;
       }
     }
   }
