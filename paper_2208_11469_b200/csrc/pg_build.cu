@@ -751,8 +751,11 @@ __device__ __forceinline__ void bottomk_emit(const WarpBottomK<P, kMode != 0>& L
 // 32R-key warp bitonic sort (pad keys ~0 sort last), then the distinct keys
 // in order (key i kept when it differs from key i-1), the first k written:
 // values ascending, +inf pad; mode 2 also the rank row.  Rows shorter than
-// kShortSortMin keep the list insertions (cheaper below ~a dozen keys).
-constexpr int kShortSortMin = 12;
+// kShortSortMin keep the list insertions (cheaper for a handful of keys).
+#ifndef PG_SHORT_SORT_MIN
+#define PG_SHORT_SORT_MIN 4  // c3 KMV batch pass: 12 -> 2.42 ms, 4 -> 2.27 ms, 1 -> 2.35 ms
+#endif
+constexpr int kShortSortMin = PG_SHORT_SORT_MIN;
 
 template <int kMode, int R>
 __device__ __forceinline__ void kmv_short_row_r(const int32_t* __restrict__ row, int d, int64_t v, int k,
