@@ -1,26 +1,31 @@
 #!/usr/bin/env python
 """Benchmark: edge-intersections/s of the fused Bloom triangle-count pass.
 
-Workload (BASELINE.json configs[1], the metric's config that fits one GPU):
-R-MAT scale 20, edge factor 16, seed 1 (15.7 M undirected edges), Bloom
-sketches B=1024, b=2, seed DEFAULT_HASH_SEED; one step = one
-``tc_estimate(graph, sketched, "bf_and")`` pass over every edge (the fused
-gather + AND + popcount + histogram kernel) plus, for N>1, the NCCL
-all-reduce of the popcount histogram.  Other configs are parity-test cases.
+Workload (BASELINE.json configs[4], the metric's "1/2/4/8 B200" config; it
+fits one GPU): R-MAT scale 24, edge factor 16, seed 4 (260.4 M undirected
+edges), Bloom sketches B=2048, b=2, seed DEFAULT_HASH_SEED; one step = one
+``tc_estimate(graph, sketched, "bf_and")`` pass over every edge of this
+rank's shard (the fused gather + AND + popcount + histogram kernel) plus, for
+N>1, the NCCL all-reduce of the popcount histogram.  The other configs are
+parity-test cases (and ``secondary`` lines).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
+``--gpus N`` outside torchrun re-launches itself under
+``torch.distributed.run`` with N ranks (one per GPU, 127.0.0.1 rendezvous).
 One JSON line on rank 0.  ``--impl reference`` times the reference's CPU
-algorithm (oracle/ numpy port: the reference's own vectorised strategy and
-16,384-edge thread-pool grid) on the host's cores.
+algorithm on the host's cores: the graph from the oracle's C restatement of
+the reference generator, Bloom rows from the oracle's C builder, and the
+oracle's numpy port of the reference's chunked thread-pool pass -- no code of
+the product package is imported on that arm.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,8 +40,8 @@ sys.path.insert(0, REPO)
 WORKLOAD = {
     "c2": dict(desc="R-MAT s20 ef16 seed1 (a,b,c,d=.57,.19,.19,.05), Bloom B=1024 b=2, "
                     "tc_estimate bf_and", scale=20, ef=16, seed=1, bits=1024, b=2),
-    "c5": dict(desc="R-MAT s24 ef16 seed4, Bloom B=2048 b=2, tc_estimate bf_and",
-               scale=24, ef=16, seed=4, bits=2048, b=2),
+    "c5": dict(desc="R-MAT s24 ef16 seed4 (a,b,c,d=.57,.19,.19,.05), Bloom B=2048 b=2, "
+                    "tc_estimate bf_and", scale=24, ef=16, seed=4, bits=2048, b=2),
 }
 METRIC = "edge-intersections/s (BF/MinHash TC) at 1/2/4/8 B200; % of HBM roofline"
 
@@ -44,16 +49,16 @@ METRIC = "edge-intersections/s (BF/MinHash TC) at 1/2/4/8 B200; % of HBM rooflin
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=sorted(WORKLOAD), default="c2")
+    ap.add_argument("--config", choices=sorted(WORKLOAD), default="c5")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=15)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-busy", action="store_true",
                     help="skip the untimed clock-sampling tail (for ncu runs)")
     ap.add_argument("--no-secondary", action="store_true",
-                    help="skip the per-config measurements of configs 1, 3, 4, 5")
+                    help="skip the per-config measurements of configs 1-4 and 5b")
     return ap.parse_args()
 
 
@@ -64,9 +69,28 @@ def dist_env():
     return rank, world, local
 
 
-def make_graph(cfg):
-    from paper_2208_11469_b200.graphs import generate_kronecker
-    return generate_kronecker(cfg["scale"], cfg["ef"], cfg["seed"])
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> int:
+    """Re-run this command under torch.distributed.run with n ranks."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes", "1",
+           "--nproc-per-node", str(n), "--master-addr", "127.0.0.1",
+           "--master-port", str(_free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def config_dict(args, cfg, n, m):
+    """The workload description both arms print (same keys and values)."""
+    return {"workload": f"{args.config}: {cfg['desc']}", "n": int(n), "m": int(m),
+            "sketch_bytes": int(n) * cfg["bits"] // 8,
+            "l2": "flushed between timed steps (256 MiB write, outside the events); "
+                  "the sketch matrix exceeds L2 at c5",
+            "parallelism": (f"edge-range shards x{args.gpus}, replicated sketches, NCCL "
+                            "all_reduce(int64[B+2])") if args.gpus > 1 else "1 GPU"}
 
 
 # ---------------------------------------------------------------------------
@@ -139,14 +163,14 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(config: str, key: str = "dram_bytes_per_launch"):
-    """Per-launch bytes of the TC kernel from the committed ncu summary."""
+def load_profile(config: str) -> dict:
+    """The committed ncu summary of this config's TC kernel (profiles/)."""
     path = os.path.join(REPO, "profiles", "ncu_summary.json")
     try:
         with open(path) as fh:
-            return json.load(fh).get(config, {}).get(key)
+            return json.load(fh).get(config, {})
     except Exception:
-        return None
+        return {}
 
 
 # ---------------------------------------------------------------------------
@@ -169,14 +193,13 @@ def run_ours(args, cfg, rank, world, local):
     from paper_2208_11469_b200.sharding import allreduce_counts, edge_range
 
     t0 = time.time()
-    g = make_graph(cfg)
+    g = pg.generate_kronecker(cfg["scale"], cfg["ef"], cfg["seed"])  # on the device
     gen_s = time.time() - t0
     bits, b = cfg["bits"], cfg["b"]
     stream = torch.cuda.current_stream()
 
     # sketch build on the device (reported separately, not in the timed step)
     dev = g.device()
-    us, vs = dev.upper_edges()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     build_ms = []
@@ -187,20 +210,26 @@ def run_ours(args, cfg, rank, world, local):
         torch.cuda.synchronize()
         build_ms.append(ev0.elapsed_time(ev1))
     provider = pg.make_provider("bf_and", sketched=sk)
-    m = us.numel()
-    # the fused kernel's edge-slot layout (rows padded to its lane-group size)
-    lus, lvs, slots, padded = provider._tc_layout(dev)
+    m = g.m
+    # the fused kernel's edge-slot layout
+    t_lay = time.time()
+    lay = provider._tc_layout(dev)
+    torch.cuda.synchronize()
+    layout_s = time.time() - t_lay
+    lus, lvs, slots, padded = lay[:4]
     e_begin, e_end = edge_range(slots, rank, world, align=32 if padded else 1)
-    rank_edges = int(((lvs[e_begin:e_end] >= 0).sum()).item())
+    rank_edges = int(((lvs[e_begin:e_end] != -1).sum()).item())
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def l2_flush():
         N.call("pg_l2_flush", N.ptr(flush), flush.numel(), N.stream_handle())
 
+    def kernel():
+        return provider._tc_counts_layout(lay, e_begin, e_end)
+
     def step():
-        counts = provider._tc_counts(lus, lvs, e_begin, e_end, padded)
-        return allreduce_counts(counts)
+        return allreduce_counts(kernel())
 
     for _ in range(args.warmup):
         step()
@@ -209,15 +238,15 @@ def run_ours(args, cfg, rank, world, local):
         import torch.distributed as dist
         dist.barrier()
 
-    # one CUDA graph per step (kernel + all-reduce: one launch, no host gaps
-    # -- they matter at N=8 where a rank's kernel is ~26 us) and a
-    # kernel-only graph for the roofline's kernel time; eager if capture fails
+    # one CUDA graph per step (kernel + all-reduce: one launch, no host gaps)
+    # and a kernel-only graph for the roofline's kernel time; eager if
+    # capture fails (gloo)
     gstep = gkern = None
     graph_note = None
     try:
         gk, gs = torch.cuda.CUDAGraph(), torch.cuda.CUDAGraph()
         with torch.cuda.graph(gk):
-            provider._tc_counts(lus, lvs, e_begin, e_end, padded)
+            kernel()
         with torch.cuda.graph(gs):
             step()
         gk.replay()
@@ -225,7 +254,8 @@ def run_ours(args, cfg, rank, world, local):
         torch.cuda.synchronize()
         gkern, gstep = gk, gs
     except Exception as exc:  # pragma: no cover - capture unsupported
-        graph_note = f"eager ({type(exc).__name__})"
+        graph_note = f"eager ({type(exc).__name__}: capture failed)"
+        torch.cuda.synchronize()
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
@@ -257,7 +287,7 @@ def run_ours(args, cfg, rank, world, local):
             for i in range(args.steps):
                 l2_flush()  # between timed steps, outside the events
                 starts[i].record(stream)
-                counts = provider._tc_counts(lus, lvs, e_begin, e_end, padded)
+                counts = kernel()
                 kends[i].record(stream)
                 counts = allreduce_counts(counts)
                 ends[i].record(stream)
@@ -266,7 +296,7 @@ def run_ours(args, cfg, rank, world, local):
         # keep the GPU busy for the clock sampler's benefit, untimed
         tq = time.time()
         while not args.no_busy and time.time() - tq < 0.5:
-            provider._tc_counts(lus, lvs, e_begin, e_end, padded)
+            kernel()
         torch.cuda.synchronize()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     kern_ms = [s.elapsed_time(e) for s, e in zip(kstarts, kends)]
@@ -280,28 +310,49 @@ def run_ours(args, cfg, rank, world, local):
         kern_total = sum(kern_ms)
     ms_per_step = total_ms / args.steps
     kern_ms_avg = kern_total / args.steps
-    value = m / (ms_per_step / 1e3)
+    value = m / (ms_per_step / 1e3)  # whole-job edges per second
 
     counts = step().cpu().numpy()
     estimate = provider._tc_combine(counts) / 3.0
 
-    # roofline: algorithmic bytes per launch = edges of this rank x (2 rows + 2 int32)
-    bytes_per_edge = 2 * (bits // 8) + 8
-    launch_bytes = rank_edges * bytes_per_edge
-    achieved = launch_bytes / (kern_ms_avg / 1e3) / 1e9
+    # roofline of the dominant kernel.  achieved = the physical DRAM traffic
+    # of one launch (committed ncu --set full capture of this config) over
+    # the live kernel time; the algorithmic figure (two rows +
+    # two int32 endpoints per edge, no reuse credit) is reported beside it.
     peak, peak_src = load_peaks()
-    traffic = load_traffic(args.config) if world == 1 else None
+    prof = load_profile(args.config) if world == 1 else {}
+    bytes_per_edge = 2 * (bits // 8) + 8
+    alg_gbs = rank_edges * bytes_per_edge / (kern_ms_avg / 1e3) / 1e9
+    traffic = prof.get("dram_bytes_per_launch")
+    phys_gbs = traffic / (kern_ms_avg / 1e3) / 1e9 if traffic else None
+    roofline = {
+        "bound": prof.get("bound", "hbm"),
+        "achieved": phys_gbs if phys_gbs is not None else alg_gbs,
+        "peak": peak, "unit": "GB/s",
+        "frac": (phys_gbs if phys_gbs is not None else alg_gbs) / peak,
+        "traffic": traffic,
+        "achieved_basis": ("physical: ncu dram bytes per launch / live kernel time"
+                           if phys_gbs is not None else "algorithmic (no capture for this N)"),
+        "kernel_ms": kern_ms_avg,
+        "algorithmic": {"bytes_per_edge": bytes_per_edge, "edges_per_launch": rank_edges,
+                        "effective_gbs": alg_gbs, "frac_of_peak": alg_gbs / peak},
+        "l2_to_sm_bytes": prof.get("l2_to_sm_bytes"),
+        "l2_to_sm_tbs": (prof["l2_to_sm_bytes"] / (kern_ms_avg / 1e3) / 1e12
+                         if prof.get("l2_to_sm_bytes") else None),
+        "capture": prof.get("source"),
+        "peak_source": peak_src,
+    }
 
-    # e2e through the public API: pinned host graph + host sketches -> device ->
-    # fused pass -> host estimate, every step
+    # e2e through the public API: pinned host CSR -> device sketches -> fused
+    # pass -> host estimate, every step
     e2e = None
     if rank == 0 and world == 1 and args.e2e_steps > 0:
-        e2e = run_e2e(pg, g, sk, args.e2e_steps, bits, b, m)
+        e2e = run_e2e(pg, g, args.e2e_steps, bits, b, m)
 
     secondary = None
     if rank == 0 and world == 1 and not args.no_secondary:
-        del sk, provider
-        secondary = run_secondary()
+        del sk, provider, lay, lus, lvs
+        secondary = run_secondary(skip=args.config)
 
     out = None
     if rank == 0:
@@ -313,26 +364,15 @@ def run_ours(args, cfg, rank, world, local):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u64",
-            "data": "synthetic (seeded R-MAT, reference generator draw order)",
-            "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "m": m,
-                       "edges_per_rank": rank_edges,
-                       "edge_slots": slots, "row_padded_layout": bool(padded),
-                       "u_per_slot_group": padded == 2,
-                       "sketch_bytes": g.n * bits // 8,
-                       "l2": "flushed between timed steps (256 MiB write, outside the events)",
-                       "parallelism": f"edge-range shards x{world}, replicated sketches, "
-                                      "NCCL all_reduce(int64[B+2])" if world > 1 else "1 GPU"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "bytes_per_edge": bytes_per_edge, "kernel_ms": kern_ms_avg,
-                         "peak_source": peak_src,
-                         # physical picture from the same ncu capture: bytes the
-                         # L2 delivered to the SMs per launch (u rows stay in
-                         # registers across u runs; traffic = what L2 missed)
-                         "l2_to_sm_bytes": load_traffic(args.config, "l2_to_sm_bytes") if world == 1 else None},
+            "data": "synthetic (seeded R-MAT, the reference generator's draw order)",
+            "config": config_dict(args, cfg, g.n, m),
+            "layout": {"edges_per_rank": rank_edges, "edge_slots": slots,
+                       "slot_range": [e_begin, e_end], "kind": provider._tc_layout_name(lay),
+                       "layout_build_s": layout_s},
+            "roofline": roofline,
             "clocks": clk.summary(),
             "gpu_launches": args.steps,
-            "cuda_graph": graph_note or "one graph replay per step",
+            "cuda_graph": graph_note or "one graph replay per step (kernel + all-reduce)",
             "e2e": e2e,
             "cpu_baseline": cpu,
             "secondary": secondary,
@@ -381,15 +421,15 @@ def _time_device(fn, reps=5, warm=2, flush=None, graph=False):
     return statistics.median(ts), out
 
 
-def run_secondary():
+def run_secondary(skip: str = "c5"):
     """The other BASELINE configs, one GPU: per-edge estimator throughput
-    (device-resident inputs, L2 flushed before every timed call)."""
+    (device-resident inputs, L2 flushed before every timed call), each with
+    the oracle port timed on a seeded sample of the same edges."""
     import gc
     import torch
     import paper_2208_11469_b200 as pg
     from paper_2208_11469_b200 import _native as N
-    from paper_2208_11469_b200.mining import (four_clique_counts, jaccard_counts,
-                                              tc_counts)
+    from paper_2208_11469_b200.mining import four_clique_counts, jaccard_counts, tc_counts
     peak, _ = load_peaks()
     flush_buf = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -400,7 +440,7 @@ def run_secondary():
         r = {"graph": name, "n": g.n, "m": g.m, "ms": ms,
              "edge_intersections_per_s": g.m / (ms / 1e3),
              "algorithmic_gbs": g.m * bytes_per_edge / (ms / 1e3) / 1e9,
-             "frac_of_hbm_peak": g.m * bytes_per_edge / (ms / 1e3) / 1e9 / peak}
+             "algorithmic_frac_of_hbm_peak": g.m * bytes_per_edge / (ms / 1e3) / 1e9 / peak}
         r.update(extra)
         return r
 
@@ -408,8 +448,6 @@ def run_secondary():
     port = O.NumpyPort(threads=len(os.sched_getaffinity(0)))
 
     def cpu_leg(g, p, chunk, sample):
-        """The reference's per-edge strategy (numpy port, all host cores) on
-        a seeded edge sample, with the GPU's sum over the same sample."""
         e = g.edges()
         rng = np.random.default_rng(0)
         idx = np.sort(rng.choice(len(e), size=min(sample, len(e)), replace=False))
@@ -419,8 +457,7 @@ def run_secondary():
         dt = time.perf_counter() - t0
         gpu = float(np.sum(p.pair_many(us, vs)))
         return {"cpu_edges_per_s": len(us) / dt, "cpu_sample_edges": int(len(us)),
-                "cpu_cores": port.threads, "cpu_kind": "port",
-                "speedup_vs_cpu": None,
+                "cpu_cores": port.threads, "cpu_kind": "port", "speedup_vs_cpu": None,
                 "cpu_gpu_sample_rel_err": abs(cpu - gpu) / max(1.0, abs(cpu))}
 
     def with_speedup(r, leg):
@@ -428,31 +465,36 @@ def run_secondary():
         r.update(leg)
         return r
 
+    def bloom_tc(key, g, bits, b, sample):
+        sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=b, bits_override=bits)
+        p = pg.make_provider("bf_and", sketched=sk)
+        dev = g.device()
+        p._tc_layout(dev)
+        small = g.m < (1 << 20)
+        ms, c = _time_device(lambda: tc_counts(p, dev), flush=flush, graph=small,
+                             reps=20 if small else 5)
+        r = rec(key, g, ms, 2 * bits // 8 + 8, {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0})
+        rows, sz = sk.bit_matrix, sk.sizes
+        return with_speedup(r, cpu_leg(
+            g, p, lambda a, b_: O.NumpyPort.bloom_chunk(rows, bits, b, "bf_and", sz, a, b_), sample))
+
     out = {}
     try:
-        # config 1: ER G(16384, 262144), Bloom 512/1
         g = pg.generate_erdos_renyi_gnm(16384, 262144, 0)
-        sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=1, bits_override=512)
-        p = pg.make_provider("bf_and", sketched=sk)
-        ms, c = _time_device(lambda: tc_counts(p, g.device()), flush=flush, graph=True, reps=20)
-        r = rec("ER n=16384 m=262144 seed 0", g, ms, 2 * 64 + 8,
-                {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0})
-        rows, sz = sk.bit_matrix, sk.sizes
-        out["c1_bloom512_tc"] = with_speedup(r, cpu_leg(
-            g, p, lambda a, b_: O.NumpyPort.bloom_chunk(rows, 512, 1, "bf_and", sz, a, b_), 1 << 22))
+        out["c1_bloom512_tc"] = bloom_tc("ER n=16384 m=262144 seed 0", g, 512, 1, 1 << 22)
+        if skip != "c2":
+            g = pg.generate_kronecker(20, 16, 1)
+            out["c2_bloom1024_tc"] = bloom_tc("R-MAT s20 ef16 seed 1", g, 1024, 2, 1 << 22)
         # config 3: R-MAT s22 seed 2, 1-Hash k=64 and KMV k=64
         g = pg.generate_kronecker(22, 16, 2)
         for kind, bpe in (("onehash", 2 * 4 * 64 + 16), ("kmv", 2 * 8 * 64 + 24)):
-            # sketch build: CUDA-event time after warm-up builds
             bms, sk = _time_device(lambda: pg.build_sketched_graph(g, kind, s=1.0, k_override=64),
                                    reps=1, flush=flush)
             p = pg.make_provider(kind, sketched=sk)
             ms, c = _time_device(lambda: tc_counts(p, g.device()), reps=3, flush=flush)
             extra = {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0, "build_ms": bms}
             if kind == "kmv":
-                # the rank-directory kernel reads 4-byte global value ranks,
-                # not the 8-byte values the algorithmic figure counts
-                kb = 2 * 4 * 64 + 24
+                kb = 2 * 4 * 64 + 24  # the rank kernel reads 4-byte ranks
                 extra.update(kernel_bytes_per_edge=kb,
                              frac_at_kernel_bytes=g.m * kb / (ms / 1e3) / 1e9 / peak)
             r = rec("R-MAT s22 ef16 seed 2", g, ms, bpe, extra)
@@ -474,24 +516,15 @@ def run_secondary():
         c = c.cpu().numpy()
         r = rec("Chung-Lu n=2^23 avg 32 gamma 2.1 seed 3", g, ms, 2 * 4 * 32 + 8,
                 {"kept_jhat_ge_0.1": int(c[0]), "kept_vertex_similarity_ge_0.1": int(c[1])})
-        # CPU: the reference has no batch Jaccard; SURVEY 8(d) times its
-        # k-Hash gather + positional-match path (tc_estimate(khash))
         ent, sz = sk.entries, sk.sizes
         out["c4_khash32_jaccard"] = with_speedup(r, cpu_leg(
             g, pg.make_provider("khash", sketched=sk),
             lambda a, b_: O.NumpyPort.khash_chunk(ent, 32, sz, a, b_), 1 << 23))
-        del sk, ent
-        # config 5: R-MAT s24 seed 4, Bloom 2048/2
-        g = pg.generate_kronecker(24, 16, 4)
-        sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=2, bits_override=2048)
-        p = pg.make_provider("bf_and", sketched=sk)
-        ms, c = _time_device(lambda: tc_counts(p, g.device()), flush=flush)
-        r = rec("R-MAT s24 ef16 seed 4", g, ms, 2 * 256 + 8,
-                {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0})
-        rows, sz = sk.bit_matrix, sk.sizes
-        out["c5_bloom2048_tc"] = with_speedup(r, cpu_leg(
-            g, p, lambda a, b_: O.NumpyPort.bloom_chunk(rows, 2048, 2, "bf_and", sz, a, b_), 1 << 23))
-        del sk, p, g, rows
+        del sk, ent, g
+        if skip != "c5":
+            g = pg.generate_kronecker(24, 16, 4)
+            out["c5_bloom2048_tc"] = bloom_tc("R-MAT s24 ef16 seed 4", g, 2048, 2, 1 << 23)
+            del g
         gc.collect()
         torch.cuda.empty_cache()
         # config 5b: 4-clique, R-MAT s18 seed 4, Bloom 2048/2 over N+
@@ -524,14 +557,13 @@ def run_secondary():
     return out
 
 
-def run_e2e(pg, g, sk, steps, bits, b, m):
+def run_e2e(pg, g, steps, bits, b, m):
     """Same metric through the public API with HOST inputs every step.
 
     Input: the graph as a host int32 CSR in pinned memory (BASELINE's graph
     format).  Each step: CsrGraph(host arrays) -> build_sketched_graph (H2D of
     the CSR + device sketch build) -> tc_estimate (device edge slots, fused
-    kernel, histogram D2H) -> float.  Shipping prebuilt host sketches instead
-    would add 134 MB of H2D per step, more than building them on the device.
+    kernel, histogram D2H) -> float.
     """
     import torch
 
@@ -553,26 +585,37 @@ def run_e2e(pg, g, sk, steps, bits, b, m):
         torch.cuda.synchronize()
         if i:  # first call is warm-up
             times.append(time.perf_counter() - t0)
+        del graph, skd
     t = statistics.median(times)
     return {"value": m / t, "unit": "edge-intersections/s", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": 8 * (bits + 2), "ms_per_step": t * 1e3,
+            "h2d_floor_ms": None,
             "path": "CsrGraph(pinned int32 CSR) -> build_sketched_graph(bloom, device) -> "
-                    "tc_estimate(bf_and): H2D of the CSR in 8 vertex-range chunks (highest "
-                    "first), per-chunk device sketch build, per-chunk device edge slots and "
-                    "fused kernel as each chunk's sketches land, histogram D2H, host combine",
+                    "tc_estimate(bf_and): chunked H2D of the CSR, per-chunk device sketch "
+                    "build, device edge slots and fused kernel, histogram D2H, host combine",
             "estimate": est}
 
 
 # ---------------------------------------------------------------------------
-# CPU: the reference's algorithm on the host cores
+# CPU: the reference's algorithm on the host cores (oracle/ only)
+
+
+def _cpu_rows(offsets, adjacency, bits, b):
+    from oracle import oracle as O
+    O.C.set_threads(len(os.sched_getaffinity(0)))
+    rows, _ = O.C.build_bloom(offsets, adjacency, bits, b)
+    return rows
 
 
 def cpu_baseline(g, cfg, gpu_estimate, budget_s=12.0):
+    """The oracle port of the reference's tc_estimate on all host cores over
+    the same graph (rows from the C oracle builder, bit-identical to the
+    device's): full passes until budget_s."""
     from oracle import oracle as O
     threads = len(os.sched_getaffinity(0))
     port = O.NumpyPort(threads=threads)
     bits, b = cfg["bits"], cfg["b"]
-    rows, _ = port.build_bloom(g.offsets, g.adjacency, bits, b)
+    rows = _cpu_rows(g.offsets, g.adjacency, bits, b)
     us, vs = O.upper_edges(g.offsets, g.adjacency)
     sizes = np.diff(g.offsets)
 
@@ -598,45 +641,59 @@ def cpu_baseline(g, cfg, gpu_estimate, budget_s=12.0):
 
 
 def run_reference(args, cfg, rank, world):
+    """The reference's CPU path on this host, without the product package:
+    graph = oracle C restatement of generate_kronecker (bit-identical, pinned
+    in tests), rows = oracle C Bloom builder, each step = the numpy port of
+    BloomProvider.pair_many + _chunked_sum over a seeded 2^24-edge slice."""
     if rank != 0:
         return None
     from oracle import oracle as O
     threads = len(os.sched_getaffinity(0))
+    O.C.set_threads(threads)
     port = O.NumpyPort(threads=threads)
-    g = make_graph(cfg)
+    t0 = time.time()
+    off, adj = O.C.generate_kronecker(cfg["scale"], cfg["ef"], cfg["seed"])
+    gen_s = time.time() - t0
     bits, b = cfg["bits"], cfg["b"]
-    rows, _ = port.build_bloom(g.offsets, g.adjacency, bits, b)
-    us, vs = O.upper_edges(g.offsets, g.adjacency)
-    sizes = np.diff(g.offsets)
-    sample = min(len(us), 1 << 21)  # each step: a bounded 2 Mi-edge sample
+    t0 = time.time()
+    rows, _ = O.C.build_bloom(off, adj, bits, b)
+    build_s = time.time() - t0
+    us, vs = O.upper_edges(off, adj)
+    sizes = np.diff(off)
+    n, m = len(off) - 1, len(us)
+    sample = min(m, 1 << 24)
 
     def chunk(a, c):
         return O.NumpyPort.bloom_chunk(rows, bits, b, "bf_and", sizes, a, c)
 
     rng = np.random.default_rng(0)
-    starts = rng.integers(0, max(1, len(us) - sample), size=args.warmup + args.steps)
+    starts = rng.integers(0, max(1, m - sample), size=args.warmup + args.steps)
     for i in range(args.warmup):
         s0 = int(starts[i])
         port.tc_sum(chunk, us[s0:s0 + sample], vs[s0:s0 + sample])
     times = []
     for i in range(args.steps):
         s0 = int(starts[args.warmup + i])
-        t0 = time.perf_counter()
+        t1 = time.perf_counter()
         port.tc_sum(chunk, us[s0:s0 + sample], vs[s0:s0 + sample])
-        times.append(time.perf_counter() - t0)
+        times.append(time.perf_counter() - t1)
     ms = 1e3 * sum(times) / len(times)
     value = sample / (ms / 1e3)
     out = {"metric": METRIC, "value": value, "unit": "edge-intersections/s", "impl": "reference",
            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64",
-           "data": "synthetic (seeded R-MAT)",
-           "config": {"workload": f"{args.config}: {cfg['desc']}", "n": g.n, "m": len(us)},
+           "data": "synthetic (seeded R-MAT, the reference generator's draw order)",
+           "config": config_dict(args, cfg, n, m),
            "cpu_baseline": {"value": value, "unit": "edge-intersections/s", "cores": threads,
                             "kind": "port",
                             "sample": f"per step a contiguous {sample}-edge slice of the "
-                                      "upper edge list (random offset, seed 0)"},
+                                      "upper edge list at a seeded random offset (seed 0); "
+                                      "numpy port of BloomProvider.pair_many + _chunked_sum"},
            "e2e": {"value": value, "unit": "edge-intersections/s", "h2d_bytes_per_step": 0,
-                   "d2h_bytes_per_step": 0}}
+                   "d2h_bytes_per_step": 0},
+           "setup": {"graph_gen_s": gen_s, "bloom_build_s": build_s,
+                     "graph": "oracle C generate_kronecker (pgo_rmat_pairs + "
+                              "pgo_csr_from_pairs), rows from pgo_build_bloom"}}
     print(json.dumps(out), flush=True)
     return out
 
@@ -644,6 +701,10 @@ def run_reference(args, cfg, rank, world):
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     cfg = WORKLOAD[args.config]
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)

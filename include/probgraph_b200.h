@@ -194,6 +194,34 @@ PG_API int pg_tc_bloom_range(const uint64_t* rows, int32_t bits, int32_t op,
                       const int32_t* vs, const int64_t* range_dev, int64_t max_slots,
                       int32_t accumulate, int64_t* out_hist, int64_t* out_sum_pos,
                       void* stream);
+/* ---- degree-oriented, hub-cached Bloom TC (2048-bit rows) ---------------
+ *      same per-edge popcounts as pg_tc_bloom (providers.py:150-162,
+ *      mining.py:105-130), every edge oriented low -> high (degree, ID)
+ *      rank (graphs.py:154-166 degree_order).                             */
+/* Every entry of an oriented CSR (e.g. the N+ lists of pg_degree_order) as
+ * row-padded slots (pad a power of two <= 32, (u, -1) padding): the
+ * pg_csr_upper_edges_padded layout without the v > u filter.  Workspace
+ * from pg_csr_upper_edges_workspace; slots_host receives the count. */
+PG_API int pg_csr_row_slots_padded(const int64_t* offsets, const int32_t* adj, int64_t n,
+                            int32_t pad, int32_t* us, int32_t* vs, int64_t capacity,
+                            int64_t* slots_host, void* workspace, size_t workspace_bytes,
+                            void* stream);
+/* hub_ids[i] = the vertex of rank n - n_hubs + i (rank from
+ * pg_degree_order), and every slot vs[e] >= 0 naming such a vertex becomes
+ * the tag -2 - i (in place). */
+PG_API int pg_hub_tag(const int32_t* rank, int64_t n, int32_t n_hubs, int32_t* vs,
+               int64_t slots, int32_t* hub_ids, void* stream);
+/* most hub rows the engine can stage in one CTA's shared memory (0 when
+ * `bits` has no hub engine) */
+PG_API int pg_tc_bloom_hub_capacity(int32_t bits, int32_t* max_hubs);
+/* pg_tc_bloom over hub-tagged group-u slots (ug[e / 8] = u of slots
+ * [8q, 8q+8), e_begin a multiple of 8): hub v rows read from shared memory.
+ * Same outputs and overwrite semantics as pg_tc_bloom. */
+PG_API int pg_tc_bloom_hub(const uint64_t* rows, int32_t bits, int32_t op,
+                    const int32_t* sizes, const double* lut, const int32_t* ug,
+                    const int32_t* vs, int64_t e_begin, int64_t e_end,
+                    const int32_t* hub_ids, int32_t n_hubs, int64_t* out_hist,
+                    int64_t* out_sum_pos, void* stream);
 /* slot pad of the 1-Hash per-warp-table TC engine for k (the layout pad
  * pg_tc_minhash expects with onehash = 1 and padded = 1; 1 = no such engine
  * for k, padded slots are then not needed) */

@@ -63,13 +63,16 @@ class _C:
                 "pgo_pairs_kmv": [P, P, i32, P, P, P, i64, P, P, P],
                 "pgo_pairs_exact": [P, P, P, P, i64, P],
                 "pgo_4clique_bloom": [i64, P, P, P, i32, i32, P, i32, P, i64, P, P],
+                "pgo_rmat_pairs": [i32, i64, u64, u64, u64, u64, P, P],
+                "pgo_csr_from_pairs": [i64, i64, P, P, P, P],
                 "pgo_num_threads": [],
                 "pgo_set_threads": [i32],
             }
             for name, args in sig.items():
                 f = getattr(L, name)
                 f.argtypes = args
-                f.restype = None if name not in ("pgo_num_threads",) else ctypes.c_int
+                f.restype = {"pgo_num_threads": ctypes.c_int,
+                             "pgo_csr_from_pairs": ctypes.c_int64}.get(name)
             self._lib = L
         return self._lib
 
@@ -81,6 +84,27 @@ class _C:
         out = np.empty(count, dtype=np.uint64)
         self.lib().pgo_family_seeds(base & M64, count, self._p(out))
         return out
+
+    def generate_kronecker(self, scale: int, edge_factor: int, seed: int):
+        """(offsets int64[n+1], adjacency int64[2m]) of the reference's
+        generate_kronecker(scale, edge_factor, seed) (graphs.py:251-276):
+        the same PCG64 draws (pgo_rmat_pairs) and CsrGraph.from_edges
+        (graphs.py:57-89, pgo_csr_from_pairs), in C with OpenMP."""
+        if scale < 1:
+            raise ValueError("scale must be >= 1")
+        n = 1 << scale
+        count = edge_factor * n
+        st = np.random.default_rng(seed).bit_generator.state["state"]
+        src = np.empty(max(1, count), dtype=np.int32)
+        dst = np.empty(max(1, count), dtype=np.int32)
+        self.lib().pgo_rmat_pairs(scale, count, st["state"] >> 64, st["state"] & M64,
+                                  st["inc"] >> 64, st["inc"] & M64, self._p(src), self._p(dst))
+        off = np.empty(n + 1, dtype=np.int64)
+        adj = np.empty(max(1, 2 * count), dtype=np.int64)
+        nnz = self.lib().pgo_csr_from_pairs(n, count, self._p(src), self._p(dst),
+                                            self._p(off), self._p(adj))
+        del src, dst
+        return off, adj[:nnz].copy()
 
     def set_threads(self, t: int):
         self.lib().pgo_set_threads(t)

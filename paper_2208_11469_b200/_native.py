@@ -44,6 +44,13 @@ SIGNATURES = {
                                   c_i64, ctypes.POINTER(c_i64), c_ptr, c_size,
                                   c_ptr],
     "pg_group_pad": [c_i32, ctypes.POINTER(c_i32)],
+    "pg_csr_row_slots_padded": [c_ptr, c_ptr, c_i64, c_i32, c_ptr, c_ptr,
+                                c_i64, ctypes.POINTER(c_i64), c_ptr, c_size,
+                                c_ptr],
+    "pg_hub_tag": [c_ptr, c_i64, c_i32, c_ptr, c_i64, c_ptr, c_ptr],
+    "pg_tc_bloom_hub_capacity": [c_i32, ctypes.POINTER(c_i32)],
+    "pg_tc_bloom_hub": [c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_i64,
+                        c_i64, c_ptr, c_i32, c_ptr, c_ptr, c_ptr],
     "pg_csr_range_slots_workspace": [c_i64, c_i64, ctypes.POINTER(c_size)],
     "pg_csr_range_slots_append": [c_ptr, c_ptr, c_i64, c_i64, c_i32, c_i32, c_i64,
                                   c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_ptr, c_size, c_ptr],

@@ -127,8 +127,10 @@ __global__ void __launch_bounds__(kThreads, PG_BB_MINB) build_bloom_kernel(
     meta->pref[lane] = incl - (int)d;
     meta->off[lane] = o;
     if (lane == 31) meta->pref[32] = incl;
-    uint4* brows4 = reinterpret_cast<uint4*>(brows);
-    for (uint32_t i = lane; i < (uint32_t)R * words32 / 4; i += 32) brows4[i] = make_uint4(0u, 0u, 0u, 0u);
+    // zero the batch rows: 64-bit granularity (R * words64 may be odd, and
+    // then a warp's slot is only 8-byte aligned)
+    uint64_t* brows64 = reinterpret_cast<uint64_t*>(brows);
+    for (uint32_t i = lane; i < (uint32_t)R * words64; i += 32) brows64[i] = 0ull;
     __syncwarp();
     const int total = meta->pref[32];
     int j = 0;  // batch vertex of the lane's current entry (non-decreasing)
@@ -147,8 +149,16 @@ __global__ void __launch_bounds__(kThreads, PG_BB_MINB) build_bloom_kernel(
     // here; pass 2 ORs into them) -- and the non-hub ones (each lane its own
     // row, words read in a lane-rotated order to spread the banks)
     const uint64_t* b64 = reinterpret_cast<const uint64_t*>(brows);
-    uint4* out4 = reinterpret_cast<uint4*>(rows + vb * words64);
-    for (uint32_t i = lane; i < (uint32_t)nb * words64 / 2; i += 32) out4[i] = brows4[i];
+    uint64_t* out = rows + vb * words64;
+    const uint32_t nw = (uint32_t)nb * words64;
+    if (((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(b64)) & 15u) == 0) {
+      const uint4* src4 = reinterpret_cast<const uint4*>(b64);
+      uint4* out4 = reinterpret_cast<uint4*>(out);
+      for (uint32_t i = lane; i < nw / 2; i += 32) out4[i] = src4[i];
+      if ((nw & 1u) && lane == 0) out[nw - 1] = b64[nw - 1];
+    } else {  // odd words64 with an odd row base (chunked builds, R == 1)
+      for (uint32_t i = lane; i < nw; i += 32) out[i] = b64[i];
+    }
     if (mine && !hub) {
       int c = 0;
       for (uint32_t i = 0; i < words64; ++i) c += __popcll(b64[lane * words64 + (i + lane) % words64]);

@@ -15,11 +15,12 @@ namespace pg {
 // first index of row u holding a neighbour > u, and the row's upper count
 __global__ void upper_count_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ adj,
                                    int64_t n, int64_t* __restrict__ first, int64_t* __restrict__ cnt,
-                                   int64_t pad) {
+                                   int64_t pad, bool all) {
   for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < n;
        u += (int64_t)gridDim.x * blockDim.x) {
     int64_t lo = offsets[u], hi = offsets[u + 1];
     const int64_t end = hi;
+    if (all) hi = lo;  // every entry of the row (an oriented CSR)
     while (lo < hi) {  // lower_bound of u+1
       const int64_t mid = (lo + hi) >> 1;
       if (adj[mid] <= u) lo = mid + 1;
@@ -336,7 +337,7 @@ int pg_csr_upper_edges_workspace(int64_t n, int64_t capacity, size_t* out_bytes_
 
 static int upper_edges_impl(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t* us, int32_t* vs,
                             int64_t capacity, int64_t* m_host, void* workspace, size_t workspace_bytes,
-                            void* stream, int64_t pad) {
+                            void* stream, int64_t pad, bool all = false) {
   PG_REQUIRE(n >= 0 && capacity >= 0, "bad sizes");
   PG_REQUIRE(offsets && workspace && m_host, "null pointer");
   size_t need = 0;
@@ -353,7 +354,7 @@ static int upper_edges_impl(const int64_t* offsets, const int32_t* adj, int64_t 
   void* temp = ws + 3 * arr;
   size_t temp_bytes = workspace_bytes - 3 * arr;
   const int grid = sm_count() * 8;
-  upper_count_kernel<<<grid, 256, 0, s>>>(offsets, adj, n, first, cnt, pad);
+  upper_count_kernel<<<grid, 256, 0, s>>>(offsets, adj, n, first, cnt, pad, all);
   if (int rc = check_launch("upper_count")) return rc;
   cudaError_t e = cub::DeviceScan::ExclusiveSum(temp, temp_bytes, cnt, start, n, s);
   if (e != cudaSuccess) return fail(PG_ERR_CUDA, "scan: %s", cudaGetErrorString(e));
@@ -392,6 +393,14 @@ int pg_csr_upper_edges_padded(const int64_t* offsets, const int32_t* adj, int64_
   PG_REQUIRE(pad >= 1 && pad <= 32 && (pad & (pad - 1)) == 0, "pad must be a power of two <= 32");
   return upper_edges_impl(offsets, adj, n, us, vs, capacity, slots_host, workspace, workspace_bytes, stream,
                           pad);
+}
+
+int pg_csr_row_slots_padded(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t pad, int32_t* us,
+                            int32_t* vs, int64_t capacity, int64_t* slots_host, void* workspace,
+                            size_t workspace_bytes, void* stream) {
+  PG_REQUIRE(pad >= 1 && pad <= 32 && (pad & (pad - 1)) == 0, "pad must be a power of two <= 32");
+  return upper_edges_impl(offsets, adj, n, us, vs, capacity, slots_host, workspace, workspace_bytes, stream,
+                          pad, true);
 }
 
 int pg_csr_range_slots_workspace(int64_t rows, int64_t max_slots, size_t* bytes) {

@@ -205,6 +205,52 @@ class DeviceCsr:
             self._layouts[key] = (us[::pad].contiguous(), vs, slots)
         return self._layouts[key]
 
+    def degree_rank(self):
+        """(rank int32[n], N+ offsets int64[n+1], N+ adjacency int32[m]):
+        degree_order on the device (pg_degree_order), cached."""
+        key = ("degree",)
+        if key not in self._layouts:
+            import torch
+            from . import _native as N
+            half = self.nnz // 2
+            rank = torch.empty(max(1, self.n), dtype=torch.int32, device="cuda")
+            off = torch.empty(self.n + 1, dtype=torch.int64, device="cuda")
+            adj = torch.empty(max(1, half), dtype=torch.int32, device="cuda")
+            N.call("pg_degree_order", N.ptr(self.offsets), N.ptr(self.adj), self.n, self.nnz,
+                   N.ptr(rank), N.ptr(off), N.ptr(adj), N.stream_handle())
+            self._layouts[key] = (rank[:self.n], off, adj[:half])
+        return self._layouts[key]
+
+    def hub_slots(self, pad: int, n_hubs: int):
+        """Degree-oriented group-u slots with hub tags (pg_tc_bloom_hub):
+        (ug, vs, slots, hub_ids).  Every edge once, from its lower- to its
+        higher-(degree, ID)-rank endpoint (the N+ lists of degree_order),
+        rows padded to `pad`; vs of the n_hubs highest-ranked vertices is
+        the tag -2 - hub index, hub_ids maps it back."""
+        key = ("hub", pad, n_hubs)
+        if key not in self._layouts:
+            import ctypes
+            import torch
+            from . import _native as N
+            rank, off, adj = self.degree_rank()
+            cap = adj.numel() + (pad - 1) * self.n + 1
+            us = torch.empty(cap, dtype=torch.int32, device="cuda")
+            vs = torch.empty(cap, dtype=torch.int32, device="cuda")
+            ws_bytes = ctypes.c_size_t()
+            N.call("pg_csr_upper_edges_workspace", self.n, cap, ctypes.byref(ws_bytes))
+            ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device="cuda")
+            slots = ctypes.c_int64()
+            N.call("pg_csr_row_slots_padded", N.ptr(off), N.ptr(adj), self.n, pad, N.ptr(us),
+                   N.ptr(vs), cap, ctypes.byref(slots), N.ptr(ws), ws_bytes.value,
+                   N.stream_handle())
+            k = slots.value
+            hub_ids = torch.empty(max(1, n_hubs), dtype=torch.int32, device="cuda")
+            N.call("pg_hub_tag", N.ptr(rank), self.n, n_hubs, N.ptr(vs), k, N.ptr(hub_ids),
+                   N.stream_handle())
+            del ws
+            self._layouts[key] = (us[:k:pad].contiguous(), vs[:k], k, hub_ids)
+        return self._layouts[key]
+
     def row_sources(self):
         """int32 device array src[j] = row of adjacency entry j."""
         if self._src is None:
@@ -372,6 +418,48 @@ class DirectedView:
         return self._dev[0]
 
 
+def as_csr_graph(graph) -> CsrGraph:
+    """This package's CsrGraph for any object with the reference CsrGraph's
+    ``offsets`` / ``adjacency`` arrays (graphs.py:32-56) -- e.g. a graph
+    built by the reference itself.  The wrapper is cached on the object, so
+    its device mirror is uploaded once."""
+    if isinstance(graph, CsrGraph):
+        return graph
+    try:
+        offsets, adjacency = graph.offsets, graph.adjacency
+    except AttributeError as exc:
+        raise TypeError(f"expected a CSR graph (offsets, adjacency): {exc}") from None
+    cached = _ADOPTED.get(id(graph))
+    if cached is not None and cached[0] is graph:
+        return cached[1]
+    g = CsrGraph(offsets, adjacency, getattr(graph, "original_ids", None))
+    _ADOPTED[id(graph)] = (graph, g)
+    return g
+
+
+def as_directed_view(view) -> DirectedView:
+    """This package's DirectedView for any object with the reference
+    DirectedView fields (n, m, rank, offsets, adjacency; graphs.py:132-151)."""
+    if isinstance(view, DirectedView):
+        return view
+    try:
+        fields = (int(view.n), int(view.m), np.asarray(view.rank, dtype=np.int64),
+                  np.asarray(view.offsets, dtype=np.int64), np.asarray(view.adjacency))
+    except AttributeError as exc:
+        raise TypeError(f"expected a degree-ordered view: {exc}") from None
+    cached = _ADOPTED.get(id(view))
+    if cached is not None and cached[0] is view:
+        return cached[1]
+    v = DirectedView(*fields)
+    _ADOPTED[id(view)] = (view, v)
+    return v
+
+
+# id(foreign object) -> (object, adopted wrapper); keeps the object alive so
+# the id is not reused while the entry exists
+_ADOPTED: dict = {}
+
+
 def degree_order(graph: CsrGraph) -> DirectedView:
     """Keep u in N+(v) iff (deg v, v) < (deg u, u) (reference graphs.py:154-166).
 
@@ -379,6 +467,7 @@ def degree_order(graph: CsrGraph) -> DirectedView:
     device (pg_degree_order) and the view keeps them resident; host arrays
     are copied back for the reference contract.
     """
+    graph = as_csr_graph(graph)
     if graph.n > 0 and _cuda_available():
         return _degree_order_device(graph)
     return _degree_order_host(graph)

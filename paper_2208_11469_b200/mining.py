@@ -25,10 +25,10 @@ import numpy as np
 
 from . import _native as N
 from .estimators import EstimatorKind, swamidass_table
-from .graphs import CsrGraph, DirectedView, degree_order
+from .graphs import CsrGraph, DirectedView, as_csr_graph, as_directed_view, degree_order
 from .providers import (BloomProvider, ExactProvider, IntersectionProvider,
                         UnsupportedCombinationError, make_provider)
-from .sketches import SketchedGraph, SketchKind
+from .sketches import SketchedGraph, SketchKind, as_sketched_graph
 
 __all__ = ["SimilarityMeasure", "ClusterResult", "JaccardCount", "LinkPredSplit",
            "triangle_count", "tc_estimate", "tc_counts", "four_clique_count",
@@ -58,6 +58,7 @@ def _is_exact(kind: EstimatorKind) -> bool:
 def triangle_count(view: DirectedView, provider: IntersectionProvider,
                    threads: int = 1):
     """Sum of |N+v & N+u| over directed edges (exact int for exact providers)."""
+    view = as_directed_view(view)
     dev = view.device()
     if isinstance(provider, ExactProvider):
         # fused intersections + sum over the provider's CSR
@@ -74,7 +75,9 @@ def triangle_count(view: DirectedView, provider: IntersectionProvider,
 
 
 def _tc_provider(graph: CsrGraph, sketched, kind):
-    kind = EstimatorKind(kind)
+    kind = EstimatorKind(getattr(kind, "value", kind))
+    if sketched is not None:
+        sketched = as_sketched_graph(sketched)
     if _is_exact(kind):
         return make_provider(kind, graph=graph)
     if sketched is None:
@@ -98,9 +101,9 @@ def tc_counts(provider, dev, rank: int = 0, world: int = 1):
             1, dtype=torch.int64, device="cuda")
     if world == 1 and _chunk_pipelined(provider, dev):
         return _tc_counts_chunked(provider, dev)
-    us, vs, slots, padded = provider._tc_layout(dev)
-    b, e = edge_range(slots, rank, world, align=32 if padded else 1)
-    return provider._tc_counts(us, vs, b, e, padded)
+    lay = provider._tc_layout(dev)
+    b, e = edge_range(lay.slots, rank, world, align=32 if lay.padded else 1)
+    return provider._tc_counts_layout(lay, b, e)
 
 
 def _chunk_pipelined(provider, dev) -> bool:
@@ -184,6 +187,7 @@ def tc_combine(provider, counts: np.ndarray) -> float:
 def tc_estimate(graph: CsrGraph, sketched: SketchedGraph | None = None,
                 kind=EstimatorKind.BF_AND, threads: int = 1) -> float:
     """(1/3) * sum over undirected edges of the intersection estimate."""
+    graph = as_csr_graph(graph)
     provider = _tc_provider(graph, sketched, kind)
     counts = tc_counts(provider, graph.device()).cpu().numpy()
     return tc_combine(provider, counts) / 3.0
@@ -197,6 +201,7 @@ def four_clique_count(view: DirectedView, provider: IntersectionProvider,
     |N+w & C3| from BF+(w) and BF(C3), fused in one kernel.
     """
     import torch
+    view = as_directed_view(view)
     dev = view.device()
     src, nnz = dev.row_sources(), dev.nnz
     if isinstance(provider, ExactProvider):
@@ -254,7 +259,8 @@ def vertex_similarity(u: int, v: int, measure, provider: IntersectionProvider,
                       graph: CsrGraph) -> float:
     if u == v:
         raise ValueError("vertex similarity needs two distinct vertices")
-    measure = SimilarityMeasure(measure)
+    graph = as_csr_graph(graph)
+    measure = SimilarityMeasure(getattr(measure, "value", measure))
     du, dv = graph.degree(u), graph.degree(v)
     if measure in _COUNTING:
         c = float(provider.pair(u, v))
@@ -300,6 +306,7 @@ def jarvis_patrick_cluster(graph: CsrGraph, provider: IntersectionProvider,
     kept edge list comes back to the host.
     """
     import torch
+    graph = as_csr_graph(graph)
     us, vs = graph.device().upper_edges()
     scores = provider._pairs_device(us, vs).to(torch.float64)
     keep = torch.empty(max(1, us.numel()), dtype=torch.uint8, device="cuda")
@@ -339,6 +346,7 @@ def jaccard_counts(graph: CsrGraph, sketched: SketchedGraph, tau: float,
     import torch
     from .providers import MinHashProvider
     from .sharding import edge_range
+    graph, sketched = as_csr_graph(graph), as_sketched_graph(sketched)
     if sketched.kind is not SketchKind.KHASH:
         raise ValueError("Jaccard clustering needs k-Hash sketches")
     k = sketched.capacity

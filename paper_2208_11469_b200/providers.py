@@ -29,8 +29,9 @@ from .estimators import (EstimatorKind, est_intersection_kmv,
                          est_intersection_minhash, swamidass_table,
                          swamidass_value)
 from .graphs import CsrGraph, DeviceCsr, DirectedView
-from .sketches import (SketchKind, SketchedGraph, build_bloom, build_khash,
-                       build_kmv, build_onehash)
+from .graphs import as_csr_graph, as_directed_view
+from .sketches import (SketchKind, SketchedGraph, as_sketched_graph, build_bloom,
+                       build_khash, build_kmv, build_onehash)
 
 __all__ = ["UnsupportedCombinationError", "IntersectionProvider",
            "ExactProvider", "BloomProvider", "MinHashProvider", "KmvProvider",
@@ -156,9 +157,27 @@ class ExactProvider(IntersectionProvider):
         return np.intersect1d(a, b, assume_unique=True)
 
 
+class TcLayout:
+    """Edge slots of a fused whole-graph pass: (us, vs, slots, padded)
+    unpack like a tuple; ``kind`` names the schedule ("id": every edge u < v
+    in CSR order; "hub": degree-oriented with hub tags, ``hub_ids``)."""
+
+    __slots__ = ("us", "vs", "slots", "padded", "kind", "hub_ids", "n_hubs")
+
+    def __init__(self, us, vs, slots, padded, kind="id", hub_ids=None, n_hubs=0):
+        self.us, self.vs, self.slots, self.padded = us, vs, slots, padded
+        self.kind, self.hub_ids, self.n_hubs = kind, hub_ids, n_hubs
+
+    def __iter__(self):
+        return iter((self.us, self.vs, self.slots, self.padded))
+
+    def __getitem__(self, i):
+        return (self.us, self.vs, self.slots, self.padded)[i]
+
+
 class _SketchProvider(IntersectionProvider):
     def __init__(self, sketched: SketchedGraph):
-        self.sketched = sketched
+        self.sketched = as_sketched_graph(sketched)
 
     @property
     def sizes(self) -> np.ndarray:
@@ -173,9 +192,21 @@ class _SketchProvider(IntersectionProvider):
         pad = self.tc_pad()
         if pad > 1:
             us, vs, slots = dev.upper_edges_padded(pad)
-            return us, vs, slots, True
+            return TcLayout(us, vs, slots, True)
         us, vs = dev.upper_edges()
-        return us, vs, us.numel(), False
+        return TcLayout(us, vs, us.numel(), False)
+
+    def _tc_counts_layout(self, lay, e_begin: int, e_end: int):
+        """The fused pass over slots [e_begin, e_end) of a _tc_layout."""
+        return self._tc_counts(lay.us, lay.vs, e_begin, e_end, lay.padded)
+
+    @staticmethod
+    def _tc_layout_name(lay) -> str:
+        if lay.kind == "hub":
+            return (f"degree-oriented group-u slots (pad 8), {lay.n_hubs} hub rows staged "
+                    "in shared memory per CTA")
+        return {0: "upper edges u < v (CSR order)", 1: "row-padded upper edges",
+                2: "row-padded upper edges, one u per slot group"}[int(lay.padded)]
 
     def _dev(self) -> dict:
         return self.sketched.device_tensors()
@@ -201,9 +232,10 @@ class BloomProvider(_SketchProvider):
     """Bloom estimates; ``kind`` picks the AND, limit or OR form."""
 
     def __init__(self, sketched: SketchedGraph, kind: EstimatorKind):
+        sketched = as_sketched_graph(sketched)
         if sketched.kind is not SketchKind.BLOOM:
             raise ValueError("BloomProvider needs Bloom sketches")
-        kind = EstimatorKind(kind)
+        kind = EstimatorKind(getattr(kind, "value", kind))
         if kind not in (EstimatorKind.BF_AND, EstimatorKind.BF_L,
                         EstimatorKind.BF_OR):
             raise ValueError(f"{kind} is not a Bloom estimator")
@@ -247,14 +279,44 @@ class BloomProvider(_SketchProvider):
     def tc_pad(self) -> int:
         return N.group_pad(self.sketched.bit_length // 8)
 
+    def hub_capacity(self) -> int:
+        """Hub rows the degree-oriented engine stages per CTA (0: none for
+        this row width, or disabled with PG_TC_HUB=0)."""
+        import ctypes
+        import os
+        if os.environ.get("PG_TC_HUB", "1") == "0":
+            return 0
+        cap = ctypes.c_int32()
+        N.call("pg_tc_bloom_hub_capacity", self.sketched.bit_length, ctypes.byref(cap))
+        env = os.environ.get("PG_TC_HUBS")
+        return min(cap.value, int(env)) if env else cap.value
+
     def _tc_layout(self, dev):
-        """Bloom TC: the row-padded layout with one u per slot group
-        (padded mode 2 of pg_tc_bloom)."""
+        """Bloom TC: 2048-bit rows take the degree-oriented hub-cached
+        schedule (pg_tc_bloom_hub); other widths the row-padded layout with
+        one u per slot group (padded mode 2 of pg_tc_bloom)."""
+        cap = self.hub_capacity()
+        if cap > 0 and dev.n > 0:
+            n_hubs = min(cap, dev.n)
+            ug, vs, slots, hub_ids = dev.hub_slots(8, n_hubs)
+            return TcLayout(ug, vs, slots, 2, "hub", hub_ids, n_hubs)
         pad = self.tc_pad()
         if pad > 1:
             ug, vs, slots = dev.upper_edges_group_u(pad)
-            return ug, vs, slots, 2
+            return TcLayout(ug, vs, slots, 2)
         return super()._tc_layout(dev)
+
+    def _tc_counts_layout(self, lay, e_begin: int, e_end: int):
+        if lay.kind != "hub":
+            return super()._tc_counts_layout(lay, e_begin, e_end)
+        import torch
+        d, sg = self._dev(), self.sketched
+        out = torch.empty(sg.bit_length + 2, dtype=torch.int64, device="cuda")
+        N.call("pg_tc_bloom_hub", N.ptr(d["rows"]), sg.bit_length, self.op,
+               N.ptr(d["sizes"]), N.ptr(self.lut_device()), N.ptr(lay.us), N.ptr(lay.vs),
+               e_begin, e_end, N.ptr(lay.hub_ids), lay.n_hubs, N.ptr(out),
+               N.ptr(out) + 8 * (sg.bit_length + 1), N.stream_handle())
+        return out
 
     def _tc_counts(self, us, vs, e_begin: int, e_end: int, padded: bool = False):
         import torch
@@ -305,6 +367,7 @@ class MinHashProvider(_SketchProvider):
     """k-Hash or 1-Hash estimates from entry matrices."""
 
     def __init__(self, sketched: SketchedGraph):
+        sketched = as_sketched_graph(sketched)
         if sketched.kind is SketchKind.KHASH:
             self.kind = EstimatorKind.KHASH
         elif sketched.kind is SketchKind.ONEHASH:
@@ -383,6 +446,7 @@ class MinHashProvider(_SketchProvider):
 
 class KmvProvider(_SketchProvider):
     def __init__(self, sketched: SketchedGraph):
+        sketched = as_sketched_graph(sketched)
         if sketched.kind is not SketchKind.KMV:
             raise ValueError("KmvProvider needs KMV sketches")
         super().__init__(sketched)
@@ -448,7 +512,16 @@ class KmvProvider(_SketchProvider):
 def make_provider(kind, *, graph: CsrGraph | None = None,
                   view: DirectedView | None = None,
                   sketched: SketchedGraph | None = None) -> IntersectionProvider:
-    kind = EstimatorKind(kind)
+    """Reference providers.py:310-338.  Graphs, views and sketches may be
+    this package's objects or any objects with the reference's fields
+    (adopted by value: as_csr_graph / as_directed_view / as_sketched_graph)."""
+    kind = EstimatorKind(getattr(kind, "value", kind))
+    if graph is not None:
+        graph = as_csr_graph(graph)
+    if view is not None:
+        view = as_directed_view(view)
+    if sketched is not None:
+        sketched = as_sketched_graph(sketched)
     if kind in (EstimatorKind.EXACT_MERGE, EstimatorKind.EXACT_GALLOP):
         strategy = "gallop" if kind is EstimatorKind.EXACT_GALLOP else "merge"
         if view is not None:

@@ -31,7 +31,7 @@ __all__ = ["WORD_BITS", "SketchKind", "BudgetError", "BudgetPlan",
            "plan_budget", "BloomSketch", "KHashSketch", "OneHashSketch",
            "KmvSketch", "build_bloom", "build_khash", "build_onehash",
            "build_kmv", "SketchedGraph", "build_sketched_graph",
-           "dump_sketches", "load_sketches"]
+           "dump_sketches", "load_sketches", "as_sketched_graph"]
 
 WORD_BITS = 64
 
@@ -332,6 +332,42 @@ class SketchedGraph:
         return self.extra_bits_used() // 8
 
 
+def as_sketched_graph(obj) -> SketchedGraph:
+    """This package's SketchedGraph for any object exposing the reference
+    SketchedGraph fields (sketches.py:244-307: kind, plan, family, source,
+    sizes and the kind's bit_matrix/ones, entries(/lengths) or
+    values/lengths host arrays) -- e.g. sketches built or loaded by the
+    reference itself.  Enums are matched by value, the arrays are uploaded
+    on first device use, and the wrapper is cached on the object."""
+    if isinstance(obj, SketchedGraph):
+        return obj
+    from .graphs import _ADOPTED
+    cached = _ADOPTED.get(id(obj))
+    if cached is not None and cached[0] is obj:
+        return cached[1]
+    try:
+        kind = SketchKind(getattr(obj.kind, "value", obj.kind))
+        p, fam = obj.plan, obj.family
+        plan = BudgetPlan(kind, float(p.s), int(p.bits_per_vertex), int(p.entries_per_vertex),
+                          int(p.hash_count), int(p.total_bits), int(p.budget_bits))
+        family = HashFamily(int(fam.base_seed), int(fam.count),
+                            getattr(fam, "algorithm", "mix64"))
+        source = str(getattr(obj.source, "value", obj.source))
+        sizes = np.asarray(obj.sizes, dtype=np.int64)
+    except AttributeError as exc:
+        raise TypeError(f"expected a SketchedGraph: {exc}") from None
+
+    def arr(name):
+        a = getattr(obj, name, None)
+        return None if a is None else np.asarray(a)
+
+    sg = SketchedGraph(kind, plan, family, source, sizes, bit_matrix=arr("bit_matrix"),
+                       ones=arr("ones"), entries=arr("entries"), lengths=arr("lengths"),
+                       values=arr("values"))
+    _ADOPTED[id(obj)] = (obj, sg)
+    return sg
+
+
 def _launch_builders(dev: DeviceCsr, kind: SketchKind, plan: BudgetPlan, seeds, out,
                      v0: int, v1: int, stream: int) -> None:
     """Build the sketches of vertices [v0, v1) into the rows of `out`."""
@@ -455,7 +491,11 @@ def build_sketched_graph(graph: CsrGraph, kind, s: float, b: int = 1,
                          k_override: int | None = None,
                          bits_override: int | None = None) -> SketchedGraph:
     """Sketch every neighbourhood on the device (reference :399-451)."""
-    kind = SketchKind(kind)
+    from .graphs import as_csr_graph, as_directed_view
+    graph = as_csr_graph(graph)
+    if view is not None:
+        view = as_directed_view(view)
+    kind = SketchKind(getattr(kind, "value", kind))
     if source == "undirected":
         host_off, dev_src = graph.offsets, graph
     elif source == "directed":

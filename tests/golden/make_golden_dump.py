@@ -37,3 +37,28 @@ view = R.degree_order(g)
 sk = R.build_sketched_graph(g, "bloom", s=1.0, b=2, bits_override=256, seed=16, source="directed", view=view)
 R.dump_sketches(sk, os.path.join(out, "bloom_directed.bin"))
 print(sorted(os.listdir(out)))
+
+# reference results on the same sketches, for the plugin-boundary tests
+# (tests/test_gpu_plugin_boundary.py): tc_estimate per estimator, per-edge
+# pair_many doubles, the 4-clique count over the directed Bloom sketches
+import hashlib  # noqa: E402
+import json  # noqa: E402
+
+est_kinds = {"bloom": ["bf_and", "bf_l", "bf_or"], "khash": ["khash"], "onehash": ["onehash"],
+             "kmv": ["kmv"]}
+e = g.edges()
+expected = {"graph": "generate_kronecker(7, 8, 3)", "m": int(g.m)}
+for name in cases:
+    ld = R.load_sketches(os.path.join(out, name + ".bin"))
+    for kind in est_kinds[ld.kind.value]:
+        p = R.make_provider(kind, sketched=ld)
+        pm = p.pair_many(e[:, 0], e[:, 1])
+        expected[f"{name}/{kind}"] = {
+            "tc_estimate": R.tc_estimate(g, ld, kind),
+            "pair_many_sha": hashlib.sha256(np.ascontiguousarray(pm, "<f8").tobytes()).hexdigest()}
+ld = R.load_sketches(os.path.join(out, "bloom_directed.bin"))
+expected["bloom_directed/four_clique_count"] = R.four_clique_count(
+    view, R.make_provider("bf_and", sketched=ld))
+with open(os.path.join(out, "expected.json"), "w") as fh:
+    json.dump(expected, fh, indent=1)
+print(expected)

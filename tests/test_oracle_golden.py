@@ -170,3 +170,27 @@ def test_config2_bloom_checksums():
     import math
     got = math.fsum(float(h) * float(l) for h, l in zip(hist, lut) if h) / 3.0
     assert got == pytest.approx(rec["tc"]["bf_and"], rel=1e-12)
+
+
+def test_oracle_rmat_generator_s20():
+    """The oracle's C restatement of generate_kronecker (graphs.py:251-276,
+    PCG64 draws + CsrGraph.from_edges) reproduces the reference's s20 seed 1
+    CSR byte for byte (config2.json, written by the reference)."""
+    import hashlib
+    from conftest import load_config
+    from oracle import oracle as O
+    cfg = load_config("config2.json")
+    off, adj = O.C.generate_kronecker(20, 16, 1)
+    assert len(adj) // 2 == cfg["m"]
+    assert hashlib.sha256(off.astype("<i8").tobytes()).hexdigest() == cfg["offsets_sha"]
+    assert hashlib.sha256(adj.astype("<i8").tobytes()).hexdigest() == cfg["adjacency_sha"]
+
+
+def test_oracle_rmat_generator_small_matches_numpy():
+    """Small scales against the numpy restatement of the same draws."""
+    from oracle import oracle as O
+    from paper_2208_11469_b200 import graphs as G
+    for scale, ef, seed in ((1, 2, 0), (5, 3, 7), (10, 16, 3)):
+        off, adj = O.C.generate_kronecker(scale, ef, seed)
+        g = G.generate_kronecker(scale, ef, seed, device=False)
+        assert np.array_equal(off, g.offsets) and np.array_equal(adj, g.adjacency)
