@@ -219,6 +219,7 @@ def run_ours(args, cfg, rank, world, local):
     lus, lvs, slots, padded = lay[:4]
     e_begin, e_end = edge_range(slots, rank, world, align=32 if padded else 1)
     rank_edges = int(((lvs[e_begin:e_end] != -1).sum()).item())
+    layout_name = provider._tc_layout_name(lay)
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
@@ -367,7 +368,7 @@ def run_ours(args, cfg, rank, world, local):
             "data": "synthetic (seeded R-MAT, the reference generator's draw order)",
             "config": config_dict(args, cfg, g.n, m),
             "layout": {"edges_per_rank": rank_edges, "edge_slots": slots,
-                       "slot_range": [e_begin, e_end], "kind": provider._tc_layout_name(lay),
+                       "slot_range": [e_begin, e_end], "kind": layout_name,
                        "layout_build_s": layout_s},
             "roofline": roofline,
             "clocks": clk.summary(),

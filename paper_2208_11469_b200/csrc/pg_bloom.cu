@@ -169,6 +169,10 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
     static const char* vc_env = getenv("PG_TC_VCACHE");
     const bool vcache = vc_env ? vc_env[0] != '0' : (padded && w4 == 16);
     const int minb = tc_minb(w4, padded);
+    // Harley-Seal popcount for 256-byte rows (XU-pipe bound once the row
+    // stream hits L1/L2); PG_TC_CSA=0/1 overrides
+    static const char* csa_env = getenv("PG_TC_CSA");
+    const bool csa = csa_env ? csa_env[0] != '0' : w4 >= 16;
     const unsigned char* rb = reinterpret_cast<const unsigned char*>(rows);
     cudaError_t le = cudaSuccess;
     static const bool dyn = [] {
@@ -182,14 +186,16 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
     // one spills 216 bytes there and keeps 2
     ChunkCounter ctr;
     if (dyn && !range_dev && e_end - e_begin >= kDynamicMinSlots && (le = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(le));
+#define PG_WK(W8, MB, VC, PD, SCH)                                                                    \
+  (op == PG_BF_OR ? (csa ? tc_bloom_wide_kernel<W8, OpOrCsa, MB, VC, PD, SCH>                          \
+                         : tc_bloom_wide_kernel<W8, OpOr, MB, VC, PD, SCH>)                            \
+                  : (csa ? tc_bloom_wide_kernel<W8, OpAndCsa, MB, VC, PD, SCH>                         \
+                         : tc_bloom_wide_kernel<W8, OpAnd, MB, VC, PD, SCH>))
 #define PG_W(W8, MB, VC, PD)                                                                          \
   {                                                                                                  \
-    auto k = op == PG_BF_OR ? tc_bloom_wide_kernel<W8, OpOr, MB, VC, PD>                             \
-                            : tc_bloom_wide_kernel<W8, OpAnd, MB, VC, PD>;                           \
-    if (range_dev) k = op == PG_BF_OR ? tc_bloom_wide_kernel<W8, OpOr, MB, VC, PD, 2>               \
-                                      : tc_bloom_wide_kernel<W8, OpAnd, MB, VC, PD, 2>;             \
-    else if (ctr.p) k = op == PG_BF_OR ? tc_bloom_wide_kernel<W8, OpOr, MB, VC, PD, 1>              \
-                                       : tc_bloom_wide_kernel<W8, OpAnd, MB, VC, PD, 1>;            \
+    auto k = PG_WK(W8, MB, VC, PD, 0);                                                               \
+    if (range_dev) k = PG_WK(W8, MB, VC, PD, 2);                                                     \
+    else if (ctr.p) k = PG_WK(W8, MB, VC, PD, 1);                                                    \
     le = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
     if (le != cudaSuccess) return fail(PG_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(le));  \
     const int grid = grid_cap(grid_for_kernel(k, smem), e_end - e_begin, kBlock);                    \
@@ -214,6 +220,7 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
     else PG_WM(8)
 #undef PG_WM
 #undef PG_W
+#undef PG_WK
     return check_launch("tc_bloom_wide");
   }
   if (!fast_w4(w4)) {

@@ -60,6 +60,40 @@ struct OpOr {
     return c;
   }
 };
+// Harley-Seal variants: the 8 words a lane holds per edge pass through four
+// carry-save adders (LOP3s, ALU pipe) so 4 POPC replace 8 -- POPC issues on
+// the XU pipe (16/clk/SM), the ceiling of the 2048-bit rows once the row
+// stream is cached.  Same counts.
+__device__ __forceinline__ void csa3(uint32_t& carry, uint32_t& s, uint32_t a, uint32_t b, uint32_t c) {
+  const uint32_t u = a ^ b;
+  carry = (a & b) | (u & c);
+  s = u ^ c;
+}
+__device__ __forceinline__ int popc8_csa(const uint32_t (&x)[8]) {
+  uint32_t s1, c1, s2, c2, s3, c3, s4, c4;
+  csa3(c1, s1, x[0], x[1], x[2]);
+  csa3(c2, s2, x[3], x[4], x[5]);
+  csa3(c3, s3, s1, s2, x[6]);
+  csa3(c4, s4, c1, c2, c3);
+  return __popc(s3) + __popc(x[7]) + 2 * __popc(s4) + 4 * __popc(c4);  // ones, twos, fours
+}
+struct OpAndCsa : OpAnd {
+  __device__ __forceinline__ static int apply8(const uint32_t (&a)[8], const uint32_t (&b)[8]) {
+    uint32_t x[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) x[w] = a[w] & b[w];
+    return popc8_csa(x);
+  }
+};
+struct OpOrCsa : OpOr {
+  __device__ __forceinline__ static int apply8(const uint32_t (&a)[8], const uint32_t (&b)[8]) {
+    uint32_t x[8];
+#pragma unroll
+    for (int w = 0; w < 8; ++w) x[w] = a[w] | b[w];
+    return popc8_csa(x);
+  }
+};
+
 // k-Hash positional matches: (eu == ev) & (eu >= 0)   (providers.py:197-198)
 struct OpEqPos {
   __device__ __forceinline__ static int apply(uint4 a, uint4 b) {

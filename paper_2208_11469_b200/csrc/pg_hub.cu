@@ -39,31 +39,10 @@ __device__ __forceinline__ uint4 lds128(uint32_t addr) {
   return r;
 }
 
-// carry-save adder: (a + b + c) = s + 2 * carry, bitwise (one LOP3 each)
-__device__ __forceinline__ void csa(uint32_t& carry, uint32_t& s, uint32_t a, uint32_t b, uint32_t c) {
-  const uint32_t u = a ^ b;
-  carry = (a & b) | (u & c);
-  s = u ^ c;
-}
-
 template <class Op, bool kCsa>
 __device__ __forceinline__ int count8(const uint32_t (&a)[8], const uint32_t (&b)[8]) {
-  uint32_t x[8];
-#pragma unroll
-  for (int w = 0; w < 8; ++w) x[w] = std::is_same<Op, OpOr>::value ? (a[w] | b[w]) : (a[w] & b[w]);
-  if (!kCsa) {
-    int c = 0;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) c += __popc(x[w]);
-    return c;
-  }
-  uint32_t s1, c1, s2, c2, s3, c3, s4, c4;
-  csa(c1, s1, x[0], x[1], x[2]);
-  csa(c2, s2, x[3], x[4], x[5]);
-  csa(c3, s3, s1, s2, x[6]);
-  csa(c4, s4, c1, c2, c3);
-  // s3, x7 weigh 1; s4 (twos) 2; c4 (fours) 4
-  return __popc(s3) + __popc(x[7]) + 2 * __popc(s4) + 4 * __popc(c4);
+  if (kCsa) return std::is_same<Op, OpOr>::value ? OpOrCsa::apply8(a, b) : OpAndCsa::apply8(a, b);
+  return Op::apply8(a, b);
 }
 
 // Slot layout (group-u, pad G = 8): ug[e / 8] is the u of slots

@@ -205,6 +205,9 @@ class _SketchProvider(IntersectionProvider):
         if lay.kind == "hub":
             return (f"degree-oriented group-u slots (pad 8), {lay.n_hubs} hub rows staged "
                     "in shared memory per CTA")
+        if lay.kind == "degree":
+            return ("degree-oriented row-padded slots (u = lower (degree, ID) rank, N+ lists "
+                    "of degree_order), one u per slot group")
         return {0: "upper edges u < v (CSR order)", 1: "row-padded upper edges",
                 2: "row-padded upper edges, one u per slot group"}[int(lay.padded)]
 
@@ -279,12 +282,14 @@ class BloomProvider(_SketchProvider):
     def tc_pad(self) -> int:
         return N.group_pad(self.sketched.bit_length // 8)
 
+    DEGREE_ORIENT_MIN_BYTES = 512 << 20
+
     def hub_capacity(self) -> int:
         """Hub rows the degree-oriented engine stages per CTA (0: none for
         this row width, or disabled with PG_TC_HUB=0)."""
         import ctypes
         import os
-        if os.environ.get("PG_TC_HUB", "1") == "0":
+        if os.environ.get("PG_TC_HUB", "0") == "0":
             return 0
         cap = ctypes.c_int32()
         N.call("pg_tc_bloom_hub_capacity", self.sketched.bit_length, ctypes.byref(cap))
@@ -292,9 +297,17 @@ class BloomProvider(_SketchProvider):
         return min(cap.value, int(env)) if env else cap.value
 
     def _tc_layout(self, dev):
-        """Bloom TC: 2048-bit rows take the degree-oriented hub-cached
-        schedule (pg_tc_bloom_hub); other widths the row-padded layout with
-        one u per slot group (padded mode 2 of pg_tc_bloom)."""
+        """Bloom TC edge schedule.  Row widths with a lane-group engine take
+        the row-padded layout with one u per slot group (padded mode 2 of
+        pg_tc_bloom), every edge oriented from its lower- to its higher-
+        (degree, ID)-rank endpoint (the N+ lists of degree_order): the u row
+        held in registers across its run is the low-degree side, and the
+        streamed v rows are the hub side, which stays resident in L1/L2
+        (PG_TC_ORIENT=id: u < v by ID instead).  PG_TC_HUB=1 selects the
+        shared-memory hub engine (pg_tc_bloom_hub, 2048-bit rows).  Every
+        per-edge popcount is symmetric in (u, v), so any schedule yields the
+        same histogram."""
+        import os
         cap = self.hub_capacity()
         if cap > 0 and dev.n > 0:
             n_hubs = min(cap, dev.n)
@@ -302,6 +315,15 @@ class BloomProvider(_SketchProvider):
             return TcLayout(ug, vs, slots, 2, "hub", hub_ids, n_hubs)
         pad = self.tc_pad()
         if pad > 1:
+            # measured (scripts/probe_tc.py): degree orientation wins where
+            # the matrix streams from HBM (c5 4 GiB: 5.48 -> 4.70 ms) and
+            # loses where it is L2-resident (c2 128 MiB: 0.196 -> 0.21 ms)
+            sg = self.sketched
+            big = sg.n * sg.bit_length // 8 > self.DEGREE_ORIENT_MIN_BYTES
+            orient = os.environ.get("PG_TC_ORIENT", "degree" if big else "id")
+            if orient == "degree" and dev.n > 0:
+                ug, vs, slots, _ = dev.hub_slots(pad, 0)
+                return TcLayout(ug, vs, slots, 2, "degree")
             ug, vs, slots = dev.upper_edges_group_u(pad)
             return TcLayout(ug, vs, slots, 2)
         return super()._tc_layout(dev)

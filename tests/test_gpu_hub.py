@@ -87,3 +87,25 @@ def test_hub_sharded_ranges_sum(pg, monkeypatch):
     whole = tc_counts(p, dev).cpu().numpy()
     parts = sum(tc_counts(p, dev, r, 3).cpu().numpy() for r in range(3))
     assert np.array_equal(parts, whole)
+
+
+@pytest.mark.parametrize("bits", [512, 1024, 2048])
+@pytest.mark.parametrize("kind", ["bf_and", "bf_l", "bf_or"])
+def test_degree_orientation_equals_id_orientation(pg, bits, kind, monkeypatch):
+    """The degree-oriented schedule of the wide engine (default) against
+    the ID-oriented one: identical histograms (and BF_OR sums)."""
+    from paper_2208_11469_b200.mining import tc_counts
+    g = pg.generate_kronecker(15, 16, 6)
+    sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=2, bits_override=bits)
+    p = pg.make_provider(kind, sketched=sk)
+    dev = g.device()
+    monkeypatch.setenv("PG_TC_HUB", "0")
+    monkeypatch.setenv("PG_TC_ORIENT", "id")
+    want = tc_counts(p, dev).cpu().numpy()
+    monkeypatch.setenv("PG_TC_ORIENT", "degree")
+    lay = p._tc_layout(dev)
+    assert lay.kind == "degree"
+    got = tc_counts(p, dev).cpu().numpy()
+    assert np.array_equal(got, want)
+    parts = sum(tc_counts(p, dev, r, 4).cpu().numpy() for r in range(4))
+    assert np.array_equal(parts, want)

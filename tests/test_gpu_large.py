@@ -1,6 +1,12 @@
 """Full-size parity (BASELINE configs 3-5) against values the UNMODIFIED
 reference computed in the build container (tests/golden/make_golden_large.py
--> large.json, c5b_sample.npz).  The graphs come from the device generators,
+and make_golden_large2.py -> large.json, c5b_sample.npz).
+
+Bit-exact pins (north star: sketches and per-edge integer counts bit-exact
+on all 5 configs): sha256 of the reference's adjacency (its own generator at
+c3/c5), of every sketch array, of the per-edge pair_many doubles in edge
+order, and the full per-edge integer histograms (AND popcounts at c5, 1-Hash
+matches at c3, k-Hash matches at c4).  The graphs come from the device generators,
 which are pinned bit-exact to the reference generator elsewhere
 (test_gpu_generators.py); the edge counts below re-check that here.
 
@@ -9,6 +15,7 @@ the device reduces exact integer statistics (mining.py docstring); 1e-12
 relative is far inside the north-star 1e-6.
 """
 
+import hashlib
 import json
 import os
 
@@ -73,3 +80,80 @@ def test_c5_bloom2048_tc(pg):
     assert g.m == rec["m"]
     sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=2, bits_override=2048)
     assert pg.tc_estimate(g, sk, "bf_and") == pytest.approx(rec["bf_and"], rel=RTOL)
+
+
+def _sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def _upper(g):
+    return g.device().upper_edges()
+
+
+@pytest.mark.skipif("c3_bitexact" not in LARGE, reason="c3 bit-exact golden not generated")
+def test_c3_bitexact(pg):
+    rec = LARGE["c3_bitexact"]
+    g = pg.generate_kronecker(22, 16, 2)
+    assert g.m == rec["m"]
+    assert _sha(g.offsets.astype("<i8")) == rec["offsets_sha"]
+    assert _sha(g.adjacency.astype("<i8")) == rec["adjacency_sha"]
+    us, vs = _upper(g)
+    sk = pg.build_sketched_graph(g, "onehash", s=1.0, k_override=64)
+    assert _sha(sk.entries.astype("<i8")) == rec["onehash_entries_sha"]
+    assert _sha(sk.lengths.astype("<i8")) == rec["onehash_lengths_sha"]
+    p = pg.make_provider("onehash", sketched=sk)
+    m = p.pair_counts(us, vs)
+    hist = np.bincount(m.cpu().numpy(), minlength=65)
+    assert hist.tolist() == rec["onehash_match_hist"]
+    assert _sha(p.pair_many(us, vs).cpu().numpy().astype("<f8")) == rec["onehash_pair_many_sha"]
+    del sk, p, m
+    sk = pg.build_sketched_graph(g, "kmv", s=1.0, k_override=64)
+    assert _sha(sk.values.astype("<f8")) == rec["kmv_values_sha"]
+    assert _sha(sk.lengths.astype("<i8")) == rec["kmv_lengths_sha"]
+    p = pg.make_provider("kmv", sketched=sk)
+    assert _sha(p.pair_many(us, vs).cpu().numpy().astype("<f8")) == rec["kmv_pair_many_sha"]
+
+
+@pytest.mark.skipif("c4_bitexact" not in LARGE, reason="c4 bit-exact golden not generated")
+def test_c4_bitexact(pg):
+    from paper_2208_11469_b200.mining import similarity_scores
+    rec = LARGE["c4_bitexact"]
+    g = pg.generate_chung_lu(1 << 23, 32, 2.1, 3)
+    assert g.m == rec["m"]
+    assert _sha(g.adjacency.astype("<i8")) == rec["adjacency_sha"]
+    sk = pg.build_sketched_graph(g, "khash", s=1.0, k_override=32)
+    assert _sha(sk.entries.astype("<i8")) == rec["khash_entries_sha"]
+    p = pg.make_provider("khash", sketched=sk)
+    us, vs = _upper(g)
+    assert _sha(p.pair_many(us, vs).cpu().numpy().astype("<f8")) == rec["khash_pair_many_sha"]
+    jc = pg.jaccard_cluster_count(g, sk, 0.1)
+    assert jc.kept_similarity == rec["vertex_similarity_jaccard_ge_0.1"]
+    keys = us.to(torch_int64()) * g.n + vs.to(torch_int64())
+    sims = similarity_scores(g, keys, "jaccard", p).cpu().numpy()
+    assert _sha(sims.astype("<f8")) == rec["vertex_similarity_sha"]
+
+
+def torch_int64():
+    import torch
+    return torch.int64
+
+
+@pytest.mark.skipif("bit_matrix_sha" not in LARGE.get("c5_bitexact", {}),
+                    reason="c5 bit-exact golden not generated")
+def test_c5_bitexact(pg, monkeypatch):
+    from paper_2208_11469_b200.mining import tc_counts
+    rec = LARGE["c5_bitexact"]
+    g = pg.generate_kronecker(24, 16, 4)
+    assert g.m == rec["m"]
+    assert _sha(g.offsets.astype("<i8")) == rec["offsets_sha"]
+    assert _sha(g.adjacency.astype("<i8")) == rec["adjacency_sha"]
+    sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=2, bits_override=2048)
+    assert _sha(sk.bit_matrix.astype("<u8")) == rec["bit_matrix_sha"]
+    assert _sha(sk.ones.astype("<i8")) == rec["ones_sha"]
+    p = pg.make_provider("bf_and", sketched=sk)
+    for orient in ("degree", "id"):  # the bench schedule and the u < v one
+        monkeypatch.setenv("PG_TC_ORIENT", orient)
+        hist = tc_counts(p, g.device()).cpu().numpy()[:-1]
+        assert hist.tolist() == rec["and_popcount_hist"], orient
+    us, vs = _upper(g)
+    assert _sha(p.pair_many(us, vs).cpu().numpy().astype("<f8")) == rec["bf_and_pair_many_sha"]
