@@ -173,9 +173,14 @@ PG_API int pg_pairs_kmv(const double* values, const int32_t* lengths, int32_t k,
  * row-padded layout of pg_csr_upper_edges_padded with pad =
  * pg_group_pad(row bytes) and e_begin a multiple of pad (precondition, not
  * checked: every aligned group of pad slots holds one u).  Slots with
- * vs[j] < 0 are padding and skipped.  pg_tc_bloom also takes 2 = the same
- * layout with us[] holding one u per pad-slot group (us[j / pad], a pad-fold
- * smaller u stream).
+ * vs[j] < 0 are padding and skipped.  pg_tc_bloom, and pg_tc_minhash /
+ * pg_jaccard_count_khash for k-Hash rows of 64/128/256 bytes, also take 2 =
+ * the same layout with us[] holding one u per pad-slot group (us[j / pad], a
+ * pad-fold smaller u stream).  Any orientation of an edge gives the same
+ * per-edge count (every estimator is symmetric in (u, v)), so the slots may
+ * run from the lower- to the higher-(degree, ID)-rank endpoint (the N+ lists
+ * of degree_order) -- the layout the library picks for matrices that stream
+ * from HBM.
  * Bloom TC.
  * out_hist: int64[bits+1] histogram of per-edge popcounts
  * (for PG_BF_OR only edges with raw > 0 are counted, and out_sum_pos
@@ -286,6 +291,42 @@ PG_API int pg_4clique_bloom_edges(const int64_t* dir_off, const int32_t* dir_adj
 PG_API int pg_4clique_exact(const int64_t* dir_off, const int32_t* dir_adj,
                      const int32_t* src, int64_t e_begin, int64_t e_end,
                      int64_t* out_count, void* stream);
+
+/* the same with the w rows N(w) taken from a second CSR (w_off, w_adj): the
+ * ExactProvider's own rows (providers.py:117-118 with_set over
+ * ExactProvider._slice), e.g. a provider built for_graph (undirected N(w))
+ * while C3 comes from the view's N+ lists.  pg_4clique_exact is this with
+ * w_off = dir_off, w_adj = dir_adj. */
+PG_API int pg_4clique_exact_rows(const int64_t* dir_off, const int32_t* dir_adj,
+                     const int32_t* src, int64_t e_begin, int64_t e_end,
+                     const int64_t* w_off, const int32_t* w_adj,
+                     int64_t* out_count, void* stream);
+
+/* 4-clique with MinHash / KMV providers (mining.py:133-154 driving
+ * MinHashProvider.with_set / KmvProvider.with_set, providers.py:234-241,
+ * 303-307): for each directed edge j (edge_ids[j] when edge_ids is not
+ * NULL) C3 = N+u & N+v exactly; the member sketch of C3 (build_khash /
+ * build_onehash / build_kmv, sketches.py:201-237) is built once per edge and
+ * every w in C3 adds est_intersection_minhash / est_intersection_kmv
+ * (estimators.py:157-200) of (sketch(w), member sketch, sizes[w], |C3|).
+ * kind = PG_KHASH | PG_ONEHASH | PG_KMV; rows = int32 entries (k-Hash /
+ * 1-Hash) or double values (KMV), k columns; lengths: 1-Hash / KMV stored
+ * lengths (NULL for k-Hash); seeds_dev: k (k-Hash) or 1 seeds.
+ * out_sum[0] = sum of the per-triple estimates (fp64, fixed reduction
+ * order: reproducible), out_triples[0] = number of (u,v,w) triples.
+ * max_out_degree bounds |N+| over the view (C3 scratch for long lists);
+ * the caller allocates `workspace` of pg_4clique_sketch_workspace_size
+ * bytes.  k in [1, 256] (PG_ERR_UNSUPPORTED otherwise). */
+PG_API int pg_4clique_sketch_workspace_size(int32_t kind, int32_t k,
+                     int64_t max_out_degree, size_t* bytes);
+PG_API int pg_4clique_sketch(int32_t kind, const int64_t* dir_off,
+                     const int32_t* dir_adj, const int32_t* src,
+                     const int64_t* edge_ids, int64_t e_begin, int64_t e_end,
+                     const void* rows, const int32_t* lengths,
+                     const int32_t* sizes, int32_t k, const uint64_t* seeds_dev,
+                     int64_t max_out_degree, void* workspace,
+                     size_t workspace_bytes, double* out_sum,
+                     int64_t* out_triples, void* stream);
 
 /* Jarvis-Patrick clustering tail (mining.py:213-245): edge i = (us[i],
  * vs[i]) is kept iff scores[i] > tau; out[0] = kept edges, out[1] =

@@ -91,6 +91,11 @@ SIGNATURES = {
                                c_i32, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_ptr,
                                c_ptr, c_ptr],
     "pg_4clique_exact": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr],
+    "pg_4clique_exact_rows": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr,
+                              c_ptr],
+    "pg_4clique_sketch_workspace_size": [c_i32, c_i32, c_i64, ctypes.POINTER(c_size)],
+    "pg_4clique_sketch": [c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr,
+                          c_ptr, c_i32, c_ptr, c_i64, c_ptr, c_size, c_ptr, c_ptr, c_ptr],
     "pg_pairs_exact": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
     "pg_tc_exact": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
     "pg_two_hop_candidates": [c_ptr, c_ptr, c_i64, c_ptr, c_i64, ctypes.POINTER(c_i64),

@@ -275,7 +275,7 @@ __device__ __forceinline__ long long clique4_exact_edge_global(const int64_t* __
       const int t = __ffs(mask) - 1;
       mask &= mask - 1;
       const int32_t wv = __shfl_sync(0xffffffffu, x, t);
-      const int32_t* Wr = adjp + off[wv];
+      const int32_t* Wr = adjp + off[wv];  // (the caller's w-row CSR)
       const int64_t lw = off[wv + 1] - off[wv];
       for (int64_t q = lane; q < lw; q += 32) {
         const int32_t y = Wr[q];
@@ -292,9 +292,13 @@ __device__ __forceinline__ long long clique4_exact_edge_global(const int64_t* __
 // search in the prefix, test its entry against C3 in shared memory), so
 // short rows do not idle the warp.  Edges whose shorter list exceeds kC4Cap
 // take the global path.
+// w rows (N(w) of ExactProvider.with_set, providers.py:117-118) come from
+// (woff, wadj): the view's own CSR, or the provider's when it was built
+// for another CSR (e.g. ExactProvider.for_graph: undirected N(w)).
 __global__ void __launch_bounds__(kBlock) clique4_exact_kernel(
     const int64_t* __restrict__ off, const int32_t* __restrict__ adjp, const int32_t* __restrict__ src,
-    int64_t e_begin, int64_t e_end, int64_t* out_count) {
+    int64_t e_begin, int64_t e_end, const int64_t* __restrict__ woff, const int32_t* __restrict__ wadj,
+    int64_t* out_count) {
   extern __shared__ __align__(16) int32_t smem_i[];  // (kBlock/32) * (3*kC4Cap + 1)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int32_t* sB = smem_i + w * (3 * kC4Cap + 1);
@@ -314,7 +318,7 @@ __global__ void __launch_bounds__(kBlock) clique4_exact_kernel(
     }
     if (la == 0) continue;
     if (la > kC4Cap) {
-      total += clique4_exact_edge_global(off, adjp, A, la, Bv, lb, lane);
+      total += clique4_exact_edge_global(woff, wadj, A, la, Bv, lb, lane);
       continue;
     }
     const bool staged = lb <= kC4Cap;
@@ -340,7 +344,7 @@ __global__ void __launch_bounds__(kBlock) clique4_exact_kernel(
     int carry = 0;
     for (int base = 0; base < c3; base += 32) {
       const int t = base + lane;
-      const int d = t < c3 ? (int)(off[sC[t] + 1] - off[sC[t]]) : 0;
+      const int d = t < c3 ? (int)(woff[sC[t] + 1] - woff[sC[t]]) : 0;
       int inc = d;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -360,7 +364,7 @@ __global__ void __launch_bounds__(kBlock) clique4_exact_kernel(
         if (sP[mid] <= f) lo = mid;
         else hi = mid - 1;
       }
-      const int32_t y = adjp[off[sC[lo]] + (f - sP[lo])];
+      const int32_t y = wadj[woff[sC[lo]] + (f - sP[lo])];
       total += smem_contains(sC, c3, y);
     }
     __syncwarp();
@@ -441,17 +445,24 @@ int pg_4clique_bloom_edges(const int64_t* dir_off, const int32_t* dir_adj, const
 
 int pg_4clique_exact(const int64_t* dir_off, const int32_t* dir_adj, const int32_t* src, int64_t e_begin,
                      int64_t e_end, int64_t* out_count, void* stream) {
+  return pg_4clique_exact_rows(dir_off, dir_adj, src, e_begin, e_end, dir_off, dir_adj, out_count, stream);
+}
+
+int pg_4clique_exact_rows(const int64_t* dir_off, const int32_t* dir_adj, const int32_t* src, int64_t e_begin,
+                          int64_t e_end, const int64_t* w_off, const int32_t* w_adj, int64_t* out_count,
+                          void* stream) {
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
   PG_REQUIRE(out_count, "null output");
   cudaStream_t s = as_stream(stream);
   cudaError_t ce = cudaMemsetAsync(out_count, 0, sizeof(int64_t), s);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
   if (e_end == e_begin) return PG_OK;
-  PG_REQUIRE(dir_off && dir_adj && src, "null pointer");
+  PG_REQUIRE(dir_off && dir_adj && src && w_off && w_adj, "null pointer");
   const size_t smem = sizeof(int32_t) * (kBlock / 32) * (3 * kC4Cap + 1);
   cudaFuncSetAttribute(clique4_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = grid_cap(grid_for_kernel(clique4_exact_kernel, smem), e_end - e_begin, kBlock / 32);
-  clique4_exact_kernel<<<grid, kBlock, smem, s>>>(dir_off, dir_adj, src, e_begin, e_end, out_count);
+  clique4_exact_kernel<<<grid, kBlock, smem, s>>>(dir_off, dir_adj, src, e_begin, e_end, w_off, w_adj,
+                                                  out_count);
   return check_launch("4clique_exact");
 }
 

@@ -24,7 +24,7 @@ constexpr int kKhash128Minb = 4;
 constexpr bool kKhashVCache = PG_KHASH_VCACHE;  // L1-allocated v rows in the wide k-Hash engine
 
 // kEngine: 0 scalar fallback, 1 group (128-bit) engine, 2 wide padded engine
-template <int V, int G, int kEngine, int MINB = 1, bool kDyn = false>
+template <int V, int G, int kEngine, int MINB = 1, bool kDyn = false, int kLayout = 1>
 __global__ void __launch_bounds__(kBlock, MINB) tc_khash_kernel(const uint4* ent, int k, const int32_t* sizes,
                                                                const int32_t* us, const int32_t* vs,
                                                                int64_t e_begin, int64_t e_end,
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_khash_kernel(const uint4* ent
   EpiMinhashHist epi{sizes, cnt_s, slo_s, shi_s};
   if (kEngine == 0) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
   else if (kEngine == 1) group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
-  else wide_edge_loop<V, OpEqPos, EpiMinhashHist, kKhashVCache, true, kDyn>(reinterpret_cast<const unsigned char*>(ent),
+  else wide_edge_loop<V, OpEqPos, EpiMinhashHist, kKhashVCache, kLayout, kDyn>(reinterpret_cast<const unsigned char*>(ent),
                                                                       us, vs, e_begin, e_end, epi, ctr);
   __syncthreads();
   for (int i = threadIdx.x; i <= k; i += blockDim.x) {
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(kBlock, MINB) tc_khash_kernel(const uint4* ent
   }
 }
 
-template <int V, int G, int kEngine, int MINB = 1, bool kDyn = false>
+template <int V, int G, int kEngine, int MINB = 1, bool kDyn = false, int kLayout = 1>
 __global__ void __launch_bounds__(kBlock, MINB) jaccard_khash_kernel(const uint4* ent, int k, const int32_t* deg,
                                                                     const int32_t* us, const int32_t* vs,
                                                                     int64_t e_begin, int64_t e_end,
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(kBlock, MINB) jaccard_khash_kernel(const uint4
   EpiJaccard epi{k, min_matches, tau, deg, hist_s, 0, 0};
   if (kEngine == 0) scalar_edge_loop_khash(reinterpret_cast<const int32_t*>(ent), k, us, vs, e_begin, e_end, epi);
   else if (kEngine == 1) group_edge_loop<V, G, OpEqPos>(ent, us, vs, e_begin, e_end, epi);
-  else wide_edge_loop<V, OpEqPos, EpiJaccard, kKhashVCache, true, kDyn>(reinterpret_cast<const unsigned char*>(ent), us,
+  else wide_edge_loop<V, OpEqPos, EpiJaccard, kKhashVCache, kLayout, kDyn>(reinterpret_cast<const unsigned char*>(ent), us,
                                                                   vs, e_begin, e_end, epi, ctr);
   __syncthreads();
   for (int i = threadIdx.x; i <= k; i += blockDim.x)
@@ -564,6 +564,8 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
   {                                                                                      \
     auto kern = tc_khash_kernel<W8, 1, 2, MB>;                                           \
     if (e_end - e_begin >= kDynamicMinSlots) kern = tc_khash_kernel<W8, 1, 2, MB, true>; \
+    if (padded == 2) kern = e_end - e_begin >= kDynamicMinSlots ? tc_khash_kernel<W8, 1, 2, MB, true, 2> \
+                                                                : tc_khash_kernel<W8, 1, 2, MB, false, 2>; \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);        \
     ChunkCounter ctr;                                                                    \
     if (e_end - e_begin >= kDynamicMinSlots && (ce = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce)); \
@@ -608,6 +610,8 @@ int pg_jaccard_count_khash(const int32_t* entries, int32_t k, const int32_t* deg
   {                                                                                                    \
     auto kern = jaccard_khash_kernel<W8, 1, 2, MB>;                                                    \
     if (e_end - e_begin >= kDynamicMinSlots) kern = jaccard_khash_kernel<W8, 1, 2, MB, true>;          \
+    if (padded == 2) kern = e_end - e_begin >= kDynamicMinSlots ? jaccard_khash_kernel<W8, 1, 2, MB, true, 2> \
+                                                                : jaccard_khash_kernel<W8, 1, 2, MB, false, 2>; \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock);                      \
     ChunkCounter ctr;                                                                                  \
     if (e_end - e_begin >= kDynamicMinSlots && (ce = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce)); \

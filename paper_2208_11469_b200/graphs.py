@@ -251,6 +251,12 @@ class DeviceCsr:
             self._layouts[key] = (us[:k:pad].contiguous(), vs[:k], k, hub_ids)
         return self._layouts[key]
 
+    def max_degree(self) -> int:
+        """Largest row length (one device reduction, cached)."""
+        if getattr(self, "_maxd", None) is None:
+            self._maxd = int(self.degrees.max().item()) if self.n > 0 else 0
+        return self._maxd
+
     def row_sources(self):
         """int32 device array src[j] = row of adjacency entry j."""
         if self._src is None:

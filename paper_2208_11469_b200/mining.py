@@ -17,6 +17,7 @@ count surviving edges); the reference has no batch form of it.
 
 from __future__ import annotations
 
+import ctypes
 import enum
 import math
 from dataclasses import dataclass
@@ -26,8 +27,8 @@ import numpy as np
 from . import _native as N
 from .estimators import EstimatorKind, swamidass_table
 from .graphs import CsrGraph, DirectedView, as_csr_graph, as_directed_view, degree_order
-from .providers import (BloomProvider, ExactProvider, IntersectionProvider,
-                        UnsupportedCombinationError, make_provider)
+from .providers import (BloomProvider, ExactProvider, IntersectionProvider, KmvProvider,
+                        MinHashProvider, UnsupportedCombinationError, make_provider)
 from .sketches import SketchedGraph, SketchKind, as_sketched_graph
 
 __all__ = ["SimilarityMeasure", "ClusterResult", "JaccardCount", "LinkPredSplit",
@@ -195,26 +196,78 @@ def tc_estimate(graph: CsrGraph, sketched: SketchedGraph | None = None,
 
 def four_clique_count(view: DirectedView, provider: IntersectionProvider,
                       threads: int = 1):
-    """sum over directed (u,v), w in C3 = N+u & N+v of |N+w & C3|.
+    """sum over directed (u,v), w in C3 = N+u & N+v of |S_w & C3|
+    (reference mining.py:133-154).
 
-    Exact providers give the exact integer count; Bloom providers estimate
-    |N+w & C3| from BF+(w) and BF(C3), fused in one kernel.
+    Exact providers give the exact integer count, with N(w) from the
+    provider's own CSR (``ExactProvider._slice``); Bloom providers estimate
+    |N+w & C3| from BF+(w) and BF(C3) (fused kernel, integer histogram);
+    k-Hash / 1-Hash / KMV providers build the member sketch of C3 once per
+    directed edge on the device and add ``with_set``'s estimate for every w
+    in C3 (pg_4clique_sketch).
     """
     import torch
     view = as_directed_view(view)
     dev = view.device()
     src, nnz = dev.row_sources(), dev.nnz
     if isinstance(provider, ExactProvider):
+        pdev = provider.device()
+        if pdev.n < view.n:
+            raise ValueError("exact provider covers fewer vertices than the view")
         out = torch.empty(1, dtype=torch.int64, device="cuda")
-        N.call("pg_4clique_exact", N.ptr(dev.offsets), N.ptr(dev.adj), N.ptr(src),
-               0, nnz, N.ptr(out), N.stream_handle())
+        N.call("pg_4clique_exact_rows", N.ptr(dev.offsets), N.ptr(dev.adj), N.ptr(src),
+               0, nnz, N.ptr(pdev.offsets), N.ptr(pdev.adj), N.ptr(out), N.stream_handle())
         return int(out.item())
-    if not isinstance(provider, BloomProvider):
-        raise UnsupportedCombinationError(
-            f"four_clique_count on the device supports exact and Bloom "
-            f"providers, not {provider.kind.value}")
-    counts = four_clique_counts(view, provider, 0, nnz).cpu().numpy()
-    return four_clique_combine(provider, counts)
+    if isinstance(provider, BloomProvider):
+        counts = four_clique_counts(view, provider, 0, nnz).cpu().numpy()
+        return four_clique_combine(provider, counts)
+    if isinstance(provider, (MinHashProvider, KmvProvider)):
+        total, _ = four_clique_sketch_sum(view, provider)
+        return total
+    raise UnsupportedCombinationError(
+        f"four_clique_count on the device supports exact, Bloom, MinHash and KMV "
+        f"providers, not {type(provider).__name__}")
+
+
+_C4_KIND = {SketchKind.KHASH: 3, SketchKind.ONEHASH: 4, SketchKind.KMV: 5}
+
+
+def four_clique_sketch_sum(view: DirectedView, provider, edge_ids=None):
+    """(sum of with_set estimates, triple count) over every directed edge of
+    the view, or over the directed-edge indices ``edge_ids`` (a sample), for
+    a k-Hash / 1-Hash / KMV provider (pg_4clique_sketch)."""
+    import torch
+    view = as_directed_view(view)
+    dev = view.device()
+    sg = provider.sketched
+    if sg.n < view.n:
+        raise ValueError("sketches cover fewer vertices than the view")
+    d = sg.device_tensors()
+    kind = _C4_KIND[sg.kind]
+    k = sg.capacity
+    maxd = dev.max_degree()
+    ws_bytes = ctypes.c_size_t(0)
+    N.call("pg_4clique_sketch_workspace_size", kind, k, maxd, ctypes.byref(ws_bytes))
+    ws = torch.empty(max(16, ws_bytes.value), dtype=torch.uint8, device="cuda")
+    out_sum = torch.empty(1, dtype=torch.float64, device="cuda")
+    out_trip = torch.empty(1, dtype=torch.int64, device="cuda")
+    rows = d["values"] if sg.kind is SketchKind.KMV else d["entries"]
+    lengths = d.get("lengths") if sg.kind is not SketchKind.KHASH else None
+    if edge_ids is None:
+        ids, e0, e1 = None, 0, dev.nnz
+    else:
+        ids = torch.as_tensor(np.asarray(edge_ids, dtype=np.int64)
+                              if not isinstance(edge_ids, torch.Tensor) else edge_ids)
+        ids = ids.to(device="cuda", dtype=torch.int64).contiguous()
+        if ids.numel() and (int(ids.min()) < 0 or int(ids.max()) >= dev.nnz):
+            raise ValueError("edge id out of range")
+        e0, e1 = 0, ids.numel()
+    N.call("pg_4clique_sketch", kind, N.ptr(dev.offsets), N.ptr(dev.adj),
+           N.ptr(dev.row_sources()), N.ptr(ids) if ids is not None else None, e0, e1,
+           N.ptr(rows), N.ptr(lengths) if lengths is not None else None, N.ptr(d["sizes"]),
+           k, N.ptr(d["seeds"]), maxd, N.ptr(ws), ws.numel(), N.ptr(out_sum),
+           N.ptr(out_trip), N.stream_handle())
+    return float(out_sum.item()), int(out_trip.item())
 
 
 def four_clique_counts(view: DirectedView, provider: BloomProvider,

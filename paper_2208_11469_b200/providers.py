@@ -408,6 +408,25 @@ class MinHashProvider(_SketchProvider):
             return N.onehash_block_pad(k)
         return N.group_pad(4 * k)
 
+    def _tc_layout(self, dev):
+        """k-Hash rows of 64/128/256 bytes take the degree-oriented group-u
+        layout (as BloomProvider._tc_layout) when the entry matrix streams
+        from HBM: the register-held u row is then the low-degree endpoint
+        and the streamed v rows the hub side, which stays in L2 (with u < v
+        by ID, the Chung-Lu hubs at low IDs are the u side and every edge
+        misses on its v row).  Positional matches and s_u + s_v are
+        symmetric, so the statistics are the same integers.  1-Hash keeps
+        its per-warp-table layout; PG_TC_ORIENT=id restores u < v."""
+        import os
+        sg = self.sketched
+        pad = self.tc_pad()
+        if (not self.onehash and pad > 1 and sg.capacity in (16, 32, 64) and dev.n > 0
+                and sg.n * sg.capacity * 4 > BloomProvider.DEGREE_ORIENT_MIN_BYTES
+                and os.environ.get("PG_TC_ORIENT", "degree") == "degree"):
+            ug, vs, slots, _ = dev.hub_slots(pad, 0)
+            return TcLayout(ug, vs, slots, 2, "degree")
+        return super()._tc_layout(dev)
+
     def _pairs_device(self, us, vs):
         import torch
         d, sg = self._dev(), self.sketched
