@@ -60,6 +60,16 @@ struct OpOr {
     return c;
   }
 };
+// Integer adds steered onto the FMA pipe: a * kImadW[i] + b with the
+// multiplier read from constant memory is an IMAD (FMA pipe) rather than an
+// IADD3 / LEA (ALU pipe).  The Bloom kernels at 2048 bits are ALU-bound
+// (LOP3 for AND and the carry-save adders), the FMA pipe idles.
+#ifndef PG_IMAD_ADDS
+#define PG_IMAD_ADDS 1
+#endif
+static __constant__ int kImadW[4] = {1, 2, 4, 8};
+__device__ __forceinline__ int imad(int a, int b, int c) { return a * b + c; }
+
 // Harley-Seal variants: the 8 words a lane holds per edge pass through four
 // carry-save adders (LOP3s, ALU pipe) so 4 POPC replace 8 -- POPC issues on
 // the XU pipe (16/clk/SM), the ceiling of the 2048-bit rows once the row
@@ -69,13 +79,27 @@ __device__ __forceinline__ void csa3(uint32_t& carry, uint32_t& s, uint32_t a, u
   carry = (a & b) | (u & c);
   s = u ^ c;
 }
+#ifndef PG_CSA_LEVEL
+#define PG_CSA_LEVEL 4
+#endif
 __device__ __forceinline__ int popc8_csa(const uint32_t (&x)[8]) {
   uint32_t s1, c1, s2, c2, s3, c3, s4, c4;
   csa3(c1, s1, x[0], x[1], x[2]);
   csa3(c2, s2, x[3], x[4], x[5]);
   csa3(c3, s3, s1, s2, x[6]);
+#if PG_CSA_LEVEL == 3
+  // three adders, five POPC: one LOP3 pair fewer per 8 words, one POPC more
+  return imad(__popc(c1) + __popc(c2) + __popc(c3), kImadW[1], imad(__popc(s3), kImadW[0], __popc(x[7])));
+#endif
   csa3(c4, s4, c1, c2, c3);
+#if PG_IMAD_ADDS
+  // ones + 2*twos + 4*fours as two IMADs on the FMA pipe (the multipliers
+  // come from constant memory, so ptxas cannot turn them into ALU LEAs):
+  // the ALU pipe is the 2048-bit kernel's binding resource
+  return imad(__popc(c4), kImadW[2], imad(__popc(s4), kImadW[1], imad(__popc(s3), kImadW[0], __popc(x[7]))));
+#else
   return __popc(s3) + __popc(x[7]) + 2 * __popc(s4) + 4 * __popc(c4);  // ones, twos, fours
+#endif
 }
 struct OpAndCsa : OpAnd {
   __device__ __forceinline__ static int apply8(const uint32_t (&a)[8], const uint32_t (&b)[8]) {
@@ -120,7 +144,11 @@ __device__ __forceinline__ int group_transpose_reduce(int (&c)[G], int gl) {
     for (int j = 0; j < w; ++j) {
       const int send = upper ? c[j] : c[j + w];
       const int keep = upper ? c[j + w] : c[j];
+#if PG_IMAD_ADDS
+      c[j] = imad(__shfl_xor_sync(0xffffffffu, send, w), kImadW[0], keep);
+#else
       c[j] = keep + __shfl_xor_sync(0xffffffffu, send, w);
+#endif
     }
   }
   return c[0];
@@ -259,6 +287,19 @@ __device__ __forceinline__ void ldg256_keep(const void* p, uint32_t (&r)[8]) {
                : "l"(p));
 }
 
+// base + r * bytes as one mad.wide.u32 (IMAD.WIDE.U32, FMA pipe); written in
+// PTX so the compiler cannot re-split it into multiply + OR + 64-bit add on
+// the ALU pipe
+// Row sizes in constant memory: a multiplier ptxas cannot see keeps the
+// product on IMAD.WIDE (a known power of two becomes LEA + LEA.HI.X, ALU).
+static __constant__ uint32_t kRowBytesC[17] = {0, 32, 64, 96, 128, 160, 192, 224, 256,
+                                               288, 320, 352, 384, 416, 448, 480, 512};
+__device__ __forceinline__ const unsigned char* row_addr(const unsigned char* base, uint32_t r, uint32_t bytes) {
+  uint64_t out;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(out) : "r"(r), "r"(bytes), "l"(base));
+  return reinterpret_cast<const unsigned char*>(out);
+}
+
 // kLayout: 0 any edge list; 1 row-padded slots (every aligned group of G
 // slots shares one u; us[] per slot); 2 the same with us[] holding one u per
 // group (us[e / G]) -- a G-fold smaller u stream.
@@ -274,6 +315,7 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
   const int lane = threadIdx.x & 31;
   const int gl = lane & (G - 1);
   const int gbase = lane & ~(G - 1);
+  const unsigned char* rows_gl = rows + gl * 32;
   int32_t ucur = -1;
   uint32_t ur[V][8];
 #pragma unroll
@@ -313,8 +355,10 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
     uint32_t vr[G][V][8];
 #pragma unroll
     for (int j = 0; j < G; ++j) {
-      const int32_t vj = __shfl_sync(0xffffffffu, vl, gbase + j);
-      const unsigned char* rv = rows + (int64_t)(vj < 0 ? 0 : vj) * kRowBytes + gl * 32;
+      const int32_t vj = __shfl_sync(0xffffffffu, vl, j, G);
+      // lane base + row * bytes: one IMAD.WIDE.U32 (FMA pipe) per row
+      // instead of multiply, OR and a 64-bit add on the ALU pipe
+      const unsigned char* rv = row_addr(rows_gl, (uint32_t)(vj < 0 ? 0 : vj), kRowBytesC[W8]);
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         if (kVCache) ldg256_keep(rv + i * G * 32, vr[j][i]);
@@ -324,17 +368,17 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
     // u rows: with the row-padded edge layout (pg_csr_upper_edges_padded)
     // all G edges of a group share one u, cached across iterations; for any
     // other input the per-edge rows are loaded speculatively in parallel.
-    const int32_t u0 = __shfl_sync(0xffffffffu, ul, gbase);
+    const int32_t u0 = __shfl_sync(0xffffffffu, ul, 0, G);
     bool uniform = true;
     if (!kPadded) {
 #pragma unroll
-      for (int j = 1; j < G; ++j) uniform &= __shfl_sync(0xffffffffu, ul, gbase + j) == u0;
+      for (int j = 1; j < G; ++j) uniform &= __shfl_sync(0xffffffffu, ul, j, G) == u0;
     }
     int c[G];
     if (kPadded || __all_sync(0xffffffffu, uniform)) {
       if (u0 != ucur) {
         ucur = u0;
-        const unsigned char* ru = rows + (int64_t)u0 * kRowBytes + gl * 32;
+        const unsigned char* ru = row_addr(rows_gl, (uint32_t)u0, kRowBytesC[W8]);
 #pragma unroll
         for (int i = 0; i < V; ++i) ldg256_keep(ru + i * G * 32, ur[i]);
       }
@@ -348,10 +392,10 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
     } else if (!kPadded) {
 #pragma unroll
       for (int j = 0; j < G; ++j) {
-        const int32_t uj = __shfl_sync(0xffffffffu, ul, gbase + j);
+        const int32_t uj = __shfl_sync(0xffffffffu, ul, j, G);
         if (uj != ucur) {
           ucur = uj;
-          const unsigned char* ru = rows + (int64_t)uj * kRowBytes + gl * 32;
+          const unsigned char* ru = row_addr(rows_gl, (uint32_t)uj, kRowBytesC[W8]);
 #pragma unroll
           for (int i = 0; i < V; ++i) ldg256_keep(ru + i * G * 32, ur[i]);
         }
