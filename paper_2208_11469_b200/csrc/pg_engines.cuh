@@ -200,6 +200,30 @@ struct ChunkCounter {
   }
 };
 
+// Reproducible fp64 sums: kernels write partial sums to fixed slots (one
+// per block of a fixed grid, or one per dynamic edge chunk), and
+// fixed_order_sum_kernel adds them in index order (a strided pass per thread,
+// then a fixed tree), so a sum does not depend on scheduling or atomics.
+__global__ void fixed_order_sum_kernel(const double* __restrict__ part, int64_t n, double* out);
+
+struct PartialSums {
+  double* p = nullptr;
+  int64_t n = 0;
+  cudaStream_t s = nullptr;
+  cudaError_t init(cudaStream_t st, int64_t count) {
+    s = st;
+    n = count;
+    retain_default_pool();
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&p), sizeof(double) * (count > 0 ? count : 1), s);
+    if (e == cudaSuccess) e = cudaMemsetAsync(p, 0, sizeof(double) * (count > 0 ? count : 1), s);
+    return e;
+  }
+  void finish(double* out) { fixed_order_sum_kernel<<<1, 256, 0, s>>>(p, n, out); }
+  ~PartialSums() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
 // Group engine: calls epi.edge(e, u, v, count) once per edge of the warp's
 // slice, from the lane that loaded the edge.
 //

@@ -112,11 +112,16 @@ __global__ void range_slot_gather_kernel(const int32_t* __restrict__ adj, int64_
   }
 }
 
-// advance the cursor past the range and record [begin, end) of its slots
+// advance the cursor past the range and record [begin, end) of the slots
+// actually written (clamped to max_slots and capacity, as the gather; the
+// overflow flag tells the caller the range was cut short)
 __global__ void range_slot_finish_kernel(const int64_t* __restrict__ cnt, const int64_t* __restrict__ start,
-                                         int64_t rows, int64_t* __restrict__ cursor, int64_t* __restrict__ range) {
+                                         int64_t rows, int64_t max_slots, int64_t capacity,
+                                         int64_t* __restrict__ cursor, int64_t* __restrict__ range) {
   const int64_t base = cursor[0];
-  const int64_t total = rows > 0 ? start[rows - 1] + cnt[rows - 1] : 0;
+  int64_t total = rows > 0 ? start[rows - 1] + cnt[rows - 1] : 0;
+  total = min(total, max_slots);
+  total = max(int64_t(0), min(total, capacity - base));
   range[0] = base;
   range[1] = base + total;
   cursor[0] = base + total;
@@ -454,7 +459,8 @@ int pg_csr_range_slots_append(const int64_t* offsets, const int32_t* adj, int64_
                                                   __builtin_ctz(pad), capacity, cursor_dev, cursor_dev + 1, ug, vs);
     if (int rc = check_launch("range_slot_gather")) return rc;
   }
-  range_slot_finish_kernel<<<1, 1, 0, s>>>(cnt, start, rows > 0 && max_slots > 0 ? rows : 0, cursor_dev, range_dev);
+  range_slot_finish_kernel<<<1, 1, 0, s>>>(cnt, start, rows > 0 && max_slots > 0 ? rows : 0, max_slots, capacity,
+                                           cursor_dev, range_dev);
   return check_launch("range_slot_finish");
 }
 

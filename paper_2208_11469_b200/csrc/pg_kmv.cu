@@ -121,10 +121,10 @@ __global__ void __launch_bounds__(kBlock) kmv_kernel(const uint64_t* vals, int k
   if (kFused) {
     if (lane == 0) red[w] = acc;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // out_sum: one partial per block (PartialSums)
       double t = 0.0;
       for (int i = 0; i < kBlock / 32; ++i) t = __dadd_rn(t, red[i]);
-      if (t != 0.0) atomicAdd(out_sum, t);
+      out_sum[blockIdx.x] = t;
     }
   }
 }
@@ -172,10 +172,10 @@ __global__ void __launch_bounds__(kBlock, 4) kmv_sorted_kernel(const uint64_t* v
     for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = a;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0) {  // out_sum: one partial per block (PartialSums)
       double t = 0.0;
       for (int i = 0; i < kBlock / 32; ++i) t = __dadd_rn(t, red[i]);
-      if (t != 0.0) atomicAdd(out_sum, t);
+      out_sum[blockIdx.x] = t;
     }
   }
 }
@@ -189,7 +189,11 @@ static void launch_kmv_sorted(cudaStream_t s, const uint64_t* vals, int k, const
   const size_t sm = (size_t)(kBlock / 32) * merge_warp_smem<G, CH, true>();
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / G);
-  kern<<<grid, kBlock, sm, s>>>(vals, k, sizes, us, vs, b, e, out_common, out_union, out_kth, out_est, out_sum);
+  PartialSums ps;  // fused: one partial per block, summed in block order
+  if (kFused && ps.init(s, grid) != cudaSuccess) return;
+  kern<<<grid, kBlock, sm, s>>>(vals, k, sizes, us, vs, b, e, out_common, out_union, out_kth, out_est,
+                                kFused ? ps.p : nullptr);
+  if (kFused) ps.finish(out_sum);
 }
 
 static bool kmv_sorted(cudaStream_t s, bool fused, const uint64_t* vals, int k, const int32_t* sizes,
@@ -358,7 +362,6 @@ __global__ void __launch_bounds__(kBlock, PG_RANKED_MINB) kmv_ranked_kernel(cons
   constexpr int G = K / P, E = 32 / G, IT = 32 / E;
   constexpr int64_t kChunk = 512;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double red[kBlock / 32];
   RankWarp<K>& Wp = reinterpret_cast<RankWarp<K>*>(smem_raw)[threadIdx.x >> 5];
   RankDir<K>& W = Wp.dir;
   const int lane = threadIdx.x & 31, gl = lane & (G - 1), grp = lane / G;
@@ -500,15 +503,11 @@ __global__ void __launch_bounds__(kBlock, PG_RANKED_MINB) kmv_ranked_kernel(cons
       svl = svn;
       lvl = lvn;
     }
-  }
-  double a = acc;
-  for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
-  if (lane == 0) red[threadIdx.x >> 5] = a;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double t = 0.0;
-    for (int i = 0; i < kBlock / 32; ++i) t = __dadd_rn(t, red[i]);
-    if (t != 0.0) atomicAdd(out_sum, t);
+    // one partial per dynamic chunk (fixed boundaries), whichever warp ran it
+    double a = acc;
+    for (int o = 16; o > 0; o >>= 1) a = __dadd_rn(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (lane == 0) out_sum[(wb - e_begin) / kChunk] = a;
+    acc = 0.0;
   }
 }
 
@@ -522,9 +521,12 @@ static int launch_kmv_ranked(cudaStream_t s, const int32_t* ranks, const double*
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / P));
   ChunkCounter ctr;
-  const cudaError_t ce = ctr.init(s);
-  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(ce));
-  kern<<<grid, kBlock, sm, s>>>(ranks, rank_values, lengths, sizes, us, vs, b, e, out_sum, ctr.p);
+  PartialSums ps;  // one partial per 512-slot chunk, summed in chunk order
+  cudaError_t ce = ctr.init(s);
+  if (ce == cudaSuccess) ce = ps.init(s, (e - b + 511) / 512);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "scratch: %s", cudaGetErrorString(ce));
+  kern<<<grid, kBlock, sm, s>>>(ranks, rank_values, lengths, sizes, us, vs, b, e, ps.p, ctr.p);
+  ps.finish(out_sum);
   return check_launch("tc_kmv_ranked");
 }
 }  // namespace pg
@@ -577,7 +579,10 @@ int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k, const int
   {                                                                                                 \
     auto kern = kmv_kernel<P, true>;                                                                \
     const int grid = grid_cap(grid_for_kernel(kern, 0), e_end - e_begin, kBlock / 32);              \
-    kern<<<grid, kBlock, 0, s>>>(vb, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, nullptr, nullptr, out_sum); \
+    PartialSums ps;                                                                                 \
+    if ((ce = ps.init(s, grid)) != cudaSuccess) return fail(PG_ERR_CUDA, "scratch: %s", cudaGetErrorString(ce)); \
+    kern<<<grid, kBlock, 0, s>>>(vb, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, nullptr, nullptr, ps.p); \
+    ps.finish(out_sum);                                                                             \
   }
   if (k <= 32) PG_KM(1)
   else if (k <= 64) PG_KM(2)

@@ -7,6 +7,20 @@
 
 namespace pg {
 
+__global__ void fixed_order_sum_kernel(const double* __restrict__ part, int64_t n, double* out) {
+  __shared__ double red[256];
+  double a = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a = __dadd_rn(a, part[i]);
+  red[threadIdx.x] = a;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] = __dadd_rn(red[threadIdx.x], red[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[0] = red[0];
+}
+
+
 static thread_local char g_err[512] = {0};
 
 void set_error(const char* fmt, ...) {

@@ -175,6 +175,10 @@ def _tc_counts_chunked(provider, dev):
         t.record_stream(ts)
     cur.wait_stream(ts)
     out.record_stream(cur)
+    # cur_rng[1]: a range's slots exceeded its bound (they were dropped); the
+    # bounds above cannot be exceeded, so this is an internal error
+    if int(cur_rng[1].item()) != 0:
+        raise N.EngineError("edge-slot range overflow in the chunked TC layout")
     return out
 
 
