@@ -118,7 +118,14 @@ PG_API int pg_csr_expand_rows(const int64_t* offsets, int64_t n, int64_t nnz,
                        int32_t* src, void* stream);
 
 /* ---- (1) sketch builders  (sketches.py:314-396 _build_*_matrix,
- *      :399-451 build_sketched_graph) ------------------------------------ */
+ *      :399-451 build_sketched_graph) ------------------------------------
+ * Every size plan_budget produces is served: Bloom rows up to 65,536 bits and
+ * k <= 256 by the tuned kernels; wider rows / larger k by generic kernels
+ * (pg_generic.cu: global atomics, a thread per (vertex, function), CUB
+ * segmented sorts -- the 1-Hash / KMV generic builders synchronise the
+ * stream once to cut vertex ranges).  The estimators below likewise fall
+ * back to warp-per-edge kernels with global statistics for k > 256 and
+ * Bloom rows over 32,768 bits (16,384 for the 4-clique count). */
 /* seeds_dev: the HashFamily seeds (count = b, k, 1, 1 respectively) */
 PG_API int pg_build_bloom(const int64_t* offsets, const int32_t* adj, int64_t n,
                    int32_t bits, int32_t b, const uint64_t* seeds_dev,
@@ -316,7 +323,8 @@ PG_API int pg_4clique_exact_rows(const int64_t* dir_off, const int32_t* dir_adj,
  * order: reproducible), out_triples[0] = number of (u,v,w) triples.
  * max_out_degree bounds |N+| over the view (C3 scratch for long lists);
  * the caller allocates `workspace` of pg_4clique_sketch_workspace_size
- * bytes.  k in [1, 256] (PG_ERR_UNSUPPORTED otherwise). */
+ * bytes (k > 256: the member sketch and the 1-Hash member table are in the
+ * workspace too). */
 PG_API int pg_4clique_sketch_workspace_size(int32_t kind, int32_t k,
                      int64_t max_out_degree, size_t* bytes);
 PG_API int pg_4clique_sketch(int32_t kind, const int64_t* dir_off,

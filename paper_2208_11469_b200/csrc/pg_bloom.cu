@@ -1,7 +1,7 @@
 // Bloom per-edge estimates (providers.py:137-162 pair_many, _estimate_ones;
 // estimators.py:65-70 swamidass_value) and the fused Bloom TC reduction
 // (mining.py:105-130 tc_estimate over _chunked_sum :63-80).
-#include "pg_engines.cuh"
+#include "pg_generic.cuh"
 
 namespace pg {
 
@@ -153,6 +153,9 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
   if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
   PG_REQUIRE(op != PG_BF_OR || (sizes && lut), "BF_OR needs sizes and the table");
   PG_REQUIRE(rows && us && vs, "null pointer");
+  if (bits > kGenBloomTcBits && !range_dev)  // histogram too large for shared memory
+    return gen_tc_bloom(rows, bits, op, sizes, lut, us, vs, e_begin, e_end, out_hist, out_sum_pos, s);
+  PG_REQUIRE(bits <= kGenBloomTcBits, "device slot ranges support Bloom widths up to %d", kGenBloomTcBits);
   EpiBloomHist epi{op, sizes, lut, nullptr, 0};
   const size_t smem = sizeof(int) * (bits + 1);
   const int w4 = bits % 128 == 0 ? bits / 128 : 0;

@@ -20,6 +20,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include "pg_common.cuh"
+#include "pg_generic.cuh"
 
 namespace pg {
 
@@ -1188,12 +1189,12 @@ int pg_build_bloom(const int64_t* offsets, const int32_t* adj, int64_t n, int32_
                    const uint64_t* seeds_dev, uint64_t* rows, int32_t* ones, void* stream) {
   PG_REQUIRE(n >= 0, "n must be >= 0");
   PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
-  if (bits > kMaxBloomBits)
-    return fail(PG_ERR_UNSUPPORTED, "Bloom width %d exceeds the device limit %d", bits, kMaxBloomBits);
   PG_REQUIRE(b >= 1 && b <= 64, "Bloom hash count must be in [1, 64]");
   PG_REQUIRE(offsets && seeds_dev && rows && ones, "null pointer");
   if (n == 0) return PG_OK;
   cudaStream_t s = as_stream(stream);
+  if (bits > kMaxBloomBits)  // rows wider than the shared-memory batch rows
+    return gen_build_bloom(offsets, adj, n, bits, b, seeds_dev, rows, ones, s);
   HubList hubs;
   if (int rc = hubs.init(offsets, n, s, true)) return rc;
   // batch size: 32 vertices per warp while the rows fit ~96 KB per CTA
@@ -1230,10 +1231,10 @@ int pg_build_khash(const int64_t* offsets, const int32_t* adj, int64_t n, int32_
                    const uint64_t* seeds_dev, int32_t* entries, void* stream) {
   PG_REQUIRE(n >= 0, "n must be >= 0");
   PG_REQUIRE(k >= 1, "k must be >= 1");
-  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(offsets && seeds_dev && entries, "null pointer");
   if (n == 0) return PG_OK;
   cudaStream_t s = as_stream(stream);
+  if (k > kMaxSketchK) return gen_build_khash(offsets, adj, n, k, seeds_dev, entries, s);
   HubList hubs;
   if (int rc = hubs.init(offsets, n, s)) return rc;
 #define PG_KB(S)                                                                                         \
@@ -1256,9 +1257,11 @@ int pg_build_onehash(const int64_t* offsets, const int32_t* adj, int64_t n, int3
                      const uint64_t* seeds_dev, int32_t* entries, int32_t* lengths, void* stream) {
   PG_REQUIRE(n >= 0, "n must be >= 0");
   PG_REQUIRE(k >= 1, "k must be >= 1");
-  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(offsets && seeds_dev && entries && lengths, "null pointer");
   if (n == 0) return PG_OK;
+  if (k > kMaxSketchK)
+    return gen_build_bottomk(offsets, adj, n, k, seeds_dev, entries, nullptr, nullptr, nullptr, lengths,
+                             as_stream(stream));
   return launch_bottomk<0>(offsets, adj, n, k, seeds_dev, entries, nullptr, lengths, stream);
 }
 
@@ -1266,9 +1269,11 @@ int pg_build_kmv(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t 
                  const uint64_t* seeds_dev, double* values, int32_t* lengths, void* stream) {
   PG_REQUIRE(n >= 0, "n must be >= 0");
   PG_REQUIRE(k >= 1, "k must be >= 1");
-  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(offsets && seeds_dev && values && lengths, "null pointer");
   if (n == 0) return PG_OK;
+  if (k > kMaxSketchK)
+    return gen_build_bottomk(offsets, adj, n, k, seeds_dev, nullptr, values, nullptr, nullptr, lengths,
+                             as_stream(stream));
   return launch_bottomk<1>(offsets, adj, n, k, seeds_dev, nullptr, values, lengths, stream);
 }
 
@@ -1315,9 +1320,11 @@ int pg_build_kmv_ranked(const int64_t* offsets, const int32_t* adj, int64_t n, i
                         double* values, int32_t* ranks, int32_t* lengths, void* stream) {
   PG_REQUIRE(n >= 0, "n must be >= 0");
   PG_REQUIRE(k >= 1, "k must be >= 1");
-  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(offsets && seeds_dev && rank_of && rank_values && values && ranks && lengths, "null pointer");
   if (n == 0) return PG_OK;
+  if (k > kMaxSketchK)
+    return gen_build_bottomk(offsets, adj, n, k, seeds_dev, nullptr, values, ranks, rank_of, lengths,
+                             as_stream(stream));
   BottomKRank rk;
   rk.rank_of = rank_of;
   rk.rank_values = rank_values;

@@ -1,6 +1,6 @@
 // 4-clique counting (mining.py:133-154 four_clique_count with
 // BloomProvider.with_set / ExactProvider, providers.py:164-175).
-#include "pg_engines.cuh"
+#include "pg_generic.cuh"
 
 namespace pg {
 
@@ -383,7 +383,6 @@ static int clique4_bloom(const int64_t* dir_off, const int32_t* dir_adj, const i
                          const double* lut, int64_t* out_hist, int64_t* out_sum_pos, int64_t* out_triples,
                          void* stream) {
   PG_REQUIRE(bits >= 64 && bits % 64 == 0, "Bloom size must be a positive multiple of 64");
-  if (bits > 16384) return fail(PG_ERR_UNSUPPORTED, "4-clique kernel supports Bloom widths up to 16384");
   PG_REQUIRE(b >= 1 && b <= 64, "Bloom hash count must be in [1, 64]");
   PG_REQUIRE(op == PG_BF_AND || op == PG_BF_L || op == PG_BF_OR, "op is not a Bloom estimator");
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
@@ -396,6 +395,9 @@ static int clique4_bloom(const int64_t* dir_off, const int32_t* dir_adj, const i
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
   if (e_end == e_begin) return PG_OK;
   PG_REQUIRE(dir_off && dir_adj && src && rows_plus && seeds_dev, "null pointer");
+  if (bits > 16384)  // BF(C3) rows and histogram beyond the shared-memory kernels
+    return gen_4clique_bloom(dir_off, dir_adj, src, edge_ids, e_begin, e_end, rows_plus, bits, b, seeds_dev, op,
+                             sizes, lut, out_hist, out_sum_pos, out_triples, s);
   static const bool global_only = getenv("PG_C4_GLOBAL") != nullptr;
   const int G = bits % 256 == 0 ? bits / 256 : 0;
   if (!global_only && (G == 1 || G == 2 || G == 4 || G == 8 || G == 16 || G == 32)) {

@@ -65,6 +65,11 @@ struct C4SketchArgs {
   const int32_t* sizes;   // |S_w| (degrees of the sketched source)
   const uint64_t* seeds;  // k (k-Hash) or 1 seeds
   int k;
+  // k > kMaxSketchK: the member sketch and the 1-Hash member table live in
+  // per-warp global scratch (gM: k values, gT: tcap slots); else nullptr
+  uint64_t* gM;
+  int32_t* gT;
+  int tcap;
 };
 
 template <int KIND>
@@ -86,7 +91,7 @@ __global__ void __launch_bounds__(kCSBlock) clique4_sketch_kernel(
   __shared__ double wsum[kWarps];
   const int k = a.k;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const int nseeds = KIND == PG_KHASH ? k : 1;
+  const int nseeds = KIND == PG_KHASH ? min(k, kMaxSketchK) : 1;
   for (int i = threadIdx.x; i < nseeds; i += blockDim.x) seeds_s[i] = a.seeds[i];
   __syncthreads();
   int32_t* sB = sB_all + wid * kCSCap;
@@ -130,14 +135,14 @@ __global__ void __launch_bounds__(kCSBlock) clique4_sketch_kernel(
     __syncwarp();
     if (c3 == 0) continue;
     triples += c3;
-    uint64_t* M = sM_all + wid * kMaxSketchK;
+    uint64_t* M = a.gM ? a.gM + gw * k : sM_all + wid * kMaxSketchK;
     const uint64_t s0 = seeds_s[0];
     int lm = 0;          // KMV: stored member values
     uint64_t thr = ~0ull;  // 1-Hash: largest selected h_0
     int tb = 5;          // 1-Hash: log2 of the member-set table size
     if (KIND == PG_KHASH) {
       for (int i = lane; i < k; i += 32) {
-        const uint64_t s = seeds_s[i];
+        const uint64_t s = i < kMaxSketchK ? seeds_s[i] : a.seeds[i];
         uint64_t mn = ~0ull;
         for (int t = 0; t < c3; ++t) {
           const uint64_t h = hash_word(s, C[t]);
@@ -169,7 +174,7 @@ __global__ void __launch_bounds__(kCSBlock) clique4_sketch_kernel(
         const int sel = c3 < k ? c3 : k;
         tb = 5;
         while ((1 << tb) < 2 * sel) ++tb;
-        int32_t* tab = reinterpret_cast<int32_t*>(sH_all + wid * kCSCap);
+        int32_t* tab = a.gT ? a.gT + gw * a.tcap : reinterpret_cast<int32_t*>(sH_all + wid * kCSCap);
         for (int i = lane; i < (1 << tb); i += 32) tab[i] = -1;
         __syncwarp();
         for (int t = lane; t < c3; t += 32) {
@@ -230,7 +235,7 @@ __global__ void __launch_bounds__(kCSBlock) clique4_sketch_kernel(
       } else if (KIND == PG_ONEHASH) {
         const int lw = a.lengths[w];
         const int32_t* row = a.ent + (int64_t)w * k;
-        const int32_t* tab = reinterpret_cast<const int32_t*>(sH_all + wid * kCSCap);
+        const int32_t* tab = a.gT ? a.gT + gw * a.tcap : reinterpret_cast<const int32_t*>(sH_all + wid * kCSCap);
         const uint32_t tmask = (1u << tb) - 1;
         int common = 0;
         // 8 entries per 32-byte load (rows of k % 8 == 0 are 32-byte
@@ -249,7 +254,8 @@ __global__ void __launch_bounds__(kCSBlock) clique4_sketch_kernel(
             const int32_t y = (int32_t)y8[t];
             uint32_t h = (y8[t] * 0x9E3779B1u) >> (32 - tb);
             int32_t c;
-            while ((c = tab[h]) != y && c != -1) h = (h + 1) & tmask;
+            // (global table: read through L2, where the atomicCAS claims landed)
+            while ((c = a.gT ? __ldcg(tab + h) : tab[h]) != y && c != -1) h = (h + 1) & tmask;
             common += c == y;
           }
         }
@@ -368,6 +374,13 @@ static int c4s_cap() {
   return c >= 1 && c <= kCSCap ? c : kCSCap;
 }
 
+// 1-Hash member-table slots for k > kMaxSketchK (>= 2 * min(|C3|, k))
+static int c4s_tcap(int k) {
+  int t = 32;
+  while (t < 2 * k) t <<= 1;
+  return t;
+}
+
 constexpr size_t c4s_smem() {
   return (size_t)(kCSBlock / 32) * (kCSCap * 8 + kMaxSketchK * 8 + 2 * kCSCap * 4) + kMaxSketchK * 8;
 }
@@ -397,11 +410,12 @@ int pg_4clique_sketch_workspace_size(int32_t kind, int32_t k, int64_t max_out_de
   PG_REQUIRE(bytes, "null output");
   PG_REQUIRE(kind == PG_KHASH || kind == PG_ONEHASH || kind == PG_KMV, "kind must be PG_KHASH/ONEHASH/KMV");
   PG_REQUIRE(max_out_degree >= 0, "max_out_degree must be >= 0");
-  if (k < 1 || k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "4-clique sketch kernel supports k in [1, %d]", kMaxSketchK);
+  PG_REQUIRE(k >= 1, "k must be >= 1");
   const int64_t grid = c4s_grid_for(kind);
   const int64_t per_warp = max_out_degree > c4s_cap() ? max_out_degree : 0;
   const int64_t warps = grid * (kCSBlock / 32);
   *bytes = (size_t)(grid * 8 + 16) + (size_t)(warps * per_warp) * 16 + 16;
+  if (k > kMaxSketchK) *bytes += (size_t)warps * ((size_t)k * 8 + (size_t)c4s_tcap(k) * 4) + 16;
   return PG_OK;
 }
 
@@ -411,7 +425,7 @@ int pg_4clique_sketch(int32_t kind, const int64_t* dir_off, const int32_t* dir_a
                       int64_t max_out_degree, void* workspace, size_t workspace_bytes, double* out_sum,
                       int64_t* out_triples, void* stream) {
   PG_REQUIRE(kind == PG_KHASH || kind == PG_ONEHASH || kind == PG_KMV, "kind must be PG_KHASH/ONEHASH/KMV");
-  if (k < 1 || k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "4-clique sketch kernel supports k in [1, %d]", kMaxSketchK);
+  PG_REQUIRE(k >= 1, "k must be >= 1");
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
   PG_REQUIRE(out_sum && out_triples, "null output");
   size_t need = 0;
@@ -434,8 +448,17 @@ int pg_4clique_sketch(int32_t kind, const int64_t* dir_off, const int32_t* dir_a
   uint64_t* gH = reinterpret_cast<uint64_t*>(ws + (((size_t)grid * 8 + 15) & ~size_t(15)));
   int32_t* gC = reinterpret_cast<int32_t*>(gH + warps * per_warp);
   int32_t* gF = gC + warps * per_warp;
+  uint64_t* gM = nullptr;
+  int32_t* gT = nullptr;
+  const int tcap = c4s_tcap(k);
+  if (k > kMaxSketchK) {
+    gM = reinterpret_cast<uint64_t*>(
+        (reinterpret_cast<uintptr_t>(gF + warps * per_warp) + 15) & ~uintptr_t(15));
+    gT = reinterpret_cast<int32_t*>(gM + warps * (int64_t)k);
+  }
   C4SketchArgs args{kind == PG_KMV ? nullptr : static_cast<const int32_t*>(rows),
-                    kind == PG_KMV ? static_cast<const double*>(rows) : nullptr, lengths, sizes, seeds_dev, k};
+                    kind == PG_KMV ? static_cast<const double*>(rows) : nullptr, lengths, sizes, seeds_dev, k,
+                    gM, gT, tcap};
   auto* trip = reinterpret_cast<unsigned long long*>(out_triples);
 #define PG_C4S(KK)                                                                                       \
   clique4_sketch_kernel<KK><<<grid, kCSBlock, c4s_smem(), s>>>(dir_off, dir_adj, src, edge_ids, e_begin, e_end, \

@@ -1,6 +1,6 @@
 // KMV per-edge estimates (providers.py:266-301 KmvProvider.pair_many) and
 // the fused KMV TC sum.
-#include "pg_engines.cuh"
+#include "pg_generic.cuh"
 
 namespace pg {
 
@@ -541,12 +541,13 @@ int pg_pairs_kmv(const double* values, const int32_t* lengths, int32_t k, const 
                  int32_t* out_union, double* out_kth, double* out_est, void* stream) {
   (void)lengths;  // lengths are implied by the +inf pads of each row
   PG_REQUIRE(k >= 1, "k must be >= 1");
-  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(count >= 0, "count must be >= 0");
   if (count == 0) return PG_OK;
   PG_REQUIRE(values && sizes && us && vs, "null pointer");
   cudaStream_t s = as_stream(stream);
   const uint64_t* vb = reinterpret_cast<const uint64_t*>(values);
+  if (k > kMaxSketchK)
+    return gen_pairs_kmv(vb, k, sizes, us, vs, count, out_common, out_union, out_kth, out_est, s);
   if (kmv_sorted(s, false, vb, k, sizes, us, vs, 0, count, out_common, out_union, out_kth, out_est, nullptr))
     return check_launch("pairs_kmv_sorted");
   const int grid = grid_cap(sm_count() * 8, count, kBlock / 32);
@@ -564,7 +565,6 @@ int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k, const int
               void* stream) {
   (void)lengths;
   PG_REQUIRE(k >= 1, "k must be >= 1");
-  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
   PG_REQUIRE(out_sum, "null pointer");
   cudaStream_t s = as_stream(stream);
@@ -573,6 +573,7 @@ int pg_tc_kmv(const double* values, const int32_t* lengths, int32_t k, const int
   if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
   PG_REQUIRE(values && us && vs && sizes, "null pointer");
   const uint64_t* vb = reinterpret_cast<const uint64_t*>(values);
+  if (k > kMaxSketchK) return gen_tc_kmv(vb, k, sizes, us, vs, e_begin, e_end, out_sum, s);
   if (kmv_sorted(s, true, vb, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, nullptr, nullptr, out_sum))
     return check_launch("tc_kmv_sorted");
 #define PG_KM(P)                                                                                    \

@@ -1,7 +1,7 @@
 // k-Hash / 1-Hash per-edge estimates (providers.py:197-232 pair_many,
 // _matches_khash / _matches_onehash), their fused TC reductions and the
 // Jaccard threshold count (estimators.py:123-168, mining.py:157-186).
-#include "pg_engines.cuh"
+#include "pg_generic.cuh"
 
 namespace pg {
 
@@ -475,12 +475,14 @@ int pg_pairs_minhash(const int32_t* entries, int32_t k, int32_t onehash, const i
                      const int32_t* us, const int32_t* vs, int64_t count, int32_t* out_count,
                      double* out_est, void* stream) {
   PG_REQUIRE(k >= 1, "k must be >= 1");
-  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
   PG_REQUIRE(count >= 0, "count must be >= 0");
   if (count == 0) return PG_OK;
   PG_REQUIRE(entries && us && vs, "null pointer");
   PG_REQUIRE(!out_est || sizes, "estimate needs sizes");
+  PG_REQUIRE(!onehash || sizes, "1-Hash needs sizes");
   cudaStream_t s = as_stream(stream);
+  if (k > kMaxSketchK)
+    return gen_pairs_minhash(entries, k, onehash != 0, sizes, us, vs, count, out_count, out_est, s);
   if (onehash) {
     PG_REQUIRE(sizes, "1-Hash needs sizes");
     if (onehash_sorted(s, false, entries, k, sizes, us, vs, 0, count, out_count, out_est, nullptr, nullptr,
@@ -519,7 +521,7 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
                   const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end, int32_t padded,
                   int64_t* out_cnt, int64_t* out_ssum, int64_t* out_verbatim, void* stream) {
   PG_REQUIRE(k >= 1, "k must be >= 1");
-  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(k <= kMaxSketchK || padded != 2, "group-u slots need k <= %d", kMaxSketchK);
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
   PG_REQUIRE(out_cnt && out_ssum && out_verbatim, "null pointer");
   cudaStream_t s = as_stream(stream);
@@ -531,6 +533,9 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
   if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
   PG_REQUIRE(entries && us && vs && sizes, "null pointer");
+  if (k > kMaxSketchK)
+    return gen_tc_minhash(entries, k, onehash != 0, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim,
+                          s);
   if (onehash && padded && (k == 32 || k == 64 || k == 128)) {
     // the row-padded layout of pad 32 * kOnehashPerLane / k: one u per warp iteration
     const int pad = 32 * kOnehashPerLane / k;
@@ -594,7 +599,7 @@ int pg_jaccard_count_khash(const int32_t* entries, int32_t k, const int32_t* deg
                            const int32_t* vs, int64_t e_begin, int64_t e_end, int32_t padded,
                            int32_t min_matches, double tau, int64_t* out_counts, void* stream) {
   PG_REQUIRE(k >= 1, "k must be >= 1");
-  if (k > kMaxSketchK) return fail(PG_ERR_UNSUPPORTED, "k=%d exceeds the device limit %d", k, kMaxSketchK);
+  PG_REQUIRE(k <= kMaxSketchK || padded != 2, "group-u slots need k <= %d", kMaxSketchK);
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
   PG_REQUIRE(out_counts, "null pointer");
   cudaStream_t s = as_stream(stream);
@@ -602,6 +607,8 @@ int pg_jaccard_count_khash(const int32_t* entries, int32_t k, const int32_t* deg
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
   if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
   PG_REQUIRE(entries && us && vs && degrees, "null pointer");
+  if (k > kMaxSketchK)
+    return gen_jaccard_khash(entries, k, degrees, us, vs, e_begin, e_end, min_matches, tau, out_counts, s);
   const int w4 = k % 4 == 0 ? k / 4 : 0;
   const uint4* e4 = reinterpret_cast<const uint4*>(entries);
   const int w8 = k % 8 == 0 ? k / 8 : 0;  // 32-byte chunks per row
