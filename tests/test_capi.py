@@ -58,7 +58,12 @@ def test_seed_derivation_and_error_reporting_without_gpu():
     rc = lib.pg_build_bloom(None, None, 10, 100, 1, None, None, None, None)
     assert rc == N.PG_ERR_INVALID
     assert "multiple of 64" in N.last_error()
+    # k > 256 has a generic device path: only the null pointers are rejected
     rc = lib.pg_build_khash(None, None, 10, 1000, None, None, None)
+    assert rc == N.PG_ERR_INVALID
+    assert "null pointer" in N.last_error()
+    # an engine-specific range is reported as unsupported (callers fall back)
+    rc = lib.pg_tc_kmv_ranked(None, None, None, 40, None, None, None, 0, 1, None, None)
     assert rc == N.PG_ERR_UNSUPPORTED
     with pytest.raises(ValueError):
         N.check(N.PG_ERR_INVALID)
