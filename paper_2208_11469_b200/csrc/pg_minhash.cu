@@ -17,7 +17,10 @@ __global__ void __launch_bounds__(kBlock) pairs_khash_kernel(const uint4* ent, i
 // CTAs/SM of the wide k-Hash engine for 128-byte rows (k = 32): 4 (64
 // registers) measured 3.70 vs 4.04 ms at c4 over 3 -- the random row gathers
 // are latency-bound, more warps in flight win
-constexpr int kKhash128Minb = 4;
+#ifndef PG_KHASH128_MINB
+#define PG_KHASH128_MINB 4
+#endif
+constexpr int kKhash128Minb = PG_KHASH128_MINB;
 #ifndef PG_KHASH_VCACHE
 #define PG_KHASH_VCACHE 0
 #endif
