@@ -3,6 +3,10 @@
 // (mining.py:105-130 tc_estimate over _chunked_sum :63-80).
 #include "pg_generic.cuh"
 
+#ifndef PG_WIDE_MINB
+#define PG_WIDE_MINB 3  // CTAs/SM of the L1-cached group-u wide kernel
+#endif
+
 namespace pg {
 
 // ------------------------------------------------ fixed-row kernels ----
@@ -207,7 +211,7 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
   }
 #define PG_WM(W8)                                                                  \
   if (padded == 2) {                                                             \
-    if (vcache) { if (minb <= 2 && !ctr.p) PG_W(W8, 2, true, 2) else PG_W(W8, 3, true, 2) } \
+    if (vcache) { if (minb <= 2 && !ctr.p) PG_W(W8, 2, true, 2) else PG_W(W8, PG_WIDE_MINB, true, 2) } \
     else if (minb <= 2) PG_W(W8, 2, false, 2)                                    \
     else PG_W(W8, 3, false, 2)                                                   \
   } else if (padded) {                                                           \

@@ -67,6 +67,9 @@ struct OpOr {
 #ifndef PG_IMAD_ADDS
 #define PG_IMAD_ADDS 1
 #endif
+#ifndef PG_WIDE_SUB
+#define PG_WIDE_SUB 8  // v rows in flight per sub-step of the padded wide engine
+#endif
 static __constant__ int kImadW[4] = {1, 2, 4, 8};
 __device__ __forceinline__ int imad(int a, int b, int c) { return a * b + c; }
 
@@ -376,17 +379,24 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
       un = kLayout == 2 ? us[(e + 32) / G] : us[e + 32];
       vn = vs[e + 32];
     }
-    uint32_t vr[G][V][8];
+    // rows in flight per sub-step: all G (default), or kSub at a time so
+    // fewer registers hold rows (more CTAs per SM)
+    constexpr int kSub = (kPadded && PG_WIDE_SUB < G) ? PG_WIDE_SUB : G;
+    int c[G];
 #pragma unroll
-    for (int j = 0; j < G; ++j) {
+    for (int j0 = 0; j0 < G; j0 += kSub) {
+    uint32_t vr[kSub][V][8];
+#pragma unroll
+    for (int jj = 0; jj < kSub; ++jj) {
+      const int j = j0 + jj;
       const int32_t vj = __shfl_sync(0xffffffffu, vl, j, G);
       // lane base + row * bytes: one IMAD.WIDE.U32 (FMA pipe) per row
       // instead of multiply, OR and a 64-bit add on the ALU pipe
       const unsigned char* rv = row_addr(rows_gl, (uint32_t)(vj < 0 ? 0 : vj), kRowBytesC[W8]);
 #pragma unroll
       for (int i = 0; i < V; ++i) {
-        if (kVCache) ldg256_keep(rv + i * G * 32, vr[j][i]);
-        else ldg256(rv + i * G * 32, vr[j][i]);
+        if (kVCache) ldg256_keep(rv + i * G * 32, vr[jj][i]);
+        else ldg256(rv + i * G * 32, vr[jj][i]);
       }
     }
     // u rows: with the row-padded edge layout (pg_csr_upper_edges_padded)
@@ -398,7 +408,6 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
 #pragma unroll
       for (int j = 1; j < G; ++j) uniform &= __shfl_sync(0xffffffffu, ul, j, G) == u0;
     }
-    int c[G];
     if (kPadded || __all_sync(0xffffffffu, uniform)) {
       if (u0 != ucur) {
         ucur = u0;
@@ -407,11 +416,11 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
         for (int i = 0; i < V; ++i) ldg256_keep(ru + i * G * 32, ur[i]);
       }
 #pragma unroll
-      for (int j = 0; j < G; ++j) {
+      for (int jj = 0; jj < kSub; ++jj) {
         int acc = 0;
 #pragma unroll
-        for (int i = 0; i < V; ++i) acc += Op::apply8(ur[i], vr[j][i]);
-        c[j] = acc;
+        for (int i = 0; i < V; ++i) acc += Op::apply8(ur[i], vr[jj][i]);
+        c[j0 + jj] = acc;
       }
     } else if (!kPadded) {
 #pragma unroll
@@ -429,6 +438,7 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
         c[j] = acc;
       }
     }
+    }  // sub-steps
     const int cnt = group_transpose_reduce<G>(c, gl);
     if (valid) epi.edge(e, ul, vl, cnt);
     ul = un;
