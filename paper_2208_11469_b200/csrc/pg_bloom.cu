@@ -191,6 +191,11 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
     // dynamic variant of the 256-byte-row kernel fits 3 CTAs/SM in 80
     // registers without spills (c5: 5.48 vs 6.09 ms at 2 CTAs/SM); the static
     // one spills 216 bytes there and keeps 2
+    // shared-memory carveout hint (percent; PG_TC_CARVEOUT, default: driver)
+    static const int carveout = [] {
+      const char* v = getenv("PG_TC_CARVEOUT");
+      return v ? atoi(v) : -1;
+    }();
     ChunkCounter ctr;
     if (dyn && !range_dev && e_end - e_begin >= kDynamicMinSlots && (le = ctr.init(s)) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter: %s", cudaGetErrorString(le));
 #define PG_WK(W8, MB, VC, PD, SCH)                                                                    \
@@ -204,6 +209,8 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
     if (range_dev) k = PG_WK(W8, MB, VC, PD, 2);                                                     \
     else if (ctr.p) k = PG_WK(W8, MB, VC, PD, 1);                                                    \
     le = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);            \
+    if (le == cudaSuccess && carveout >= 0)                                                          \
+      le = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, carveout);        \
     if (le != cudaSuccess) return fail(PG_ERR_CUDA, "smem attribute: %s", cudaGetErrorString(le));  \
     const int grid = grid_cap(grid_for_kernel(k, smem), e_end - e_begin, kBlock);                    \
     k<<<grid, kBlock, smem, s>>>(rb, bits, us, vs, e_begin, e_end, epi, out_hist, out_sum_pos, ctr.p,  \
