@@ -170,7 +170,7 @@ static int tc_bloom_impl(const uint64_t* rows, int32_t bits, int32_t op, const i
     return 2;                        // 256-bit loads (wide_edge_loop, default)
   }();
   if (engine == 2 && (w4 == 4 || w4 == 8 || w4 == 16)) {
-    // measured on B200 (scripts/sweep_tc.py, R-MAT s20/s22): B=1024 best with
+    // measured on B200 (scripts/probe_tc.py, R-MAT s20/s22): B=1024 best with
     // 3 blocks/SM and streaming v rows; B=2048 best with L1-allocated v rows
     // (hub rows reused within an SM)
     static const char* vc_env = getenv("PG_TC_VCACHE");
