@@ -121,9 +121,8 @@ PG_API int pg_csr_expand_rows(const int64_t* offsets, int64_t n, int64_t nnz,
  *      :399-451 build_sketched_graph) ------------------------------------
  * Every size plan_budget produces is served: Bloom rows up to 65,536 bits and
  * k <= 256 by the tuned kernels; wider rows / larger k by generic kernels
- * (pg_generic.cu: global atomics, a thread per (vertex, function), CUB
- * segmented sorts -- the 1-Hash / KMV generic builders synchronise the
- * stream once to cut vertex ranges).  The estimators below likewise fall
+ * (pg_generic.cu: global atomics, a thread per (vertex, function), a
+ * warp-level radix select per vertex).  The estimators below likewise fall
  * back to warp-per-edge kernels with global statistics for k > 256 and
  * Bloom rows over 32,768 bits (16,384 for the 4-clique count). */
 /* seeds_dev: the HashFamily seeds (count = b, k, 1, 1 respectively) */

@@ -20,7 +20,16 @@
 #include <cub/device/device_scan.cuh>
 
 #include "pg_common.cuh"
-#include "pg_generic.cuh"
+
+namespace pg {  // generic builders (pg_generic.cu, declared in pg_generic.cuh)
+int gen_build_bloom(const int64_t* off, const int32_t* adj, int64_t n, int bits, int b, const uint64_t* seeds,
+                    uint64_t* rows, int32_t* ones, cudaStream_t s);
+int gen_build_khash(const int64_t* off, const int32_t* adj, int64_t n, int k, const uint64_t* seeds,
+                    int32_t* entries, cudaStream_t s);
+int gen_build_bottomk(const int64_t* off, const int32_t* adj, int64_t n, int k, const uint64_t* seeds,
+                      int32_t* entries, double* values, int32_t* ranks, const int32_t* rank_of,
+                      int32_t* lengths, cudaStream_t s);
+}  // namespace pg
 
 namespace pg {
 

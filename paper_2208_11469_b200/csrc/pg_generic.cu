@@ -7,16 +7,11 @@
 // warp-per-edge loops over global memory.
 //
 // Builders  (sketches.py:314-396): Bloom by global 64-bit atomicOr, k-Hash
-//           by a thread per (vertex, hash function), 1-Hash / KMV by CUB
-//           segmented sorts of (h_0(x), x) per vertex range.
+//           by a thread per (vertex, hash function), 1-Hash / KMV by a
+//           warp-level radix select of the k-th smallest h_0 per vertex.
 // Estimators (providers.py:137-301): warp per edge; integer statistics in
 //           global memory (histograms, per-match sums), fp64 KMV sums from
 //           fixed-slot partials (PartialSums).
-#include <cub/device/device_segmented_sort.cuh>
-
-#include <algorithm>
-#include <vector>
-
 #include "pg_generic.cuh"
 
 namespace pg {
@@ -128,82 +123,150 @@ int gen_build_khash(const int64_t* off, const int32_t* adj, int64_t n, int k, co
   return check_launch("build_khash_generic");
 }
 
-// (h_0(x), x) pairs of the entries of vertices [c0, c1) and the segment
-// offsets relative to the chunk's first entry
-__global__ void gen_fill_keys_kernel(const int64_t* __restrict__ off, const int32_t* __restrict__ adj, int64_t c0,
-                                     int64_t c1, uint64_t seed0, uint64_t* __restrict__ keys,
-                                     int32_t* __restrict__ vals, int64_t* __restrict__ rel) {
-  const int64_t base = off[c0], cnt = off[c1] - base;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < cnt; j += stride) {
-    const int32_t x = adj[base + j];
-    keys[j] = hash_word(seed0, x);
-    vals[j] = x;
+// k-th smallest h_0 over a vertex's neighbours by MSB radix select (8-bit
+// digits, a warp-private 256-bin histogram per pass); keys are distinct
+// (h_0 is a bijection), so exactly `target` keys are <= the result
+__device__ uint64_t gen_select_kth(const int32_t* __restrict__ nb, int64_t d, uint64_t seed0, int64_t target,
+                                   unsigned* __restrict__ hist) {
+  const int lane = threadIdx.x & 31;
+  uint64_t prefix = 0, pmask = 0;
+  int64_t rem = target;  // rank still to find inside the current prefix class
+  for (int shift = 56; shift >= 0; shift -= 8) {
+    for (int i = lane; i < 256; i += 32) hist[i] = 0u;
+    __syncwarp();
+    for (int64_t j = lane; j < d; j += 32) {
+      const uint64_t h = hash_word(seed0, nb[j]);
+      if ((h & pmask) == prefix) atomicAdd(hist + ((h >> shift) & 255u), 1u);
+    }
+    __syncwarp();
+    // the digit whose cumulative count reaches rem (one lane scans)
+    unsigned dig = 0;
+    int64_t before = 0;
+    if (lane == 0) {
+      int64_t c = 0;
+      for (int i = 0; i < 256; ++i) {
+        if (c + hist[i] >= (uint64_t)rem) {
+          dig = i;
+          before = c;
+          break;
+        }
+        c += hist[i];
+      }
+    }
+    dig = __shfl_sync(0xffffffffu, dig, 0);
+    before = __shfl_sync(0xffffffffu, before, 0);
+    rem -= before;
+    prefix |= (uint64_t)dig << shift;
+    pmask |= 255ull << shift;
+    __syncwarp();
   }
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= c1 - c0; v += stride)
-    rel[v] = off[c0 + v] - base;
+  return prefix;
 }
 
-// Finish vertex v's row from its sorted (key, x) segment.
+// Bottom-k rows for any k (warp per vertex; no sorting of whole rows):
 // 1-Hash (_select_bottom_k, sketches.py:346-372): the min(d, k) members of
-// smallest h_0 as ascending IDs -- the keys are distinct (h_0 is a
-// bijection), so the selection is {x : h_0(x) <= the min(d,k)-th key}, taken
-// from the ID-sorted adjacency in order.
-// KMV (_build_kmv_matrix, :375-396): the first min(k, distinct) distinct
-// unit values of the hash-sorted keys (unit_value is monotone in the key).
+// smallest h_0 -- those with h_0 <= the min(d,k)-th smallest key -- taken in
+// ID order from the sorted adjacency.
+// KMV (_build_kmv_matrix, :375-396): the first min(k, distinct) distinct unit
+// values.  unit_value is monotone in h_0, so the candidates are the t
+// members of smallest h_0 with t grown past k until they hold k distinct
+// values (equal doubles from distinct words are rare); the candidates are
+// then placed by distinct rank (O(t^2 / 32) per vertex, in the warp's
+// global scratch of `cap` slots).
 template <bool kKmv>
-__global__ void __launch_bounds__(kGB) gen_bottomk_finish_kernel(
-    const int64_t* __restrict__ off, const int32_t* __restrict__ adj, int64_t c0, int64_t c1, int k,
-    uint64_t seed0, const uint64_t* __restrict__ keys, const int32_t* __restrict__ vals,
-    const int64_t* __restrict__ rel, int32_t* __restrict__ entries, double* __restrict__ values,
-    int32_t* __restrict__ ranks, const int32_t* __restrict__ rank_of, int32_t* __restrict__ lengths) {
+__global__ void __launch_bounds__(kGB) gen_bottomk_kernel(
+    const int64_t* __restrict__ off, const int32_t* __restrict__ adj, int64_t n, int k,
+    const uint64_t* __restrict__ seeds, int32_t* __restrict__ entries, double* __restrict__ values,
+    int32_t* __restrict__ ranks, const int32_t* __restrict__ rank_of, int32_t* __restrict__ lengths,
+    uint64_t* __restrict__ scratch, int32_t* __restrict__ scratch_x, int32_t* __restrict__ scratch_f, int64_t cap) {
+  __shared__ unsigned hist_all[kGB / 32][256];
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  for (int64_t r = warp_id_global(); r < c1 - c0; r += warps_total()) {
-    const int64_t v = c0 + r;
-    const int64_t sb = rel[r], d = rel[r + 1] - sb;
+  unsigned* hist = hist_all[threadIdx.x >> 5];
+  const uint64_t seed0 = seeds[0];
+  uint64_t* U = scratch + warp_id_global() * cap;    // KMV candidate unit bits
+  int32_t* X = scratch_x + warp_id_global() * cap;   // their IDs
+  int32_t* F = scratch_f + warp_id_global() * cap;   // repeat flags
+  for (int64_t v = warp_id_global(); v < n; v += warps_total()) {
+    const int32_t* nb = adj + off[v];
+    const int64_t d = off[v + 1] - off[v];
     int cnt = 0;
     if (!kKmv) {
       int32_t* row = entries + v * (int64_t)k;
-      if (d > 0) {
-        const int64_t sel = d < k ? d : k;
-        const uint64_t thr = keys[sb + sel - 1];
-        for (int64_t j0 = 0; j0 < d && cnt < sel; j0 += 32) {
-          const int64_t j = j0 + lane;
-          const int32_t x = j < d ? adj[off[v] + j] : 0;
-          const bool take = j < d && hash_word(seed0, x) <= thr;
-          const unsigned m = __ballot_sync(0xffffffffu, take);
-          if (take) row[cnt + __popc(m & lt)] = x;
-          cnt += __popc(m);
-        }
+      const int64_t sel = d < k ? d : k;
+      const uint64_t thr = d > k ? gen_select_kth(nb, d, seed0, sel, hist) : ~0ull;
+      for (int64_t j0 = 0; j0 < d && cnt < sel; j0 += 32) {
+        const int64_t j = j0 + lane;
+        const int32_t x = j < d ? nb[j] : 0;
+        const bool take = j < d && hash_word(seed0, x) <= thr;
+        const unsigned m = __ballot_sync(0xffffffffu, take);
+        if (take) row[cnt + __popc(m & lt)] = x;
+        cnt += __popc(m);
       }
       for (int i = cnt + lane; i < k; i += 32) row[i] = -1;
     } else {
       double* row = values + v * (int64_t)k;
       int32_t* rrow = ranks ? ranks + v * (int64_t)k : nullptr;
-      for (int64_t j0 = 0; j0 < d && cnt < k; j0 += 32) {
-        const int64_t j = j0 + lane;
-        double u = 0.0;
-        bool first = false;
-        if (j < d) {
-          u = unit_value(keys[sb + j]);
-          first = j == 0 || unit_value(keys[sb + j - 1]) != u;  // drop repeats of a value
+      int64_t t = d < k ? d : k;
+      int nd = 0;
+      for (;;) {  // candidates: the t members of smallest h_0
+        const uint64_t thr = t < d ? gen_select_kth(nb, d, seed0, t, hist) : ~0ull;
+        int c = 0;
+        for (int64_t j0 = 0; j0 < d; j0 += 32) {
+          const int64_t j = j0 + lane;
+          const int32_t x = j < d ? nb[j] : 0;
+          const uint64_t h = hash_word(seed0, x);
+          const bool take = j < d && h <= thr;
+          const unsigned m = __ballot_sync(0xffffffffu, take);
+          if (take) {
+            U[c + __popc(m & lt)] = dbits(unit_value(h));
+            X[c + __popc(m & lt)] = x;
+          }
+          c += __popc(m);
         }
-        const unsigned m = __ballot_sync(0xffffffffu, first);
-        const int pos = cnt + __popc(m & lt);
-        if (first && pos < k) {
-          row[pos] = u;
-          if (rrow) rrow[pos] = rank_of[vals[sb + j]];
+        __syncwarp();
+        // distinct values among the candidates (first copy by index)
+        nd = 0;
+        for (int i = lane; i < c; i += 32) {
+          bool dup = false;
+          for (int q = 0; q < i; ++q) dup |= U[q] == U[i];
+          F[i] = dup;
+          nd += !dup;
         }
-        cnt += __popc(m);
+        nd = __reduce_add_sync(0xffffffffu, nd);
+        if (nd >= k || t >= d) {
+          // repeats get the sign bit (unit values are positive doubles, so
+          // flagged bits compare above every value); place the first copies
+          // by distinct rank and keep ranks < k
+          for (int i = lane; i < c; i += 32)
+            if (F[i]) U[i] |= 1ull << 63;
+          __syncwarp();
+          for (int i = lane; i < c; i += 32) {
+            const uint64_t x = U[i];
+            if (x >> 63) continue;
+            int r = 0;
+            for (int q = 0; q < c; ++q) r += U[q] < x;
+            if (r < k) {
+              row[r] = bitsd(x);
+              if (rrow) rrow[r] = rank_of[X[i]];
+            }
+          }
+          break;
+        }
+        __syncwarp();
+        t += k - nd;  // room for the repeats
+        if (t > d) t = d;
+        __syncwarp();
       }
-      cnt = cnt < k ? cnt : k;
+      cnt = nd < k ? nd : k;
+      __syncwarp();
       for (int i = cnt + lane; i < k; i += 32) {
         row[i] = __longlong_as_double((long long)kInfBits);
         if (rrow) rrow[i] = INT32_MAX;
       }
     }
     if (lane == 0) lengths[v] = cnt;
+    __syncwarp();
   }
 }
 
@@ -211,72 +274,26 @@ int gen_build_bottomk(const int64_t* off, const int32_t* adj, int64_t n, int k, 
                       int32_t* entries, double* values, int32_t* ranks, const int32_t* rank_of,
                       int32_t* lengths, cudaStream_t s) {
   const bool kmv = values != nullptr;
-  // host copy of the offsets to cut vertex ranges of bounded volume (the
-  // generic path synchronises here)
-  std::vector<int64_t> h(n + 1);
-  cudaError_t e = cudaMemcpyAsync(h.data(), off, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "offsets: %s", cudaGetErrorString(e));
-  uint64_t seed0 = 0;
-  e = cudaMemcpyAsync(&seed0, seeds, sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "seed: %s", cudaGetErrorString(e));
-  constexpr int64_t kVol = int64_t(1) << 25;  // entries per range
-  std::vector<std::pair<int64_t, int64_t>> ranges;
-  int64_t max_items = 0, max_rows = 0;
-  for (int64_t c0 = 0; c0 < n;) {
-    int64_t c1 = c0 + 1;
-    while (c1 < n && h[c1 + 1] - h[c0] <= kVol && c1 - c0 < kVol) ++c1;
-    ranges.emplace_back(c0, c1);
-    max_items = std::max(max_items, h[c1] - h[c0]);
-    max_rows = std::max(max_rows, c1 - c0);
-    c0 = c1;
+  const int grid = gen_grid();
+  if (!kmv) {
+    gen_bottomk_kernel<false><<<grid, kGB, 0, s>>>(off, adj, n, k, seeds, entries, nullptr, nullptr, nullptr,
+                                                   lengths, nullptr, nullptr, nullptr, 0);
+    return check_launch("build_onehash_generic");
   }
-  size_t temp = 0;
-  e = cub::DeviceSegmentedSort::SortPairs(nullptr, temp, (const uint64_t*)nullptr, (uint64_t*)nullptr,
-                                          (const int32_t*)nullptr, (int32_t*)nullptr,
-                                          (int)(max_items > 0 ? max_items : 1), (int)max_rows,
-                                          (const int64_t*)nullptr, (const int64_t*)nullptr, s);
-  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "segmented sort: %s", cudaGetErrorString(e));
-  const size_t items = (size_t)(max_items > 0 ? max_items : 1);
-  const size_t bytes = items * 8 * 2 + items * 4 * 2 + (size_t)(max_rows + 1) * 8 + temp + 1024;
+  // KMV candidates: up to 2k per warp (t grows past k only by the repeats)
+  const int64_t cap = 2 * (int64_t)k + 64;
+  const int64_t warps = (int64_t)grid * (kGB / 32);
   retain_default_pool();
   unsigned char* ws = nullptr;
-  e = cudaMallocAsync(reinterpret_cast<void**>(&ws), bytes, s);
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&ws), (size_t)warps * cap * 16 + 256, s);
   if (e != cudaSuccess) return fail(PG_ERR_CUDA, "scratch: %s", cudaGetErrorString(e));
-  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
-  unsigned char* p = ws;
-  uint64_t* kin = reinterpret_cast<uint64_t*>(p);
-  p += al(items * 8);
-  uint64_t* kout = reinterpret_cast<uint64_t*>(p);
-  p += al(items * 8);
-  int32_t* vin = reinterpret_cast<int32_t*>(p);
-  p += al(items * 4);
-  int32_t* vout = reinterpret_cast<int32_t*>(p);
-  p += al(items * 4);
-  int64_t* rel = reinterpret_cast<int64_t*>(p);
-  p += al((size_t)(max_rows + 1) * 8);
-  // (the al() padding above is within the 1 KiB slack)
-  void* tmp = p;
-  for (auto [c0, c1] : ranges) {
-    const int64_t cnt = h[c1] - h[c0];
-    gen_fill_keys_kernel<<<gen_grid(), kGB, 0, s>>>(off, adj, c0, c1, seed0, kin, vin, rel);
-    if (cnt > 0) {
-      size_t tb = temp;
-      e = cub::DeviceSegmentedSort::SortPairs(tmp, tb, kin, kout, vin, vout, (int)cnt, (int)(c1 - c0), rel,
-                                              rel + 1, s);
-      if (e != cudaSuccess) break;
-    }
-    if (kmv)
-      gen_bottomk_finish_kernel<true><<<gen_grid(), kGB, 0, s>>>(off, adj, c0, c1, k, seed0, kout, vout, rel,
-                                                                 nullptr, values, ranks, rank_of, lengths);
-    else
-      gen_bottomk_finish_kernel<false><<<gen_grid(), kGB, 0, s>>>(off, adj, c0, c1, k, seed0, kout, vout, rel,
-                                                                  entries, nullptr, nullptr, nullptr, lengths);
-  }
+  uint64_t* U = reinterpret_cast<uint64_t*>(ws);
+  int32_t* X = reinterpret_cast<int32_t*>(U + warps * cap);
+  int32_t* F = X + warps * cap;
+  gen_bottomk_kernel<true><<<grid, kGB, 0, s>>>(off, adj, n, k, seeds, nullptr, values, ranks, rank_of, lengths,
+                                                U, X, F, cap);
   cudaFreeAsync(ws, s);
-  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "segmented sort: %s", cudaGetErrorString(e));
-  return check_launch("build_bottomk_generic");
+  return check_launch("build_kmv_generic");
 }
 
 // ----------------------------------------------------------- estimators --

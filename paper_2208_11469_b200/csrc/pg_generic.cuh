@@ -15,7 +15,7 @@ int gen_build_bloom(const int64_t* off, const int32_t* adj, int64_t n, int bits,
 int gen_build_khash(const int64_t* off, const int32_t* adj, int64_t n, int k, const uint64_t* seeds,
                     int32_t* entries, cudaStream_t s);
 // 1-Hash (values == nullptr) or KMV (entries == nullptr; ranks / rank_of
-// nullable) bottom-k rows for any k, by segmented sorts of (h_0(x), x)
+// nullable) bottom-k rows for any k, by a warp radix select of h_0(x)
 int gen_build_bottomk(const int64_t* off, const int32_t* adj, int64_t n, int k, const uint64_t* seeds,
                       int32_t* entries, double* values, int32_t* ranks, const int32_t* rank_of,
                       int32_t* lengths, cudaStream_t s);

@@ -1,0 +1,6 @@
+set -x
+for r in _r1 _b_a127576 _b_4b52a2a _b_1e2d429 _b_eec858b .; do
+  echo "== $r" >> gpurun_out/e2e_v.log
+  PG_REPO=$PWD/$r timeout 600 python scripts/time_e2e_c5.py 20 >> gpurun_out/e2e_v.log 2>&1
+done
+cat gpurun_out/e2e_v.log
