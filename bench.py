@@ -378,7 +378,11 @@ def run_ours(args, cfg, rank, world, local):
                        "layout_build_s": layout_s},
             "roofline": roofline,
             "clocks": clk.summary(),
-            "gpu_launches": args.steps,
+            # per timed step: the fused TC kernel (one graph replay) and the
+            # L2-flush kernel between steps (outside the events, inside the
+            # synchronised region)
+            "gpu_launches": 2 * args.steps,
+            "gpu_launches_per_step": {"tc_bloom_wide_kernel": 1, "l2_flush_kernel": 1},
             "cuda_graph": graph_note or "one graph replay per step (kernel + all-reduce)",
             "e2e": e2e,
             "cpu_baseline": cpu,
