@@ -45,8 +45,10 @@ extern "C" {
 #define PG_OK 0
 #define PG_ERR_INVALID (-1)     /* bad argument            -> ValueError     */
 #define PG_ERR_CUDA (-2)        /* CUDA runtime failure    -> RuntimeError   */
-#define PG_ERR_UNSUPPORTED (-3) /* parameter outside the device kernels'
-                                   supported range (e.g. k > 256)            */
+#define PG_ERR_UNSUPPORTED (-3) /* parameter outside an engine's range (e.g.
+                                   the rank-directory KMV engine's k in
+                                   {32, 64, 128}); the library's public paths
+                                   fall back to a general engine            */
 
 /* estimator / op selectors (reference EstimatorKind, estimators.py:54-62) */
 #define PG_BF_AND 0
