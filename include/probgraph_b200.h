@@ -16,6 +16,14 @@
  *   - `stream` is a cudaStream_t passed as void*; NULL means the legacy
  *     default stream.  Calls are asynchronous and stream-ordered; none of
  *     them synchronises the host except where stated;
+ *   - scratch: the large, input-sized scratch is caller-allocated with a
+ *     size query (pg_csr_upper_edges_workspace, pg_csr_range_slots_workspace,
+ *     pg_4clique_sketch_workspace_size); small or launch-shaped scratch
+ *     (dynamic-chunk counters, per-block fp64 partial sums, hub lists, the
+ *     generic kernels' per-warp rows) is taken stream-ordered from the
+ *     device's default memory pool (cudaMallocAsync / cudaFreeAsync on the
+ *     call's stream; the pool's release threshold is raised once so repeated
+ *     calls reuse it) -- no call allocates persistently;
  *   - vertex IDs are int32 (n < 2^31), CSR offsets are int64;
  *   - sketch layouts in HBM (row-major, one row per vertex):
  *       Bloom : uint64 rows[n][bits/64], little-endian bit p of the row is

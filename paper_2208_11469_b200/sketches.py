@@ -307,19 +307,42 @@ class SketchedGraph:
     lengths = property(lambda self: self._mirror("lengths"))
     values = property(lambda self: self._mirror("values"))
 
+    def _row(self, name: str, v: int):
+        """Row v of a sketch array: from the host mirror when it exists,
+        else one row copied from the device (a scalar call must not pull
+        the whole matrix -- 4 GiB at config 5 -- to the host)."""
+        h = self._host.get(name)
+        if h is not None or not self._dev:
+            return self._mirror(name)[v]
+        t = self._dev.get({"bit_matrix": "rows"}.get(name, name))
+        if t is None:
+            return self._mirror(name)[v]
+        self._wait_ready()
+        a = t[int(v)].cpu().numpy()
+        if name == "bit_matrix":
+            return a.view(np.uint64)
+        if name == "values":
+            return a.astype(np.float64)
+        return np.asarray(a, dtype=np.int64)
+
     def sketch(self, v: int):
+        v = int(v)
+        if v < 0:  # numpy row indexing, as the reference's self.bit_matrix[v]
+            v += self.n
+        if not 0 <= v < self.n:
+            raise IndexError(f"index {v} is out of bounds for axis 0 with size {self.n}")
         if self.kind is SketchKind.BLOOM:
-            return BloomSketch(self.bit_matrix[v], self.bit_length,
-                               self.hash_count, int(self.ones[v]), self.seed)
+            return BloomSketch(self._row("bit_matrix", v), self.bit_length,
+                               self.hash_count, int(self._row("ones", v)), self.seed)
         if self.kind is SketchKind.KHASH:
-            row = self.entries[v]
+            row = self._row("entries", v)
             return KHashSketch(row if self.sizes[v] > 0 else row[:0],
                                self.capacity, self.seed)
         if self.kind is SketchKind.ONEHASH:
-            return OneHashSketch(self.entries[v, :self.lengths[v]],
+            return OneHashSketch(self._row("entries", v)[:int(self._row("lengths", v))],
                                  self.capacity, self.seed)
-        return KmvSketch(self.values[v, :self.lengths[v]], self.capacity,
-                         self.seed)
+        return KmvSketch(self._row("values", v)[:int(self._row("lengths", v))],
+                         self.capacity, self.seed)
 
     def extra_bits_used(self) -> int:
         if self.kind is SketchKind.BLOOM:
