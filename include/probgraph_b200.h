@@ -345,6 +345,25 @@ PG_API int pg_4clique_sketch(int32_t kind, const int64_t* dir_off,
                      size_t workspace_bytes, double* out_sum,
                      int64_t* out_triples, void* stream);
 
+/* Scalar with_set (providers.py:164-175, 234-241, 303-307): the estimate
+ * of |S_w & members| for vertex w and an explicit member set in one
+ * one-warp launch (the member sketch is built in shared memory with the
+ * per-set builders' semantics, sketches.py:187-237).  kind = PG_BF_AND |
+ * PG_BF_L | PG_BF_OR (rows: uint64 Bloom rows of `width` bits, hash_count
+ * functions, lut: the Swamidass table; NULL for BF_L) or PG_KHASH |
+ * PG_ONEHASH (int32 entry rows) | PG_KMV (double value rows), width = k;
+ * lengths: 1-Hash / KMV stored lengths.  members: the caller's `count`
+ * IDs sorted ascending, repeats kept (the reference builders see them:
+ * build_onehash keeps repeats and intersect_merge counts them; `count` is
+ * len(members) in the estimates).  out[0] = the estimate.  members and out may be pinned mapped host
+ * memory.  PG_ERR_UNSUPPORTED beyond 2048 members, 65,536 bits or k = 256
+ * (callers then build the member sketch with the batch builders). */
+PG_API int pg_with_set(int32_t kind, const void* rows, const int32_t* lengths,
+                     const int32_t* sizes, int32_t width, int32_t hash_count,
+                     const uint64_t* seeds_dev, const double* lut, int32_t w,
+                     const int32_t* members, int32_t count, double* out,
+                     void* stream);
+
 /* Jarvis-Patrick clustering tail (mining.py:213-245): edge i = (us[i],
  * vs[i]) is kept iff scores[i] > tau; out[0] = kept edges, out[1] =
  * connected components of the kept-edge graph (ClusterResult.cluster_count),

@@ -94,6 +94,8 @@ SIGNATURES = {
     "pg_4clique_exact_rows": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr,
                               c_ptr],
     "pg_4clique_sketch_workspace_size": [c_i32, c_i32, c_i64, ctypes.POINTER(c_size)],
+    "pg_with_set": [c_i32, c_ptr, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_i32, c_ptr, c_i32,
+                    c_ptr, c_ptr],
     "pg_4clique_sketch": [c_i32, c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr,
                           c_ptr, c_i32, c_ptr, c_i64, c_ptr, c_size, c_ptr, c_ptr, c_ptr],
     "pg_pairs_exact": [c_ptr, c_ptr, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],

@@ -21,6 +21,7 @@ current stream, which is safe.
 from __future__ import annotations
 
 import math
+import threading
 
 import numpy as np
 
@@ -68,12 +69,53 @@ def _as_device_ids(a, n: int | None = None):
     return torch.from_numpy(arr.astype(np.int32)).cuda(), False
 
 
+_SCALAR = threading.local()
+
+
+def _scalar_staging():
+    """Per-thread pinned (device-mapped) buffers for the scalar calls: the
+    two IDs go in and the result comes back without device allocations or
+    copy launches -- the kernel reads and writes them over the mapped
+    pointers, and one stream synchronisation ends the call."""
+    st = getattr(_SCALAR, "buf", None)
+    if st is None:
+        import torch
+        ids = torch.empty(2, dtype=torch.int32, pin_memory=True)
+        out = torch.empty(2, dtype=torch.int64, pin_memory=True)
+        st = _SCALAR.buf = (ids, ids.numpy(), out, out.numpy())
+    return st
+
+
+def _row_index(i, n: int) -> int:
+    """numpy's row-index rules, as the reference's row gathers."""
+    i = int(i)
+    if i < -n or i >= n:
+        raise IndexError(f"index {i} is out of bounds for axis 0 with size {n}")
+    return i + n if i < 0 else i
+
+
 class IntersectionProvider:
     kind: EstimatorKind
     is_exact = False
 
     def pair(self, u: int, v: int) -> float:
-        return float(self.pair_many(np.asarray([u]), np.asarray([v]))[0])
+        """One edge's estimate: the batch kernel on one slot, with the IDs
+        and the result in pinned mapped memory (one launch + one stream
+        synchronisation, no allocations)."""
+        import torch
+        n = self._num_vertices()
+        u, v = _row_index(u, n), _row_index(v, n)
+        ids_t, ids, out_t, out = _scalar_staging()
+        ids[0], ids[1] = u, v
+        self._pairs_launch(ids_t.data_ptr(), ids_t.data_ptr() + 4, 1, out_t.data_ptr())
+        torch.cuda.current_stream().synchronize()
+        if self.is_exact:
+            return int(out[0])
+        return float(out.view(np.float64)[0])
+
+    def _pairs_launch(self, us_ptr: int, vs_ptr: int, count: int, out_ptr: int) -> None:
+        """Enqueue the per-edge kernel over raw pointers (device or mapped)."""
+        raise NotImplementedError
 
     def _num_vertices(self) -> int:
         raise NotImplementedError
@@ -134,15 +176,15 @@ class ExactProvider(IntersectionProvider):
     def _num_vertices(self) -> int:
         return len(self.offsets) - 1
 
-    def pair(self, u: int, v: int) -> int:
-        return int(self.pair_many(np.asarray([u]), np.asarray([v]))[0])
+    def _pairs_launch(self, us_ptr, vs_ptr, count, out_ptr):
+        d = self.device()
+        N.call("pg_pairs_exact", N.ptr(d.offsets), N.ptr(d.adj), us_ptr, vs_ptr, count,
+               out_ptr, N.stream_handle())
 
     def _pairs_device(self, us, vs):
         import torch
-        d = self.device()
         out = torch.empty(max(1, us.numel()), dtype=torch.int64, device="cuda")
-        N.call("pg_pairs_exact", N.ptr(d.offsets), N.ptr(d.adj), N.ptr(us),
-               N.ptr(vs), us.numel(), N.ptr(out), N.stream_handle())
+        self._pairs_launch(N.ptr(us), N.ptr(vs), us.numel(), N.ptr(out))
         return out[:us.numel()]
 
     def with_set(self, w: int, members) -> int:
@@ -175,9 +217,45 @@ class TcLayout:
         return (self.us, self.vs, self.slots, self.padded)[i]
 
 
+_WITH_SET_CAP = 2048  # members the one-warp with_set kernel holds (pg_scalar.cu)
+
+
 class _SketchProvider(IntersectionProvider):
     def __init__(self, sketched: SketchedGraph):
         self.sketched = as_sketched_graph(sketched)
+
+    def _with_set_device(self, w, members, code: int, width: int, lut=None):
+        """with_set in one launch (pg_with_set): the members go to the
+        device sorted, repeats kept, through a pinned mapped buffer.
+        None when the set or the sketch exceeds the one-warp kernel (the
+        caller then builds the member sketch with the batch builders)."""
+        import torch
+        sg = self.sketched
+        raw = np.sort(np.asarray(members, dtype=np.int64).reshape(-1))
+        w = _row_index(w, sg.n)
+        if len(raw) and (raw[0] < 0 or raw[-1] >= 2 ** 31):
+            raise ValueError("set members must be int32 vertex IDs")
+        if len(raw) > _WITH_SET_CAP:
+            return None
+        st = getattr(_SCALAR, "set", None)
+        if st is None:
+            mt = torch.empty(_WITH_SET_CAP, dtype=torch.int32, pin_memory=True)
+            ot = torch.empty(1, dtype=torch.float64, pin_memory=True)
+            st = _SCALAR.set = (mt, mt.numpy(), ot, ot.numpy())
+        mt, mv, ot, ov = st
+        mv[:len(raw)] = raw
+        d = self._dev()
+        rows = d.get("rows") if "rows" in d else d.get("values", d.get("entries"))
+        lengths = d.get("lengths")
+        rc = N.lib().pg_with_set(code, N.ptr(rows), N.ptr(lengths) if lengths is not None else None,
+                                 N.ptr(d["sizes"]), width, sg.hash_count, N.ptr(d["seeds"]),
+                                 N.ptr(lut) if lut is not None else None, w, mt.data_ptr(),
+                                 len(raw), ot.data_ptr(), N.stream_handle())
+        if rc == N.PG_ERR_UNSUPPORTED:
+            return None
+        N.check(rc, "pg_with_set")
+        torch.cuda.current_stream().synchronize()
+        return float(ov[0])
 
     @property
     def sizes(self) -> np.ndarray:
@@ -256,14 +334,16 @@ class BloomProvider(_SketchProvider):
             self._lut = _device_lut(self.sketched.bit_length, self.sketched.hash_count)
         return self._lut
 
+    def _pairs_launch(self, us_ptr, vs_ptr, count, out_ptr):
+        d, sg = self._dev(), self.sketched
+        N.call("pg_pairs_bloom", N.ptr(d["rows"]), sg.bit_length, sg.hash_count, self.op,
+               N.ptr(d["sizes"]), N.ptr(self.lut_device()), us_ptr, vs_ptr, count, None,
+               out_ptr, N.stream_handle())
+
     def _pairs_device(self, us, vs):
         import torch
-        d, sg = self._dev(), self.sketched
         out = torch.empty(max(1, us.numel()), dtype=torch.float64, device="cuda")
-        N.call("pg_pairs_bloom", N.ptr(d["rows"]), sg.bit_length,
-               sg.hash_count, self.op, N.ptr(d["sizes"]),
-               N.ptr(self.lut_device()), N.ptr(us), N.ptr(vs), us.numel(), None,
-               N.ptr(out), N.stream_handle())
+        self._pairs_launch(N.ptr(us), N.ptr(vs), us.numel(), N.ptr(out))
         return out[:us.numel()]
 
     def pair_counts(self, us, vs):
@@ -368,6 +448,10 @@ class BloomProvider(_SketchProvider):
 
     def with_set(self, w: int, members) -> float:
         sg = self.sketched
+        got = self._with_set_device(w, members, self.op, sg.bit_length,
+                                    None if self.kind is EstimatorKind.BF_L else self.lut_device())
+        if got is not None:
+            return got
         members = np.asarray(members, dtype=np.int64)
         mem = build_bloom(members, sg.plan, sg.family)
         from .estimators import _bloom_count
@@ -427,13 +511,15 @@ class MinHashProvider(_SketchProvider):
             return TcLayout(ug, vs, slots, 2, "degree")
         return super()._tc_layout(dev)
 
+    def _pairs_launch(self, us_ptr, vs_ptr, count, out_ptr):
+        d, sg = self._dev(), self.sketched
+        N.call("pg_pairs_minhash", N.ptr(d["entries"]), sg.capacity, int(self.onehash),
+               N.ptr(d["sizes"]), us_ptr, vs_ptr, count, None, out_ptr, N.stream_handle())
+
     def _pairs_device(self, us, vs):
         import torch
-        d, sg = self._dev(), self.sketched
         out = torch.empty(max(1, us.numel()), dtype=torch.float64, device="cuda")
-        N.call("pg_pairs_minhash", N.ptr(d["entries"]), sg.capacity,
-               int(self.onehash), N.ptr(d["sizes"]), N.ptr(us), N.ptr(vs),
-               us.numel(), None, N.ptr(out), N.stream_handle())
+        self._pairs_launch(N.ptr(us), N.ptr(vs), us.numel(), N.ptr(out))
         return out[:us.numel()]
 
     def pair_counts(self, us, vs):
@@ -472,6 +558,10 @@ class MinHashProvider(_SketchProvider):
 
     def with_set(self, w: int, members) -> float:
         sg = self.sketched
+        got = self._with_set_device(w, members, N.PG_ONEHASH if self.onehash else N.PG_KHASH,
+                                    sg.capacity)
+        if got is not None:
+            return got
         members = np.asarray(members, dtype=np.int64)
         if sg.kind is SketchKind.KHASH:
             mem = build_khash(members, sg.capacity, sg.family)
@@ -493,13 +583,16 @@ class KmvProvider(_SketchProvider):
         super().__init__(sketched)
         self.kind = EstimatorKind.KMV
 
+    def _pairs_launch(self, us_ptr, vs_ptr, count, out_ptr):
+        d, sg = self._dev(), self.sketched
+        N.call("pg_pairs_kmv", N.ptr(d["values"]), N.ptr(d["lengths"]), sg.capacity,
+               N.ptr(d["sizes"]), us_ptr, vs_ptr, count, None, None, None, out_ptr,
+               N.stream_handle())
+
     def _pairs_device(self, us, vs):
         import torch
-        d, sg = self._dev(), self.sketched
         out = torch.empty(max(1, us.numel()), dtype=torch.float64, device="cuda")
-        N.call("pg_pairs_kmv", N.ptr(d["values"]), N.ptr(d["lengths"]),
-               sg.capacity, N.ptr(d["sizes"]), N.ptr(us), N.ptr(vs), us.numel(),
-               None, None, None, N.ptr(out), N.stream_handle())
+        self._pairs_launch(N.ptr(us), N.ptr(vs), us.numel(), N.ptr(out))
         return out[:us.numel()]
 
     def pair_stats(self, us, vs):
@@ -544,6 +637,9 @@ class KmvProvider(_SketchProvider):
 
     def with_set(self, w: int, members) -> float:
         sg = self.sketched
+        got = self._with_set_device(w, members, N.PG_KMV, sg.capacity)
+        if got is not None:
+            return got
         members = np.asarray(members, dtype=np.int64)
         mem = build_kmv(members, sg.capacity, sg.family)
         return est_intersection_kmv(sg.sketch(w), mem, int(self.sizes[w]),

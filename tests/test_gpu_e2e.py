@@ -216,3 +216,28 @@ def test_tc_bloom_range_accumulates_to_whole():
         N.call("pg_tc_bloom_range", N.ptr(d["rows"]), 1024, p.op, None, None, N.ptr(ug), N.ptr(vs),
                rng, bound, 1, N.ptr(out), N.ptr(out) + 8 * 1025, N.stream_handle())
     assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_scalar_sketch_row_does_not_materialise_matrix():
+    """sketch(v) (and the scalar with_set / est_* built on it) copies one
+    row from the device; the whole host mirror appears only when the
+    matrix attribute itself is read (reference sketches.py:282-295)."""
+    import paper_2208_11469_b200 as pg
+    g = pg.generate_kronecker(12, 16, 1)
+    for kind, kw in (("bloom", {"b": 2, "bits_override": 1024}), ("khash", {"k_override": 32}),
+                     ("onehash", {"k_override": 32}), ("kmv", {"k_override": 32})):
+        sk = pg.build_sketched_graph(g, kind, s=1.0, **kw)
+        rows = [sk.sketch(v) for v in (0, 5, g.n - 1, -1)]
+        name = {"bloom": "bit_matrix", "khash": "entries", "onehash": "entries",
+                "kmv": "values"}[kind]
+        assert sk._host.get(name) is None, kind
+        full = getattr(sk, name)  # now materialise and compare
+        for v, r in zip((0, 5, g.n - 1, -1), rows):
+            got = {"bloom": lambda s: s.words, "khash": lambda s: s.entries,
+                   "onehash": lambda s: s.entries, "kmv": lambda s: s.hashes}[kind](r)
+            want = full[v]
+            if kind in ("onehash", "kmv"):
+                want = want[:sk.lengths[v]]
+            if kind == "khash" and sk.sizes[v] == 0:
+                want = want[:0]
+            assert np.array_equal(got, want), (kind, v)
