@@ -16,6 +16,7 @@ bit-identical to the reference's per-edge value.
 from __future__ import annotations
 
 import enum
+import threading
 from functools import lru_cache
 
 import numpy as np
@@ -75,30 +76,54 @@ def est_single_delta_class(ones: int, delta: float) -> float:
 # two-row device batches
 
 
-def _two_rows(rows: np.ndarray, kernel: str, *args, outputs):
-    """Upload a 2-row sketch matrix and evaluate edge (0, 1) on the device."""
-    import torch
-    from . import _native as N
-    dev_rows = torch.from_numpy(np.ascontiguousarray(rows)).cuda()
-    us = torch.zeros(1, dtype=torch.int32, device="cuda")
-    vs = torch.ones(1, dtype=torch.int32, device="cuda")
-    outs = [torch.zeros(1, dtype=dt, device="cuda") for dt in outputs]
-    return dev_rows, us, vs, outs
+_STAGE = threading.local()
+
+
+class _Pinned:
+    """Per-thread pinned (device-mapped) staging for the two-row scalar
+    estimators: the rows, the edge (0, 1), the sizes and the outputs sit in
+    one host buffer the kernel reads and writes directly -- one launch and
+    one stream synchronisation per call, no device allocations or copies."""
+
+    def __init__(self, rows: np.ndarray, n_out: int):
+        import torch
+        rows = np.ascontiguousarray(rows)
+        need = rows.nbytes + 16 + 8 + 8 * n_out + 64
+        buf = getattr(_STAGE, "buf", None)
+        if buf is None or buf.numel() < need:
+            buf = _STAGE.buf = torch.empty(max(need, 1 << 16), dtype=torch.uint8, pin_memory=True)
+        self.base = buf.data_ptr()
+        host = buf.numpy()
+        host[:rows.nbytes] = rows.view(np.uint8).reshape(-1)
+        self.rows = self.base
+        o = (rows.nbytes + 15) & ~15
+        ids = host[o:o + 8].view(np.int32)
+        ids[0], ids[1] = 0, 1
+        self.us, self.vs = self.base + o, self.base + o + 4
+        self.sizes_host = host[o + 8:o + 16].view(np.int32)
+        self.sizes = self.base + o + 8
+        self.out_host = host[o + 16:o + 16 + 8 * n_out].view(np.int64)
+        self.outs = [self.base + o + 16 + 8 * i for i in range(n_out)]
+        self.out_host[:] = 0
+
+    def sync(self):
+        import torch
+        torch.cuda.current_stream().synchronize()
 
 
 def _bloom_count(sx: BloomSketch, sy: BloomSketch, use_or: bool) -> int:
-    import torch
     from . import _native as N
     if (sx.bit_length != sy.bit_length or sx.hash_count != sy.hash_count
             or sx.seed != sy.seed):
         raise ValueError("Bloom sketches have mismatched parameters")
     rows = np.stack([np.asarray(sx.words, dtype=np.uint64),
-                     np.asarray(sy.words, dtype=np.uint64)]).view(np.int64)
-    dr, us, vs, (cnt,) = _two_rows(rows, "", outputs=[torch.int32])
+                     np.asarray(sy.words, dtype=np.uint64)])
+    st = _Pinned(rows, 1)
     op = N.PG_BF_OR if use_or else N.PG_BF_AND
-    N.call("pg_pairs_bloom", N.ptr(dr), sx.bit_length, sx.hash_count, op, None,
-           None, N.ptr(us), N.ptr(vs), 1, N.ptr(cnt), None, N.stream_handle())
-    return int(cnt.item())
+    N.call("pg_pairs_bloom", st.rows, sx.bit_length, sx.hash_count, op, None,
+           None, st.us, st.vs, 1, st.outs[0], None, N.stream_handle())
+    st.sync()
+    return int(st.out_host[0:1].view(np.int32)[0])
 
 
 def est_intersection_bf_and(sx: BloomSketch, sy: BloomSketch) -> float:
@@ -128,12 +153,12 @@ def _minhash_matches(mx, my, onehash: bool) -> int:
     from . import _native as N
     k = mx.capacity
     rows = np.stack([_padded_ids(mx.entries, k), _padded_ids(my.entries, k)])
-    dr, us, vs, (cnt,) = _two_rows(rows, "", outputs=[torch.int32])
-    sizes = torch.tensor([len(mx.entries), len(my.entries)], dtype=torch.int32,
-                         device="cuda")
-    N.call("pg_pairs_minhash", N.ptr(dr), k, int(onehash), N.ptr(sizes),
-           N.ptr(us), N.ptr(vs), 1, N.ptr(cnt), None, N.stream_handle())
-    return int(cnt.item())
+    st = _Pinned(rows, 1)
+    st.sizes_host[0], st.sizes_host[1] = len(mx.entries), len(my.entries)
+    N.call("pg_pairs_minhash", st.rows, k, int(onehash), st.sizes, st.us, st.vs, 1,
+           st.outs[0], None, N.stream_handle())
+    st.sync()
+    return int(st.out_host[0:1].view(np.int32)[0])
 
 
 def est_jaccard_minhash(mx, my) -> float:
@@ -177,14 +202,13 @@ def kmv_union_stats(kx: KmvSketch, ky: KmvSketch):
     rows = np.full((2, k), np.inf, dtype=np.float64)
     rows[0, :len(kx.hashes)] = kx.hashes
     rows[1, :len(ky.hashes)] = ky.hashes
-    dr, us, vs, (com, uni, kth) = _two_rows(
-        rows, "", outputs=[torch.int32, torch.int32, torch.float64])
-    sizes = torch.zeros(2, dtype=torch.int32, device="cuda")
-    N.call("pg_pairs_kmv", N.ptr(dr), None, k, N.ptr(sizes), N.ptr(us),
-           N.ptr(vs), 1, N.ptr(com), N.ptr(uni), N.ptr(kth), None,
-           N.stream_handle())
-    return (int(com.item()), int(uni.item()),
-            min(len(kx.hashes), len(ky.hashes)), float(kth.item()))
+    st = _Pinned(rows, 3)
+    st.sizes_host[:] = 0
+    N.call("pg_pairs_kmv", st.rows, None, k, st.sizes, st.us, st.vs, 1, st.outs[0],
+           st.outs[1], st.outs[2], None, N.stream_handle())
+    st.sync()
+    return (int(st.out_host[0:1].view(np.int32)[0]), int(st.out_host[1:2].view(np.int32)[0]),
+            min(len(kx.hashes), len(ky.hashes)), float(st.out_host[2:3].view(np.float64)[0]))
 
 
 def est_intersection_kmv(kx: KmvSketch, ky: KmvSketch, size_x: int,

@@ -45,5 +45,20 @@ for name, n, p, seed in (("g200", 200, 0.08, 42), ("dense120", 120, 0.6, 7)):
         rec[key] = {"with_set": [[float(pv.with_set(w, np.asarray(m, dtype=np.int64)))
                                   for m in sets] for w in ws],
                     "pair": [float(pv.pair(u, v)) for u, v in pairs], "kw": kw, "skind": skind}
+        # the scalar estimators on sketch objects (reference estimators.py)
+        est = []
+        for u, v in pairs[:8]:
+            a, b = sk.sketch(u), sk.sketch(v)
+            su, sv = int(sk.sizes[u]), int(sk.sizes[v])
+            if skind == "bloom":
+                est.append([R.est_intersection_bf_and(a, b), R.est_intersection_bf_limit(a, b),
+                            R.est_intersection_bf_or(a, b, su, sv),
+                            R.est_intersection_bf_or(a, b, su, sv, clamp=False)])
+            elif skind in ("khash", "onehash"):
+                est.append([R.est_jaccard_minhash(a, b), R.est_intersection_minhash(a, b, su, sv)])
+            else:
+                est.append([R.est_intersection_kmv(a, b, su, sv),
+                            R.est_intersection_kmv(a, b, su, sv, clamp=False)])
+        rec[key]["est"] = [[float(x) for x in r] for r in est]
     print(name, flush=True)
 json.dump(out, open(os.path.join(HERE, "withset.json"), "w"), indent=1)

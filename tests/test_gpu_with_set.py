@@ -45,3 +45,17 @@ def test_with_set_and_pair(gold, name):
                 assert got == want, (key, w, m[:8], got, want)
         for (u, v), want in zip(rec["pairs"], r["pair"]):
             assert p.pair(u, v) == want, (key, u, v)
+        # scalar estimators over sketch objects (reference estimators.py)
+        for (u, v), want in zip(rec["pairs"][:8], r["est"]):
+            a, b = sk.sketch(u), sk.sketch(v)
+            su, sv = int(sk.sizes[u]), int(sk.sizes[v])
+            if r["skind"] == "bloom":
+                got = [pg.est_intersection_bf_and(a, b), pg.est_intersection_bf_limit(a, b),
+                       pg.est_intersection_bf_or(a, b, su, sv),
+                       pg.est_intersection_bf_or(a, b, su, sv, clamp=False)]
+            elif r["skind"] in ("khash", "onehash"):
+                got = [pg.est_jaccard_minhash(a, b), pg.est_intersection_minhash(a, b, su, sv)]
+            else:
+                got = [pg.est_intersection_kmv(a, b, su, sv),
+                       pg.est_intersection_kmv(a, b, su, sv, clamp=False)]
+            assert [float(x) for x in got] == want, (key, u, v)
