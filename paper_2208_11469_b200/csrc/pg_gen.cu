@@ -190,6 +190,20 @@ __global__ void orient_flags_kernel(const int32_t* __restrict__ src, const int32
 
 using namespace pg;
 
+// counts[v] = sum of flags over row v, a warp per row (grid-stride)
+__global__ void row_flag_count_kernel(const int64_t* __restrict__ offsets, const int32_t* __restrict__ flags,
+                                      int64_t n, int64_t* __restrict__ counts) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n; v += warps) {
+    int64_t c = 0;
+    for (int64_t j = offsets[v] + lane; j < offsets[v + 1]; j += 32) c += flags[j];
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if (lane == 0) counts[v] = c;
+  }
+}
+
+
 extern "C" {
 
 int pg_rmat_pairs(uint64_t state_hi, uint64_t state_lo, uint64_t inc_hi, uint64_t inc_lo, int32_t scale,
@@ -315,15 +329,13 @@ int pg_degree_order(const int64_t* offsets, const int32_t* adj, int64_t n, int64
     return e == cudaSuccess ? PG_OK : fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
   }
   PG_REQUIRE(nnz == 0 || (adj && dir_adj), "null pointer");
-  size_t t_sort = 0, t_sel = 0, t_red = 0, t_scan = 0;
+  size_t t_sort = 0, t_sel = 0, t_scan = 0;
   cub::DeviceRadixSort::SortKeys(nullptr, t_sort, (const uint64_t*)nullptr, (uint64_t*)nullptr, n);
   cub::DeviceSelect::Flagged(nullptr, t_sel, (const int32_t*)nullptr, (const int32_t*)nullptr, (int32_t*)nullptr,
                              (int64_t*)nullptr, nnz);
-  cub::DeviceSegmentedReduce::Sum(nullptr, t_red, (const int32_t*)nullptr, (int64_t*)nullptr, n,
-                                  (const int64_t*)nullptr, (const int64_t*)nullptr);
   cub::DeviceScan::ExclusiveSum(nullptr, t_scan, (const int64_t*)nullptr, (int64_t*)nullptr, n + 1);
   size_t temp = t_sort;
-  for (size_t t : {t_sel, t_red, t_scan}) temp = t > temp ? t : temp;
+  for (size_t t : {t_sel, t_scan}) temp = t > temp ? t : temp;
   temp = al256(temp);
   // keys (2n u64) | src, flags (nnz i32 each) | counts (n+1 i64) | num | temp
   const size_t kb = al256(sizeof(uint64_t) * 2 * n), eb = al256(sizeof(int32_t) * (nnz > 0 ? nnz : 1)),
@@ -357,9 +369,11 @@ int pg_degree_order(const int64_t* offsets, const int32_t* adj, int64_t n, int64
       tb = temp;
       e = cub::DeviceSelect::Flagged(tmp, tb, adj, flags, dir_adj, d_num, nnz, s);
       if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "select: %s", cudaGetErrorString(e)); break; }
-      tb = temp;
-      e = cub::DeviceSegmentedReduce::Sum(tmp, tb, flags, counts, n, offsets, offsets + 1, s);
-      if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "segmented sum: %s", cudaGetErrorString(e)); break; }
+      // d+ per row: a warp per row (CUB's segmented reduce gives each
+      // segment one block, and R-MAT hub rows of 10^5 entries serialised
+      // it: 41 ms at s24)
+      row_flag_count_kernel<<<grid, 256, 0, s>>>(offsets, flags, n, counts);
+      if ((rc = check_launch("row_flag_count"))) break;
     } else {
       e = cudaMemsetAsync(counts, 0, sizeof(int64_t) * n, s);
       if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(e)); break; }
