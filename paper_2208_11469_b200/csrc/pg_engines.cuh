@@ -71,6 +71,13 @@ struct OpOr {
 #define PG_WIDE_SUB 8  // v rows in flight per sub-step of the padded wide engine
 #endif
 static __constant__ int kImadW[4] = {1, 2, 4, 8};
+static __constant__ int kImadHi = 65536;  // packs a second 16-bit count into a register on the FMA pipe
+#ifndef PG_WIDE_PACK
+#define PG_WIDE_PACK 1  // packed transpose-reduce in the 8-lane wide engine
+#endif
+#ifndef PG_WIDE_CLAMP1
+#define PG_WIDE_CLAMP1 1  // pad slots (v < 0) clamped once by the loading lane
+#endif
 __device__ __forceinline__ int imad(int a, int b, int c) { return a * b + c; }
 
 // Harley-Seal variants: the 8 words a lane holds per edge pass through four
@@ -155,6 +162,31 @@ __device__ __forceinline__ int group_transpose_reduce(int (&c)[G], int gl) {
     }
   }
   return c[0];
+}
+
+// The same for G = 8 with two 16-bit counts per register (p[i] = c[2i] |
+// c[2i+1] << 16; each count <= 2048): the w = 4 and w = 2 rounds move half the
+// registers (6 SEL + 3 SHFL instead of 12 + 6), the last round adds the
+// shuffled pair and picks the lane's half.  ALU-pipe diet for the 2048-bit
+// Bloom kernel.
+__device__ __forceinline__ int group_transpose_reduce_packed8(uint32_t (&p)[4], int gl) {
+  {
+    const bool upper = (gl & 4) != 0;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const uint32_t send = upper ? p[j] : p[j + 2];
+      const uint32_t keep = upper ? p[j + 2] : p[j];
+      p[j] = (uint32_t)imad((int)__shfl_xor_sync(0xffffffffu, send, 4), kImadW[0], (int)keep);
+    }
+  }
+  {
+    const bool upper = (gl & 2) != 0;
+    const uint32_t send = upper ? p[0] : p[1];
+    const uint32_t keep = upper ? p[1] : p[0];
+    p[0] = (uint32_t)imad((int)__shfl_xor_sync(0xffffffffu, send, 2), kImadW[0], (int)keep);
+  }
+  const uint32_t t = (uint32_t)imad((int)__shfl_xor_sync(0xffffffffu, p[0], 1), kImadW[0], (int)p[0]);
+  return (gl & 1) ? (int)(t >> 16) : (int)(t & 0xffffu);
 }
 
 // contiguous per-warp slice of [e_begin, e_end), rounded to 32 edges
@@ -323,6 +355,7 @@ static __constant__ uint32_t kRowBytesC[17] = {0, 32, 64, 96, 128, 160, 192, 224
                                                288, 320, 352, 384, 416, 448, 480, 512};
 __device__ __forceinline__ const unsigned char* row_addr(const unsigned char* base, uint32_t r, uint32_t bytes) {
   uint64_t out;
+
   asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(out) : "r"(r), "r"(bytes), "l"(base));
   return reinterpret_cast<const unsigned char*>(out);
 }
@@ -349,6 +382,7 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
   for (int i = 0; i < V; ++i)
 #pragma unroll
     for (int w = 0; w < 8; ++w) ur[i][w] = 0;
+  const uint32_t row_bytes_r = kRowBytesC[W8];
   // ranges: dynamic 512-slot chunks (kDyn: the launcher passes a counter),
   // else one static per-warp slice (the cached u row survives chunk ends)
   int64_t wb, we;
@@ -362,37 +396,54 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
     if (wb >= we) return;
   }
   first = false;
+  // 32-bit slot indices relative to the range start (wb is a multiple of G
+  // for the padded layouts), so the index arithmetic of the prefetch is one
+  // shift and two IMAD.WIDE instead of 64-bit divides and adds
+  const int32_t* __restrict__ usb = kLayout == 2 ? us + wb / G : us + wb;
+  const int32_t* __restrict__ vsb = vs + wb;
   int32_t ul = 0, vl = 0;
   if (wb + lane < we) {
-    ul = kLayout == 2 ? us[(wb + lane) / G] : us[wb + lane];
-    vl = vs[wb + lane];
+    ul = kLayout == 2 ? usb[(unsigned)lane / G] : usb[lane];
+    vl = vsb[lane];
   }
   // 32-bit remaining-slot count instead of 64-bit bound checks (registers)
   const int nslots = (int)(we - wb);
 #pragma unroll 1
   for (int r0 = 0; r0 < nslots; r0 += 32) {
-    const int64_t e = wb + r0 + lane;
+    const unsigned i = (unsigned)(r0 + lane);
+    const int64_t e = wb + i;
     const int rem = nslots - r0;
     const bool valid = lane < rem && vl >= 0;  // v < 0: padding slot
     int32_t un = 0, vn = 0;
     if (lane + 32 < rem) {
-      un = kLayout == 2 ? us[(e + 32) / G] : us[e + 32];
-      vn = vs[e + 32];
+      un = kLayout == 2 ? usb[(i + 32) / G] : usb[i + 32];
+      vn = vsb[i + 32];
     }
     // rows in flight per sub-step: all G (default), or kSub at a time so
     // fewer registers hold rows (more CTAs per SM)
     constexpr int kSub = (kPadded && PG_WIDE_SUB < G) ? PG_WIDE_SUB : G;
+    constexpr bool kPack = PG_WIDE_PACK && kPadded && G == 8 && V == 1 && kSub == G;
     int c[G];
+    uint32_t cp[4];
+#if PG_WIDE_CLAMP1
+    const int32_t vls = vl < 0 ? 0 : vl;
+#endif
 #pragma unroll
     for (int j0 = 0; j0 < G; j0 += kSub) {
     uint32_t vr[kSub][V][8];
 #pragma unroll
     for (int jj = 0; jj < kSub; ++jj) {
       const int j = j0 + jj;
+#if PG_WIDE_CLAMP1
+      // pad slots were clamped to row 0 by the loading lane (vls)
+      const uint32_t vrow = (uint32_t)__shfl_sync(0xffffffffu, vls, j, G);
+#else
       const int32_t vj = __shfl_sync(0xffffffffu, vl, j, G);
+      const uint32_t vrow = (uint32_t)(vj < 0 ? 0 : vj);
+#endif
       // lane base + row * bytes: one IMAD.WIDE.U32 (FMA pipe) per row
       // instead of multiply, OR and a 64-bit add on the ALU pipe
-      const unsigned char* rv = row_addr(rows_gl, (uint32_t)(vj < 0 ? 0 : vj), kRowBytesC[W8]);
+      const unsigned char* rv = row_addr(rows_gl, vrow, row_bytes_r);
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         if (kVCache) ldg256_keep(rv + i * G * 32, vr[jj][i]);
@@ -411,7 +462,7 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
     if (kPadded || __all_sync(0xffffffffu, uniform)) {
       if (u0 != ucur) {
         ucur = u0;
-        const unsigned char* ru = row_addr(rows_gl, (uint32_t)u0, kRowBytesC[W8]);
+        const unsigned char* ru = row_addr(rows_gl, (uint32_t)u0, row_bytes_r);
 #pragma unroll
         for (int i = 0; i < V; ++i) ldg256_keep(ru + i * G * 32, ur[i]);
       }
@@ -420,7 +471,13 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
         int acc = 0;
 #pragma unroll
         for (int i = 0; i < V; ++i) acc += Op::apply8(ur[i], vr[jj][i]);
-        c[j0 + jj] = acc;
+        if (kPack) {
+          // two 16-bit counts per register: the odd edge joins on the FMA pipe
+          if (jj & 1) cp[jj >> 1] = (uint32_t)imad(acc, kImadHi, (int)cp[jj >> 1]);
+          else cp[jj >> 1] = (uint32_t)acc;
+        } else {
+          c[j0 + jj] = acc;
+        }
       }
     } else if (!kPadded) {
 #pragma unroll
@@ -428,7 +485,7 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
         const int32_t uj = __shfl_sync(0xffffffffu, ul, j, G);
         if (uj != ucur) {
           ucur = uj;
-          const unsigned char* ru = row_addr(rows_gl, (uint32_t)uj, kRowBytesC[W8]);
+          const unsigned char* ru = row_addr(rows_gl, (uint32_t)uj, row_bytes_r);
 #pragma unroll
           for (int i = 0; i < V; ++i) ldg256_keep(ru + i * G * 32, ur[i]);
         }
@@ -439,7 +496,9 @@ __device__ __forceinline__ void wide_edge_loop(const unsigned char* __restrict__
       }
     }
     }  // sub-steps
-    const int cnt = group_transpose_reduce<G>(c, gl);
+    int cnt;
+    if constexpr (kPack) cnt = group_transpose_reduce_packed8(cp, gl);
+    else cnt = group_transpose_reduce<G>(c, gl);
     if (valid) epi.edge(e, ul, vl, cnt);
     ul = un;
     vl = vn;
