@@ -82,6 +82,11 @@ SIGNATURES = {
     "pg_onehash_block_pad": [c_i32, ctypes.POINTER(c_i32)],
     "pg_tc_kmv_ranked": [c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
                          c_i64, c_ptr, c_ptr],
+    "pg_kmv_merge_supported": [c_i32, ctypes.POINTER(c_i32)],
+    "pg_tc_kmv_merge": [c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
+                        c_i64, c_ptr, c_ptr],
+    "pg_kmv_merge_partition": [c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i32, c_ptr, c_ptr,
+                               ctypes.POINTER(c_i64), c_ptr],
     "pg_jaccard_count_khash": [c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
                                c_i64, c_i32, c_i32, c_dbl, c_ptr, c_ptr],
     "pg_4clique_bloom": [c_ptr, c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_i32,
@@ -201,6 +206,13 @@ def kmv_ranked_pad(k: int) -> int:
     pad = ctypes.c_int32()
     check(load_library().pg_kmv_ranked_pad(int(k), ctypes.byref(pad)), "pg_kmv_ranked_pad")
     return pad.value
+
+
+def kmv_merge_supported(k: int) -> bool:
+    """Whether the thread-per-edge KMV merge engine serves this k."""
+    ok = ctypes.c_int32()
+    check(load_library().pg_kmv_merge_supported(int(k), ctypes.byref(ok)), "pg_kmv_merge_supported")
+    return bool(ok.value)
 
 
 def onehash_block_pad(k: int) -> int:

@@ -529,6 +529,267 @@ static int launch_kmv_ranked(cudaStream_t s, const int32_t* ranks, const double*
   ps.finish(out_sum);
   return check_launch("tc_kmv_ranked");
 }
+
+// -------------------------------------- KMV thread-per-edge merge engine ----
+// One lane per edge slot over the rank rows (int32 ascending, INT32_MAX pad).
+// The reference's merged-row quantities (providers.py:266-301) need, for an
+// edge whose estimate is s_u + s_v - (k_eff - 1) / kth, only the T-th
+// (T = k_eff = min(lu, lv)) smallest distinct value of A | B: a sequential
+// two-pointer merge yields it after exactly T steps (each step consumes the
+// smaller head, or both heads when they are equal), never reading past index
+// T - 1 of either row.  Edges of the other two branches (both sizes <= K:
+// s_u + s_v - |A | B|; k_eff < 2: |A & B|) continue the same merge until one
+// row is exhausted; |A & B| = i + j - steps.  The per-lane work is ~9
+// instructions per step instead of K directory probes per edge.
+//
+// Shared memory: each lane's two row prefixes word-interleaved ([K][32] per
+// row side), so lane l only ever touches bank l: the data-dependent indices
+// of the 32 merges never conflict, and no warp synchronisation is needed
+// (a lane reads only what it wrote).  Each lane loads its own rows in 32-byte
+// sectors (lanes of a u run share the sectors of A).
+#ifndef PG_TMERGE_PREFETCH
+#define PG_TMERGE_PREFETCH 1
+#endif
+__device__ __forceinline__ int32_t lds_s32(uint32_t addr) {
+  int32_t x;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(x) : "r"(addr));
+  return x;
+}
+// one merge step: consume the smaller head (both when equal); a column's
+// elements are 128 bytes apart
+__device__ __forceinline__ void tm_step(uint32_t& pa, uint32_t& pb) {
+  const int32_t a = lds_s32(pa), b = lds_s32(pb);
+  if (a <= b) pa += 128;
+  if (b <= a) pb += 128;
+}
+template <int K>
+__global__ void __launch_bounds__(32) kmv_tmerge_kernel(const int32_t* __restrict__ R,
+                                                        const double* __restrict__ rank_values,
+                                                        const int32_t* __restrict__ lengths,
+                                                        const int32_t* __restrict__ sizes,
+                                                        const int32_t* __restrict__ us,
+                                                        const int32_t* __restrict__ vs, int64_t e_begin,
+                                                        int64_t e_end, double* out_sum,
+                                                        unsigned long long* ctr) {
+  constexpr int64_t kChunk = 512;
+  constexpr int S = K / 8;  // 32-byte sectors per row
+  extern __shared__ __align__(16) int32_t tm_smem[];
+  const int lane = threadIdx.x;
+  int32_t* sA = tm_smem + lane;
+  int32_t* sB = tm_smem + K * 32 + lane;
+  const uint32_t sa0 = (uint32_t)__cvta_generic_to_shared(sA), sb0 = (uint32_t)__cvta_generic_to_shared(sB);
+  int64_t wb, we;
+  while (next_chunk(ctr, e_begin, e_end, kChunk, wb, we)) {
+    double acc = 0.0;
+#pragma unroll 1
+    for (int64_t b0 = wb; b0 < we; b0 += 32) {
+      const int64_t e = b0 + lane;
+      int32_t u = 0, v = -1;
+      if (e < we) {
+        u = us[e];
+        v = vs[e];
+      }
+      const bool valid = v >= 0;
+      int lu = 0, lv = 0, su = 0, sv = 0;
+      if (valid) {
+        lu = lengths[u];
+        lv = lengths[v];
+        su = sizes[u];
+        sv = sizes[v];
+      }
+      const int T = min(lu, lv);
+      // both sizes <= K (union count) or k_eff < 2 (common count): full merge
+      const bool full = valid && ((su <= K && sv <= K) || T < 2);
+      const int na = full ? lu : T, nb = full ? lv : T;
+      const int32_t* ra = R + (int64_t)u * K;
+      const int32_t* rb = R + (int64_t)(valid ? v : 0) * K;
+#pragma unroll
+      for (int h = 0; h < S; h += 4) {
+        uint32_t xa[4][8], xb[4][8];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          if (h + s < S && (h + s) * 8 < na) ldg256_keep(ra + (h + s) * 8, xa[s]);
+          if (h + s < S && (h + s) * 8 < nb) ldg256_keep(rb + (h + s) * 8, xb[s]);
+        }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          if (h + s < S && (h + s) * 8 < na) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sA[((h + s) * 8 + q) * 32] = (int32_t)xa[s][q];
+          }
+          if (h + s < S && (h + s) * 8 < nb) {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sB[((h + s) * 8 + q) * 32] = (int32_t)xb[s][q];
+          }
+        }
+      }
+      // T steps: the T-th distinct value of A | B is the last one consumed
+      uint32_t pa = sa0, pb = sb0;  // shared-space byte addresses of the heads
+      int s = T;
+#pragma unroll 1
+      for (; s >= 2; s -= 2) {
+        tm_step(pa, pb);
+        tm_step(pa, pb);
+      }
+      if (s) tm_step(pa, pb);
+      int32_t kr = 0;
+      if (T >= 1) {
+        const int32_t la = pa > sa0 ? lds_s32(pa - 128) : -1, lb = pb > sb0 ? lds_s32(pb - 128) : -1;
+        kr = max(la, lb);
+      }
+      int steps = T;
+      if (full) {
+        const uint32_t ea = sa0 + lu * 128, eb = sb0 + lv * 128;
+#pragma unroll 1
+        while (pa < ea && pb < eb) {
+          tm_step(pa, pb);
+          ++steps;
+        }
+      }
+      const int ia = (int)(pa - sa0), jb = (int)(pb - sb0);  // element index * 128
+      if (valid) {
+        KmvEdge r;
+        r.common = ((ia + jb) >> 7) - steps;  // exact once a row is exhausted (used only when full)
+        r.uni = lu + lv - r.common;
+        r.k_eff = T;
+        r.kth = T >= 2 ? __ldg(rank_values + kr) : 0.0;
+        acc = __dadd_rn(acc, kmv_estimate(r, K, su, sv));
+      }
+    }
+    // one partial per dynamic chunk (fixed boundaries), whichever warp ran it
+    for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
+    if (lane == 0) out_sum[(wb - e_begin) / kChunk] = acc;
+  }
+}
+
+template <int K>
+static int launch_kmv_tmerge(cudaStream_t s, const int32_t* ranks, const double* rank_values,
+                             const int32_t* lengths, const int32_t* sizes, const int32_t* us, const int32_t* vs,
+                             int64_t b, int64_t e, double* out_sum) {
+  auto kern = kmv_tmerge_kernel<K>;
+  const size_t sm = (size_t)2 * K * 32 * sizeof(int32_t);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32, sm) != cudaSuccess || per_sm < 1) per_sm = 1;
+  static const int cap = [] {
+    const char* v = getenv("PG_TMERGE_WARPS");
+    return v ? atoi(v) : 0;
+  }();
+  if (cap > 0) per_sm = min(per_sm, cap);
+  const int grid = grid_cap(sm_count() * per_sm, e - b, 512);
+  ChunkCounter ctr;
+  PartialSums ps;  // one partial per 512-slot chunk, summed in chunk order
+  cudaError_t ce = ctr.init(s);
+  if (ce == cudaSuccess) ce = ps.init(s, (e - b + 511) / 512);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "scratch: %s", cudaGetErrorString(ce));
+  kern<<<grid, 32, sm, s>>>(ranks, rank_values, lengths, sizes, us, vs, b, e, ps.p, ctr.p);
+  ps.finish(out_sum);
+  return check_launch("tc_kmv_merge");
+}
+
+// Stable two-way partition of edge slots for the merge engine: slots whose
+// merge stops after k_eff steps first, the full-merge slots (both sizes <= k,
+// or k_eff < 2) and pads after them, so the long merges do not hold up the
+// warps of the short ones.
+constexpr int kPartTile = 2048;
+__device__ __forceinline__ bool tmerge_is_short(const int32_t* __restrict__ sizes,
+                                                const int32_t* __restrict__ lengths, int k, int32_t u,
+                                                int32_t v) {
+  if (v < 0) return false;
+  const int su = sizes[u], sv = sizes[v];
+  return !(su <= k && sv <= k) && min(lengths[u], lengths[v]) >= 2;
+}
+__global__ void __launch_bounds__(256) tmerge_count_kernel(const int32_t* __restrict__ us,
+                                                           const int32_t* __restrict__ vs, int64_t count,
+                                                           const int32_t* __restrict__ sizes,
+                                                           const int32_t* __restrict__ lengths, int k,
+                                                           int64_t* tile_short) {
+  __shared__ int red[8];
+  const int64_t base = (int64_t)blockIdx.x * kPartTile;
+  int c = 0;
+  for (int i = threadIdx.x; i < kPartTile; i += 256) {
+    const int64_t e = base + i;
+    if (e < count) c += tmerge_is_short(sizes, lengths, k, us[e], vs[e]);
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int i = 0; i < 8; ++i) t += red[i];
+    tile_short[blockIdx.x] = t;
+  }
+}
+// exclusive scan of the tile counts in place (one block); total -> tile_short[tiles]
+__global__ void __launch_bounds__(1024) tmerge_scan_kernel(int64_t* tile_short, int64_t tiles) {
+  __shared__ int64_t part[1024];
+  const int64_t per = (tiles + 1023) / 1024;
+  const int64_t lo = min((int64_t)threadIdx.x * per, tiles), hi = min(lo + per, tiles);
+  int64_t t = 0;
+  for (int64_t i = lo; i < hi; ++i) t += tile_short[i];
+  part[threadIdx.x] = t;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t run = 0;
+    for (int i = 0; i < 1024; ++i) {
+      const int64_t x = part[i];
+      part[i] = run;
+      run += x;
+    }
+    tile_short[tiles] = run;
+  }
+  __syncthreads();
+  int64_t run = part[threadIdx.x];
+  for (int64_t i = lo; i < hi; ++i) {
+    const int64_t x = tile_short[i];
+    tile_short[i] = run;
+    run += x;
+  }
+}
+__global__ void __launch_bounds__(256) tmerge_scatter_kernel(const int32_t* __restrict__ us,
+                                                             const int32_t* __restrict__ vs, int64_t count,
+                                                             const int32_t* __restrict__ sizes,
+                                                             const int32_t* __restrict__ lengths, int k,
+                                                             const int64_t* __restrict__ tile_short,
+                                                             int64_t tiles, int32_t* out_us, int32_t* out_vs) {
+  __shared__ int wsum[8];
+  __shared__ int tile_run;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t base = (int64_t)blockIdx.x * kPartTile;
+  const int64_t short_base = tile_short[blockIdx.x];
+  const int64_t long_base = tile_short[tiles] + (base - short_base);
+  if (threadIdx.x == 0) tile_run = 0;
+  __syncthreads();
+  for (int i0 = 0; i0 < kPartTile; i0 += 256) {
+    const int64_t e = base + i0 + threadIdx.x;
+    int32_t u = 0, v = -1;
+    bool in = e < count, sh = false;
+    if (in) {
+      u = us[e];
+      v = vs[e];
+      sh = tmerge_is_short(sizes, lengths, k, u, v);
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, sh);
+    if (lane == 0) wsum[w] = __popc(bal);
+    __syncthreads();
+    int before = tile_run;
+    for (int i = 0; i < w; ++i) before += wsum[i];
+    const int rank_short = before + __popc(bal & lanemask_lt());
+    if (in) {
+      const int64_t pos = sh ? short_base + rank_short : long_base + (i0 + threadIdx.x - rank_short);
+      out_us[pos] = u;
+      out_vs[pos] = v;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int t = 0;
+      for (int i = 0; i < 8; ++i) t += wsum[i];
+      tile_run += t;
+    }
+    __syncthreads();
+  }
+}
 }  // namespace pg
 
 using namespace pg;
@@ -616,6 +877,56 @@ int pg_tc_kmv_ranked(const int32_t* ranks, const double* rank_values, const int3
   if (k == 32) return launch_kmv_ranked<32>(s, ranks, rank_values, lengths, sizes, us, vs, e_begin, e_end, out_sum);
   if (k == 64) return launch_kmv_ranked<64>(s, ranks, rank_values, lengths, sizes, us, vs, e_begin, e_end, out_sum);
   return launch_kmv_ranked<128>(s, ranks, rank_values, lengths, sizes, us, vs, e_begin, e_end, out_sum);
+}
+
+int pg_kmv_merge_supported(int32_t k, int32_t* ok_host) {
+  PG_REQUIRE(ok_host, "null output");
+  *ok_host = (k == 32 || k == 64 || k == 128) ? 1 : 0;
+  return PG_OK;
+}
+
+int pg_tc_kmv_merge(const int32_t* ranks, const double* rank_values, const int32_t* lengths, int32_t k,
+                    const int32_t* sizes, const int32_t* us, const int32_t* vs, int64_t e_begin, int64_t e_end,
+                    double* out_sum, void* stream) {
+  if (k != 32 && k != 64 && k != 128)
+    return fail(PG_ERR_UNSUPPORTED, "the KMV merge engine supports k = 32, 64, 128 (got %d)", k);
+  PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
+  PG_REQUIRE(out_sum, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  cudaError_t ce = cudaMemsetAsync(out_sum, 0, sizeof(double), s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  if (e_end == e_begin) return PG_OK;  // an empty range needs no inputs
+  PG_REQUIRE(ranks && rank_values && lengths && sizes && us && vs, "null pointer");
+  if (k == 32) return launch_kmv_tmerge<32>(s, ranks, rank_values, lengths, sizes, us, vs, e_begin, e_end, out_sum);
+  if (k == 64) return launch_kmv_tmerge<64>(s, ranks, rank_values, lengths, sizes, us, vs, e_begin, e_end, out_sum);
+  return launch_kmv_tmerge<128>(s, ranks, rank_values, lengths, sizes, us, vs, e_begin, e_end, out_sum);
+}
+
+int pg_kmv_merge_partition(const int32_t* us, const int32_t* vs, int64_t count, const int32_t* sizes,
+                           const int32_t* lengths, int32_t k, int32_t* out_us, int32_t* out_vs,
+                           int64_t* split_host, void* stream) {
+  PG_REQUIRE(k >= 1, "k must be >= 1");
+  PG_REQUIRE(count >= 0, "count must be >= 0");
+  PG_REQUIRE(split_host, "null output");
+  *split_host = 0;
+  if (count == 0) return PG_OK;
+  PG_REQUIRE(us && vs && sizes && lengths && out_us && out_vs, "null pointer");
+  PG_REQUIRE(us != out_us && vs != out_vs, "the partition is not in place");
+  cudaStream_t s = as_stream(stream);
+  const int64_t tiles = (count + kPartTile - 1) / kPartTile;
+  int64_t* tile_short = nullptr;
+  retain_default_pool();
+  cudaError_t ce = cudaMallocAsync(reinterpret_cast<void**>(&tile_short), sizeof(int64_t) * (tiles + 1), s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "scratch: %s", cudaGetErrorString(ce));
+  tmerge_count_kernel<<<(unsigned)tiles, 256, 0, s>>>(us, vs, count, sizes, lengths, k, tile_short);
+  tmerge_scan_kernel<<<1, 1024, 0, s>>>(tile_short, tiles);
+  tmerge_scatter_kernel<<<(unsigned)tiles, 256, 0, s>>>(us, vs, count, sizes, lengths, k, tile_short, tiles,
+                                                         out_us, out_vs);
+  ce = cudaMemcpyAsync(split_host, tile_short + tiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+  cudaFreeAsync(tile_short, s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "partition: %s", cudaGetErrorString(ce));
+  return check_launch("kmv_merge_partition");
 }
 
 }  // extern "C"

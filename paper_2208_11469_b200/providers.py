@@ -286,6 +286,9 @@ class _SketchProvider(IntersectionProvider):
         if lay.kind == "degree":
             return ("degree-oriented row-padded slots (u = lower (degree, ID) rank, N+ lists "
                     "of degree_order), one u per slot group")
+        if lay.kind.endswith("+kmv-merge"):
+            return ("every edge once, " + ("lower -> higher (degree, ID) rank" if lay.kind.startswith("degree")
+                                          else "u < v") + ", partitioned [k_eff-step merges | full merges]")
         return {0: "upper edges u < v (CSR order)", 1: "row-padded upper edges",
                 2: "row-padded upper edges, one u per slot group"}[int(lay.padded)]
 
@@ -615,13 +618,60 @@ class KmvProvider(_SketchProvider):
         rank-directory engine for this k."""
         return "ranks" in self._dev() and N.kmv_ranked_pad(self.sketched.capacity) > 0
 
+    def _merge_engine(self) -> bool:
+        """The thread-per-edge merge engine (pg_tc_kmv_merge) over rank rows;
+        PG_KMV_ENGINE=ranked restores the rank-directory engine."""
+        import os
+        return ("ranks" in self._dev() and N.kmv_merge_supported(self.sketched.capacity)
+                and os.environ.get("PG_KMV_ENGINE", "merge") == "merge")
+
     def tc_pad(self) -> int:
+        if self._merge_engine():
+            return 1
         return N.kmv_ranked_pad(self.sketched.capacity) if self._ranked() else 1
+
+    def _tc_layout(self, dev):
+        """Merge engine: every edge once from its lower- to its higher-(degree,
+        ID)-rank endpoint (so k_eff, the merge length, is the low-degree
+        side's and the streamed v rows are the hub side), stably partitioned
+        into [merges that stop after k_eff steps | full merges]
+        (pg_kmv_merge_partition).  The estimate is symmetric in (u, v)."""
+        import ctypes
+        import os
+        import torch
+        if not self._merge_engine() or dev.n == 0:
+            return super()._tc_layout(dev)
+        sg = self.sketched
+        cached = getattr(sg, "_kmv_merge_layout", None)
+        if cached is not None and cached[0] is dev:
+            return cached[1]
+        d = self._dev()
+        if os.environ.get("PG_TC_ORIENT", "degree") == "degree":
+            us, vs, slots, _ = dev.hub_slots(1, 0)
+            kind = "degree"
+        else:
+            us, vs = dev.upper_edges()
+            slots, kind = us.numel(), "id"
+        if os.environ.get("PG_KMV_PARTITION", "1") == "1" and slots > 0:
+            pu, pv = torch.empty_like(us), torch.empty_like(vs)
+            split = ctypes.c_int64()
+            N.call("pg_kmv_merge_partition", N.ptr(us), N.ptr(vs), slots, N.ptr(d["sizes"]),
+                   N.ptr(d["lengths"]), sg.capacity, N.ptr(pu), N.ptr(pv), ctypes.byref(split),
+                   N.stream_handle())
+            us, vs = pu, pv
+        lay = TcLayout(us, vs, slots, False, kind + "+kmv-merge")
+        sg._kmv_merge_layout = (dev, lay)
+        return lay
 
     def _tc_counts(self, us, vs, e_begin: int, e_end: int, padded: bool = False):
         import torch
         d, sg = self._dev(), self.sketched
         out = torch.empty(1, dtype=torch.float64, device="cuda")
+        if self._merge_engine():
+            N.call("pg_tc_kmv_merge", N.ptr(d["ranks"]), N.ptr(d["rank_values"]),
+                   N.ptr(d["lengths"]), sg.capacity, N.ptr(d["sizes"]), N.ptr(us),
+                   N.ptr(vs), e_begin, e_end, N.ptr(out), N.stream_handle())
+            return out
         if padded and self._ranked():
             N.call("pg_tc_kmv_ranked", N.ptr(d["ranks"]), N.ptr(d["rank_values"]),
                    N.ptr(d["lengths"]), sg.capacity, N.ptr(d["sizes"]), N.ptr(us),
