@@ -547,23 +547,81 @@ static int launch_kmv_ranked(cudaStream_t s, const int32_t* ranks, const double*
 // of the 32 merges never conflict, and no warp synchronisation is needed
 // (a lane reads only what it wrote).  Each lane loads its own rows in 32-byte
 // sectors (lanes of a u run share the sectors of A).
-#ifndef PG_TMERGE_PREFETCH
-#define PG_TMERGE_PREFETCH 1
+#ifndef PG_TMERGE_NU
+#define PG_TMERGE_NU 8
 #endif
 __device__ __forceinline__ int32_t lds_s32(uint32_t addr) {
   int32_t x;
   asm volatile("ld.shared.s32 %0, [%1];" : "=r"(x) : "r"(addr));
   return x;
 }
-// one merge step: consume the smaller head (both when equal); a column's
-// elements are 128 bytes apart
+// v rows in shared memory: element j of lane r's row at byte X = base + j*128
+// + r*4 (base 128-aligned), stored at swz(X) = X ^ (sector index of j moved
+// onto the top bits of the lane field).  A warp-wide load instruction then
+// covers 256/K whole rows (coalesced) and its transposing stores still hit 32
+// distinct banks; lanes reading the same sector index never conflict.
+template <int K>
+__device__ __forceinline__ uint32_t tm_swz(uint32_t x) {
+  constexpr int LP = K == 32 ? 2 : K == 64 ? 3 : 4;  // log2(sectors per row)
+  return x ^ ((x >> (3 + LP)) & (((1u << LP) - 1u) << (7 - LP)));
+}
+// one merge step: consume the smaller head (both when equal); A rows are
+// contiguous, a B column's elements are 128 bytes apart before the swizzle
+template <int K>
 __device__ __forceinline__ void tm_step(uint32_t& pa, uint32_t& pb) {
-  const int32_t a = lds_s32(pa), b = lds_s32(pb);
-  if (a <= b) pa += 128;
+  const int32_t a = lds_s32(pa), b = lds_s32(tm_swz<K>(pb));
+  if (a <= b) pa += 4;
   if (b <= a) pb += 128;
 }
-template <int K>
-__global__ void __launch_bounds__(32) kmv_tmerge_kernel(const int32_t* __restrict__ R,
+__device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t x) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(x) : "memory");
+}
+__device__ __forceinline__ unsigned lanemask_le() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_le;" : "=r"(m));
+  return m;
+}
+
+// Shared memory per warp (one warp per CTA): the v rows word-interleaved
+// ([K][32]: lane l only touches bank l, so the data-dependent indices of the
+// 32 merges never conflict), the u rows of the block once per distinct u
+// (edge slots are in u runs; a block takes the slots of at most NU runs,
+// rows skewed by 32/NU banks), 10 KB at K = 64: ~22 resident warps per SM.
+// Pipeline per warp: the slots of the next two blocks and the lengths/sizes
+// of the next block are loaded while the current block merges, and a block's
+// rank -> value gather is consumed one block later.
+template <int K, int NU>
+struct TmergeSmem {
+  static constexpr int SK = 32 / NU, AS = K + SK;
+  int32_t b[K * 32];
+  int32_t a[NU * AS];
+  int32_t uq[NU];
+};
+
+struct TmSlots {  // a block's slots, one per lane
+  int32_t u, v;
+  int q;       // index of the lane's u run within the block
+  bool valid;  // a real edge of one of the first NU runs
+  int cons;    // slots the block consumes (a prefix of the 32)
+  unsigned heads;
+};
+template <int NU>
+__device__ __forceinline__ void tm_form(TmSlots& b, int64_t start, int64_t we) {
+  const int lane = threadIdx.x;
+  const bool in = start + lane < we;
+  const int32_t uu = in ? b.u : -1;
+  const int32_t up = __shfl_up_sync(0xffffffffu, uu, 1);
+  const bool head = lane == 0 || uu != up;
+  b.heads = __ballot_sync(0xffffffffu, head);
+  b.q = __popc(b.heads & lanemask_le()) - 1;
+  const bool act = b.q < NU;
+  b.cons = __popc(__ballot_sync(0xffffffffu, act));
+  b.valid = act && in && b.v >= 0;
+  b.u = uu;
+}
+
+template <int K, int NU, int MINB>
+__global__ void __launch_bounds__(32, MINB) kmv_tmerge_kernel(const int32_t* __restrict__ R,
                                                         const double* __restrict__ rank_values,
                                                         const int32_t* __restrict__ lengths,
                                                         const int32_t* __restrict__ sizes,
@@ -571,103 +629,186 @@ __global__ void __launch_bounds__(32) kmv_tmerge_kernel(const int32_t* __restric
                                                         const int32_t* __restrict__ vs, int64_t e_begin,
                                                         int64_t e_end, double* out_sum,
                                                         unsigned long long* ctr) {
-  constexpr int64_t kChunk = 512;
-  constexpr int S = K / 8;  // 32-byte sectors per row
-  extern __shared__ __align__(16) int32_t tm_smem[];
+  using SM = TmergeSmem<K, NU>;
+  constexpr int64_t kChunk = 2048;
+  constexpr int S = K / 8;   // 32-byte sectors per row
+  constexpr int W = K / 32;  // words of a u row per lane
+  constexpr int AS = SM::AS;
+  extern __shared__ __align__(1024) unsigned char tm_raw[];
+  SM& sm = *reinterpret_cast<SM*>(tm_raw);
   const int lane = threadIdx.x;
-  int32_t* sA = tm_smem + lane;
-  int32_t* sB = tm_smem + K * 32 + lane;
-  const uint32_t sa0 = (uint32_t)__cvta_generic_to_shared(sA), sb0 = (uint32_t)__cvta_generic_to_shared(sB);
+  constexpr int RP = 32 / S;  // v rows per load instruction
+  const int lp = lane % S, la = lane / S;  // the lane's sector and row within a load instruction
+  const uint32_t sbb = (uint32_t)__cvta_generic_to_shared(sm.b);
+  const uint32_t sb0 = sbb + 4u * lane;
+  const uint32_t sa00 = (uint32_t)__cvta_generic_to_shared(sm.a);
   int64_t wb, we;
   while (next_chunk(ctr, e_begin, e_end, kChunk, wb, we)) {
     double acc = 0.0;
+    // pending estimate of the previous block (its kth gather is in flight)
+    bool p_valid = false;
+    int p_su = 0, p_sv = 0;
+    KmvEdge p_r{0, 0, 0, 0.0};
+    // prime: the first block's slots and metadata, the second block's slots
+    int64_t start = wb;
+    TmSlots cur{0, -1, 0, false, 0, 0u};
+    if (start + lane < we) {
+      cur.u = us[start + lane];
+      cur.v = vs[start + lane];
+    }
+    tm_form<NU>(cur, start, we);
+    int lu = 0, lv = 0, su = 0, sv = 0;
+    if (cur.valid) {
+      lu = lengths[cur.u];
+      lv = lengths[cur.v];
+      su = sizes[cur.u];
+      sv = sizes[cur.v];
+    }
+    int64_t start_n = start + cur.cons;
+    TmSlots nxt{0, -1, 0, false, 0, 0u};
+    if (start_n + lane < we) {
+      nxt.u = us[start_n + lane];
+      nxt.v = vs[start_n + lane];
+    }
 #pragma unroll 1
-    for (int64_t b0 = wb; b0 < we; b0 += 32) {
-      const int64_t e = b0 + lane;
-      int32_t u = 0, v = -1;
-      if (e < we) {
-        u = us[e];
-        v = vs[e];
+    while (start < we) {
+      // ---- next block: form it, fetch its metadata and the block after it
+      tm_form<NU>(nxt, start_n, we);
+      int lun = 0, lvn = 0, sun = 0, svn = 0;
+      if (nxt.valid) {
+        lun = lengths[nxt.u];
+        lvn = lengths[nxt.v];
+        sun = sizes[nxt.u];
+        svn = sizes[nxt.v];
       }
-      const bool valid = v >= 0;
-      int lu = 0, lv = 0, su = 0, sv = 0;
-      if (valid) {
-        lu = lengths[u];
-        lv = lengths[v];
-        su = sizes[u];
-        sv = sizes[v];
+      const int64_t start_nn = start_n + nxt.cons;
+      int32_t u2 = 0, v2 = -1;
+      if (start_nn + lane < we) {
+        u2 = us[start_nn + lane];
+        v2 = vs[start_nn + lane];
       }
+      // ---- current block: rows into shared memory
+      const bool valid = cur.valid;
       const int T = min(lu, lv);
       // both sizes <= K (union count) or k_eff < 2 (common count): full merge
       const bool full = valid && ((su <= K && sv <= K) || T < 2);
-      const int na = full ? lu : T, nb = full ? lv : T;
-      const int32_t* ra = R + (int64_t)u * K;
-      const int32_t* rb = R + (int64_t)(valid ? v : 0) * K;
+      const int nb = valid ? (full ? lv : T) : 0;
+      const int nq = min(__popc(cur.heads), NU);
+      __syncwarp();  // every lane is done with the previous block's u rows
+      if (cur.q < NU && ((cur.heads >> lane) & 1u)) sm.uq[cur.q] = cur.u;
+      __syncwarp();
+      uint32_t xa[NU][W];
 #pragma unroll
-      for (int h = 0; h < S; h += 4) {
-        uint32_t xa[4][8], xb[4][8];
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          if (h + s < S && (h + s) * 8 < na) ldg256_keep(ra + (h + s) * 8, xa[s]);
-          if (h + s < S && (h + s) * 8 < nb) ldg256_keep(rb + (h + s) * 8, xb[s]);
-        }
-#pragma unroll
-        for (int s = 0; s < 4; ++s) {
-          if (h + s < S && (h + s) * 8 < na) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) sA[((h + s) * 8 + q) * 32] = (int32_t)xa[s][q];
-          }
-          if (h + s < S && (h + s) * 8 < nb) {
-#pragma unroll
-            for (int q = 0; q < 8; ++q) sB[((h + s) * 8 + q) * 32] = (int32_t)xb[s][q];
+      for (int r = 0; r < NU; ++r) {
+        if (r < nq) {
+          const int32_t ur = sm.uq[r];
+          const int32_t* ra = R + (int64_t)(ur < 0 ? 0 : ur) * K + W * lane;
+          if (W == 1) xa[r][0] = __ldg(reinterpret_cast<const uint32_t*>(ra));
+          else if (W == 2) {
+            const uint2 t = __ldg(reinterpret_cast<const uint2*>(ra));
+            xa[r][0] = t.x;
+            xa[r][1] = t.y;
+          } else {
+            const uint4 t = __ldg(reinterpret_cast<const uint4*>(ra));
+            xa[r][0] = t.x;
+            xa[r][1] = t.y;
+            xa[r][2 % W] = t.z;
+            xa[r][3 % W] = t.w;
           }
         }
       }
-      // T steps: the T-th distinct value of A | B is the last one consumed
+#pragma unroll
+      for (int h = 0; h < S; h += 4) {
+        // instruction i covers rows RP*i .. RP*i + RP - 1, S lanes (sectors) each
+        uint32_t xb[4][8];
+        bool ok[4];
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          const int r = RP * (h + s) + la;
+          const int32_t vr = __shfl_sync(0xffffffffu, valid ? cur.v : 0, r);
+          const int nbr = __shfl_sync(0xffffffffu, nb, r);
+          ok[s] = h + s < S && lp * 8 < nbr;
+          if (ok[s]) ldg256_keep(R + (int64_t)vr * K + lp * 8, xb[s]);
+        }
+        if (h == 0) {
+#pragma unroll
+          for (int r = 0; r < NU; ++r) {
+            if (r < nq) {
+              int32_t* dst = sm.a + r * AS + W * lane;
+              if (W == 1) dst[0] = (int32_t)xa[r][0];
+              else if (W == 2) *reinterpret_cast<uint2*>(dst) = make_uint2(xa[r][0], xa[r][1]);
+              else *reinterpret_cast<uint4*>(dst) = make_uint4(xa[r][0], xa[r][1], xa[r][2 % W], xa[r][3 % W]);
+            }
+          }
+        }
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+          if (ok[s]) {
+            const uint32_t x0 = sbb + (uint32_t)(lp * 8) * 128u + (uint32_t)(RP * (h + s) + la) * 4u;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sts_u32(tm_swz<K>(x0 + q * 128u), xb[s][q]);
+          }
+        }
+      }
+      // the previous block's estimates (their kth gathers have landed)
+      if (p_valid) acc = __dadd_rn(acc, kmv_estimate(p_r, K, p_su, p_sv));
+      __syncwarp();  // the u rows are visible to every lane
+      // ---- T steps: the T-th distinct value of A | B is the last one consumed
+      const uint32_t sa0 = sa00 + (uint32_t)(min(cur.q, NU - 1) * AS) * 4u;
       uint32_t pa = sa0, pb = sb0;  // shared-space byte addresses of the heads
       int s = T;
 #pragma unroll 1
       for (; s >= 2; s -= 2) {
-        tm_step(pa, pb);
-        tm_step(pa, pb);
+        tm_step<K>(pa, pb);
+        tm_step<K>(pa, pb);
       }
-      if (s) tm_step(pa, pb);
+      if (s) tm_step<K>(pa, pb);
       int32_t kr = 0;
       if (T >= 1) {
-        const int32_t la = pa > sa0 ? lds_s32(pa - 128) : -1, lb = pb > sb0 ? lds_s32(pb - 128) : -1;
+        const int32_t la = pa > sa0 ? lds_s32(pa - 4) : -1, lb = pb > sb0 ? lds_s32(tm_swz<K>(pb - 128)) : -1;
         kr = max(la, lb);
       }
       int steps = T;
       if (full) {
-        const uint32_t ea = sa0 + lu * 128, eb = sb0 + lv * 128;
+        const uint32_t ea = sa0 + lu * 4, eb = sb0 + lv * 128;
 #pragma unroll 1
         while (pa < ea && pb < eb) {
-          tm_step(pa, pb);
+          tm_step<K>(pa, pb);
           ++steps;
         }
       }
-      const int ia = (int)(pa - sa0), jb = (int)(pb - sb0);  // element index * 128
-      if (valid) {
-        KmvEdge r;
-        r.common = ((ia + jb) >> 7) - steps;  // exact once a row is exhausted (used only when full)
-        r.uni = lu + lv - r.common;
-        r.k_eff = T;
-        r.kth = T >= 2 ? __ldg(rank_values + kr) : 0.0;
-        acc = __dadd_rn(acc, kmv_estimate(r, K, su, sv));
-      }
+      p_valid = valid;
+      p_su = su;
+      p_sv = sv;
+      // |A & B| is exact once a row is exhausted (used only by full merges)
+      p_r.common = (int)((pa - sa0) >> 2) + (int)((pb - sb0) >> 7) - steps;
+      p_r.uni = lu + lv - p_r.common;
+      p_r.k_eff = T;
+      p_r.kth = (valid && T >= 2) ? __ldg(rank_values + kr) : 0.0;
+      // ---- rotate
+      start = start_n;
+      start_n = start_nn;
+      cur = nxt;
+      lu = lun;
+      lv = lvn;
+      su = sun;
+      sv = svn;
+      nxt.u = u2;
+      nxt.v = v2;
     }
+    if (p_valid) acc = __dadd_rn(acc, kmv_estimate(p_r, K, p_su, p_sv));
     // one partial per dynamic chunk (fixed boundaries), whichever warp ran it
     for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
     if (lane == 0) out_sum[(wb - e_begin) / kChunk] = acc;
   }
 }
 
-template <int K>
-static int launch_kmv_tmerge(cudaStream_t s, const int32_t* ranks, const double* rank_values,
-                             const int32_t* lengths, const int32_t* sizes, const int32_t* us, const int32_t* vs,
-                             int64_t b, int64_t e, double* out_sum) {
-  auto kern = kmv_tmerge_kernel<K>;
-  const size_t sm = (size_t)2 * K * 32 * sizeof(int32_t);
+template <int K, int NU, int MINB>
+static int launch_kmv_tmerge_v(cudaStream_t s, const int32_t* ranks, const double* rank_values,
+                               const int32_t* lengths, const int32_t* sizes, const int32_t* us,
+                               const int32_t* vs, int64_t b, int64_t e, double* out_sum) {
+  auto kern = kmv_tmerge_kernel<K, NU, MINB>;
+  const size_t sm = sizeof(TmergeSmem<K, NU>);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   int per_sm = 0;
@@ -677,15 +818,33 @@ static int launch_kmv_tmerge(cudaStream_t s, const int32_t* ranks, const double*
     return v ? atoi(v) : 0;
   }();
   if (cap > 0) per_sm = min(per_sm, cap);
-  const int grid = grid_cap(sm_count() * per_sm, e - b, 512);
+  const int grid = grid_cap(sm_count() * per_sm, e - b, 2048);
   ChunkCounter ctr;
-  PartialSums ps;  // one partial per 512-slot chunk, summed in chunk order
+  PartialSums ps;  // one partial per 2048-slot chunk, summed in chunk order
   cudaError_t ce = ctr.init(s);
-  if (ce == cudaSuccess) ce = ps.init(s, (e - b + 511) / 512);
+  if (ce == cudaSuccess) ce = ps.init(s, (e - b + 2047) / 2048);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "scratch: %s", cudaGetErrorString(ce));
   kern<<<grid, 32, sm, s>>>(ranks, rank_values, lengths, sizes, us, vs, b, e, ps.p, ctr.p);
   ps.finish(out_sum);
   return check_launch("tc_kmv_merge");
+}
+
+template <int K>
+static int launch_kmv_tmerge(cudaStream_t s, const int32_t* ranks, const double* rank_values,
+                             const int32_t* lengths, const int32_t* sizes, const int32_t* us, const int32_t* vs,
+                             int64_t b, int64_t e, double* out_sum) {
+  // resident warps per SM at K = 64: shared memory allows 20 (NU = 8) / 22 (NU = 4)
+  constexpr int M1 = K == 32 ? 32 : K == 64 ? 20 : 11, M0 = K == 32 ? 24 : K == 64 ? 16 : 8;
+  static const int var = [] {
+    const char* v = getenv("PG_TMERGE_VARIANT");
+    return v ? atoi(v) : 0;
+  }();
+#define PG_TM(NU, MB) return launch_kmv_tmerge_v<K, NU, MB>(s, ranks, rank_values, lengths, sizes, us, vs, b, e, out_sum)
+  if (var == 1) PG_TM(8, M0);
+  if (var == 2) PG_TM(4, M1);
+  if (var == 3) PG_TM(4, M0);
+  PG_TM(8, M1);
+#undef PG_TM
 }
 
 // Stable two-way partition of edge slots for the merge engine: slots whose
