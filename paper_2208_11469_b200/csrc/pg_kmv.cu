@@ -573,6 +573,47 @@ __device__ __forceinline__ void tm_step(uint32_t& pa, uint32_t& pb) {
   if (a <= b) pa += 4;
   if (b <= a) pb += 128;
 }
+#ifndef PG_TM_UNCOND
+#define PG_TM_UNCOND 1
+#endif
+#ifndef PG_TM_STEP2
+#define PG_TM_STEP2 1
+#endif
+#ifndef PG_TM_STFAST
+#define PG_TM_STFAST 0
+#endif
+#ifndef PG_TM_DEFER
+#define PG_TM_DEFER 1
+#endif
+#ifndef PG_TM_CHUNK
+#define PG_TM_CHUNK 1024
+#endif
+#ifndef PG_TM_REVERSE
+#define PG_TM_REVERSE 1
+#endif
+__device__ __forceinline__ int32_t lds_s32_always(uint32_t addr) {
+  int32_t x;
+  asm volatile("ld.volatile.shared.s32 %0, [%1];" : "=r"(x) : "r"(addr));
+  return x;
+}
+// two merge steps from one round of loads (both heads and their successors):
+// the loop-carried chain is load -> compare -> select -> compare instead of
+// two load -> compare rounds.  A successor that is out of the row is read
+// but never selected: step s only ever looks at indices <= s < k_eff.
+template <int K>
+__device__ __forceinline__ void tm_step2(uint32_t& pa, uint32_t& pb) {
+  const int32_t a0 = lds_s32(pa), b0 = lds_s32(tm_swz<K>(pb));
+#if PG_TM_STEP2 == 2
+  const int32_t a1 = lds_s32_always(pa + 4), b1 = lds_s32_always(tm_swz<K>(pb + 128));
+#else
+  const int32_t a1 = lds_s32(pa + 4), b1 = lds_s32(tm_swz<K>(pb + 128));
+#endif
+  const bool ta = a0 <= b0, tb = b0 <= a0;
+  const int32_t a = ta ? a1 : a0, b = tb ? b1 : b0;
+  const bool ta2 = a <= b, tb2 = b <= a;
+  pa += (ta ? 4u : 0u) + (ta2 ? 4u : 0u);
+  pb += (tb ? 128u : 0u) + (tb2 ? 128u : 0u);
+}
 __device__ __forceinline__ void sts_u32(uint32_t addr, uint32_t x) {
   asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(x) : "memory");
 }
@@ -630,7 +671,7 @@ __global__ void __launch_bounds__(32, MINB) kmv_tmerge_kernel(const int32_t* __r
                                                         int64_t e_end, double* out_sum,
                                                         unsigned long long* ctr) {
   using SM = TmergeSmem<K, NU>;
-  constexpr int64_t kChunk = 2048;
+  constexpr int64_t kChunk = PG_TM_CHUNK;
   constexpr int S = K / 8;   // 32-byte sectors per row
   constexpr int W = K / 32;  // words of a u row per lane
   constexpr int AS = SM::AS;
@@ -643,7 +684,20 @@ __global__ void __launch_bounds__(32, MINB) kmv_tmerge_kernel(const int32_t* __r
   const uint32_t sb0 = sbb + 4u * lane;
   const uint32_t sa00 = (uint32_t)__cvta_generic_to_shared(sm.a);
   int64_t wb, we;
+#if PG_TM_REVERSE
+  // chunks are handed out last to first: the full merges, which the partition
+  // puts at the end of the slot list, are the long jobs and start first
+  const int64_t n_chunks = (e_end - e_begin + kChunk - 1) / kChunk;
+  for (;;) {
+    unsigned long long c = 0;
+    if (lane == 0) c = atomicAdd(ctr, 1ull);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if ((int64_t)c >= n_chunks) break;
+    wb = e_begin + (n_chunks - 1 - (int64_t)c) * kChunk;
+    we = min(wb + kChunk, e_end);
+#else
   while (next_chunk(ctr, e_begin, e_end, kChunk, wb, we)) {
+#endif
     double acc = 0.0;
     // pending estimate of the previous block (its kth gather is in flight)
     bool p_valid = false;
@@ -674,6 +728,17 @@ __global__ void __launch_bounds__(32, MINB) kmv_tmerge_kernel(const int32_t* __r
     while (start < we) {
       // ---- next block: form it, fetch its metadata and the block after it
       tm_form<NU>(nxt, start_n, we);
+      const int64_t start_nn = start_n + nxt.cons;
+#if PG_TM_DEFER
+      // unconditional loads (clamped indices), masked where they are used one
+      // iteration later: a guarded load compiles to load + predicated move,
+      // i.e. a wait for the load right where it is issued
+      const int32_t mu = nxt.valid ? nxt.u : 0, mv = nxt.valid ? nxt.v : 0;
+      int lun = lengths[mu], lvn = lengths[mv], sun = sizes[mu], svn = sizes[mv];
+      const bool validn = nxt.valid;
+      const int64_t e2 = min(start_nn + lane, e_end - 1);
+      int32_t u2 = us[e2], v2 = vs[e2];
+#else
       int lun = 0, lvn = 0, sun = 0, svn = 0;
       if (nxt.valid) {
         lun = lengths[nxt.u];
@@ -681,12 +746,12 @@ __global__ void __launch_bounds__(32, MINB) kmv_tmerge_kernel(const int32_t* __r
         sun = sizes[nxt.u];
         svn = sizes[nxt.v];
       }
-      const int64_t start_nn = start_n + nxt.cons;
       int32_t u2 = 0, v2 = -1;
       if (start_nn + lane < we) {
         u2 = us[start_nn + lane];
         v2 = vs[start_nn + lane];
       }
+#endif
       // ---- current block: rows into shared memory
       const bool valid = cur.valid;
       const int T = min(lu, lv);
@@ -728,7 +793,14 @@ __global__ void __launch_bounds__(32, MINB) kmv_tmerge_kernel(const int32_t* __r
           const int32_t vr = __shfl_sync(0xffffffffu, valid ? cur.v : 0, r);
           const int nbr = __shfl_sync(0xffffffffu, nb, r);
           ok[s] = h + s < S && lp * 8 < nbr;
+#if PG_TM_UNCOND
+          // unconditional (a lane with nothing to fetch re-reads the first
+          // sector of the matrix): a predicated asm load is followed by
+          // predicated moves of its results, i.e. a wait right where it is issued
+          if (h + s < S) ldg256_keep(ok[s] ? R + (int64_t)vr * K + lp * 8 : R, xb[s]);
+#else
           if (ok[s]) ldg256_keep(R + (int64_t)vr * K + lp * 8, xb[s]);
+#endif
         }
         if (h == 0) {
 #pragma unroll
@@ -743,11 +815,27 @@ __global__ void __launch_bounds__(32, MINB) kmv_tmerge_kernel(const int32_t* __r
         }
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
+#if PG_TM_STFAST
+          // every lane stores what it holds (a sector the merge cannot reach is
+          // never looked at); the 8 words of a sector share its swizzle term
+          if (h + s < S) {
+            const uint32_t base = tm_swz<K>(sbb + (uint32_t)(lp * 8) * 128u + (uint32_t)(RP * (h + s) + la) * 4u);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sts_u32(base + q * 128u, xb[s][q]);
+          }
+#elif PG_TM_STFAST == 2
+          if (ok[s]) {
+            const uint32_t base = tm_swz<K>(sbb + (uint32_t)(lp * 8) * 128u + (uint32_t)(RP * (h + s) + la) * 4u);
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sts_u32(base + q * 128u, xb[s][q]);
+          }
+#else
           if (ok[s]) {
             const uint32_t x0 = sbb + (uint32_t)(lp * 8) * 128u + (uint32_t)(RP * (h + s) + la) * 4u;
 #pragma unroll
             for (int q = 0; q < 8; ++q) sts_u32(tm_swz<K>(x0 + q * 128u), xb[s][q]);
           }
+#endif
         }
       }
       // the previous block's estimates (their kth gathers have landed)
@@ -758,10 +846,14 @@ __global__ void __launch_bounds__(32, MINB) kmv_tmerge_kernel(const int32_t* __r
       uint32_t pa = sa0, pb = sb0;  // shared-space byte addresses of the heads
       int s = T;
 #pragma unroll 1
+#if PG_TM_STEP2
+      for (; s >= 2; s -= 2) tm_step2<K>(pa, pb);
+#else
       for (; s >= 2; s -= 2) {
         tm_step<K>(pa, pb);
         tm_step<K>(pa, pb);
       }
+#endif
       if (s) tm_step<K>(pa, pb);
       int32_t kr = 0;
       if (T >= 1) {
@@ -789,10 +881,17 @@ __global__ void __launch_bounds__(32, MINB) kmv_tmerge_kernel(const int32_t* __r
       start = start_n;
       start_n = start_nn;
       cur = nxt;
+#if PG_TM_DEFER
+      lu = validn ? lun : 0;
+      lv = validn ? lvn : 0;
+      su = validn ? sun : 0;
+      sv = validn ? svn : 0;
+#else
       lu = lun;
       lv = lvn;
       su = sun;
       sv = svn;
+#endif
       nxt.u = u2;
       nxt.v = v2;
     }
@@ -818,11 +917,11 @@ static int launch_kmv_tmerge_v(cudaStream_t s, const int32_t* ranks, const doubl
     return v ? atoi(v) : 0;
   }();
   if (cap > 0) per_sm = min(per_sm, cap);
-  const int grid = grid_cap(sm_count() * per_sm, e - b, 2048);
+  const int grid = grid_cap(sm_count() * per_sm, e - b, PG_TM_CHUNK);
   ChunkCounter ctr;
-  PartialSums ps;  // one partial per 2048-slot chunk, summed in chunk order
+  PartialSums ps;  // one partial per chunk, summed in chunk order
   cudaError_t ce = ctr.init(s);
-  if (ce == cudaSuccess) ce = ps.init(s, (e - b + 2047) / 2048);
+  if (ce == cudaSuccess) ce = ps.init(s, (e - b + PG_TM_CHUNK - 1) / PG_TM_CHUNK);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "scratch: %s", cudaGetErrorString(ce));
   kern<<<grid, 32, sm, s>>>(ranks, rank_values, lengths, sizes, us, vs, b, e, ps.p, ctr.p);
   ps.finish(out_sum);
