@@ -539,14 +539,9 @@ static int launch_kmv_ranked(cudaStream_t s, const int32_t* ranks, const double*
 // smaller head, or both heads when they are equal), never reading past index
 // T - 1 of either row.  Edges of the other two branches (both sizes <= K:
 // s_u + s_v - |A | B|; k_eff < 2: |A & B|) continue the same merge until one
-// row is exhausted; |A & B| = i + j - steps.  The per-lane work is ~9
-// instructions per step instead of K directory probes per edge.
-//
-// Shared memory: each lane's two row prefixes word-interleaved ([K][32] per
-// row side), so lane l only ever touches bank l: the data-dependent indices
-// of the 32 merges never conflict, and no warp synchronisation is needed
-// (a lane reads only what it wrote).  Each lane loads its own rows in 32-byte
-// sectors (lanes of a u run share the sectors of A).
+// row is exhausted; |A & B| = i + j - steps.  The per-lane work is ~10
+// instructions per step instead of K directory probes per edge (c3: 4.6 ms
+// against 10.8 ms for the rank-directory engine above).
 #ifndef PG_TMERGE_NU
 #define PG_TMERGE_NU 8
 #endif
@@ -578,9 +573,6 @@ __device__ __forceinline__ void tm_step(uint32_t& pa, uint32_t& pb) {
 #endif
 #ifndef PG_TM_STEP2
 #define PG_TM_STEP2 1
-#endif
-#ifndef PG_TM_STFAST
-#define PG_TM_STFAST 0
 #endif
 #ifndef PG_TM_DEFER
 #define PG_TM_DEFER 1
@@ -623,14 +615,13 @@ __device__ __forceinline__ unsigned lanemask_le() {
   return m;
 }
 
-// Shared memory per warp (one warp per CTA): the v rows word-interleaved
-// ([K][32]: lane l only touches bank l, so the data-dependent indices of the
-// 32 merges never conflict), the u rows of the block once per distinct u
-// (edge slots are in u runs; a block takes the slots of at most NU runs,
-// rows skewed by 32/NU banks), 10 KB at K = 64: ~22 resident warps per SM.
-// Pipeline per warp: the slots of the next two blocks and the lengths/sizes
-// of the next block are loaded while the current block merges, and a block's
-// rank -> value gather is consumed one block later.
+// Shared memory per warp (one warp per CTA): the v rows word-interleaved and
+// swizzled ([K][32], tm_swz above), the u rows of the block once per distinct
+// u (edge slots are in u runs; a block takes the slots of at most NU runs,
+// rows skewed by 32/NU banks); 10.4 KB at K = 64: 20 resident warps per SM.
+// Pipeline per warp: the slots of the block after next and the lengths/sizes
+// of the next block are requested before the current block's rows, and a
+// block's rank -> value gather is consumed one block later.
 template <int K, int NU>
 struct TmergeSmem {
   static constexpr int SK = 32 / NU, AS = K + SK;
@@ -815,27 +806,11 @@ __global__ void __launch_bounds__(32, MINB) kmv_tmerge_kernel(const int32_t* __r
         }
 #pragma unroll
         for (int s = 0; s < 4; ++s) {
-#if PG_TM_STFAST
-          // every lane stores what it holds (a sector the merge cannot reach is
-          // never looked at); the 8 words of a sector share its swizzle term
-          if (h + s < S) {
-            const uint32_t base = tm_swz<K>(sbb + (uint32_t)(lp * 8) * 128u + (uint32_t)(RP * (h + s) + la) * 4u);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) sts_u32(base + q * 128u, xb[s][q]);
-          }
-#elif PG_TM_STFAST == 2
-          if (ok[s]) {
-            const uint32_t base = tm_swz<K>(sbb + (uint32_t)(lp * 8) * 128u + (uint32_t)(RP * (h + s) + la) * 4u);
-#pragma unroll
-            for (int q = 0; q < 8; ++q) sts_u32(base + q * 128u, xb[s][q]);
-          }
-#else
           if (ok[s]) {
             const uint32_t x0 = sbb + (uint32_t)(lp * 8) * 128u + (uint32_t)(RP * (h + s) + la) * 4u;
 #pragma unroll
             for (int q = 0; q < 8; ++q) sts_u32(tm_swz<K>(x0 + q * 128u), xb[s][q]);
           }
-#endif
         }
       }
       // the previous block's estimates (their kth gathers have landed)
