@@ -502,8 +502,14 @@ def run_secondary(skip: str = "c5"):
             bms, sk = _time_device(lambda: pg.build_sketched_graph(g, kind, s=1.0, k_override=64),
                                    reps=1, flush=flush)
             p = pg.make_provider(kind, sketched=sk)
+            torch.cuda.synchronize()
+            t_lay = time.perf_counter()
+            p._tc_layout(g.device())  # one-off edge-slot layout (cached on the graph / sketches)
+            torch.cuda.synchronize()
+            t_lay = time.perf_counter() - t_lay
             ms, c = _time_device(lambda: tc_counts(p, g.device()), reps=3, flush=flush)
-            extra = {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0, "build_ms": bms}
+            extra = {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0, "build_ms": bms,
+                     "layout_build_ms": t_lay * 1e3}
             if kind == "kmv":
                 kb = 2 * 4 * 64 + 24  # the rank kernels read 4-byte ranks
                 lay = p._tc_layout(g.device())

@@ -660,9 +660,8 @@ __global__ void __launch_bounds__(32, MINB) kmv_tmerge_kernel(const int32_t* __r
                                                         const int32_t* __restrict__ us,
                                                         const int32_t* __restrict__ vs, int64_t e_begin,
                                                         int64_t e_end, double* out_sum,
-                                                        unsigned long long* ctr) {
+                                                        unsigned long long* ctr, int64_t kChunk) {
   using SM = TmergeSmem<K, NU>;
-  constexpr int64_t kChunk = PG_TM_CHUNK;
   constexpr int S = K / 8;   // 32-byte sectors per row
   constexpr int W = K / 32;  // words of a u row per lane
   constexpr int AS = SM::AS;
@@ -892,13 +891,20 @@ static int launch_kmv_tmerge_v(cudaStream_t s, const int32_t* ranks, const doubl
     return v ? atoi(v) : 0;
   }();
   if (cap > 0) per_sm = min(per_sm, cap);
-  const int grid = grid_cap(sm_count() * per_sm, e - b, PG_TM_CHUNK);
+  // dynamic chunks of PG_TM_CHUNK slots; a short range (one shard's share of
+  // the full-merge part, say) takes smaller ones so that every resident warp
+  // still gets about four (the chunk size is a function of the range alone:
+  // sums stay reproducible for a given (e_begin, e_end))
+  const int64_t warps = (int64_t)sm_count() * per_sm;
+  int64_t chunk = ((e - b) / (warps * 4)) / 32 * 32;
+  chunk = chunk < 128 ? 128 : chunk > PG_TM_CHUNK ? PG_TM_CHUNK : chunk;
+  const int grid = grid_cap((int)warps, e - b, (int)chunk);
   ChunkCounter ctr;
   PartialSums ps;  // one partial per chunk, summed in chunk order
   cudaError_t ce = ctr.init(s);
-  if (ce == cudaSuccess) ce = ps.init(s, (e - b + PG_TM_CHUNK - 1) / PG_TM_CHUNK);
+  if (ce == cudaSuccess) ce = ps.init(s, (e - b + chunk - 1) / chunk);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "scratch: %s", cudaGetErrorString(ce));
-  kern<<<grid, 32, sm, s>>>(ranks, rank_values, lengths, sizes, us, vs, b, e, ps.p, ctr.p);
+  kern<<<grid, 32, sm, s>>>(ranks, rank_values, lengths, sizes, us, vs, b, e, ps.p, ctr.p, chunk);
   ps.finish(out_sum);
   return check_launch("tc_kmv_merge");
 }

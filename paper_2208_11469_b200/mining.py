@@ -103,8 +103,7 @@ def tc_counts(provider, dev, rank: int = 0, world: int = 1):
     if world == 1 and _chunk_pipelined(provider, dev):
         return _tc_counts_chunked(provider, dev)
     lay = provider._tc_layout(dev)
-    b, e = edge_range(lay.slots, rank, world, align=32 if lay.padded else 1)
-    return provider._tc_counts_layout(lay, b, e)
+    return provider._tc_counts_shard(lay, rank, world)
 
 
 def _chunk_pipelined(provider, dev) -> bool:

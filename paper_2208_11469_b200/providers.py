@@ -204,11 +204,12 @@ class TcLayout:
     unpack like a tuple; ``kind`` names the schedule ("id": every edge u < v
     in CSR order; "hub": degree-oriented with hub tags, ``hub_ids``)."""
 
-    __slots__ = ("us", "vs", "slots", "padded", "kind", "hub_ids", "n_hubs")
+    __slots__ = ("us", "vs", "slots", "padded", "kind", "hub_ids", "n_hubs", "split")
 
-    def __init__(self, us, vs, slots, padded, kind="id", hub_ids=None, n_hubs=0):
+    def __init__(self, us, vs, slots, padded, kind="id", hub_ids=None, n_hubs=0, split=None):
         self.us, self.vs, self.slots, self.padded = us, vs, slots, padded
         self.kind, self.hub_ids, self.n_hubs = kind, hub_ids, n_hubs
+        self.split = split  # KMV merge layout: slots [0, split) stop after k_eff steps
 
     def __iter__(self):
         return iter((self.us, self.vs, self.slots, self.padded))
@@ -277,6 +278,13 @@ class _SketchProvider(IntersectionProvider):
     def _tc_counts_layout(self, lay, e_begin: int, e_end: int):
         """The fused pass over slots [e_begin, e_end) of a _tc_layout."""
         return self._tc_counts(lay.us, lay.vs, e_begin, e_end, lay.padded)
+
+    def _tc_counts_shard(self, lay, rank: int, world: int):
+        """This rank's share of a _tc_layout: a contiguous, balanced slot
+        range (sharding.edge_range; padded layouts split on 32-slot units)."""
+        from .sharding import edge_range
+        b, e = edge_range(lay.slots, rank, world, align=32 if lay.padded else 1)
+        return self._tc_counts_layout(lay, b, e)
 
     @staticmethod
     def _tc_layout_name(lay) -> str:
@@ -659,9 +667,24 @@ class KmvProvider(_SketchProvider):
                    N.ptr(d["lengths"]), sg.capacity, N.ptr(pu), N.ptr(pv), ctypes.byref(split),
                    N.stream_handle())
             us, vs = pu, pv
-        lay = TcLayout(us, vs, slots, False, kind + "+kmv-merge")
+            split = split.value
+        else:
+            split = None
+        lay = TcLayout(us, vs, slots, False, kind + "+kmv-merge", split=split)
         sg._kmv_merge_layout = (dev, lay)
         return lay
+
+    def _tc_counts_shard(self, lay, rank: int, world: int):
+        """Partitioned merge layout: a rank takes its balanced share of the
+        k_eff-step merges and of the full merges (which run ~2x longer per
+        slot and all sit at the end of the slot list), two passes."""
+        if world == 1 or getattr(lay, "split", None) is None:
+            return super()._tc_counts_shard(lay, rank, world)
+        from .sharding import edge_range
+        b0, e0 = edge_range(lay.split, rank, world)
+        b1, e1 = edge_range(lay.slots - lay.split, rank, world)
+        return (self._tc_counts_layout(lay, b0, e0)
+                + self._tc_counts_layout(lay, lay.split + b1, lay.split + e1))
 
     def _tc_counts(self, us, vs, e_begin: int, e_end: int, padded: bool = False):
         import torch

@@ -1,6 +1,6 @@
 """Per-shard kernel time of the fused passes when the edge slots are split
-into N equal ranges (sharding.edge_range, as bench.py --gpus N does): the
-load balance of a multi-GPU run, measured on one GPU."""
+into N shares (provider._tc_counts_shard, as tc_counts(rank, world) does):
+the load balance of a multi-GPU run, measured on one GPU."""
 import os
 import statistics
 import sys
@@ -9,7 +9,6 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2208_11469_b200 as pg  # noqa: E402
-from paper_2208_11469_b200.sharding import edge_range  # noqa: E402
 
 W = int(os.environ.get("PG_SHARDS", "8"))
 
@@ -18,14 +17,13 @@ def shard_times(p, dev, label):
     lay = p._tc_layout(dev)
     ts = []
     for r in range(W):
-        b, e = edge_range(lay.slots, r, W, align=32 if lay.padded else 1)
-        p._tc_counts_layout(lay, b, e)
+        p._tc_counts_shard(lay, r, W)
         torch.cuda.synchronize()
         vals = []
         for _ in range(3):
             a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record()
-            p._tc_counts_layout(lay, b, e)
+            p._tc_counts_shard(lay, r, W)
             z.record()
             torch.cuda.synchronize()
             vals.append(a.elapsed_time(z))

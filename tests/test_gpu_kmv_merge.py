@@ -70,6 +70,36 @@ def test_merge_tc_vs_oracle(pg, monkeypatch, graph, k, orient, part):
     assert ranked == pytest.approx(want, rel=RTOL_SUM, abs=1e-9)
 
 
+@pytest.mark.parametrize("k", [32, 64, 128])
+def test_merge_tc_s16_vs_values_engine(pg, k):
+    """R-MAT s16 (1.0 M edges, hubs of degree > 10^4): the merge engine over
+    rank rows against the values engine (pg_tc_kmv) over the same sketches,
+    whole graph and two shard ranges."""
+    import torch
+    from paper_2208_11469_b200 import _native as N
+    g = pg.generate_kronecker(16, 16, 5)
+    sk = pg.build_sketched_graph(g, "kmv", s=1.0, k_override=k)
+    p = pg.make_provider("kmv", sketched=sk)
+    lay = p._tc_layout(g.device())
+    d = sk.device_tensors()
+    out = torch.empty(1, dtype=torch.float64, device="cuda")
+
+    def values(us, vs, b, e):
+        N.call("pg_tc_kmv", N.ptr(d["values"]), N.ptr(d["lengths"]), k, N.ptr(d["sizes"]),
+               N.ptr(us), N.ptr(vs), b, e, N.ptr(out), N.stream_handle())
+        return float(out.item())
+
+    def merge(b, e):
+        return float(p._tc_counts(lay.us, lay.vs, b, e, lay.padded).item())
+
+    whole = values(lay.us, lay.vs, 0, lay.slots)
+    assert merge(0, lay.slots) == pytest.approx(whole, rel=RTOL_SUM)
+    cut = lay.slots // 3 + 5
+    assert merge(0, cut) + merge(cut, lay.slots) == pytest.approx(whole, rel=RTOL_SUM)
+    assert merge(cut, lay.slots) == pytest.approx(values(lay.us, lay.vs, cut, lay.slots), rel=RTOL_SUM)
+    assert merge(7, 7) == 0.0
+
+
 def _crafted(k, n_rows, rng):
     pool_hi = 50_000
     rows = np.full((n_rows, k), INT32_MAX, dtype=np.int64)
