@@ -137,6 +137,9 @@ __global__ void __launch_bounds__(kBlock) clique4_bloom_kernel(
 #define PG_C4_MINB 5  // 46 registers, no spills: 5.23 vs 5.39 ms at c5b (shared memory also caps at 5)
 #endif
 constexpr int kC4Cap = 512;
+#ifndef PG_C4_ROUNDS
+#define PG_C4_ROUNDS 2  // member rows in flight per lane group
+#endif
 
 __device__ __forceinline__ bool smem_contains(const int32_t* a, int len, int32_t x) {
   int lo = 0, hi = len;
@@ -222,26 +225,38 @@ __global__ void __launch_bounds__(kBlock, PG_C4_MINB) clique4_bloom_staged_kerne
       sl[0] = a0.x; sl[1] = a0.y; sl[2] = a0.z; sl[3] = a0.w;
       sl[4] = a1.x; sl[5] = a1.y; sl[6] = a1.z; sl[7] = a1.w;
     }
-    for (int base = 0; base < c3; base += M) {
-      const int t = base + grp;
-      const bool valid = t < c3;
-      const int32_t wv = valid ? sC[t] : sC[0];
-      uint32_t r[8];
-      ldg256_keep(reinterpret_cast<const unsigned char*>(rows) + (int64_t)wv * (bits / 8) + 32 * gl, r);
-      int cnt = 0;
+    // members in rounds of kRounds * M: the rows of a round are all requested
+    // before the first is used (a row per iteration waited for every load)
+    constexpr int kRounds = PG_C4_ROUNDS;
+    for (int base = 0; base < c3; base += kRounds * M) {
+      uint32_t r[kRounds][8];
+      int32_t wv[kRounds];
+      bool valid[kRounds];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) cnt += __popc(op == PG_BF_OR ? (r[i] | sl[i]) : (r[i] & sl[i]));
+      for (int q = 0; q < kRounds; ++q) {
+        const int t = base + q * M + grp;
+        valid[q] = t < c3;
+        wv[q] = valid[q] ? sC[t] : sC[0];
+        ldg256_keep(reinterpret_cast<const unsigned char*>(rows) + (int64_t)wv[q] * (bits / 8) + 32 * gl, r[q]);
+      }
 #pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-      if (valid && gl == 0) {
-        if (op == PG_BF_OR) {
-          const int64_t S = (int64_t)sizes[wv] + c3;
-          if (__dsub_rn((double)S, lut[cnt]) > 0.0) {
+      for (int q = 0; q < kRounds; ++q) {
+        if (q > 0 && base + q * M >= c3) break;  // warp-uniform
+        int cnt = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) cnt += __popc(op == PG_BF_OR ? (r[q][i] | sl[i]) : (r[q][i] & sl[i]));
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+        if (valid[q] && gl == 0) {
+          if (op == PG_BF_OR) {
+            const int64_t S = (int64_t)sizes[wv[q]] + c3;
+            if (__dsub_rn((double)S, lut[cnt]) > 0.0) {
+              atomicAdd(hist_s + cnt, 1);
+              sum_pos += S;
+            }
+          } else {
             atomicAdd(hist_s + cnt, 1);
-            sum_pos += S;
           }
-        } else {
-          atomicAdd(hist_s + cnt, 1);
         }
       }
     }
