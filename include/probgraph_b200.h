@@ -247,6 +247,28 @@ PG_API int pg_tc_bloom_hub(const uint64_t* rows, int32_t bits, int32_t op,
  * pg_tc_minhash expects with onehash = 1 and padded = 1; 1 = no such engine
  * for k, padded slots are then not needed) */
 PG_API int pg_onehash_block_pad(int32_t k, int32_t* pad_host);
+/* 1-Hash hash-rank rows, a device layout for the TC engine with no reference
+ * counterpart: rank_of[x] = position of h0(x) = mix64(seed_0 ^ x) among the
+ * hash words of all n vertices (h0 is a bijection on IDs: an exact
+ * relabelling), and rank_rows[v] = the ranks of entries[v] ascending,
+ * INT32_MAX pad (k = 32, 64, 128), stored interleaved for `group` lanes per
+ * row (sorted element j at slot (j % group) * (k / group) + j / group; group
+ * = 32 / pg_onehash_block_pad(k) for the TC engine, 1 = plain ascending).  Two rows share an ID iff their rank rows
+ * share a rank (providers.py:200-203 _matches_onehash counts the same
+ * integer), and no rank of v above u's largest can be in u's row, so the
+ * engine stops probing there.  pg_tc_minhash takes them with onehash = 2. */
+PG_API int pg_hash_rank_table(int64_t n, const uint64_t* seeds_dev, int32_t* rank_of,
+                       void* stream);
+PG_API int pg_onehash_rank_rows(const int32_t* entries, int64_t n, int32_t k,
+                         const int32_t* rank_of, int32_t group, int32_t* rank_rows,
+                         void* stream);
+/* out[e] = the number of probes the rank-row engine makes for a slot with
+ * table row ts[e] and probe row ps[e] (ranks of ps[e] <= the largest rank of
+ * ts[e]; 0 for pads): a layout helper -- slots of one table row sorted by it
+ * keep the edges a warp processes together equally long. */
+PG_API int pg_onehash_prefix_counts(const int32_t* rank_rows, const int32_t* lengths, int32_t k,
+                             int32_t group, const int32_t* ts, const int32_t* ps,
+                             int64_t count, int32_t* out, void* stream);
 /* k-/1-Hash TC: out_cnt[m], out_ssum[m] (m = 0..k): number of edges and
  * int64 sum of (s_u+s_v) of non-verbatim edges with m matches;
  * out_verbatim[0] = sum of matches over verbatim 1-Hash edges. */

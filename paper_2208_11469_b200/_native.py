@@ -82,6 +82,9 @@ SIGNATURES = {
     "pg_onehash_block_pad": [c_i32, ctypes.POINTER(c_i32)],
     "pg_tc_kmv_ranked": [c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
                          c_i64, c_ptr, c_ptr],
+    "pg_hash_rank_table": [c_i64, c_ptr, c_ptr, c_ptr],
+    "pg_onehash_rank_rows": [c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr],
+    "pg_onehash_prefix_counts": [c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
     "pg_kmv_merge_supported": [c_i32, ctypes.POINTER(c_i32)],
     "pg_tc_kmv_merge": [c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
                         c_i64, c_ptr, c_ptr],

@@ -1192,7 +1192,123 @@ __global__ void kmv_rank_scatter_kernel(int64_t n, const uint64_t* __restrict__ 
   }
 }
 
+// ---- 1-Hash hash-rank rows (a device layout for the TC engine) ----------
+// h0 is a bijection on vertex IDs (mix64 of seed ^ id), so the position of
+// h0(x) among all n hash words is an exact, collision-free relabelling of
+// the IDs: two 1-Hash rows share an ID iff their rank rows share a rank.
+// Sorted by rank, every element of a row is at most the row's k-th smallest
+// hash, so a probe of v's ranks into u's table can stop at u's largest rank.
+__global__ void hash_universe_kernel(int64_t n, const uint64_t* __restrict__ seeds_dev,
+                                     uint64_t* __restrict__ keys, int32_t* __restrict__ ids) {
+  const uint64_t seed0 = seeds_dev[0];
+  for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < n; x += (int64_t)gridDim.x * blockDim.x) {
+    keys[x] = hash_word(seed0, (int32_t)x);
+    ids[x] = (int32_t)x;
+  }
+}
+__global__ void hash_rank_scatter_kernel(int64_t n, const int32_t* __restrict__ ids, int32_t* __restrict__ rank_of) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    rank_of[ids[i]] = (int32_t)i;
+}
+// one warp per row: ranks of the stored IDs (INT32_MAX for the -1 pads),
+// bitonic-sorted ascending across the warp's 32 * P registers
+template <int P>
+__global__ void __launch_bounds__(256) onehash_rank_rows_kernel(const int32_t* __restrict__ entries, int64_t n,
+                                                                const int32_t* __restrict__ rank_of,
+                                                                int32_t* __restrict__ out, int group) {
+  constexpr int K = 32 * P;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t v = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); v < n; v += warps) {
+    int32_t x[P];
+    // element index of register s on lane l: s * 32 + l
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const int32_t id = entries[v * K + s * 32 + lane];
+      x[s] = id < 0 ? INT32_MAX : __ldg(rank_of + id);
+    }
+    // bitonic network over indices i = s * 32 + lane
+#pragma unroll
+    for (int size = 2; size <= K; size <<= 1) {
+#pragma unroll
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+        for (int s = 0; s < P; ++s) {
+          const int i = s * 32 + lane;
+          const bool up = (i & size) == 0;  // ascending block
+          if (stride >= 32) {
+            const int t = s ^ (stride >> 5);  // partner register on the same lane
+            if (t > s) {
+              const int32_t a = x[s], b = x[t];
+              const bool sw = up ? a > b : a < b;
+              x[s] = sw ? b : a;
+              x[t] = sw ? a : b;
+            }
+          } else {
+            const int32_t o = __shfl_xor_sync(0xffffffffu, x[s], stride);
+            const bool low = (lane & stride) == 0;
+            x[s] = (low == up) ? min(x[s], o) : max(x[s], o);
+          }
+        }
+      }
+    }
+    // sorted element j goes to slot (j % group) * (K / group) + j / group:
+    // with `group` lanes per row reading K / group consecutive slots each,
+    // lane g's p-th register is sorted element p * group + g
+    const int per = K / group;
+#pragma unroll
+    for (int s = 0; s < P; ++s) {
+      const int j = s * 32 + lane;
+      out[v * K + (j % group) * per + j / group] = x[s];
+    }
+  }
+}
+
 extern "C" {
+
+int pg_hash_rank_table(int64_t n, const uint64_t* seeds_dev, int32_t* rank_of, void* stream) {
+  PG_REQUIRE(n >= 0 && n <= INT32_MAX, "n must be in [0, 2^31)");
+  if (n == 0) return PG_OK;
+  PG_REQUIRE(seeds_dev && rank_of, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  retain_default_pool();
+  size_t t_sort = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, t_sort, (const uint64_t*)nullptr, (uint64_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, n, 0, 64);
+  const size_t bytes = 2 * 8 * (size_t)n + 2 * 4 * (size_t)n + t_sort + 64;
+  char* buf = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&buf), bytes, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "rank table scratch: %s", cudaGetErrorString(e));
+  uint64_t* k0 = reinterpret_cast<uint64_t*>(buf);
+  uint64_t* k1 = k0 + n;
+  int32_t* i0 = reinterpret_cast<int32_t*>(k1 + n);
+  int32_t* i1 = i0 + n;
+  void* tmp = i1 + n + 8;
+  const int grid = sm_count() * 8;
+  hash_universe_kernel<<<grid, 256, 0, s>>>(n, seeds_dev, k0, i0);
+  size_t t = t_sort;
+  e = cub::DeviceRadixSort::SortPairs(tmp, t, k0, k1, i0, i1, n, 0, 64, s);
+  if (e == cudaSuccess) hash_rank_scatter_kernel<<<grid, 256, 0, s>>>(n, i1, rank_of);
+  cudaFreeAsync(buf, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "rank table: %s", cudaGetErrorString(e));
+  return check_launch("hash_rank_table");
+}
+
+int pg_onehash_rank_rows(const int32_t* entries, int64_t n, int32_t k, const int32_t* rank_of,
+                         int32_t group, int32_t* rank_rows, void* stream) {
+  PG_REQUIRE(n >= 0, "n must be >= 0");
+  PG_REQUIRE(group >= 1 && group <= 32 && (group & (group - 1)) == 0, "group must be a power of two <= 32");
+  if (k != 32 && k != 64 && k != 128)
+    return fail(PG_ERR_UNSUPPORTED, "1-Hash rank rows support k = 32, 64, 128 (got %d)", k);
+  if (n == 0) return PG_OK;
+  PG_REQUIRE(entries && rank_of && rank_rows, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  const int grid = (int)std::min<int64_t>((n + 7) / 8, (int64_t)sm_count() * 16);
+  if (k == 32) onehash_rank_rows_kernel<1><<<grid, 256, 0, s>>>(entries, n, rank_of, rank_rows, group);
+  else if (k == 64) onehash_rank_rows_kernel<2><<<grid, 256, 0, s>>>(entries, n, rank_of, rank_rows, group);
+  else onehash_rank_rows_kernel<4><<<grid, 256, 0, s>>>(entries, n, rank_of, rank_rows, group);
+  return check_launch("onehash_rank_rows");
+}
 
 int pg_build_bloom(const int64_t* offsets, const int32_t* adj, int64_t n, int32_t bits, int32_t b,
                    const uint64_t* seeds_dev, uint64_t* rows, int32_t* ones, void* stream) {

@@ -1,6 +1,8 @@
 // k-Hash / 1-Hash per-edge estimates (providers.py:197-232 pair_many,
 // _matches_khash / _matches_onehash), their fused TC reductions and the
 // Jaccard threshold count (estimators.py:123-168, mining.py:157-186).
+#include <algorithm>
+
 #include "pg_generic.cuh"
 
 namespace pg {
@@ -269,7 +271,12 @@ struct alignas(16) OnehashWarp {
   int sc;
 };
 
-template <int K>
+// kRank: the rows are hash-rank rows (pg_onehash_rank_rows: the ranks of the
+// stored IDs' h0 words, ascending, INT32_MAX pad) instead of ID rows.  Ranks
+// relabel IDs one to one, so the match counts are the same integers; sorted
+// by rank, nothing in v's row above u's largest rank can be in u's table, so
+// those probes (44 % of them at c3; all pads) are skipped.
+template <int K, bool kRank = false>
 __global__ void __launch_bounds__(kBlock, 5) onehash_block_kernel(const int32_t* __restrict__ R,
                                                                const int32_t* __restrict__ sizes,
                                                                const int32_t* __restrict__ us,
@@ -288,6 +295,7 @@ __global__ void __launch_bounds__(kBlock, 5) onehash_block_kernel(const int32_t*
   EpiOnehash epi{K, sizes, nullptr, nullptr, cnt_s, slo_s, shi_s, 0};
   int32_t cur_u = -1;
   int sc = 0;
+  int32_t tau = INT32_MAX - 1;  // kRank: the largest rank in u's table
   int64_t wb, we;
   while (next_chunk(ctr, e_begin, e_end, kChunk, wb, we)) {
     int32_t ul = 0, vl = -1;
@@ -325,9 +333,17 @@ __global__ void __launch_bounds__(kBlock, 5) onehash_block_kernel(const int32_t*
           for (int i = lane; i < K; i += 32) T4[i] = make_int4(-1, -1, -1, -1);
           if (lane == 0) W.sc = 0;
           __syncwarp();
+          if (kRank) {
+            int32_t mx = -1;
+#pragma unroll
+            for (int q = 0; q < K / 32; ++q) mx = max(mx, y[q] == INT32_MAX ? -1 : y[q]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            tau = mx;
+          }
 #pragma unroll
           for (int q = 0; q < K / 32; ++q) {
-            if (y[q] < 0) continue;  // -1 pad
+            if (kRank ? y[q] == INT32_MAX : y[q] < 0) continue;  // pad
             int32_t* bk = W.tab + kOnehashSlots * oh_bucket<K>(y[q]);
             bool placed = false;
 #pragma unroll
@@ -344,7 +360,11 @@ __global__ void __launch_bounds__(kBlock, 5) onehash_block_kernel(const int32_t*
 #pragma unroll
         for (int p = 0; p < P; ++p) {
           const int32_t q = (int32_t)x[p];
-          if (valid && q >= 0) {
+          // rank rows are interleaved over the row's G lanes (register p of
+          // lane g = sorted element p * G + g): once no lane of the warp has a
+          // candidate, no later register has one either
+          if (kRank && !__any_sync(0xffffffffu, valid && q <= tau)) break;
+          if (valid && (kRank ? q <= tau : q >= 0)) {
             bool hit;
             if constexpr (kOnehashSlots == 2) {
               const int2 bk = reinterpret_cast<const int2*>(W.tab)[oh_bucket<K>(q)];
@@ -386,11 +406,11 @@ __global__ void __launch_bounds__(kBlock, 5) onehash_block_kernel(const int32_t*
     atomicAdd(reinterpret_cast<unsigned long long*>(out_verbatim), (unsigned long long)vb);
 }
 
-template <int K>
+template <int K, bool kRank = false>
 static int launch_onehash_block(cudaStream_t s, const int32_t* ent, const int32_t* sizes, const int32_t* us,
                                 const int32_t* vs, int64_t b, int64_t e, int64_t* out_cnt, int64_t* out_ssum,
                                 int64_t* out_verbatim) {
-  auto kern = onehash_block_kernel<K>;
+  auto kern = onehash_block_kernel<K, kRank>;
   const size_t sm = sizeof(OnehashWarp<K>) * (kBlock / 32);
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   const int grid = grid_cap(grid_for_kernel(kern, sm), e - b, kBlock / (K / kOnehashPerLane));
@@ -467,6 +487,38 @@ static bool onehash_sorted(cudaStream_t s, bool fused, const int32_t* ent, int k
 #undef PG_OS
   return false;
 }
+// Layout helper for the hash-rank 1-Hash engine: out[e] = number of ranks of
+// the probe row ps[e] that are <= the largest rank of the table row ts[e],
+// i.e. the probes the engine makes for slot e (rows interleaved over `group`
+// lanes as pg_onehash_rank_rows stores them).
+__global__ void __launch_bounds__(256) onehash_prefix_counts_kernel(const int32_t* __restrict__ rows,
+                                                                    const int32_t* __restrict__ lengths, int k,
+                                                                    int group, const int32_t* __restrict__ ts,
+                                                                    const int32_t* __restrict__ ps,
+                                                                    int64_t count, int32_t* __restrict__ out) {
+  const int per = k / group;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = ts[e], p = ps[e];
+    int c = 0;
+    if (t >= 0 && p >= 0) {
+      const int lt = lengths[t], lp = lengths[p];
+      if (lt > 0) {
+        const int jt = lt - 1;
+        const int32_t tau = rows[(int64_t)t * k + (jt % group) * per + jt / group];
+        int lo = 0, hi = lp;  // first sorted index of p's row above tau
+        while (lo < hi) {
+          const int mid = (lo + hi) >> 1;
+          if (rows[(int64_t)p * k + (mid % group) * per + mid / group] <= tau) lo = mid + 1;
+          else hi = mid;
+        }
+        c = lo;
+      }
+    }
+    out[e] = c;
+  }
+}
+
 }  // namespace pg
 
 using namespace pg;
@@ -514,6 +566,20 @@ int pg_pairs_minhash(const int32_t* entries, int32_t k, int32_t onehash, const i
   return check_launch("pairs_khash");
 }
 
+int pg_onehash_prefix_counts(const int32_t* rank_rows, const int32_t* lengths, int32_t k, int32_t group,
+                             const int32_t* ts, const int32_t* ps, int64_t count, int32_t* out,
+                             void* stream) {
+  PG_REQUIRE(k >= 1 && count >= 0, "bad sizes");
+  PG_REQUIRE(group >= 1 && group <= 32 && (group & (group - 1)) == 0 && k % group == 0,
+             "group must be a power of two <= 32 dividing k");
+  if (count == 0) return PG_OK;
+  PG_REQUIRE(rank_rows && lengths && ts && ps && out, "null pointer");
+  const int grid = (int)std::min<int64_t>((count + 255) / 256, (int64_t)sm_count() * 16);
+  onehash_prefix_counts_kernel<<<grid, 256, 0, as_stream(stream)>>>(rank_rows, lengths, k, group, ts, ps, count,
+                                                                    out);
+  return check_launch("onehash_prefix_counts");
+}
+
 int pg_onehash_block_pad(int32_t k, int32_t* pad_host) {
   PG_REQUIRE(pad_host, "null output");
   *pad_host = (k == 32 || k == 64 || k == 128) ? 32 * kOnehashPerLane / k : 1;
@@ -527,6 +593,8 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
   PG_REQUIRE(k <= kMaxSketchK || padded != 2, "group-u slots need k <= %d", kMaxSketchK);
   PG_REQUIRE(0 <= e_begin && e_begin <= e_end, "bad edge range");
   PG_REQUIRE(out_cnt && out_ssum && out_verbatim, "null pointer");
+  if (onehash == 2 && !(padded && (k == 32 || k == 64 || k == 128)))
+    return fail(PG_ERR_UNSUPPORTED, "hash-rank rows need the row-padded layout and k = 32, 64, 128 (got k = %d)", k);
   cudaStream_t s = as_stream(stream);
   // one memset when [cnt | ssum | verbatim] is one buffer
   const bool adjacent = out_ssum == out_cnt + k + 1 && out_verbatim == out_ssum + k + 1;
@@ -543,10 +611,16 @@ int pg_tc_minhash(const int32_t* entries, int32_t k, int32_t onehash, const int3
     // the row-padded layout of pad 32 * kOnehashPerLane / k: one u per warp iteration
     const int pad = 32 * kOnehashPerLane / k;
     PG_REQUIRE(e_begin % pad == 0, "e_begin must be a multiple of the layout pad %d", pad);
+    if (onehash == 2) {  // hash-rank rows
+      if (k == 32) return launch_onehash_block<32, true>(s, entries, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim);
+      if (k == 64) return launch_onehash_block<64, true>(s, entries, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim);
+      return launch_onehash_block<128, true>(s, entries, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim);
+    }
     if (k == 32) return launch_onehash_block<32>(s, entries, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim);
     if (k == 64) return launch_onehash_block<64>(s, entries, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim);
     return launch_onehash_block<128>(s, entries, sizes, us, vs, e_begin, e_end, out_cnt, out_ssum, out_verbatim);
   }
+
   if (onehash && onehash_sorted(s, true, entries, k, sizes, us, vs, e_begin, e_end, nullptr, nullptr, out_cnt,
                                 out_ssum, out_verbatim))
     return check_launch("tc_onehash_sorted");

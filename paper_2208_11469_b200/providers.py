@@ -294,6 +294,10 @@ class _SketchProvider(IntersectionProvider):
         if lay.kind == "degree":
             return ("degree-oriented row-padded slots (u = lower (degree, ID) rank, N+ lists "
                     "of degree_order), one u per slot group")
+        if lay.kind.endswith("+onehash-rank"):
+            return ("row-padded slots grouped by the table endpoint ("
+                    + ("higher (degree, ID) rank" if lay.kind.startswith("degree") else "lower ID")
+                    + "), each row sorted by its probe count")
         if lay.kind.endswith("+kmv-merge"):
             return ("every edge once, " + ("lower -> higher (degree, ID) rank" if lay.kind.startswith("degree")
                                           else "u < v") + ", partitioned [k_eff-step merges | full merges]")
@@ -515,12 +519,70 @@ class MinHashProvider(_SketchProvider):
         import os
         sg = self.sketched
         pad = self.tc_pad()
+        if self.onehash and pad > 1 and dev.n > 0 and dev.nnz > 0:
+            lay = self._onehash_rank_layout(dev, pad)
+            if lay is not None:
+                return lay
         if (not self.onehash and pad > 1 and sg.capacity in (16, 32, 64) and dev.n > 0
                 and sg.n * sg.capacity * 4 > BloomProvider.DEGREE_ORIENT_MIN_BYTES
                 and os.environ.get("PG_TC_ORIENT", "degree") == "degree"):
             ug, vs, slots, _ = dev.hub_slots(pad, 0)
             return TcLayout(ug, vs, slots, 2, "degree")
         return super()._tc_layout(dev)
+
+    def _onehash_rank_layout(self, dev, pad: int):
+        """Edge slots for the hash-rank 1-Hash engine: the table side t of
+        every edge is its higher-(degree, ID)-rank endpoint (the smaller
+        largest-rank, so the other row's probes stop earliest; PG_TC_ORIENT=id:
+        the lower ID), rows grouped by t and, within a row, sorted by the
+        number of probes the slot needs (pg_onehash_prefix_counts), so the
+        edges a warp iteration holds are equally long; row-padded to `pad`.
+        Match counts are symmetric in (u, v)."""
+        import ctypes
+        import os
+        import torch
+        rows = self._rank_rows()
+        if rows is None or os.environ.get("PG_ONEHASH_LAYOUT", "sorted") != "sorted":
+            return None
+        sg = self.sketched
+        cached = getattr(sg, "_onehash_rank_layout", None)
+        if cached is not None and cached[0] is dev:
+            return cached[1]
+        d = self._dev()
+        orient = os.environ.get("PG_TC_ORIENT", "degree")
+        if orient == "degree":
+            lo, hi, _, _ = dev.hub_slots(1, 0)   # every edge once, lower -> higher rank
+            order = torch.sort(hi, stable=True).indices
+            ts, ps = hi[order], lo[order]
+            del order
+        else:
+            ts, ps = dev.upper_edges()
+        count = ts.numel()
+        k = sg.capacity
+        bp = torch.empty(count, dtype=torch.int32, device="cuda")
+        N.call("pg_onehash_prefix_counts", N.ptr(rows), N.ptr(d["lengths"]), k,
+               32 // N.onehash_block_pad(k), N.ptr(ts), N.ptr(ps), count, N.ptr(bp), N.stream_handle())
+        key = (ts.to(torch.int64) << 8) | bp.to(torch.int64)
+        del bp
+        order = torch.sort(key).indices
+        del key
+        ps = ps[order].contiguous()
+        del order
+        off = torch.zeros(dev.n + 1, dtype=torch.int64, device="cuda")
+        off[1:] = torch.cumsum(torch.bincount(ts, minlength=dev.n), 0)
+        cap = count + (pad - 1) * dev.n + 1
+        us = torch.empty(cap, dtype=torch.int32, device="cuda")
+        vs = torch.empty(cap, dtype=torch.int32, device="cuda")
+        ws_bytes = ctypes.c_size_t()
+        N.call("pg_csr_upper_edges_workspace", dev.n, cap, ctypes.byref(ws_bytes))
+        ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device="cuda")
+        slots = ctypes.c_int64()
+        N.call("pg_csr_row_slots_padded", N.ptr(off), N.ptr(ps), dev.n, pad, N.ptr(us), N.ptr(vs), cap,
+               ctypes.byref(slots), N.ptr(ws), ws_bytes.value, N.stream_handle())
+        torch.cuda.current_stream().synchronize()
+        lay = TcLayout(us[:slots.value], vs[:slots.value], slots.value, True, orient + "+onehash-rank")
+        sg._onehash_rank_layout = (dev, lay)
+        return lay
 
     def _pairs_launch(self, us_ptr, vs_ptr, count, out_ptr):
         d, sg = self._dev(), self.sketched
@@ -546,6 +608,27 @@ class MinHashProvider(_SketchProvider):
         out = out[:du.numel()]
         return out if on_dev else out.cpu().numpy().astype(np.int64)
 
+    def _rank_rows(self):
+        """1-Hash hash-rank rows for the fused pass (pg_onehash_rank_rows),
+        built once per sketch; None when the engine does not take them
+        (PG_ONEHASH_ROWS=id keeps the ID rows)."""
+        import os
+        import torch
+        sg = self.sketched
+        if (not self.onehash or sg.capacity not in (32, 64, 128) or sg.n == 0
+                or os.environ.get("PG_ONEHASH_ROWS", "rank") != "rank"):
+            return None
+        d = self._dev()
+        if "rank_rows" not in d:
+            rank_of = torch.empty(sg.n, dtype=torch.int32, device="cuda")
+            N.call("pg_hash_rank_table", sg.n, N.ptr(d["seeds"]), N.ptr(rank_of), N.stream_handle())
+            rows = torch.empty_like(d["entries"])
+            N.call("pg_onehash_rank_rows", N.ptr(d["entries"]), sg.n, sg.capacity, N.ptr(rank_of),
+                   32 // N.onehash_block_pad(sg.capacity), N.ptr(rows), N.stream_handle())
+            sg._dev["rank_rows"] = rows
+            d = self._dev()
+        return d["rank_rows"]
+
     def _tc_counts(self, us, vs, e_begin: int, e_end: int, padded: bool = False):
         import torch
         d, sg = self._dev(), self.sketched
@@ -553,7 +636,12 @@ class MinHashProvider(_SketchProvider):
         # [cnt(k+1) | ssum(k+1) | verbatim]: one buffer, one memset
         out = torch.empty(2 * k + 3, dtype=torch.int64, device="cuda")
         p0 = N.ptr(out)
-        N.call("pg_tc_minhash", N.ptr(d["entries"]), k, int(self.onehash),
+        rows, mode = d["entries"], int(self.onehash)
+        if self.onehash and padded:
+            rr = self._rank_rows()
+            if rr is not None:
+                rows, mode = rr, 2
+        N.call("pg_tc_minhash", N.ptr(rows), k, mode,
                N.ptr(d["sizes"]), N.ptr(us), N.ptr(vs), e_begin, e_end,
                int(padded), p0, p0 + 8 * (k + 1), p0 + 16 * (k + 1), N.stream_handle())
         return out
