@@ -269,6 +269,13 @@ PG_API int pg_onehash_rank_rows(const int32_t* entries, int64_t n, int32_t k,
 PG_API int pg_onehash_prefix_counts(const int32_t* rank_rows, const int32_t* lengths, int32_t k,
                              int32_t group, const int32_t* ts, const int32_t* ps,
                              int64_t count, int32_t* out, void* stream);
+/* adj_out = the rows of the oriented CSR (off, adj) (row = table vertex,
+ * entries = probe endpoints) counting-sorted (stable) by the register
+ * positions the rank-row engine needs per entry, ceil(probes / group)
+ * (probes as pg_onehash_prefix_counts).  Synchronises the stream once. */
+PG_API int pg_onehash_sort_rows(const int64_t* off, const int32_t* adj, int64_t n,
+                         const int32_t* rank_rows, const int32_t* lengths, int32_t k,
+                         int32_t group, int32_t* adj_out, void* stream);
 /* k-/1-Hash TC: out_cnt[m], out_ssum[m] (m = 0..k): number of edges and
  * int64 sum of (s_u+s_v) of non-verbatim edges with m matches;
  * out_verbatim[0] = sum of matches over verbatim 1-Hash edges. */
@@ -420,6 +427,11 @@ PG_API int pg_jp_components(const int32_t* us, const int32_t* vs,
 PG_API int pg_degree_order(const int64_t* offsets, const int32_t* adj, int64_t n,
                      int64_t nnz, int32_t* rank, int64_t* dir_off,
                      int32_t* dir_adj, void* stream);
+/* The transpose of pg_degree_order's lists from its ranks: x in N-(v) iff
+ * rank[x] < rank[v]; in_off n+1 entries, in_adj nnz/2 entries. */
+PG_API int pg_degree_in_lists(const int64_t* offsets, const int32_t* adj, int64_t n,
+                     int64_t nnz, const int32_t* rank, int64_t* in_off,
+                     int32_t* in_adj, void* stream);
 
 /* ---- link prediction (mining.py:248-331) ---------
  * two-hop candidates (_two_hop_candidates, :275-296): keys u*n+v (u < v),

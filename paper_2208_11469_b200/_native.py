@@ -85,6 +85,8 @@ SIGNATURES = {
     "pg_hash_rank_table": [c_i64, c_ptr, c_ptr, c_ptr],
     "pg_onehash_rank_rows": [c_ptr, c_i64, c_i32, c_ptr, c_i32, c_ptr, c_ptr],
     "pg_onehash_prefix_counts": [c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_ptr, c_i64, c_ptr, c_ptr],
+    "pg_onehash_sort_rows": [c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_ptr],
+    "pg_degree_in_lists": [c_ptr, c_ptr, c_i64, c_i64, c_ptr, c_ptr, c_ptr, c_ptr],
     "pg_kmv_merge_supported": [c_i32, ctypes.POINTER(c_i32)],
     "pg_tc_kmv_merge": [c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
                         c_i64, c_ptr, c_ptr],

@@ -178,6 +178,11 @@ __global__ void rank_scatter_kernel(const uint64_t* __restrict__ sorted, int64_t
     rank[(uint32_t)sorted[i]] = (int32_t)i;
 }
 
+__global__ void orient_flags_in_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ adj,
+                                       const int32_t* __restrict__ rank, int64_t nnz, int32_t* __restrict__ flags) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * blockDim.x)
+    flags[j] = rank[src[j]] > rank[adj[j]];
+}
 __global__ void orient_flags_kernel(const int32_t* __restrict__ src, const int32_t* __restrict__ adj,
                                     const int32_t* __restrict__ rank, int64_t nnz, int32_t* __restrict__ flags) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * blockDim.x)
@@ -380,6 +385,55 @@ int pg_degree_order(const int64_t* offsets, const int32_t* adj, int64_t n, int64
     }
     tb = temp;
     e = cub::DeviceScan::ExclusiveSum(tmp, tb, counts, dir_off, n + 1, s);
+    if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "scan: %s", cudaGetErrorString(e)); break; }
+  } while (false);
+  cudaFreeAsync(buf, s);
+  return rc;
+}
+
+// The in-lists of the degree orientation: x in N-(v) iff rank[x] < rank[v]
+// (the transpose of pg_degree_order's N+ lists, adjacency order preserved),
+// from ranks already computed.
+int pg_degree_in_lists(const int64_t* offsets, const int32_t* adj, int64_t n, int64_t nnz, const int32_t* rank,
+                       int64_t* in_off, int32_t* in_adj, void* stream) {
+  PG_REQUIRE(n >= 0 && nnz >= 0 && nnz % 2 == 0, "bad sizes");
+  PG_REQUIRE(offsets && in_off && (n == 0 || rank), "null pointer");
+  cudaStream_t s = as_stream(stream);
+  const int grid = sm_count() * 8;
+  if (n == 0 || nnz == 0) {
+    cudaError_t e = cudaMemsetAsync(in_off, 0, sizeof(int64_t) * (n + 1), s);
+    return e == cudaSuccess ? PG_OK : fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(e));
+  }
+  PG_REQUIRE(adj && in_adj, "null pointer");
+  size_t t_sel = 0, t_scan = 0;
+  cub::DeviceSelect::Flagged(nullptr, t_sel, (const int32_t*)nullptr, (const int32_t*)nullptr, (int32_t*)nullptr,
+                             (int64_t*)nullptr, nnz);
+  cub::DeviceScan::ExclusiveSum(nullptr, t_scan, (const int64_t*)nullptr, (int64_t*)nullptr, n + 1);
+  const size_t temp = al256(t_sel > t_scan ? t_sel : t_scan);
+  const size_t eb = al256(sizeof(int32_t) * nnz), cb = al256(sizeof(int64_t) * (n + 1));
+  void* buf = nullptr;
+  cudaError_t e = cudaMallocAsync(&buf, 2 * eb + cb + 256 + temp, s);
+  if (e != cudaSuccess) return fail(PG_ERR_CUDA, "cudaMallocAsync: %s", cudaGetErrorString(e));
+  char* p = static_cast<char*>(buf);
+  int32_t* src = reinterpret_cast<int32_t*>(p);
+  int32_t* flags = reinterpret_cast<int32_t*>(p + eb);
+  int64_t* counts = reinterpret_cast<int64_t*>(p + 2 * eb);
+  int64_t* d_num = reinterpret_cast<int64_t*>(p + 2 * eb + cb);
+  void* tmp = p + 2 * eb + cb + 256;
+  int rc = PG_OK;
+  do {
+    e = cudaMemsetAsync(counts + n, 0, sizeof(int64_t), s);
+    if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "memset: %s", cudaGetErrorString(e)); break; }
+    if ((rc = pg_csr_expand_rows(offsets, n, nnz, src, stream))) break;
+    orient_flags_in_kernel<<<grid, 256, 0, s>>>(src, adj, rank, nnz, flags);
+    if ((rc = check_launch("orient_flags_in"))) break;
+    size_t tb = temp;
+    e = cub::DeviceSelect::Flagged(tmp, tb, adj, flags, in_adj, d_num, nnz, s);
+    if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "select: %s", cudaGetErrorString(e)); break; }
+    row_flag_count_kernel<<<grid, 256, 0, s>>>(offsets, flags, n, counts);
+    if ((rc = check_launch("row_flag_count"))) break;
+    tb = temp;
+    e = cub::DeviceScan::ExclusiveSum(tmp, tb, counts, in_off, n + 1, s);
     if (e != cudaSuccess) { rc = fail(PG_ERR_CUDA, "scan: %s", cudaGetErrorString(e)); break; }
   } while (false);
   cudaFreeAsync(buf, s);

@@ -519,6 +519,102 @@ __global__ void __launch_bounds__(256) onehash_prefix_counts_kernel(const int32_
   }
 }
 
+// Rows of an oriented CSR (table vertex t = the row, entries = the probe
+// endpoints) counting-sorted by the register positions the rank-row engine
+// needs for each entry, ceil(probes / group) in 0 .. k / group: a warp per
+// row, two passes (bucket of every entry into `bucket`, then a stable
+// scatter by warp-aggregated ranks).
+__device__ __forceinline__ int onehash_probe_bucket(const int32_t* __restrict__ rows, int k, int group, int per,
+                                                    int32_t tau, int32_t p, int lp) {
+  int lo = 0, hi = lp;  // first sorted index of p's row above tau
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (rows[(int64_t)p * k + (mid % group) * per + mid / group] <= tau) lo = mid + 1;
+    else hi = mid;
+  }
+  return (lo + group - 1) / group;
+}
+// pass 1, a thread per entry: the entry's bucket
+__global__ void __launch_bounds__(256) onehash_row_buckets_kernel(const int32_t* __restrict__ src,
+                                                                  const int32_t* __restrict__ adj, int64_t nnz,
+                                                                  const int32_t* __restrict__ rows,
+                                                                  const int32_t* __restrict__ lengths, int k,
+                                                                  int group, unsigned char* __restrict__ bucket) {
+  const int per = k / group;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < nnz; j += (int64_t)gridDim.x * blockDim.x) {
+    const int32_t t = src[j], p = adj[j];
+    const int lt = lengths[t];
+    int32_t tau = -1;
+    if (lt > 0) tau = rows[(int64_t)t * k + ((lt - 1) % group) * per + (lt - 1) / group];
+    bucket[j] = (unsigned char)onehash_probe_bucket(rows, k, group, per, tau, p, lengths[p]);
+  }
+}
+// pass 2, a warp per row: stable counting sort of the row by bucket
+__global__ void __launch_bounds__(256) onehash_sort_rows_kernel(const int64_t* __restrict__ off,
+                                                                const int32_t* __restrict__ adj, int64_t n,
+                                                                int nb, const unsigned char* __restrict__ bucket,
+                                                                int32_t* __restrict__ out,
+                                                                unsigned long long* ctr) {
+  constexpr int kMaxB = 9;  // k / group + 1 <= 9 (the engine holds 8 ranks per lane)
+  const int lane = threadIdx.x & 31;
+  for (;;) {
+    unsigned long long t64 = 0;
+    if (lane == 0) t64 = atomicAdd(ctr, 8ull);  // eight rows per request
+    t64 = __shfl_sync(0xffffffffu, t64, 0);
+    if ((int64_t)t64 >= n) return;
+    const int64_t t_end = min((int64_t)t64 + 8, n);
+    for (int64_t t = (int64_t)t64; t < t_end; ++t) {
+      const int64_t b = off[t], e = off[t + 1];
+      if (e == b) continue;
+      int64_t base[kMaxB];
+      if (e - b <= 32) {  // one round: counts and positions from the same ballots
+        const int64_t j = b + lane;
+        const bool in = j < e;
+        const int q = in ? (int)bucket[j] : -1;
+        const int32_t p = in ? adj[j] : 0;
+        int64_t run = b;
+#pragma unroll
+        for (int z = 0; z < kMaxB; ++z) {
+          if (z >= nb) break;
+          const unsigned m = __ballot_sync(0xffffffffu, q == z);
+          if (q == z) out[run + __popc(m & lanemask_lt())] = p;
+          run += __popc(m);
+        }
+        continue;
+      }
+      int cnt[kMaxB];
+#pragma unroll
+      for (int q = 0; q < kMaxB; ++q) cnt[q] = 0;
+      for (int64_t j = b + lane; j < e; j += 32) {
+        const int q = (int)bucket[j];
+#pragma unroll
+        for (int z = 0; z < kMaxB; ++z) cnt[z] += z == q;
+      }
+      int64_t run = b;
+#pragma unroll
+      for (int q = 0; q < kMaxB; ++q) {
+        int c = cnt[q];
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        base[q] = run;
+        run += c;
+      }
+      for (int64_t j0 = b; j0 < e; j0 += 32) {
+        const int64_t j = j0 + lane;
+        const bool in = j < e;
+        const int q = in ? (int)bucket[j] : -1;
+        const int32_t p = in ? adj[j] : 0;
+#pragma unroll
+        for (int z = 0; z < kMaxB; ++z) {
+          if (z >= nb) break;
+          const unsigned m = __ballot_sync(0xffffffffu, q == z);
+          if (q == z) out[base[z] + __popc(m & lanemask_lt())] = p;
+          base[z] += __popc(m);
+        }
+      }
+    }
+  }
+}
+
 }  // namespace pg
 
 using namespace pg;
@@ -578,6 +674,40 @@ int pg_onehash_prefix_counts(const int32_t* rank_rows, const int32_t* lengths, i
   onehash_prefix_counts_kernel<<<grid, 256, 0, as_stream(stream)>>>(rank_rows, lengths, k, group, ts, ps, count,
                                                                     out);
   return check_launch("onehash_prefix_counts");
+}
+
+int pg_onehash_sort_rows(const int64_t* off, const int32_t* adj, int64_t n, const int32_t* rank_rows,
+                         const int32_t* lengths, int32_t k, int32_t group, int32_t* adj_out, void* stream) {
+  PG_REQUIRE(n >= 0 && k >= 1, "bad sizes");
+  PG_REQUIRE(group >= 1 && group <= 32 && (group & (group - 1)) == 0 && k % group == 0 && k / group <= 8,
+             "group must be a power of two <= 32 with k / group <= 8");
+  if (n == 0) return PG_OK;
+  PG_REQUIRE(off && rank_rows && lengths, "null pointer");
+  cudaStream_t s = as_stream(stream);
+  int64_t nnz = 0;
+  cudaError_t ce = cudaMemcpyAsync(&nnz, off + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+  if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "offsets: %s", cudaGetErrorString(ce));
+  if (nnz == 0) return PG_OK;
+  PG_REQUIRE(adj && adj_out && adj != adj_out, "null pointer / in place");
+  unsigned char* bucket = nullptr;
+  int32_t* src = nullptr;
+  retain_default_pool();
+  ce = cudaMallocAsync(reinterpret_cast<void**>(&bucket), (size_t)nnz, s);
+  if (ce == cudaSuccess) ce = cudaMallocAsync(reinterpret_cast<void**>(&src), sizeof(int32_t) * (size_t)nnz, s);
+  ChunkCounter ctr;
+  if (ce == cudaSuccess) ce = ctr.init(s);
+  int rc = ce == cudaSuccess ? PG_OK : fail(PG_ERR_CUDA, "scratch: %s", cudaGetErrorString(ce));
+  if (rc == PG_OK) rc = pg_csr_expand_rows(off, n, nnz, src, stream);
+  if (rc == PG_OK) {
+    const int grid = (int)std::min<int64_t>((nnz + 255) / 256, (int64_t)sm_count() * 16);
+    onehash_row_buckets_kernel<<<grid, 256, 0, s>>>(src, adj, nnz, rank_rows, lengths, k, group, bucket);
+    onehash_sort_rows_kernel<<<sm_count() * 8, 256, 0, s>>>(off, adj, n, k / group + 1, bucket, adj_out, ctr.p);
+  }
+  if (bucket) cudaFreeAsync(bucket, s);
+  if (src) cudaFreeAsync(src, s);
+  if (rc != PG_OK) return rc;
+  return check_launch("onehash_sort_rows");
 }
 
 int pg_onehash_block_pad(int32_t k, int32_t* pad_host) {

@@ -535,8 +535,8 @@ class MinHashProvider(_SketchProvider):
         every edge is its higher-(degree, ID)-rank endpoint (the smaller
         largest-rank, so the other row's probes stop earliest; PG_TC_ORIENT=id:
         the lower ID), rows grouped by t and, within a row, sorted by the
-        number of probes the slot needs (pg_onehash_prefix_counts), so the
-        edges a warp iteration holds are equally long; row-padded to `pad`.
+        register positions the slot's probes need (pg_onehash_sort_rows), so
+        the edges a warp iteration holds are equally long; row-padded to `pad`.
         Match counts are symmetric in (u, v)."""
         import ctypes
         import os
@@ -550,26 +550,26 @@ class MinHashProvider(_SketchProvider):
             return cached[1]
         d = self._dev()
         orient = os.environ.get("PG_TC_ORIENT", "degree")
-        if orient == "degree":
-            lo, hi, _, _ = dev.hub_slots(1, 0)   # every edge once, lower -> higher rank
-            order = torch.sort(hi, stable=True).indices
-            ts, ps = hi[order], lo[order]
-            del order
-        else:
-            ts, ps = dev.upper_edges()
-        count = ts.numel()
         k = sg.capacity
-        bp = torch.empty(count, dtype=torch.int32, device="cuda")
-        N.call("pg_onehash_prefix_counts", N.ptr(rows), N.ptr(d["lengths"]), k,
-               32 // N.onehash_block_pad(k), N.ptr(ts), N.ptr(ps), count, N.ptr(bp), N.stream_handle())
-        key = (ts.to(torch.int64) << 8) | bp.to(torch.int64)
-        del bp
-        order = torch.sort(key).indices
-        del key
-        ps = ps[order].contiguous()
-        del order
-        off = torch.zeros(dev.n + 1, dtype=torch.int64, device="cuda")
-        off[1:] = torch.cumsum(torch.bincount(ts, minlength=dev.n), 0)
+        group = 32 // N.onehash_block_pad(k)
+        half = dev.nnz // 2
+        if orient == "degree":
+            # rows = in-lists of the degree orientation: row t holds its
+            # lower-ranked neighbours (the probe endpoints)
+            rank = dev.degree_rank()[0]
+            off = torch.empty(dev.n + 1, dtype=torch.int64, device="cuda")
+            adj = torch.empty(max(1, half), dtype=torch.int32, device="cuda")
+            N.call("pg_degree_in_lists", N.ptr(dev.offsets), N.ptr(dev.adj), dev.n, dev.nnz,
+                   N.ptr(rank), N.ptr(off), N.ptr(adj), N.stream_handle())
+        else:
+            ts, adj = dev.upper_edges()  # rows = u, entries = v > u
+            off = torch.zeros(dev.n + 1, dtype=torch.int64, device="cuda")
+            off[1:] = torch.cumsum(torch.bincount(ts, minlength=dev.n), 0)
+        count = half
+        ps = torch.empty(max(1, count), dtype=torch.int32, device="cuda")
+        N.call("pg_onehash_sort_rows", N.ptr(off), N.ptr(adj), dev.n, N.ptr(rows), N.ptr(d["lengths"]),
+               k, group, N.ptr(ps), N.stream_handle())
+        del adj
         cap = count + (pad - 1) * dev.n + 1
         us = torch.empty(cap, dtype=torch.int32, device="cuda")
         vs = torch.empty(cap, dtype=torch.int32, device="cuda")

@@ -106,6 +106,47 @@ def test_tc_rank_rows_equal_id_rows(pg, monkeypatch, graph, k, orient, layout):
     assert hist.sum() == g.m
 
 
+def test_in_lists_and_sorted_rows(pg):
+    """pg_degree_in_lists = the transpose of degree_order's N+ lists;
+    pg_onehash_sort_rows = every row stably counting-sorted by
+    ceil(pg_onehash_prefix_counts / group)."""
+    import torch
+    from paper_2208_11469_b200 import _native as N
+    k = 64
+    g = pg.generate_kronecker(12, 16, 11)
+    dev = g.device()
+    rank = dev.degree_rank()[0]
+    half = dev.nnz // 2
+    off = torch.empty(g.n + 1, dtype=torch.int64, device="cuda")
+    adj = torch.empty(half, dtype=torch.int32, device="cuda")
+    N.call("pg_degree_in_lists", N.ptr(dev.offsets), N.ptr(dev.adj), g.n, dev.nnz, N.ptr(rank),
+           N.ptr(off), N.ptr(adj), N.stream_handle())
+    hr = rank.cpu().numpy()
+    src = np.repeat(np.arange(g.n), np.diff(g.offsets))
+    keep = hr[g.adjacency] < hr[src]
+    assert np.array_equal(adj.cpu().numpy(), g.adjacency[keep])
+    want_off = np.concatenate([[0], np.cumsum(np.bincount(src[keep], minlength=g.n))])
+    assert np.array_equal(off.cpu().numpy(), want_off)
+    # rows sorted by probe-register count
+    sk = pg.build_sketched_graph(g, "onehash", s=1.0, k_override=k)
+    p = pg.make_provider("onehash", sketched=sk)
+    rows = p._rank_rows()
+    d = sk.device_tensors()
+    group = 32 // N.onehash_block_pad(k)
+    out = torch.empty_like(adj)
+    N.call("pg_onehash_sort_rows", N.ptr(off), N.ptr(adj), g.n, N.ptr(rows), N.ptr(d["lengths"]), k, group,
+           N.ptr(out), N.stream_handle())
+    ts = torch.from_numpy(src[keep].astype(np.int32)).cuda()
+    bp = torch.empty(half, dtype=torch.int32, device="cuda")
+    N.call("pg_onehash_prefix_counts", N.ptr(rows), N.ptr(d["lengths"]), k, group, N.ptr(ts), N.ptr(adj),
+           half, N.ptr(bp), N.stream_handle())
+    bucket = (bp.cpu().numpy() + group - 1) // group
+    a, o = adj.cpu().numpy(), out.cpu().numpy()
+    t = src[keep]
+    order = np.lexsort((np.arange(half), bucket, t))  # stable by (row, bucket)
+    assert np.array_equal(o, a[order])
+
+
 def test_rank_rows_bad_arguments(pg):
     from paper_2208_11469_b200 import _native as N
     from paper_2208_11469_b200.providers import UnsupportedCombinationError
