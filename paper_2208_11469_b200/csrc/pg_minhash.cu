@@ -245,6 +245,9 @@ __global__ void __launch_bounds__(kBlock) onehash_sorted_kernel(const int32_t* e
 // the whole u run.  Slot blocks as in the KMV rank engine: lane l holds slot
 // l's endpoints one block ahead; after each 32-slot block every lane files
 // its slot's statistics.  Same bucket table and probe as htab_edge_loop.
+#ifndef PG_OH_UNROLL
+#define PG_OH_UNROLL 2  // unroll of the block's iteration loop (c3: 1: 3.13 ms, 2: 2.75, 4: 5.2 with spills)
+#endif
 #ifndef PG_OH_PER_LANE
 #define PG_OH_PER_LANE 8
 #endif
@@ -314,7 +317,8 @@ __global__ void __launch_bounds__(kBlock, 5) onehash_block_kernel(const int32_t*
         un = us[b0 + 32 + lane];
         vn = vs[b0 + 32 + lane];
       }
-#pragma unroll 1
+      constexpr int kItUnroll = PG_OH_UNROLL;
+#pragma unroll kItUnroll
       for (int it = 0; it < IT; ++it) {
         const int slot = it * E + grp;
         const int32_t u = __shfl_sync(0xffffffffu, ul, it * E);
