@@ -509,14 +509,15 @@ def run_secondary(skip: str = "c5"):
             t_lay = time.perf_counter() - t_lay
             ms, c = _time_device(lambda: tc_counts(p, g.device()), reps=3, flush=flush)
             extra = {"estimate": p._tc_combine(c.cpu().numpy()) / 3.0, "build_ms": bms,
-                     "layout_build_ms": t_lay * 1e3}
+                     "layout_build_ms": t_lay * 1e3,
+                     "layout": p._tc_layout_name(p._tc_layout(g.device()))}
             if kind == "kmv":
                 kb = 2 * 4 * 64 + 24  # the rank kernels read 4-byte ranks
-                lay = p._tc_layout(g.device())
                 extra.update(kernel_bytes_per_edge=kb,
                              frac_at_kernel_bytes=g.m * kb / (ms / 1e3) / 1e9 / peak,
-                             engine="merge" if p._merge_engine() else "rank-directory",
-                             layout=p._tc_layout_name(lay))
+                             engine="merge" if p._merge_engine() else "rank-directory")
+            else:
+                extra["rows"] = "hash-rank" if p._rank_rows() is not None else "id"
             r = rec("R-MAT s22 ef16 seed 2", g, ms, bpe, extra)
             sz = sk.sizes
             if kind == "onehash":
