@@ -303,9 +303,10 @@ PG_API int pg_tc_kmv_ranked(const int32_t* ranks, const double* rank_values,
  * (providers.py:266-301; same per-edge estimates as pg_tc_kmv), k = 32, 64,
  * 128 (pg_kmv_merge_supported).  out_sum[0] = the sum, reproducible for a
  * given (e_begin, e_end).  pg_kmv_merge_partition reorders a slot list
- * (stable) into [slots whose merge stops after k_eff steps | full-merge
- * slots and pads], *split_host = size of the first part: the layout the
- * engine runs fastest on (synchronises the stream). */
+ * (stable counting sort) into [slots whose merge stops after k_eff steps,
+ * by k_eff bucket (k_eff - 1) * keff_buckets / k ascending (1..8 buckets) |
+ * full-merge slots and pads], *split_host = size of the first part: the
+ * layout the engine runs fastest on (synchronises the stream). */
 PG_API int pg_kmv_merge_supported(int32_t k, int32_t* ok_host);
 PG_API int pg_tc_kmv_merge(const int32_t* ranks, const double* rank_values,
                     const int32_t* lengths, int32_t k, const int32_t* sizes,
@@ -313,8 +314,8 @@ PG_API int pg_tc_kmv_merge(const int32_t* ranks, const double* rank_values,
                     int64_t e_end, double* out_sum, void* stream);
 PG_API int pg_kmv_merge_partition(const int32_t* us, const int32_t* vs, int64_t count,
                     const int32_t* sizes, const int32_t* lengths, int32_t k,
-                    int32_t* out_us, int32_t* out_vs, int64_t* split_host,
-                    void* stream);
+                    int32_t keff_buckets, int32_t* out_us, int32_t* out_vs,
+                    int64_t* split_host, void* stream);
 /* Jaccard clustering count (config 4; estimators.py:123-131 + 148-154 and
  * mining.py:157-186).  out_counts[0] = #edges with matches >= min_matches
  * (J-hat = m/k >= tau), out_counts[1] = #edges whose vertex_similarity

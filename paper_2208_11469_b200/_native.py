@@ -90,7 +90,7 @@ SIGNATURES = {
     "pg_kmv_merge_supported": [c_i32, ctypes.POINTER(c_i32)],
     "pg_tc_kmv_merge": [c_ptr, c_ptr, c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
                         c_i64, c_ptr, c_ptr],
-    "pg_kmv_merge_partition": [c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i32, c_ptr, c_ptr,
+    "pg_kmv_merge_partition": [c_ptr, c_ptr, c_i64, c_ptr, c_ptr, c_i32, c_i32, c_ptr, c_ptr,
                                ctypes.POINTER(c_i64), c_ptr],
     "pg_jaccard_count_khash": [c_ptr, c_i32, c_ptr, c_ptr, c_ptr, c_i64,
                                c_i64, c_i32, c_i32, c_dbl, c_ptr, c_ptr],

@@ -942,46 +942,51 @@ static int launch_kmv_tmerge(cudaStream_t s, const int32_t* ranks, const double*
 #undef PG_TM
 }
 
-// Stable two-way partition of edge slots for the merge engine: slots whose
-// merge stops after k_eff steps first, the full-merge slots (both sizes <= k,
-// or k_eff < 2) and pads after them, so the long merges do not hold up the
-// warps of the short ones.
+// Stable counting sort of edge slots for the merge engine into B + 1
+// classes: the slots whose merge stops after k_eff steps by k_eff bucket
+// ((k_eff - 1) * B / k, ascending; B = 1: one class), then the full-merge
+// slots (both sizes <= k, or k_eff < 2) and pads, so the warps of a block of
+// slots run equally long and the long merges do not hold up the short ones.
 constexpr int kPartTile = 2048;
-__device__ __forceinline__ bool tmerge_is_short(const int32_t* __restrict__ sizes,
-                                                const int32_t* __restrict__ lengths, int k, int32_t u,
-                                                int32_t v) {
-  if (v < 0) return false;
+constexpr int kPartMaxClasses = 9;
+__device__ __forceinline__ int tmerge_class(const int32_t* __restrict__ sizes,
+                                            const int32_t* __restrict__ lengths, int k, int B, int32_t u,
+                                            int32_t v) {
+  if (v < 0) return B;
   const int su = sizes[u], sv = sizes[v];
-  return !(su <= k && sv <= k) && min(lengths[u], lengths[v]) >= 2;
+  const int T = min(lengths[u], lengths[v]);
+  if ((su <= k && sv <= k) || T < 2) return B;
+  return (T - 1) * B / k;
 }
+// tile_cnt[c * tiles + tile] = slots of class c in the tile
 __global__ void __launch_bounds__(256) tmerge_count_kernel(const int32_t* __restrict__ us,
                                                            const int32_t* __restrict__ vs, int64_t count,
                                                            const int32_t* __restrict__ sizes,
-                                                           const int32_t* __restrict__ lengths, int k,
-                                                           int64_t* tile_short) {
-  __shared__ int red[8];
+                                                           const int32_t* __restrict__ lengths, int k, int B,
+                                                           int64_t tiles, int64_t* tile_cnt) {
+  __shared__ int cnt_s[kPartMaxClasses];
+  if (threadIdx.x < kPartMaxClasses) cnt_s[threadIdx.x] = 0;
+  __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kPartTile;
-  int c = 0;
   for (int i = threadIdx.x; i < kPartTile; i += 256) {
     const int64_t e = base + i;
-    if (e < count) c += tmerge_is_short(sizes, lengths, k, us[e], vs[e]);
+    int c = -1;
+    if (e < count) c = tmerge_class(sizes, lengths, k, B, us[e], vs[e]);
+    for (int z = 0; z <= B; ++z) {
+      const unsigned m = __ballot_sync(0xffffffffu, c == z);
+      if ((threadIdx.x & 31) == 0 && m) atomicAdd(&cnt_s[z], __popc(m));
+    }
   }
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c;
   __syncthreads();
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int i = 0; i < 8; ++i) t += red[i];
-    tile_short[blockIdx.x] = t;
-  }
+  if (threadIdx.x <= B) tile_cnt[(int64_t)threadIdx.x * tiles + blockIdx.x] = cnt_s[threadIdx.x];
 }
-// exclusive scan of the tile counts in place (one block); total -> tile_short[tiles]
-__global__ void __launch_bounds__(1024) tmerge_scan_kernel(int64_t* tile_short, int64_t tiles) {
+// exclusive scan of `len` counts in place (one block); total -> a[len]
+__global__ void __launch_bounds__(1024) tmerge_scan_kernel(int64_t* a, int64_t len) {
   __shared__ int64_t part[1024];
-  const int64_t per = (tiles + 1023) / 1024;
-  const int64_t lo = min((int64_t)threadIdx.x * per, tiles), hi = min(lo + per, tiles);
+  const int64_t per = (len + 1023) / 1024;
+  const int64_t lo = min((int64_t)threadIdx.x * per, len), hi = min(lo + per, len);
   int64_t t = 0;
-  for (int64_t i = lo; i < hi; ++i) t += tile_short[i];
+  for (int64_t i = lo; i < hi; ++i) t += a[i];
   part[threadIdx.x] = t;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -991,59 +996,61 @@ __global__ void __launch_bounds__(1024) tmerge_scan_kernel(int64_t* tile_short, 
       part[i] = run;
       run += x;
     }
-    tile_short[tiles] = run;
+    a[len] = run;
   }
   __syncthreads();
   int64_t run = part[threadIdx.x];
   for (int64_t i = lo; i < hi; ++i) {
-    const int64_t x = tile_short[i];
-    tile_short[i] = run;
+    const int64_t x = a[i];
+    a[i] = run;
     run += x;
   }
 }
 __global__ void __launch_bounds__(256) tmerge_scatter_kernel(const int32_t* __restrict__ us,
                                                              const int32_t* __restrict__ vs, int64_t count,
                                                              const int32_t* __restrict__ sizes,
-                                                             const int32_t* __restrict__ lengths, int k,
-                                                             const int64_t* __restrict__ tile_short,
+                                                             const int32_t* __restrict__ lengths, int k, int B,
+                                                             const int64_t* __restrict__ tile_off,
                                                              int64_t tiles, int32_t* out_us, int32_t* out_vs) {
-  __shared__ int wsum[8];
-  __shared__ int tile_run;
+  __shared__ int wcnt[8][kPartMaxClasses];
+  __shared__ int64_t run_s[kPartMaxClasses];  // next output slot of each class for this tile
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t base = (int64_t)blockIdx.x * kPartTile;
-  const int64_t short_base = tile_short[blockIdx.x];
-  const int64_t long_base = tile_short[tiles] + (base - short_base);
-  if (threadIdx.x == 0) tile_run = 0;
+  if (threadIdx.x <= B) run_s[threadIdx.x] = tile_off[(int64_t)threadIdx.x * tiles + blockIdx.x];
   __syncthreads();
   for (int i0 = 0; i0 < kPartTile; i0 += 256) {
     const int64_t e = base + i0 + threadIdx.x;
     int32_t u = 0, v = -1;
-    bool in = e < count, sh = false;
-    if (in) {
+    int c = -1;
+    if (e < count) {
       u = us[e];
       v = vs[e];
-      sh = tmerge_is_short(sizes, lengths, k, u, v);
+      c = tmerge_class(sizes, lengths, k, B, u, v);
     }
-    const unsigned bal = __ballot_sync(0xffffffffu, sh);
-    if (lane == 0) wsum[w] = __popc(bal);
+    int my_rank = 0;
+    for (int z = 0; z <= B; ++z) {
+      const unsigned m = __ballot_sync(0xffffffffu, c == z);
+      if (lane == 0) wcnt[w][z] = __popc(m);
+      if (c == z) my_rank = __popc(m & lanemask_lt());
+    }
     __syncthreads();
-    int before = tile_run;
-    for (int i = 0; i < w; ++i) before += wsum[i];
-    const int rank_short = before + __popc(bal & lanemask_lt());
-    if (in) {
-      const int64_t pos = sh ? short_base + rank_short : long_base + (i0 + threadIdx.x - rank_short);
+    if (c >= 0) {
+      int before = 0;
+      for (int i = 0; i < w; ++i) before += wcnt[i][c];
+      const int64_t pos = run_s[c] + before + my_rank;
       out_us[pos] = u;
       out_vs[pos] = v;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x <= B) {
       int t = 0;
-      for (int i = 0; i < 8; ++i) t += wsum[i];
-      tile_run += t;
+      for (int i = 0; i < 8; ++i) t += wcnt[i][threadIdx.x];
+      run_s[threadIdx.x] += t;
     }
     __syncthreads();
   }
 }
+
 }  // namespace pg
 
 using namespace pg;
@@ -1157,28 +1164,32 @@ int pg_tc_kmv_merge(const int32_t* ranks, const double* rank_values, const int32
 }
 
 int pg_kmv_merge_partition(const int32_t* us, const int32_t* vs, int64_t count, const int32_t* sizes,
-                           const int32_t* lengths, int32_t k, int32_t* out_us, int32_t* out_vs,
-                           int64_t* split_host, void* stream) {
+                           const int32_t* lengths, int32_t k, int32_t keff_buckets, int32_t* out_us,
+                           int32_t* out_vs, int64_t* split_host, void* stream) {
   PG_REQUIRE(k >= 1, "k must be >= 1");
   PG_REQUIRE(count >= 0, "count must be >= 0");
+  PG_REQUIRE(keff_buckets >= 1 && keff_buckets < kPartMaxClasses, "keff_buckets must be in [1, %d]",
+             kPartMaxClasses - 1);
   PG_REQUIRE(split_host, "null output");
   *split_host = 0;
   if (count == 0) return PG_OK;
   PG_REQUIRE(us && vs && sizes && lengths && out_us && out_vs, "null pointer");
   PG_REQUIRE(us != out_us && vs != out_vs, "the partition is not in place");
   cudaStream_t s = as_stream(stream);
-  const int64_t tiles = (count + kPartTile - 1) / kPartTile;
-  int64_t* tile_short = nullptr;
+  const int B = keff_buckets;
+  const int64_t tiles = (count + kPartTile - 1) / kPartTile, len = (int64_t)(B + 1) * tiles;
+  int64_t* tile_cnt = nullptr;
   retain_default_pool();
-  cudaError_t ce = cudaMallocAsync(reinterpret_cast<void**>(&tile_short), sizeof(int64_t) * (tiles + 1), s);
+  cudaError_t ce = cudaMallocAsync(reinterpret_cast<void**>(&tile_cnt), sizeof(int64_t) * (len + 1), s);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "scratch: %s", cudaGetErrorString(ce));
-  tmerge_count_kernel<<<(unsigned)tiles, 256, 0, s>>>(us, vs, count, sizes, lengths, k, tile_short);
-  tmerge_scan_kernel<<<1, 1024, 0, s>>>(tile_short, tiles);
-  tmerge_scatter_kernel<<<(unsigned)tiles, 256, 0, s>>>(us, vs, count, sizes, lengths, k, tile_short, tiles,
+  tmerge_count_kernel<<<(unsigned)tiles, 256, 0, s>>>(us, vs, count, sizes, lengths, k, B, tiles, tile_cnt);
+  tmerge_scan_kernel<<<1, 1024, 0, s>>>(tile_cnt, len);
+  tmerge_scatter_kernel<<<(unsigned)tiles, 256, 0, s>>>(us, vs, count, sizes, lengths, k, B, tile_cnt, tiles,
                                                          out_us, out_vs);
-  ce = cudaMemcpyAsync(split_host, tile_short + tiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+  // the full-merge class starts where class B's first tile does
+  ce = cudaMemcpyAsync(split_host, tile_cnt + (int64_t)B * tiles, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
   if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
-  cudaFreeAsync(tile_short, s);
+  cudaFreeAsync(tile_cnt, s);
   if (ce != cudaSuccess) return fail(PG_ERR_CUDA, "partition: %s", cudaGetErrorString(ce));
   return check_launch("kmv_merge_partition");
 }

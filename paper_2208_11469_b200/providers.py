@@ -752,8 +752,8 @@ class KmvProvider(_SketchProvider):
             pu, pv = torch.empty_like(us), torch.empty_like(vs)
             split = ctypes.c_int64()
             N.call("pg_kmv_merge_partition", N.ptr(us), N.ptr(vs), slots, N.ptr(d["sizes"]),
-                   N.ptr(d["lengths"]), sg.capacity, N.ptr(pu), N.ptr(pv), ctypes.byref(split),
-                   N.stream_handle())
+                   N.ptr(d["lengths"]), sg.capacity, int(os.environ.get("PG_KMV_BUCKETS", "8")),
+                   N.ptr(pu), N.ptr(pv), ctypes.byref(split), N.stream_handle())
             us, vs = pu, pv
             split = split.value
         else:

@@ -173,7 +173,7 @@ def test_merge_crafted_rows_edge_by_edge(pg, k):
     import ctypes
     split = ctypes.c_int64()
     N.call("pg_kmv_merge_partition", N.ptr(dev["us"]), N.ptr(dev["vs"]), len(us), N.ptr(dev["sizes"]),
-           N.ptr(dev["lens"]), k, N.ptr(pu), N.ptr(pv), ctypes.byref(split), N.stream_handle())
+           N.ptr(dev["lens"]), k, 1, N.ptr(pu), N.ptr(pv), ctypes.byref(split), N.stream_handle())
     dev["pu"], dev["pv"] = pu, pv
     assert run(0, len(us), "pu", "pv") == pytest.approx(total, rel=RTOL_SUM)
     # the partition: stable, short merges first
@@ -185,8 +185,9 @@ def test_merge_crafted_rows_edge_by_edge(pg, k):
     assert np.array_equal(hu[split.value:], us[~short]) and np.array_equal(hv[split.value:], vs[~short])
 
 
+@pytest.mark.parametrize("buckets", [1, 4, 8])
 @pytest.mark.parametrize("count", [1, 31, 2048, 2049, 100_003])
-def test_partition_sizes(pg, count):
+def test_partition_sizes(pg, count, buckets):
     import ctypes
     import torch
     from paper_2208_11469_b200 import _native as N
@@ -202,14 +203,17 @@ def test_partition_sizes(pg, count):
     pu, pv = torch.empty_like(t["us"]), torch.empty_like(t["vs"])
     split = ctypes.c_int64()
     N.call("pg_kmv_merge_partition", N.ptr(t["us"]), N.ptr(t["vs"]), count, N.ptr(t["sizes"]),
-           N.ptr(t["lens"]), k, N.ptr(pu), N.ptr(pv), ctypes.byref(split), N.stream_handle())
+           N.ptr(t["lens"]), k, buckets, N.ptr(pu), N.ptr(pv), ctypes.byref(split), N.stream_handle())
     vv = np.maximum(vs, 0)
-    short = (vs >= 0) & ~((sizes[us] <= k) & (sizes[vv] <= k)) & (np.minimum(lens[us], lens[vv]) >= 2)
+    keff = np.minimum(lens[us], lens[vv]).astype(np.int64)
+    short = (vs >= 0) & ~((sizes[us] <= k) & (sizes[vv] <= k)) & (keff >= 2)
     hu, hv = pu.cpu().numpy(), pv.cpu().numpy()
     s = split.value
     assert s == int(short.sum())
-    assert np.array_equal(hu[:s], us[short]) and np.array_equal(hv[:s], vs[short])
-    assert np.array_equal(hu[s:], us[~short]) and np.array_equal(hv[s:], vs[~short])
+    # stable counting sort: k_eff buckets ascending, then the full merges and pads
+    cls = np.where(short, (keff - 1) * buckets // k, buckets)
+    order = np.lexsort((np.arange(count), cls))
+    assert np.array_equal(hu, us[order]) and np.array_equal(hv, vs[order])
 
 
 def test_merge_bad_arguments(pg):
