@@ -559,7 +559,7 @@ __global__ void __launch_bounds__(256) onehash_sort_rows_kernel(const int64_t* _
                                                                 int nb, const unsigned char* __restrict__ bucket,
                                                                 int32_t* __restrict__ out,
                                                                 unsigned long long* ctr) {
-  constexpr int kMaxB = 9;  // k / group + 1 <= 9 (the engine holds 8 ranks per lane)
+  constexpr int kMaxB = kOnehashPerLane + 1;  // k / group + 1 (the engine holds kOnehashPerLane ranks per lane)
   const int lane = threadIdx.x & 31;
   for (;;) {
     unsigned long long t64 = 0;
@@ -683,8 +683,9 @@ int pg_onehash_prefix_counts(const int32_t* rank_rows, const int32_t* lengths, i
 int pg_onehash_sort_rows(const int64_t* off, const int32_t* adj, int64_t n, const int32_t* rank_rows,
                          const int32_t* lengths, int32_t k, int32_t group, int32_t* adj_out, void* stream) {
   PG_REQUIRE(n >= 0 && k >= 1, "bad sizes");
-  PG_REQUIRE(group >= 1 && group <= 32 && (group & (group - 1)) == 0 && k % group == 0 && k / group <= 8,
-             "group must be a power of two <= 32 with k / group <= 8");
+  PG_REQUIRE(group >= 1 && group <= 32 && (group & (group - 1)) == 0 && k % group == 0 &&
+                 k / group <= kOnehashPerLane,
+             "group must be a power of two <= 32 with k / group <= %d", kOnehashPerLane);
   if (n == 0) return PG_OK;
   PG_REQUIRE(off && rank_rows && lengths, "null pointer");
   cudaStream_t s = as_stream(stream);
