@@ -553,6 +553,77 @@ __global__ void __launch_bounds__(256) onehash_row_buckets_kernel(const int32_t*
     bucket[j] = (unsigned char)onehash_probe_bucket(rows, k, group, per, tau, p, lengths[p]);
   }
 }
+// rows above this many entries are sorted by a whole CTA each: one warp walking
+// a 500,000-entry hub row 32 entries at a time took 8 ms of the 13 ms pass
+constexpr int64_t kSortLongRow = 2048;
+// pass 2 for long rows, a CTA per row: bucket counts by a block reduction,
+// then 256-entry rounds in order (stable), ranks from warp ballots and a
+// cross-warp prefix
+__global__ void __launch_bounds__(256) onehash_sort_long_rows_kernel(const int64_t* __restrict__ off,
+                                                                     const int32_t* __restrict__ adj, int64_t n,
+                                                                     int nb,
+                                                                     const unsigned char* __restrict__ bucket,
+                                                                     int32_t* __restrict__ out) {
+  constexpr int kMaxB = kOnehashPerLane + 1;
+  __shared__ int cnt_s[kMaxB];
+  __shared__ int wcnt[8][kMaxB];
+  __shared__ int64_t run_s[kMaxB];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int64_t t = blockIdx.x; t < n; t += gridDim.x) {
+    const int64_t b = off[t], e = off[t + 1];
+    if (e - b <= kSortLongRow) continue;  // block-uniform
+    if (threadIdx.x < kMaxB) cnt_s[threadIdx.x] = 0;
+    __syncthreads();
+    int cnt[kMaxB];
+#pragma unroll
+    for (int q = 0; q < kMaxB; ++q) cnt[q] = 0;
+    for (int64_t j = b + threadIdx.x; j < e; j += 256) {
+      const int q = (int)bucket[j];
+#pragma unroll
+      for (int z = 0; z < kMaxB; ++z) cnt[z] += z == q;
+    }
+#pragma unroll
+    for (int q = 0; q < kMaxB; ++q) {
+      int c = cnt[q];
+      for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+      if (lane == 0 && c) atomicAdd(&cnt_s[q], c);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int64_t run = b;
+      for (int q = 0; q < kMaxB; ++q) {
+        run_s[q] = run;
+        run += cnt_s[q];
+      }
+    }
+    __syncthreads();
+    for (int64_t j0 = b; j0 < e; j0 += 256) {
+      const int64_t j = j0 + threadIdx.x;
+      const bool in = j < e;
+      const int q = in ? (int)bucket[j] : -1;
+      const int32_t p = in ? adj[j] : 0;
+      int my_rank = 0;
+      for (int z = 0; z < nb; ++z) {
+        const unsigned m = __ballot_sync(0xffffffffu, q == z);
+        if (lane == 0) wcnt[w][z] = __popc(m);
+        if (q == z) my_rank = __popc(m & lanemask_lt());
+      }
+      __syncthreads();
+      if (in) {
+        int before = 0;
+        for (int i = 0; i < w; ++i) before += wcnt[i][q];
+        out[run_s[q] + before + my_rank] = p;
+      }
+      __syncthreads();
+      if (threadIdx.x < nb) {
+        int tsum = 0;
+        for (int i = 0; i < 8; ++i) tsum += wcnt[i][threadIdx.x];
+        run_s[threadIdx.x] += tsum;
+      }
+      __syncthreads();
+    }
+  }
+}
 // pass 2, a warp per row: stable counting sort of the row by bucket
 __global__ void __launch_bounds__(256) onehash_sort_rows_kernel(const int64_t* __restrict__ off,
                                                                 const int32_t* __restrict__ adj, int64_t n,
@@ -569,7 +640,7 @@ __global__ void __launch_bounds__(256) onehash_sort_rows_kernel(const int64_t* _
     const int64_t t_end = min((int64_t)t64 + 8, n);
     for (int64_t t = (int64_t)t64; t < t_end; ++t) {
       const int64_t b = off[t], e = off[t + 1];
-      if (e == b) continue;
+      if (e == b || e - b > kSortLongRow) continue;  // long rows: onehash_sort_long_rows_kernel
       int64_t base[kMaxB];
       if (e - b <= 32) {  // one round: counts and positions from the same ballots
         const int64_t j = b + lane;
@@ -707,6 +778,7 @@ int pg_onehash_sort_rows(const int64_t* off, const int32_t* adj, int64_t n, cons
   if (rc == PG_OK) {
     const int grid = (int)std::min<int64_t>((nnz + 255) / 256, (int64_t)sm_count() * 16);
     onehash_row_buckets_kernel<<<grid, 256, 0, s>>>(src, adj, nnz, rank_rows, lengths, k, group, bucket);
+    onehash_sort_long_rows_kernel<<<sm_count() * 4, 256, 0, s>>>(off, adj, n, k / group + 1, bucket, adj_out);
     onehash_sort_rows_kernel<<<sm_count() * 8, 256, 0, s>>>(off, adj, n, k / group + 1, bucket, adj_out, ctr.p);
   }
   if (bucket) cudaFreeAsync(bucket, s);

@@ -106,14 +106,21 @@ def test_tc_rank_rows_equal_id_rows(pg, monkeypatch, graph, k, orient, layout):
     assert hist.sum() == g.m
 
 
-def test_in_lists_and_sorted_rows(pg):
+@pytest.mark.parametrize("graph", ["rmat12", "hub6000"])
+def test_in_lists_and_sorted_rows(pg, graph):
     """pg_degree_in_lists = the transpose of degree_order's N+ lists;
     pg_onehash_sort_rows = every row stably counting-sorted by
     ceil(pg_onehash_prefix_counts / group)."""
     import torch
     from paper_2208_11469_b200 import _native as N
     k = 64
-    g = pg.generate_kronecker(12, 16, 11)
+    if graph == "rmat12":
+        g = pg.generate_kronecker(12, 16, 11)
+    else:  # rows above 2,048 entries take the CTA-per-row sort
+        rng = np.random.default_rng(5)
+        e = [[0, i] for i in range(1, 6001)] + [[1, i] for i in range(2, 3001)]
+        e += [[int(a), int(b)] for a, b in rng.integers(2, 6001, size=(40000, 2)) if a != b]
+        g = pg.CsrGraph.from_edges(e, 6100)
     dev = g.device()
     rank = dev.degree_rank()[0]
     half = dev.nnz // 2
