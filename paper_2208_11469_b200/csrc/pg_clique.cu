@@ -137,6 +137,13 @@ __global__ void __launch_bounds__(kBlock) clique4_bloom_kernel(
 #define PG_C4_MINB 5  // 46 registers, no spills: 5.23 vs 5.39 ms at c5b (shared memory also caps at 5)
 #endif
 constexpr int kC4Cap = 512;
+#ifndef PG_C4_DYNAMIC
+#define PG_C4_DYNAMIC 1
+#endif
+#ifndef PG_C4_CHUNK
+#define PG_C4_CHUNK 8
+#endif
+constexpr int64_t kC4Chunk = PG_C4_CHUNK;
 #ifndef PG_C4_ROUNDS
 #define PG_C4_ROUNDS 2  // member rows in flight per lane group
 #endif
@@ -157,7 +164,7 @@ __global__ void __launch_bounds__(kBlock, PG_C4_MINB) clique4_bloom_staged_kerne
     int64_t e_begin, int64_t e_end, const uint64_t* __restrict__ rows, int b,
     const uint64_t* __restrict__ seeds_dev, int op, const int32_t* __restrict__ sizes,
     const double* __restrict__ lut, int64_t* out_hist, int64_t* out_sum_pos, int64_t* out_triples,
-    const int64_t* __restrict__ edge_ids) {
+    const int64_t* __restrict__ edge_ids, unsigned long long* ctr) {
   constexpr int bits = 256 * G, words32 = bits / 32, M = 32 / G;
   constexpr int kWarpInts = 2 * kC4Cap + words32;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -172,8 +179,18 @@ __global__ void __launch_bounds__(kBlock, PG_C4_MINB) clique4_bloom_staged_kerne
   __syncthreads();
   const int gl = lane % G, grp = lane / G;
   long long triples = 0, sum_pos = 0;
+#if PG_C4_DYNAMIC
+  // edges in dynamic chunks of kC4Chunk per warp (per-edge work spans two
+  // orders of magnitude; a static stride left warps idle at the end)
+  int64_t wb = 0, we = 0;
+  for (;;) {
+  if (!next_chunk(ctr, e_begin, e_end, kC4Chunk, wb, we)) break;
+  for (int64_t j = wb; j < we; ++j) {
+#else
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  {
   for (int64_t j = e_begin + (int64_t)blockIdx.x * (blockDim.x >> 5) + w; j < e_end; j += nwarps) {
+#endif
     const int64_t jj = edge_ids ? edge_ids[j] : j;  // optional edge sample
     const int32_t u = src[jj], v = adjp[jj];
     const int32_t* A = adjp + off[u];
@@ -261,6 +278,7 @@ __global__ void __launch_bounds__(kBlock, PG_C4_MINB) clique4_bloom_staged_kerne
       }
     }
     __syncwarp();
+  }
   }
   __syncthreads();
   for (int i = threadIdx.x; i <= bits; i += blockDim.x)
@@ -423,8 +441,10 @@ static int clique4_bloom(const int64_t* dir_off, const int32_t* dir_adj, const i
     auto kern = clique4_bloom_staged_kernel<GG>;                                                               \
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);                        \
     const int grid = grid_cap(grid_for_kernel(kern, smem), e_end - e_begin, kBlock / 32);                     \
+    ChunkCounter ctr;                                                                                          \
+    if (ctr.init(s) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter");                                 \
     kern<<<grid, kBlock, smem, s>>>(dir_off, dir_adj, src, e_begin, e_end, rows_plus, b, seeds_dev, op, sizes, \
-                                    lut, out_hist, out_sum_pos, out_triples, edge_ids);                        \
+                                    lut, out_hist, out_sum_pos, out_triples, edge_ids, ctr.p);                 \
     return check_launch("4clique_bloom");                                                                      \
   }
     PG_C4(1) PG_C4(2) PG_C4(4) PG_C4(8) PG_C4(16) PG_C4(32)
