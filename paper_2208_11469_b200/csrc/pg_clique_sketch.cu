@@ -34,6 +34,10 @@ namespace pg {
 
 constexpr int kCSCap = 256;  // C3 entries held in shared memory per warp
 constexpr int kCSBlock = 256;
+#ifndef PG_C4S_CHUNK
+#define PG_C4S_CHUNK 8
+#endif
+constexpr int64_t kC4SChunk = PG_C4S_CHUNK;  // directed edges per dynamic chunk
 
 __device__ __forceinline__ bool contains_sorted(const int32_t* a, int len, int32_t x) {
   int lo = 0, hi = len;
@@ -82,11 +86,12 @@ struct C4SketchArgs {
 // scratch of C4SketchArgs; resolved at compile time so the common case keeps
 // shared-memory (LDS) addressing
 template <int KIND, bool kBig>
-__global__ void __launch_bounds__(kCSBlock) clique4_sketch_kernel(
+__global__ void __launch_bounds__(kCSBlock, 3) clique4_sketch_kernel(
     const int64_t* __restrict__ off, const int32_t* __restrict__ adjp, const int32_t* __restrict__ src,
     const int64_t* __restrict__ edge_ids, int64_t e_begin, int64_t e_end, C4SketchArgs a,
     int32_t* __restrict__ gC, int32_t* __restrict__ gF, uint64_t* __restrict__ gH, int64_t scratch_per_warp,
-    int cap, double* __restrict__ part, unsigned long long* __restrict__ out_triples) {
+    int cap, double* __restrict__ part, unsigned long long* __restrict__ out_triples,
+    unsigned long long* __restrict__ ctr) {
   constexpr int kWarps = kCSBlock / 32;
   // dynamic shared memory (c4s_smem): per warp the staged longer list /
   // repeat flags, C3, its keys and the member sketch; then the seeds
@@ -97,7 +102,6 @@ __global__ void __launch_bounds__(kCSBlock) clique4_sketch_kernel(
   int32_t* sB_all = reinterpret_cast<int32_t*>(seeds_s + kMaxSketchK);  // [kWarps][kCSCap]
   int32_t* sC_all = sB_all + kWarps * kCSCap;                       // [kWarps][kCSCap]
   __shared__ uint64_t thr_s[kWarps];
-  __shared__ double wsum[kWarps];
   const int k = a.k;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int nseeds = KIND == PG_KHASH ? min(k, kMaxSketchK) : 1;
@@ -108,10 +112,14 @@ __global__ void __launch_bounds__(kCSBlock) clique4_sketch_kernel(
   int32_t* gCw = gC + gw * scratch_per_warp;
   int32_t* gFw = gF + gw * scratch_per_warp;
   uint64_t* gHw = gH + gw * scratch_per_warp;
-  double acc = 0.0;
   long long triples = 0;
-  const int64_t nwarps = (int64_t)gridDim.x * kWarps;
-  for (int64_t j = e_begin + gw; j < e_end; j += nwarps) {
+  // directed edges in dynamic chunks of kC4SChunk per warp (per-edge work
+  // spans orders of magnitude); one fp64 partial per chunk, summed in chunk
+  // order afterwards, so the total does not depend on which warp ran what
+  int64_t wb = 0, we = 0;
+  while (next_chunk(ctr, e_begin, e_end, kC4SChunk, wb, we)) {
+  double acc = 0.0;
+  for (int64_t j = wb; j < we; ++j) {
     const int64_t jj = edge_ids ? edge_ids[j] : j;
     const int32_t u = src[jj], v = adjp[jj];
     const int32_t* A = adjp + off[u];
@@ -403,26 +411,11 @@ __global__ void __launch_bounds__(kCSBlock) clique4_sketch_kernel(
     if (la <= cap) edge(std::true_type{});
     else edge(std::false_type{});
   }
-  // (triples is warp-uniform: every lane added the same c3)
   for (int o = 16; o > 0; o >>= 1) acc = __dadd_rn(acc, __shfl_xor_sync(0xffffffffu, acc, o));
-  if (lane == 0) {
-    wsum[wid] = acc;
-    if (triples) atomicAdd(out_triples, (unsigned long long)triples);
+  if (lane == 0) part[(wb - e_begin) / kC4SChunk] = acc;
   }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < kWarps; ++i) s = __dadd_rn(s, wsum[i]);
-    part[blockIdx.x] = s;
-  }
-}
-
-// fixed-order sum of the per-block partials (one warp: strided lanes, xor tree)
-__global__ void sum_partials_kernel(const double* __restrict__ part, int n, double* out) {
-  double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += 32) s = __dadd_rn(s, part[i]);
-  for (int o = 16; o > 0; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
-  if (threadIdx.x == 0) out[0] = s;
+  // (triples is warp-uniform: every lane added the same c3)
+  if (lane == 0 && triples) atomicAdd(out_triples, (unsigned long long)triples);
 }
 
 // shared-memory C3 capacity; PG_C4S_CAP (1..512) lowers it so tests can
@@ -521,15 +514,21 @@ int pg_4clique_sketch(int32_t kind, const int64_t* dir_off, const int32_t* dir_a
                     kind == PG_KMV ? static_cast<const double*>(rows) : nullptr, lengths, sizes, seeds_dev, k,
                     gM, gT, tcap};
   auto* trip = reinterpret_cast<unsigned long long*>(out_triples);
+  ChunkCounter ctr;
+  PartialSums ps;  // one partial per chunk of directed edges, summed in chunk order
+  cudaError_t se = ctr.init(s);
+  if (se == cudaSuccess) se = ps.init(s, (e_end - e_begin + kC4SChunk - 1) / kC4SChunk);
+  if (se != cudaSuccess) return fail(PG_ERR_CUDA, "scratch: %s", cudaGetErrorString(se));
+  (void)part;
 #define PG_C4S(KK)                                                                                       \
   (k > kMaxSketchK ? clique4_sketch_kernel<KK, true> : clique4_sketch_kernel<KK, false>)                \
       <<<grid, kCSBlock, c4s_smem(), s>>>(dir_off, dir_adj, src, edge_ids, e_begin, e_end, \
-                                                               args, gC, gF, gH, per_warp, cap, part, trip)
+                                                               args, gC, gF, gH, per_warp, cap, ps.p, trip, ctr.p)
   if (kind == PG_KHASH) PG_C4S(PG_KHASH);
   else if (kind == PG_ONEHASH) PG_C4S(PG_ONEHASH);
   else PG_C4S(PG_KMV);
 #undef PG_C4S
-  sum_partials_kernel<<<1, 32, 0, s>>>(part, grid, out_sum);
+  ps.finish(out_sum);
   return check_launch("4clique_sketch");
 }
 
