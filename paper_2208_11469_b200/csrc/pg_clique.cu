@@ -331,15 +331,17 @@ __device__ __forceinline__ long long clique4_exact_edge_global(const int64_t* __
 __global__ void __launch_bounds__(kBlock) clique4_exact_kernel(
     const int64_t* __restrict__ off, const int32_t* __restrict__ adjp, const int32_t* __restrict__ src,
     int64_t e_begin, int64_t e_end, const int64_t* __restrict__ woff, const int32_t* __restrict__ wadj,
-    int64_t* out_count) {
+    int64_t* out_count, unsigned long long* ctr) {
   extern __shared__ __align__(16) int32_t smem_i[];  // (kBlock/32) * (3*kC4Cap + 1)
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   int32_t* sB = smem_i + w * (3 * kC4Cap + 1);
   int32_t* sC = sB + kC4Cap;
   int32_t* sP = sC + kC4Cap;  // kC4Cap + 1 entries
   long long total = 0;
-  const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t j = e_begin + (int64_t)blockIdx.x * (blockDim.x >> 5) + w; j < e_end; j += nwarps) {
+  // dynamic chunks of directed edges (as the Bloom kernel; the count is an integer)
+  int64_t wb = 0, we = 0;
+  while (next_chunk(ctr, e_begin, e_end, kC4Chunk, wb, we))
+  for (int64_t j = wb; j < we; ++j) {
     const int32_t u = src[j], v = adjp[j];
     const int32_t* A = adjp + off[u];
     int64_t la = off[u + 1] - off[u];
@@ -498,8 +500,10 @@ int pg_4clique_exact_rows(const int64_t* dir_off, const int32_t* dir_adj, const 
   const size_t smem = sizeof(int32_t) * (kBlock / 32) * (3 * kC4Cap + 1);
   cudaFuncSetAttribute(clique4_exact_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   const int grid = grid_cap(grid_for_kernel(clique4_exact_kernel, smem), e_end - e_begin, kBlock / 32);
+  ChunkCounter ctr;
+  if (ctr.init(s) != cudaSuccess) return fail(PG_ERR_CUDA, "chunk counter");
   clique4_exact_kernel<<<grid, kBlock, smem, s>>>(dir_off, dir_adj, src, e_begin, e_end, w_off, w_adj,
-                                                  out_count);
+                                                  out_count, ctr.p);
   return check_launch("4clique_exact");
 }
 
