@@ -148,14 +148,16 @@ constexpr int64_t kC4Chunk = PG_C4_CHUNK;
 #define PG_C4_ROUNDS 2  // member rows in flight per lane group
 #endif
 
+// lower bound by descending powers of two: the same trip count on every lane
+// (floor(log2 len) + 1) and five instructions per step instead of the nine of
+// a lo/hi loop (the C3 searches were 22 % of the kernel's instructions)
 __device__ __forceinline__ bool smem_contains(const int32_t* a, int len, int32_t x) {
-  int lo = 0, hi = len;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] < x) lo = mid + 1;
-    else hi = mid;
+  int pos = 0;  // elements known to be < x
+  for (int step = 1 << (31 - __clz(len | 1)); step > 0; step >>= 1) {
+    const int p = pos + step;
+    if (p <= len && a[p - 1] < x) pos = p;
   }
-  return lo < len && a[lo] == x;
+  return pos < len && a[pos] == x;
 }
 
 template <int G>
