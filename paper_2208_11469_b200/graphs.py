@@ -251,6 +251,56 @@ class DeviceCsr:
             self._layouts[key] = (us[:k:pad].contiguous(), vs[:k], k, hub_ids)
         return self._layouts[key]
 
+    def hybrid_slots(self, pad: int, thr: int):
+        """Degree-oriented group-u slots with less padding: (ug, vs, slots).
+        Rows of the N+ lists with more than `thr` entries keep their own slot
+        groups (as hub_slots(pad, 0)); the edges of the shorter rows -- 4 % of
+        the edges but two thirds of the pad slots at R-MAT -- are grouped by
+        their higher-rank endpoint instead (its row is the one a group holds
+        in registers), where they form long runs.  Every edge still appears
+        once; which endpoint is called u only matters for the schedule."""
+        key = ("hybrid", pad, thr)
+        if key not in self._layouts:
+            import ctypes
+            import torch
+            from . import _native as N
+            _, off, adj = self.degree_rank()
+            n = self.n
+            dplus = off[1:] - off[:-1]
+            keep_row = dplus > thr
+            src = torch.repeat_interleave(torch.arange(n, dtype=torch.int32, device="cuda"), dplus)
+            keep = keep_row[src.long()]
+            # part 1: the long rows by their own (lower-rank) vertex
+            off1 = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
+            off1[1:] = torch.cumsum(dplus * keep_row, 0)
+            adj1 = adj[keep].contiguous()
+            # part 2: the short rows' edges by the higher-rank endpoint
+            lo, hi = src[~keep], adj[~keep]
+            del src, keep
+            order = torch.sort(hi.long(), stable=True).indices
+            adj2 = lo[order].contiguous()
+            off2 = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
+            off2[1:] = torch.cumsum(torch.bincount(hi, minlength=n), 0)
+            del lo, hi, order
+            parts = []
+            for o, a in ((off1, adj1), (off2, adj2)):
+                cap = a.numel() + (pad - 1) * n + 1
+                us = torch.empty(cap, dtype=torch.int32, device="cuda")
+                vs = torch.empty(cap, dtype=torch.int32, device="cuda")
+                ws_bytes = ctypes.c_size_t()
+                N.call("pg_csr_upper_edges_workspace", n, cap, ctypes.byref(ws_bytes))
+                ws = torch.empty(max(1, ws_bytes.value), dtype=torch.uint8, device="cuda")
+                slots = ctypes.c_int64()
+                N.call("pg_csr_row_slots_padded", N.ptr(o), N.ptr(a), n, pad, N.ptr(us), N.ptr(vs), cap,
+                       ctypes.byref(slots), N.ptr(ws), ws_bytes.value, N.stream_handle())
+                k = slots.value
+                parts.append((us[:k:pad], vs[:k], k))
+                del ws
+            ug = torch.cat([parts[0][0], parts[1][0]])
+            vs = torch.cat([parts[0][1], parts[1][1]])
+            self._layouts[key] = (ug, vs, parts[0][2] + parts[1][2])
+        return self._layouts[key]
+
     def max_degree(self) -> int:
         """Largest row length (one device reduction, cached)."""
         if getattr(self, "_maxd", None) is None:

@@ -417,6 +417,13 @@ class BloomProvider(_SketchProvider):
             big = sg.n * sg.bit_length // 8 > self.DEGREE_ORIENT_MIN_BYTES
             orient = os.environ.get("PG_TC_ORIENT", "degree" if big else "id")
             if orient == "degree" and dev.n > 0:
+                # rows of at most `thr` N+ entries are regrouped by their other
+                # endpoint (DeviceCsr.hybrid_slots): 19 % -> 13 % pad slots at
+                # R-MAT; c5 4.43 -> 4.27 ms (thr 2; 4: 4.28, 8: 4.40)
+                thr = int(os.environ.get("PG_TC_HYBRID", "2"))
+                if thr > 0 and dev.nnz > 0:
+                    ug, vs, slots = dev.hybrid_slots(pad, thr)
+                    return TcLayout(ug, vs, slots, 2, "degree")
                 ug, vs, slots, _ = dev.hub_slots(pad, 0)
                 return TcLayout(ug, vs, slots, 2, "degree")
             ug, vs, slots = dev.upper_edges_group_u(pad)
