@@ -204,11 +204,12 @@ class TcLayout:
     unpack like a tuple; ``kind`` names the schedule ("id": every edge u < v
     in CSR order; "hub": degree-oriented with hub tags, ``hub_ids``)."""
 
-    __slots__ = ("us", "vs", "slots", "padded", "kind", "hub_ids", "n_hubs", "split")
+    __slots__ = ("us", "vs", "slots", "padded", "kind", "hub_ids", "n_hubs", "split", "regroup")
 
-    def __init__(self, us, vs, slots, padded, kind="id", hub_ids=None, n_hubs=0, split=None):
+    def __init__(self, us, vs, slots, padded, kind="id", hub_ids=None, n_hubs=0, split=None, regroup=0):
         self.us, self.vs, self.slots, self.padded = us, vs, slots, padded
         self.kind, self.hub_ids, self.n_hubs = kind, hub_ids, n_hubs
+        self.regroup = regroup  # degree layout: N+ rows of <= regroup entries grouped by their other endpoint
         self.split = split  # KMV merge layout: slots [0, split) stop after k_eff steps
 
     def __iter__(self):
@@ -292,8 +293,12 @@ class _SketchProvider(IntersectionProvider):
             return (f"degree-oriented group-u slots (pad 8), {lay.n_hubs} hub rows staged "
                     "in shared memory per CTA")
         if lay.kind == "degree":
-            return ("degree-oriented row-padded slots (u = lower (degree, ID) rank, N+ lists "
+            name = ("degree-oriented row-padded slots (u = lower (degree, ID) rank, N+ lists "
                     "of degree_order), one u per slot group")
+            if lay.regroup > 0:
+                name += (f"; N+ rows of <= {lay.regroup} entries regrouped by their higher-rank "
+                         "endpoint (fewer pad slots)")
+            return name
         if lay.kind.endswith("+onehash-rank"):
             return ("row-padded slots grouped by the table endpoint ("
                     + ("higher (degree, ID) rank" if lay.kind.startswith("degree") else "lower ID")
@@ -423,7 +428,7 @@ class BloomProvider(_SketchProvider):
                 thr = int(os.environ.get("PG_TC_HYBRID", "2"))
                 if thr > 0 and dev.nnz > 0:
                     ug, vs, slots = dev.hybrid_slots(pad, thr)
-                    return TcLayout(ug, vs, slots, 2, "degree")
+                    return TcLayout(ug, vs, slots, 2, "degree", regroup=thr)
                 ug, vs, slots, _ = dev.hub_slots(pad, 0)
                 return TcLayout(ug, vs, slots, 2, "degree")
             ug, vs, slots = dev.upper_edges_group_u(pad)
