@@ -296,8 +296,21 @@ class DeviceCsr:
                 k = slots.value
                 parts.append((us[:k:pad], vs[:k], k))
                 del ws
-            ug = torch.cat([parts[0][0], parts[1][0]])
-            vs = torch.cat([parts[0][1], parts[1][1]])
+            # the two parts interleaved in 64 segments each, so that any
+            # contiguous share of the slots (a rank's shard) holds the same mix
+            # (part 2 streams low-degree rows from HBM and runs ~13 % slower
+            # per slot: with it at the end the last of 8 shards took 0.644 ms
+            # against 0.57 for the others)
+            seg = 64
+            ugs, vss = [], []
+            for i in range(seg):
+                for g_arr, v_arr, k in parts:
+                    groups = k // pad
+                    a, b = groups * i // seg, groups * (i + 1) // seg
+                    ugs.append(g_arr[a:b])
+                    vss.append(v_arr[a * pad:b * pad])
+            ug = torch.cat(ugs)
+            vs = torch.cat(vss)
             self._layouts[key] = (ug, vs, parts[0][2] + parts[1][2])
         return self._layouts[key]
 
