@@ -253,12 +253,13 @@ class DeviceCsr:
 
     def hybrid_slots(self, pad: int, thr: int):
         """Degree-oriented group-u slots with less padding: (ug, vs, slots).
-        Rows of the N+ lists with more than `thr` entries keep their own slot
-        groups (as hub_slots(pad, 0)); the edges of the shorter rows -- 4 % of
-        the edges but two thirds of the pad slots at R-MAT -- are grouped by
-        their higher-rank endpoint instead (its row is the one a group holds
-        in registers), where they form long runs.  Every edge still appears
-        once; which endpoint is called u only matters for the schedule."""
+        The N+ rows keep their own slot groups (as hub_slots(pad, 0)) except
+        for a last group of at most `thr` entries (the whole row when it has
+        at most thr): those edges -- a few per cent of the edges, most of the
+        pad slots at R-MAT -- are grouped by their higher-rank endpoint
+        instead (its row is the one a group holds in registers), where they
+        form long runs.  Every edge still appears once; which endpoint is
+        called u only matters for the schedule."""
         key = ("hybrid", pad, thr)
         if key not in self._layouts:
             import ctypes
@@ -267,12 +268,19 @@ class DeviceCsr:
             _, off, adj = self.degree_rank()
             n = self.n
             dplus = off[1:] - off[:-1]
-            keep_row = dplus > thr
+            # a row's last (d+ mod pad) entries fill a slot group of their own:
+            # when that remainder is at most thr they move to part 2 (for rows
+            # of at most thr entries that is the whole row)
+            rem = dplus % pad
+            moved = torch.where((rem > 0) & (rem <= thr), rem, torch.zeros_like(rem))
+            kept = dplus - moved
             src = torch.repeat_interleave(torch.arange(n, dtype=torch.int32, device="cuda"), dplus)
-            keep = keep_row[src.long()]
-            # part 1: the long rows by their own (lower-rank) vertex
+            pos = torch.arange(adj.numel(), dtype=torch.int64, device="cuda") - off[:-1][src.long()]
+            keep = pos < kept[src.long()]
+            del pos
+            # part 1: the kept entries by their own (lower-rank) vertex
             off1 = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
-            off1[1:] = torch.cumsum(dplus * keep_row, 0)
+            off1[1:] = torch.cumsum(kept, 0)
             adj1 = adj[keep].contiguous()
             # part 2: the short rows' edges by the higher-rank endpoint
             lo, hi = src[~keep], adj[~keep]

@@ -296,8 +296,8 @@ class _SketchProvider(IntersectionProvider):
             name = ("degree-oriented row-padded slots (u = lower (degree, ID) rank, N+ lists "
                     "of degree_order), one u per slot group")
             if lay.regroup > 0:
-                name += (f"; N+ rows of <= {lay.regroup} entries regrouped by their higher-rank "
-                         "endpoint (fewer pad slots)")
+                name += (f"; last slot groups of <= {lay.regroup} entries regrouped by their "
+                         "higher-rank endpoint (fewer pad slots)")
             return name
         if lay.kind.endswith("+onehash-rank"):
             return ("row-padded slots grouped by the table endpoint ("
@@ -422,10 +422,10 @@ class BloomProvider(_SketchProvider):
             big = sg.n * sg.bit_length // 8 > self.DEGREE_ORIENT_MIN_BYTES
             orient = os.environ.get("PG_TC_ORIENT", "degree" if big else "id")
             if orient == "degree" and dev.n > 0:
-                # rows of at most `thr` N+ entries are regrouped by their other
-                # endpoint (DeviceCsr.hybrid_slots): 19 % -> 13 % pad slots at
-                # R-MAT; c5 4.43 -> 4.27 ms (thr 2; 4: 4.28, 8: 4.40)
-                thr = int(os.environ.get("PG_TC_HYBRID", "2"))
+                # a row's last slot group of at most `thr` entries is regrouped
+                # by the other endpoint (DeviceCsr.hybrid_slots): 19 % -> 7 % pad
+                # slots at R-MAT; c5 4.43 -> 4.11 ms (thr 4; 2: 4.16, 3: 4.12, 5: 4.12)
+                thr = int(os.environ.get("PG_TC_HYBRID", "4"))
                 if thr > 0 and dev.nnz > 0:
                     ug, vs, slots = dev.hybrid_slots(pad, thr)
                     return TcLayout(ug, vs, slots, 2, "degree", regroup=thr)
