@@ -538,6 +538,12 @@ class MinHashProvider(_SketchProvider):
         if (not self.onehash and pad > 1 and sg.capacity in (16, 32, 64) and dev.n > 0
                 and sg.n * sg.capacity * 4 > BloomProvider.DEGREE_ORIENT_MIN_BYTES
                 and os.environ.get("PG_TC_ORIENT", "degree") == "degree"):
+            # as BloomProvider: nearly empty last slot groups regrouped by the
+            # other endpoint (c4: 2.749 -> 2.712 ms at 2; 1: 2.726)
+            thr = int(os.environ.get("PG_TC_HYBRID_KHASH", "2"))
+            if thr > 0 and dev.nnz > 0:
+                ug, vs, slots = dev.hybrid_slots(pad, thr)
+                return TcLayout(ug, vs, slots, 2, "degree", regroup=thr)
             ug, vs, slots, _ = dev.hub_slots(pad, 0)
             return TcLayout(ug, vs, slots, 2, "degree")
         return super()._tc_layout(dev)
