@@ -251,7 +251,7 @@ class DeviceCsr:
             self._layouts[key] = (us[:k:pad].contiguous(), vs[:k], k, hub_ids)
         return self._layouts[key]
 
-    def hybrid_slots(self, pad: int, thr: int):
+    def hybrid_slots(self, pad: int, thr: int, base: str = "degree"):
         """Degree-oriented group-u slots with less padding: (ug, vs, slots).
         The N+ rows keep their own slot groups (as hub_slots(pad, 0)) except
         for a last group of at most `thr` entries (the whole row when it has
@@ -259,14 +259,20 @@ class DeviceCsr:
         pad slots at R-MAT -- are grouped by their higher-rank endpoint
         instead (its row is the one a group holds in registers), where they
         form long runs.  Every edge still appears once; which endpoint is
-        called u only matters for the schedule."""
-        key = ("hybrid", pad, thr)
+        called u only matters for the schedule.  base = "id" does the same
+        over the upper-triangle lists (u < v by ID)."""
+        key = ("hybrid", pad, thr, base)
         if key not in self._layouts:
             import ctypes
             import torch
             from . import _native as N
-            _, off, adj = self.degree_rank()
             n = self.n
+            if base == "degree":
+                _, off, adj = self.degree_rank()
+            else:  # "id": the upper-triangle lists (u < v by ID)
+                ts, adj = self.upper_edges()
+                off = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
+                off[1:] = torch.cumsum(torch.bincount(ts, minlength=n), 0)
             dplus = off[1:] - off[:-1]
             # a row's last (d+ mod pad) entries fill a slot group of their own:
             # when that remainder is at most thr they move to part 2 (for rows

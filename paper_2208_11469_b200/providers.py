@@ -431,6 +431,10 @@ class BloomProvider(_SketchProvider):
                     return TcLayout(ug, vs, slots, 2, "degree", regroup=thr)
                 ug, vs, slots, _ = dev.hub_slots(pad, 0)
                 return TcLayout(ug, vs, slots, 2, "degree")
+            thr = int(os.environ.get("PG_TC_HYBRID_ID", "0"))
+            if thr > 0 and dev.nnz > 0:
+                ug, vs, slots = dev.hybrid_slots(pad, thr, "id")
+                return TcLayout(ug, vs, slots, 2, regroup=thr)
             ug, vs, slots = dev.upper_edges_group_u(pad)
             return TcLayout(ug, vs, slots, 2)
         return super()._tc_layout(dev)

@@ -16,9 +16,10 @@ def pg():
     return pg
 
 
+@pytest.mark.parametrize("base", ["degree", "id"])
 @pytest.mark.parametrize("graph", ["rmat12", "rmat14", "er", "star"])
 @pytest.mark.parametrize("thr", [1, 2, 4, 8])
-def test_hybrid_slots_cover_every_edge_once(pg, graph, thr):
+def test_hybrid_slots_cover_every_edge_once(pg, graph, thr, base):
     if graph == "rmat12":
         g = pg.generate_kronecker(12, 16, 3)
     elif graph == "rmat14":
@@ -30,7 +31,7 @@ def test_hybrid_slots_cover_every_edge_once(pg, graph, thr):
         g = pg.CsrGraph.from_edges(e, 320)
     dev = g.device()
     pad = 8
-    ug, vs, slots = dev.hybrid_slots(pad, thr)
+    ug, vs, slots = dev.hybrid_slots(pad, thr, base)
     ug, vs = ug.cpu().numpy(), vs.cpu().numpy()
     assert slots % pad == 0 and len(vs) == slots and len(ug) == slots // pad
     us = np.repeat(ug, pad)
@@ -41,8 +42,21 @@ def test_hybrid_slots_cover_every_edge_once(pg, graph, thr):
     e = g.edges()
     assert np.array_equal(got, np.sort(e[:, 0] * g.n + e[:, 1]))
     # what it is for: fewer pad slots on skewed graphs
-    if graph.startswith("rmat"):
-        assert slots < dev.hub_slots(pad, 0)[2]
+    if graph.startswith("rmat") and thr < pad:
+        plain = dev.hub_slots(pad, 0)[2] if base == "degree" else dev.upper_edges_group_u(pad)[2]
+        assert slots < plain
+
+
+def test_bloom_tc_over_id_hybrid_layout(pg, monkeypatch):
+    from paper_2208_11469_b200.mining import tc_counts
+    g = pg.generate_kronecker(13, 16, 7)
+    sk = pg.build_sketched_graph(g, "bloom", s=1.0, b=2, bits_override=1024)
+    monkeypatch.setenv("PG_TC_ORIENT", "id")
+    want = tc_counts(pg.make_provider("bf_and", sketched=sk), g.device()).cpu().numpy()
+    monkeypatch.setenv("PG_TC_HYBRID_ID", "2")
+    p = pg.make_provider("bf_and", sketched=sk)
+    assert p._tc_layout(g.device()).regroup == 2
+    assert np.array_equal(tc_counts(p, g.device()).cpu().numpy(), want)
 
 
 @pytest.mark.parametrize("thr", ["0", "2", "5"])
